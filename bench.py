@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""Benchmark of the DP-KFAC second-order update (BASELINE.json metric) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--model resnet50|resnet32|densenet201|mlp] [--inv-type inverse|eigen]
+
+A "step" is one DP-KFAC second-order update (kfaclab distsim.dp_kfac_step's
+second-order part, distsim.py:300-337): Kronecker-factor SYRK + running
+average, damped inversion, gradient reduce-scatter, preconditioning,
+all-gather -- over one synthetic batch per GPU (ResNet-50: 32 x 3x224x224,
+random init, synthetic data) whose layer captures and gradients are resident in
+HBM when the timed region starts (they total > 1.4 GB, larger than L2, so no
+flush is needed).  ``value`` = samples/s of that update for the whole job
+(iter/s x 32 x N); ``e2e`` = the same through the public API for full training
+iterations (pinned-host batch H2D, forward, backward, DPKFAC.step(),
+optimizer.step(), loss D2H).
+
+``--impl reference`` times the reference algorithm on the host CPU (the
+float64 oracle port of kfaclab's kfac.py, all host threads) on a bounded,
+rotating sample of the same layers, extrapolated to a whole update by the
+per-layer cost model.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DP-KFAC 2nd-order update ms/iter + iter/s, ResNet-50 at 1/2/4/8 B200 vs CPU"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="resnet50")
+    ap.add_argument("--inv-type", default="inverse", choices=["inverse", "eigen"])
+    ap.add_argument("--gamma", type=float, default=0.002)
+    ap.add_argument("--xi", type=float, default=0.95)      # reference default (kfac.py:61)
+    ap.add_argument("--precision", default="tf32", choices=["tf32", "3xtf32"])
+    ap.add_argument("--assignment", default="round_robin")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ----------------------------------------------------------------- CPU reference (oracle port)
+def cpu_reference_sample(geom, group: int, groups: int, inv_type: str, gamma: float, xi: float, seed: int = 0):
+    """Run the reference algorithm (float64 oracle port of kfaclab kfac.py) on the
+    layers i with i % groups == group: factor SYRK (second update, so the EMA
+    blend runs), damped inverses or eigendecompositions, preconditioning.
+    Synthetic captures of the exact unfolded shapes.  Returns (seconds, sample_cost)."""
+    import numpy as np
+
+    from oracle import kfac_ref as K  # bench.py's cpu_baseline / reference leg only
+    from paper_2206_15143_b200.partition import layer_cost
+
+    rng = np.random.default_rng(seed + group)
+    h = K.Hyper(gamma=gamma, xi=xi, inv_type=inv_type)
+    total = 0.0
+    cost = 0.0
+    for i, (name, d_in, d_out, m, conv) in enumerate(geom):
+        if i % groups != group:
+            continue
+        x = np.maximum(rng.standard_normal((d_in, m)), 0.0)
+        x[-1] = 1.0
+        g = rng.standard_normal((d_out, m)) * 1e-2
+        grad = rng.standard_normal((d_out, d_in)) * 1e-3
+        st = K.LayerState()
+        a0, g0 = K.compute_factors(x[:, : min(m, 64)], g[:, : min(m, 64)])
+        K.update_running_average(st, a0, g0, xi, 0)  # initialised state: the timed update blends
+        t0 = time.perf_counter()
+        K.kfac_layer_step(st, x, g, grad, h, 1)
+        total += time.perf_counter() - t0
+        cost += layer_cost(d_in, d_out, m, inv_type)
+        del x, g
+    return total, cost
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count()
+
+
+def run_reference(args, rank, world):
+    """--impl reference: rank 0 times the CPU reference on rotating bounded samples."""
+    if rank != 0:
+        return
+    import bench_models as BM
+    from paper_2206_15143_b200.partition import layer_cost
+
+    ctor, batch, shape, classes = BM.WORKLOADS[args.model]
+    geom = BM.layer_geometry(ctor(), shape, batch)
+    full_cost = sum(layer_cost(d_in, d_out, m, args.inv_type) for _, d_in, d_out, m, _ in geom)
+    groups = 9 if len(geom) > 20 else 1
+    est = []
+    for s in range(args.warmup + args.steps):
+        secs, c = cpu_reference_sample(geom, s % groups, groups, args.inv_type, args.gamma, args.xi)
+        if s >= args.warmup and c > 0:
+            est.append(secs * full_cost / c)
+    ms = 1000.0 * statistics.median(est)
+    # P ranks of the simulated cluster run their owned layers sequentially (distsim.py:310-329),
+    # so the reference's whole-job iteration time does not shrink with P: samples/s = B*P / t.
+    value = batch * world / (ms / 1000.0)
+    line = {
+        "metric": METRIC, "impl": "reference", "value": value, "unit": "samples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "iter_per_s": 1000.0 / ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.model} DP-KFAC 2nd-order update, batch {batch}/GPU, {args.inv_type}",
+                   "model": args.model, "global_batch": batch * world, "parallelism": f"dp{world}"},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": host_threads(), "kind": "port",
+                         "sample": f"per step: layers i % {groups} == step % {groups} of {len(geom)} "
+                                   "(synthetic captures of the exact unfolded shapes), kfac_layer_step in "
+                                   "float64 numpy/scipy (OpenBLAS, all host threads), extrapolated to all "
+                                   "layers by the per-layer flop model; median over timed steps"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- ours
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import torch.nn.functional as F
+
+    import bench_models as BM
+    from paper_2206_15143_b200 import DPKFAC, _lib
+    from paper_2206_15143_b200.partition import layer_cost
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    torch.backends.cudnn.benchmark = True
+    lib = _lib.load()
+    ctor, batch, shape, classes = BM.WORKLOADS[args.model]
+    torch.manual_seed(0)
+    model = ctor().to(dev)
+    geom = BM.layer_geometry(model, shape, batch)
+    kf = DPKFAC(model, gamma=args.gamma, xi=args.xi, inv_type=args.inv_type, f_freq=1, k_freq=1,
+                assignment=args.assignment, precision=args.precision, check_numerics="deferred")
+    opt = torch.optim.SGD(model.parameters(), lr=1e-3, momentum=0.9)
+    gen = torch.Generator().manual_seed(1234 + rank)
+    x_host = torch.randn(batch, *shape, generator=gen).pin_memory()
+    y_host = torch.randint(0, classes, (batch,), generator=gen).pin_memory()
+    x = x_host.to(dev)
+    y = y_host.to(dev)
+
+    def sync_barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # one forward/backward: captures + gradients resident in HBM
+    model.zero_grad(set_to_none=False)
+    F.cross_entropy(model(x), y).backward()
+    kf.step()  # first step builds buffers/balance; captures are consumed
+    model.zero_grad(set_to_none=False)
+    F.cross_entropy(model(x), y).backward()
+    saved_caps = {ly.index: (ly.a_in, ly.g_out, ly.batch) for ly in kf.owned}
+    layer_params = [p for ly in kf.layers for p in ([ly.module.weight] + ([ly.module.bias] if ly.has_bias else []))]
+    saved_grads = [p.grad.clone() for p in layer_params]
+
+    def restore():
+        for ly in kf.owned:
+            ly.a_in, ly.g_out, ly.batch = saved_caps[ly.index]
+        torch._foreach_copy_([p.grad for p in layer_params], saved_grads)
+
+    for _ in range(args.warmup):
+        restore()
+        kf.step()
+    kf.check()
+    sync_barrier()
+    kf.enable_stage_timing(True)
+    launches0 = lib.dpk_launch_count()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        sync_barrier()
+        start.record()
+        for _ in range(args.steps):
+            restore()
+            kf.step()
+        end.record()
+        sync_barrier()
+    kf.check()
+    launches = lib.dpk_launch_count() - launches0
+    ms_local = start.elapsed_time(end) / args.steps
+    stages = {k: v / args.steps for k, v in kf.stage_ms().items()}
+    kf.enable_stage_timing(False)
+    t = torch.tensor([ms_local], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    value = batch * world / (ms / 1000.0)
+
+    # ---- roofline of the dominant stage's kernel(s)
+    peaks = {}
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk):
+        with open(pk) as f:
+            peaks = json.load(f)
+    bf16 = peaks.get("bf16_tflops")
+    tf32_peak = (bf16 / 2.0) if bf16 else 1590.0 / 2.0
+    peak_src = ("MEASURED_PEAKS.json bf16_tflops / 2 (tcgen05 kind::tf32 issues at half the bf16 rate)"
+                if bf16 else "B200_PROFILING.md fallback 1.59 PF bf16 / 2")
+    own = [geom[ly.index] for ly in kf.owned]
+    flops = {
+        "factors": sum(d_in * (d_in + 1) * m + d_out * (d_out + 1) * m for _, d_in, d_out, m, _ in own),
+        "inversion": sum(float(d_in) ** 3 + float(d_out) ** 3 for _, d_in, d_out, m, _ in own)
+        if args.inv_type == "inverse" else sum(9.0 * (float(d_in) ** 3 + float(d_out) ** 3) for _, d_in, d_out, m, _ in own),
+        "precondition": sum(2.0 * (d_out * d_out * d_in + d_out * d_in * d_in) * (1 if args.inv_type == "inverse" else 2)
+                            for _, d_in, d_out, m, _ in own),
+    }
+    compute_stages = {k: stages.get(k, 0.0) for k in flops}
+    dom = max(compute_stages, key=compute_stages.get)
+    achieved = flops[dom] / (compute_stages[dom] / 1000.0) / 1e12 if compute_stages[dom] > 0 else 0.0
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get(dom)
+        except (OSError, ValueError):
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
+                "frac": achieved / tf32_peak, "traffic": traffic, "kernel": dom,
+                "peak_source": peak_src,
+                "algorithmic_work": f"{dom}: {flops[dom] / 1e12:.4f} TFLOP per step (SURVEY 8(d) conventions)"}
+    stage_roofline = {k: {"ms": compute_stages[k], "tflops": (flops[k] / (compute_stages[k] / 1000.0) / 1e12)
+                          if compute_stages[k] > 0 else None,
+                          "frac_of_tf32": ((flops[k] / (compute_stages[k] / 1000.0) / 1e12) / tf32_peak)
+                          if compute_stages[k] > 0 else None} for k in flops}
+
+    # ---- e2e through the public API: pinned H2D + fwd + bwd + DPKFAC.step() + SGD + loss D2H
+    e2e = None
+    if not args.no_e2e:
+        k_e2e = args.e2e_steps or args.steps
+        for ly in kf.owned:
+            ly.a_in = ly.g_out = None
+        del saved_caps, saved_grads
+
+        def train_step():
+            xb = x_host.to(dev, non_blocking=True)
+            yb = y_host.to(dev, non_blocking=True)
+            opt.zero_grad(set_to_none=False)
+            loss = F.cross_entropy(model(xb), yb)
+            loss.backward()
+            kf.step()
+            opt.step()
+            return loss.item()
+
+        for _ in range(2):
+            train_step()
+        sync_barrier()
+        s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s2.record()
+        t0 = time.perf_counter()
+        for _ in range(k_e2e):
+            train_step()
+        e2.record()
+        sync_barrier()
+        e2e_ms = torch.tensor([s2.elapsed_time(e2) / k_e2e], device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        e2e_ms = float(e2e_ms.item())
+        e2e = {"value": batch * world / (e2e_ms / 1000.0), "unit": "samples/s", "ms_per_iter": e2e_ms,
+               "h2d_bytes_per_step": x_host.numel() * x_host.element_size() + y_host.numel() * y_host.element_size(),
+               "d2h_bytes_per_step": 4,
+               "what": "full training iteration: pinned-host batch H2D, forward, backward, DPKFAC.step(), "
+                       "SGD step, loss.item()"}
+
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        full_cost = sum(layer_cost(d_in, d_out, m, args.inv_type) for _, d_in, d_out, m, _ in geom)
+        groups = 9 if len(geom) > 20 else 1
+        secs, c = cpu_reference_sample(geom, 0, groups, args.inv_type, args.gamma, args.xi)
+        cpu_ms = 1000.0 * secs * full_cost / c
+        cpu_baseline = {"value": batch / (cpu_ms / 1000.0), "unit": "samples/s", "cores": host_threads(),
+                        "kind": "port", "ms_per_iter": cpu_ms,
+                        "sample": f"layers i % {groups} == 0 of {len(geom)} (synthetic captures of the exact "
+                                  "unfolded shapes), float64 kfac_layer_step (oracle port of kfaclab kfac.py, "
+                                  "numpy/scipy OpenBLAS, all host threads), extrapolated by the per-layer flop model"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "iter_per_s": 1000.0 / ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (tf32 tensor-core factors, 3xtf32 inverse/precondition)" if args.precision == "tf32" else "f32 (3xtf32)",
+            "data": "synthetic (randn images, random labels, torch.manual_seed(0) random-init weights)",
+            "config": {"workload": f"{args.model} DP-KFAC 2nd-order update, batch {batch}/GPU, "
+                                   f"inv_type={args.inv_type}, gamma={args.gamma}, xi={args.xi}, F=K=1",
+                       "model": args.model, "global_batch": batch * world, "parallelism": f"dp{world}",
+                       "assignment": args.assignment, "l2": "inputs (layer captures, >1.4 GB) larger than L2; no flush"},
+            "stages_ms": stages, "stage_roofline": stage_roofline, "roofline": roofline,
+            "cpu_baseline": cpu_baseline, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clocks.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    kf.remove_hooks()
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

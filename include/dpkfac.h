@@ -1,0 +1,244 @@
+/*
+ * dpkfac.h -- C ABI of libdpkfac.so, the B200 (sm_100a) DP-KFAC second-order update.
+ *
+ * Every entry point replaces one function of the reference's hot path
+ * (kfaclab 0.1.0, /root/reference/pkg/src/kfaclab); the citation is given
+ * beside each declaration.  The reference is Python-over-numpy, so its "FFI"
+ * is the Python call itself: INTEGRATION.md shows the ctypes binding a
+ * kfaclab maintainer would add to route kfac.py / distsim.py through here.
+ *
+ * Conventions
+ *   - All matrix / tensor pointers are DEVICE pointers owned by the caller
+ *     (torch owns every byte; the library never allocates persistent memory).
+ *     Scratch space is passed in explicitly as (workspace, bytes) and must be
+ *     zero-filled once when first allocated (split-K semaphores live there and
+ *     are restored to zero by every call).
+ *   - Matrices are row-major float32.  Factors are d x d and exactly symmetric.
+ *   - Calls are asynchronous on the given stream and stateless, hence
+ *     reentrant across streams.  No C++ exception crosses this boundary.
+ *   - Return value: DPK_OK or a synchronous error (bad argument, shape, CUDA
+ *     launch failure).  Numeric failures (non-SPD pivot, non-positive trace or
+ *     eigen denominator, non-finite values) are reported asynchronously through
+ *     caller-provided device int32 "info" words: 0 = fine, >0 = failure code.
+ *   - Precision: DPK_PREC_TF32 runs one tcgen05 kind::tf32 pass on
+ *     round-to-nearest TF32 operands; DPK_PREC_3XTF32 splits every operand into
+ *     hi + lo TF32 parts and accumulates hi*hi + hi*lo + lo*hi (fp32-grade).
+ */
+#ifndef DPKFAC_H_
+#define DPKFAC_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* dpk_stream_t; /* a cudaStream_t (torch.cuda.current_stream().cuda_stream) */
+
+enum {
+  DPK_OK = 0,
+  DPK_EARG = 1,     /* invalid argument (reference ArgumentError, errors.py:17) */
+  DPK_ESHAPE = 2,   /* incompatible shapes (reference ShapeError, errors.py:13) */
+  DPK_ECUDA = 3,    /* CUDA launch / runtime failure */
+  DPK_ENOSPACE = 4  /* workspace too small */
+};
+
+enum { DPK_PREC_TF32 = 1, DPK_PREC_3XTF32 = 3 };
+
+/* info codes written to device info words */
+enum {
+  DPK_INFO_OK = 0,
+  DPK_INFO_TRACE = 1,      /* Tr(A) <= 0 or Tr(G) <= 0 (kfac.py:133-136) */
+  DPK_INFO_NOT_SPD_A = 2,  /* damped A not positive definite (kfac.py:149-150) */
+  DPK_INFO_NOT_SPD_G = 3,  /* damped G not positive definite (kfac.py:153-154) */
+  DPK_INFO_EIG_DENOM = 4,  /* eigen damping denominator <= 0 (kfac.py:185-189) */
+  DPK_INFO_NONFINITE = 5   /* non-finite decomposition (numerics.py:87-96) */
+};
+
+/* ------------------------------------------------------------------------
+ * Operand views: how to read element (row r, column k) of a column-per-sample
+ * capture X (reference convention, model.py:14-16: d x B, columns = samples).
+ * ------------------------------------------------------------------------ */
+enum {
+  DPK_OPND_ROWS_K = 0,  /* X[r,k] = data[r*ld + k]            (rows contiguous in k)   */
+  DPK_OPND_ROWS_MN = 1, /* X[r,k] = data[k*ld + r]            (e.g. nn.Linear input B x d) */
+  DPK_OPND_IM2COL = 2   /* X[(c,i,j),(n,oh,ow)] = x[n, c, oh*sh-ph+i*dh, ow*sw-pw+j*dw] or 0:
+                           the implicit-im2col linear form of a Conv2d input (F.unfold order) */
+};
+
+typedef struct dpk_operand {
+  const float* data;
+  int32_t kind;
+  int32_t rows;      /* feature rows, excluding the bias row */
+  int32_t bias_row;  /* 1: a constant-ones row is appended LAST (model.py:140-143) */
+  int32_t _pad0;
+  int64_t cols;      /* number of sample columns M (B, or B*OH*OW for convs) */
+  int64_t ld;        /* ROWS_K / ROWS_MN leading dimension in elements */
+  /* IM2COL geometry: input tensor N x C x H x W addressed with element strides */
+  int32_t C, H, W, OH, OW;
+  int32_t kh, kw, sh, sw, ph, pw, dh, dw;
+  int32_t _pad1;
+  int64_t sn, sc, shs, sws;
+} dpk_operand;
+
+/* ------------------------------------------------------------------------
+ * K1 / K2: Kronecker-factor construction with the running average fused.
+ *   F <- alpha * X X^T + beta * F      (F d x d, d = rows + bias_row)
+ * replaces kfac.compute_factors (kfac.py:85-104) + update_running_average
+ * (kfac.py:107-125): first update alpha = s^2/M, beta = 0 (F not read);
+ * later alpha = xi*s^2/M, beta = 1 - xi, where s scales the capture
+ * (s = B_local for torch grad_output, model.py:9-12).  Lower-triangle tiles
+ * are computed on tcgen05 tensor cores and mirrored, so F is exactly
+ * symmetric like the reference's (F + F^T)/2.
+ * ------------------------------------------------------------------------ */
+typedef struct dpk_factor_job {
+  dpk_operand x;
+  float* factor;
+  float alpha;
+  float beta;
+} dpk_factor_job;
+
+size_t dpk_factor_workspace_bytes(const dpk_factor_job* jobs, int n_jobs);
+int dpk_syrk_ema(const dpk_factor_job* jobs, int n_jobs, void* workspace, size_t ws_bytes, int precision,
+                 dpk_stream_t stream);
+/* K2 entry point: identical contract; every job's operand must be DPK_OPND_IM2COL. */
+int dpk_conv_im2col_syrk_ema(const dpk_factor_job* jobs, int n_jobs, void* workspace, size_t ws_bytes,
+                             int precision, dpk_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * Grouped tensor-core GEMM used by preconditioning (and exposed for tests):
+ *   out[m,n] = alpha * sum_k A[m,k] B[n,k] + beta * cin[m,n]
+ * with A = a (rows M) and B = b (rows N) read through operand views.
+ * symmetric=1 computes lower tiles only and mirrors (requires M == N).
+ * ------------------------------------------------------------------------ */
+typedef struct dpk_gemm_job {
+  dpk_operand a;
+  dpk_operand b;
+  float* out;
+  int64_t ldo;
+  const float* cin; /* may alias out; not read when beta == 0 */
+  int64_t ldc;
+  float alpha;
+  float beta;
+  int32_t symmetric;
+  int32_t _pad0;
+} dpk_gemm_job;
+
+size_t dpk_gemm_workspace_bytes(const dpk_gemm_job* jobs, int n_jobs);
+int dpk_gemm(const dpk_gemm_job* jobs, int n_jobs, void* workspace, size_t ws_bytes, int precision,
+             dpk_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * A6: trace-balancing scalar and damping shifts on device (kfac.py:128-155).
+ *   pi = sqrt((tr A / d_A) / (tr G / d_G)); shift_a = pi*sqrt(gamma); shift_g = sqrt(gamma)/pi
+ * shifts[2*i] = shift_a, shifts[2*i+1] = shift_g, pis[i] = pi; info[i] = DPK_INFO_TRACE on tr <= 0.
+ * ------------------------------------------------------------------------ */
+typedef struct dpk_pi_job {
+  const float* a;
+  const float* g;
+  int32_t da;
+  int32_t dg;
+  float* shifts; /* 2 floats */
+  float* pi;     /* 1 float (may be NULL) */
+  int32_t* info;
+} dpk_pi_job;
+
+int dpk_trace_pi(const dpk_pi_job* jobs, int n_jobs, float gamma, dpk_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K3: batched damped SPD inverse  dst = (src + shift*I)^-1, symmetrized
+ * (numerics.sym_inverse numerics.py:100-114 via kfac.damped_inverses
+ * kfac.py:140-155).  Cholesky-based: n <= 128 runs one shared-memory CTA per
+ * matrix (potrf + trtri + lauum); larger n run a blocked symmetric sweep whose
+ * rank-64 updates are tcgen05 3xTF32 GEMMs.  On a non-positive pivot *info is
+ * set to fail_code and dst is left undefined.  src and dst may not alias.
+ * ------------------------------------------------------------------------ */
+typedef struct dpk_spd_job {
+  const float* src;
+  float* dst;
+  int32_t n;
+  int32_t fail_code;   /* DPK_INFO_NOT_SPD_A or DPK_INFO_NOT_SPD_G */
+  const float* shift;  /* device scalar added to the diagonal; NULL = 0 */
+  int32_t* info;
+} dpk_spd_job;
+
+size_t dpk_chol_inv_workspace_bytes(const dpk_spd_job* jobs, int n_jobs);
+int dpk_chol_inv_damped_batched(const dpk_spd_job* jobs, int n_jobs, void* workspace, size_t ws_bytes,
+                                dpk_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K5: inverse-mode preconditioning out = G_inv @ grad @ A_inv (kfac.py:251-254).
+ * tmp is a d_out x d_in scratch matrix per job.
+ * ------------------------------------------------------------------------ */
+typedef struct dpk_precond_job {
+  const float* grad;   /* d_out x d_in */
+  const float* a_mat;  /* d_in x d_in  (A_inv, or Q_A for eigen) */
+  const float* g_mat;  /* d_out x d_out (G_inv, or Q_G for eigen) */
+  const float* a_vals; /* eigen mode: d_in eigenvalues (descending) */
+  const float* g_vals; /* eigen mode: d_out eigenvalues */
+  float* out;          /* d_out x d_in */
+  float* tmp;          /* d_out x d_in scratch */
+  int32_t d_out;
+  int32_t d_in;
+  int32_t* info;       /* eigen mode: DPK_INFO_EIG_DENOM if min denominator <= 0 */
+} dpk_precond_job;
+
+size_t dpk_precond_workspace_bytes(const dpk_precond_job* jobs, int n_jobs);
+int dpk_precond_inverse(const dpk_precond_job* jobs, int n_jobs, void* workspace, size_t ws_bytes,
+                        int precision, dpk_stream_t stream);
+/* K6: eigen-mode preconditioning (kfac.py:174-191):
+ *   out = Q_G ((Q_G^T grad Q_A) / (max(v_G,0) max(v_A,0)^T + gamma)) Q_A^T */
+int dpk_precond_eigen(const dpk_precond_job* jobs, int n_jobs, float gamma, void* workspace, size_t ws_bytes,
+                      int precision, dpk_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K4: batched symmetric eigendecomposition (numerics.sym_eig numerics.py:75-97):
+ * symmetrize, decompose, eigenvalues DESCENDING, eigenvectors as columns of q.
+ * ------------------------------------------------------------------------ */
+typedef struct dpk_eig_job {
+  const float* src; /* n x n */
+  float* q;         /* n x n, columns = eigenvectors */
+  float* w;         /* n eigenvalues, descending */
+  int32_t n;
+  int32_t _pad0;
+  int32_t* info;    /* DPK_INFO_NONFINITE on failure */
+} dpk_eig_job;
+
+size_t dpk_syevd_workspace_bytes(const dpk_eig_job* jobs, int n_jobs);
+int dpk_syevd_batched(const dpk_eig_job* jobs, int n_jobs, void* workspace, size_t ws_bytes,
+                      dpk_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K7: owner-major gradient pack / unpack for the NCCL reduce-scatter and
+ * all-gather that replace distsim._aggregate_grads (distsim.py:259-265) and
+ * the per-layer broadcast loop (distsim.py:333-336).  A segment moves the
+ * layer gradient [W | b] (rows x (cols_w + has_bias), bias column LAST,
+ * model.py:250) between a weight tensor (+ optional bias vector) and a flat
+ * buffer at elem offset.  pack: flat = scale * [W | b]; unpack: W, b = scale * flat.
+ * ------------------------------------------------------------------------ */
+typedef struct dpk_segment {
+  float* weight;     /* rows x cols_w, row stride ldw */
+  float* bias;       /* rows, or NULL */
+  int64_t offset;    /* element offset in the flat buffer */
+  int32_t rows;
+  int32_t cols_w;
+  int64_t ldw;
+  int32_t perm_khw;  /* reserved (0) */
+  int32_t _pad0;
+} dpk_segment;
+
+int dpk_pack_owner_major(const dpk_segment* segs, int n_segs, float* flat, float scale, dpk_stream_t stream);
+int dpk_unpack_owner_major(const dpk_segment* segs, int n_segs, const float* flat, float scale,
+                           dpk_stream_t stream);
+
+/* Library / device introspection. */
+const char* dpk_version(void);
+const char* dpk_last_error(void);
+/* number of kernels this library has launched in the process (bench evidence) */
+unsigned long long dpk_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DPKFAC_H_ */

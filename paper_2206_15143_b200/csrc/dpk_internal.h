@@ -1,0 +1,55 @@
+// Internal (C++) interfaces shared by the translation units of libdpkfac.so.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+#include "../../include/dpkfac.h"
+
+namespace dpk {
+
+void set_error(const std::string& msg);
+void note_launch();  // counts every kernel this library launches (dpk_launch_count)
+int cuda_status(cudaError_t e, const char* what);
+int num_sms();
+
+// -------------------------------------------------------------- GEMM engine
+enum { EPI_LINEAR = 0, EPI_EIGDIV = 1 };
+
+struct GemmSpec {
+  dpk_gemm_job job;
+  int epi;              // EPI_LINEAR or EPI_EIGDIV
+  const float* vrow;    // EIGDIV: per-row eigenvalues (G side)
+  const float* vcol;    // EIGDIV: per-column eigenvalues (A side)
+  float gamma;          // EIGDIV damping
+  float* out_t;         // optional: also write out_t[n*ldt + m] = value (transposed copy)
+  int64_t ldt;
+};
+
+size_t gemm_workspace_bytes(const GemmSpec* specs, int n);
+int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int precision, cudaStream_t st);
+
+inline dpk_operand rows_k(const float* p, int rows, int64_t cols, int64_t ld) {
+  dpk_operand o{};
+  o.data = p;
+  o.kind = DPK_OPND_ROWS_K;
+  o.rows = rows;
+  o.cols = cols;
+  o.ld = ld;
+  return o;
+}
+inline dpk_operand rows_mn(const float* p, int rows, int64_t cols, int64_t ld) {
+  dpk_operand o{};
+  o.data = p;
+  o.kind = DPK_OPND_ROWS_MN;
+  o.rows = rows;
+  o.cols = cols;
+  o.ld = ld;
+  return o;
+}
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace dpk

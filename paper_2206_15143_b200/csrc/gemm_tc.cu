@@ -1,0 +1,729 @@
+// Grouped tcgen05 (kind::tf32) GEMM / SYRK engine for sm_100a.
+//
+//   out[m,n] = alpha * sum_k A[m,k] B[n,k] + beta * cin[m,n]     (EPI_LINEAR)
+//   out[m,n] = alpha * sum_k A[m,k] B[n,k] / (max(vr[m],0) max(vc[n],0) + gamma)   (EPI_EIGDIV)
+//
+// One persistent launch serves a whole group of problems (e.g. all Kronecker
+// factors of all owned layers).  Work units are (problem, 128x128 output tile,
+// K split).  Warp roles per CTA (416 threads, one CTA per SM):
+//   warps 0-3  epilogue: tcgen05.ld the TMEM accumulator (lane = tile row),
+//              apply alpha/beta (the fused running average) or the eigen
+//              divide, store, mirror lower tiles for symmetric outputs, and
+//              run the deterministic split-K fix-up (last split sums partials);
+//   warp 4     TMEM allocator + single-thread tcgen05.mma issuer;
+//   warps 5-12 producers: gather operand tiles straight from the torch
+//              tensors (row-major, column-major or implicit im2col of an
+//              NCHW conv input -- patches never touch HBM), round to TF32 (or
+//              split hi/lo for 3xTF32) and store them in the canonical
+//              K-major 128B-swizzled shared-memory layout the MMA reads.
+// Pipelines: smem stages full/empty (producers <-> MMA), two TMEM
+// accumulators full/empty (MMA <-> epilogue) so tile i's epilogue overlaps
+// tile i+1's MMAs.
+//
+// Reference semantics reproduced (kfaclab 0.1.0): compute_factors
+// kfac.py:85-104 (symmetric A = X X^T / M), update_running_average
+// kfac.py:107-125 (alpha/beta epilogue), precondition_inverse / _eigen
+// kfac.py:165-191 (plain and eigen-divide epilogues).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "dpk_internal.h"
+#include "dpk_ptx.cuh"
+
+namespace dpk {
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 128;
+constexpr int BK = 32;                       // fp32 elements per row of a stage = 128 B
+constexpr int TILE_BYTES = BM * BK * 4;      // 16 KB
+constexpr int EPI_WARPS = 4;                 // warps 0..3 (one per TMEM lane quadrant)
+constexpr int MMA_WARP = 4;
+constexpr int PROD_WARP0 = 5;
+constexpr int PROD_WARPS = 8;
+constexpr int NPROD = PROD_WARPS * 32;
+constexpr int NTHREADS = (PROD_WARP0 + PROD_WARPS) * 32;  // 416
+constexpr uint32_t TMEM_COLS = 2 * BN;                    // two accumulators
+constexpr int MAXP = 40;                                  // problems per launch (kernel params)
+
+struct Problem {
+  dpk_operand a;
+  dpk_operand b;
+  float* out;
+  const float* cin;
+  const float* vrow;
+  const float* vcol;
+  float* partials;
+  int* counters;
+  float* out_t;
+  int64_t ldt;
+  int64_t ldo;
+  int64_t ldc;
+  float alpha, beta, gamma;
+  int M, N;
+  int symmetric, same_ab, epi;
+  int tiles_n, ntiles, splits;
+  int chunks, cps;  // K chunks of 32, chunks per split
+  int unit_begin;
+};
+
+struct Batch {
+  int nprob;
+  int total_units;
+  Problem p[MAXP];
+};
+
+template <int NPASS>
+struct Cfg {
+  static constexpr int STAGES = NPASS == 1 ? 4 : 3;
+  static constexpr int OPS = NPASS == 1 ? 2 : 4;  // A, B (+ A_lo, B_lo)
+  static constexpr int STAGE_BYTES = OPS * TILE_BYTES;
+  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 4) + 16;
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + BAR_BYTES;
+};
+
+__device__ __forceinline__ void decode_unit(const Batch& bt, int u, int& pi, int& tm, int& tn, int& tile,
+                                            int& split) {
+  int p = 0;
+  while (p + 1 < bt.nprob && bt.p[p + 1].unit_begin <= u) ++p;
+  const Problem& P = bt.p[p];
+  int local = u - P.unit_begin;
+  tile = local / P.splits;
+  split = local - tile * P.splits;
+  if (P.symmetric) {
+    int r = static_cast<int>((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
+    while ((r + 1) * (r + 2) / 2 <= tile) ++r;
+    while (r * (r + 1) / 2 > tile) --r;
+    tm = r;
+    tn = tile - r * (r + 1) / 2;
+  } else {
+    tm = tile / P.tiles_n;
+    tn = tile - tm * P.tiles_n;
+  }
+  pi = p;
+}
+
+// ------------------------------------------------------------------ producer
+// A row task: one (row, 16-byte chunk) of a 128 x 32 stage tile.
+struct RowTask {
+  int64_t off;  // element offset of the row inside the operand
+  int ih, iw;   // im2col filter offsets (i*dh, j*dw)
+  int flag;     // 0 zero row, 1 data row, 2 ones (bias) row
+};
+
+__device__ __forceinline__ bool kfast(const dpk_operand& o) { return o.kind != DPK_OPND_ROWS_MN; }
+
+__device__ __forceinline__ void task_row_chunk(bool kf, int ptid, int j, int& row, int& chunk) {
+  if (kf) {
+    row = (ptid >> 3) + 32 * j;
+    chunk = ptid & 7;
+  } else {
+    row = ptid & 127;
+    chunk = (ptid >> 7) + 2 * j;
+  }
+}
+
+__device__ __forceinline__ void setup_tasks(const dpk_operand& o, int row0, int ptid, RowTask (&t)[4]) {
+  const bool kf = kfast(o);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    int row, chunk;
+    task_row_chunk(kf, ptid, j, row, chunk);
+    const int r = row0 + row;
+    t[j].off = 0;
+    t[j].ih = 0;
+    t[j].iw = 0;
+    if (r < o.rows) {
+      t[j].flag = 1;
+      if (o.kind == DPK_OPND_ROWS_K) {
+        t[j].off = static_cast<int64_t>(r) * o.ld;
+      } else if (o.kind == DPK_OPND_ROWS_MN) {
+        t[j].off = r;
+      } else {
+        const int kk = o.kh * o.kw;
+        const int c = r / kk;
+        const int rem = r - c * kk;
+        const int i = rem / o.kw;
+        const int jj = rem - i * o.kw;
+        t[j].ih = i * o.dh;
+        t[j].iw = jj * o.dw;
+        t[j].off = static_cast<int64_t>(c) * o.sc + static_cast<int64_t>(t[j].ih) * o.shs +
+                   static_cast<int64_t>(t[j].iw) * o.sws;
+      }
+    } else {
+      t[j].flag = (o.bias_row && r == o.rows) ? 2 : 0;
+    }
+  }
+}
+
+// Gather 4 operand tiles' worth of values for this thread and k-chunk kc.
+__device__ __forceinline__ void fetch_tasks(const dpk_operand& o, const RowTask (&t)[4], int ptid, int64_t k_base,
+                                            float4 (&v)[4]) {
+  const bool kf = kfast(o);
+  if (o.kind == DPK_OPND_IM2COL) {
+    // all 4 tasks share the same chunk -> decompose its 4 sample columns once
+    const int64_t k0 = k_base + 4 * (ptid & 7);
+    const int ohw = o.OH * o.OW;
+    int64_t kb[4];
+    int ih0[4], iw0[4];
+    bool kv[4];
+    {
+      int64_t n = k0 / ohw;
+      int rem = static_cast<int>(k0 - n * ohw);
+      int oh = rem / o.OW;
+      int ow = rem - oh * o.OW;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        kv[e] = (k0 + e) < o.cols;
+        ih0[e] = oh * o.sh - o.ph;
+        iw0[e] = ow * o.sw - o.pw;
+        kb[e] = n * o.sn + static_cast<int64_t>(ih0[e]) * o.shs + static_cast<int64_t>(iw0[e]) * o.sws;
+        if (++ow == o.OW) {
+          ow = 0;
+          if (++oh == o.OH) {
+            oh = 0;
+            ++n;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float x[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float val = 0.0f;
+        if (t[j].flag == 1) {
+          const int ih = ih0[e] + t[j].ih;
+          const int iw = iw0[e] + t[j].iw;
+          if (kv[e] && static_cast<unsigned>(ih) < static_cast<unsigned>(o.H) &&
+              static_cast<unsigned>(iw) < static_cast<unsigned>(o.W))
+            val = __ldg(o.data + kb[e] + t[j].off);
+        } else if (t[j].flag == 2) {
+          val = kv[e] ? 1.0f : 0.0f;
+        }
+        x[e] = val;
+      }
+      v[j] = make_float4(x[0], x[1], x[2], x[3]);
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    int row, chunk;
+    task_row_chunk(kf, ptid, j, row, chunk);
+    const int64_t k0 = k_base + 4 * chunk;
+    float x[4] = {0.f, 0.f, 0.f, 0.f};
+    if (t[j].flag == 1) {
+      if (o.kind == DPK_OPND_ROWS_K) {
+        const float* p = o.data + t[j].off + k0;
+        if (k0 + 3 < o.cols && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+          x[0] = q.x;
+          x[1] = q.y;
+          x[2] = q.z;
+          x[3] = q.w;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (k0 + e < o.cols) x[e] = __ldg(p + e);
+        }
+      } else {  // ROWS_MN: consecutive lanes read consecutive rows (coalesced)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (k0 + e < o.cols) x[e] = __ldg(o.data + (k0 + e) * o.ld + t[j].off);
+      }
+    } else if (t[j].flag == 2) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) x[e] = (k0 + e < o.cols) ? 1.0f : 0.0f;
+    }
+    v[j] = make_float4(x[0], x[1], x[2], x[3]);
+  }
+}
+
+// Canonical K-major SWIZZLE_128B position of (row, 16B chunk) in a 128 x 32 fp32 tile.
+__device__ __forceinline__ uint32_t sw128_offset(int row, int chunk) {
+  return static_cast<uint32_t>((row >> 3) * 1024 + (row & 7) * 128 + ((chunk ^ (row & 7)) << 4));
+}
+
+template <int NPASS>
+__device__ __forceinline__ void store_tasks(const dpk_operand& o, int ptid, uint8_t* tile, uint8_t* tile_lo,
+                                            const float4 (&v)[4]) {
+  const bool kf = kfast(o);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    int row, chunk;
+    task_row_chunk(kf, ptid, j, row, chunk);
+    const uint32_t off = sw128_offset(row, chunk);
+    const float x[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+    uint32_t hi[4], lo[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      hi[e] = to_tf32(x[e]);
+      if (NPASS == 3) lo[e] = to_tf32(x[e] - __uint_as_float(hi[e]));
+    }
+    *reinterpret_cast<uint4*>(tile + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+    if (NPASS == 3) *reinterpret_cast<uint4*>(tile_lo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  }
+}
+
+// ------------------------------------------------------------------ epilogue
+__device__ __forceinline__ void store_final(const Problem& P, int tm, int tn, int m, int c, const float (&acc)[32]) {
+  const int gm = tm * BM + m;
+  if (gm >= P.M) return;
+  const bool diag = P.symmetric && tm == tn;
+  const int gn0 = tn * BN + c * 32;
+  float vr = 0.f;
+  if (P.epi == EPI_EIGDIV) vr = fmaxf(P.vrow[gm], 0.0f);
+#pragma unroll 4
+  for (int j = 0; j < 32; ++j) {
+    const int gn = gn0 + j;
+    if (gn >= P.N || (diag && gn > gm)) break;
+    float val = P.alpha * acc[j];
+    if (P.epi == EPI_EIGDIV) {
+      val = val / (vr * fmaxf(P.vcol[gn], 0.0f) + P.gamma);
+    } else if (P.beta != 0.0f) {
+      val += P.beta * P.cin[gm * P.ldc + gn];
+    }
+    P.out[gm * P.ldo + gn] = val;
+    if (P.symmetric && gn != gm) P.out[static_cast<int64_t>(gn) * P.ldo + gm] = val;
+    if (P.out_t) P.out_t[static_cast<int64_t>(gn) * P.ldt + gm] = val;
+  }
+}
+
+template <int NPASS>
+__global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_constant__ Batch bt) {
+  using C = Cfg<NPASS>;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ int s_last;
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const uint32_t bars = base + C::STAGES * C::STAGE_BYTES;
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (C::STAGES + s); };
+  auto tfull_bar = [&](int a) { return bars + 8u * (2 * C::STAGES + a); };
+  auto tempty_bar = [&](int a) { return bars + 8u * (2 * C::STAGES + 2 + a); };
+  const uint32_t tmem_slot = bars + 8u * (2 * C::STAGES + 4);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(full_bar(s), PROD_WARPS);
+      mbar_init(empty_bar(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull_bar(a), 1);
+      mbar_init(tempty_bar(a), EPI_WARPS * 32);
+    }
+    mbar_fence_init();
+  }
+  if (warp == MMA_WARP) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(gbase + (tmem_slot - base));
+
+  if (warp >= PROD_WARP0) {
+    // =============================== producers
+    const int ptid = threadIdx.x - PROD_WARP0 * 32;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int u = blockIdx.x; u < bt.total_units; u += gridDim.x) {
+      int pi, tm, tn, tile, split;
+      decode_unit(bt, u, pi, tm, tn, tile, split);
+      const Problem& P = bt.p[pi];
+      const bool skip_b = P.same_ab && tm == tn;
+      RowTask ta[4], tb[4];
+      setup_tasks(P.a, tm * BM, ptid, ta);
+      if (!skip_b) setup_tasks(P.b, tn * BN, ptid, tb);
+      const int kc0 = split * P.cps;
+      const int kc1 = min(P.chunks, kc0 + P.cps);
+      for (int kc = kc0; kc < kc1; ++kc) {
+        float4 va[4], vb[4];
+        const int64_t kbase = static_cast<int64_t>(kc) * BK;
+        fetch_tasks(P.a, ta, ptid, kbase, va);
+        if (!skip_b) fetch_tasks(P.b, tb, ptid, kbase, vb);
+        mbar_wait(empty_bar(stage), phase ^ 1);
+        uint8_t* st = gbase + stage * C::STAGE_BYTES;
+        store_tasks<NPASS>(P.a, ptid, st, st + 2 * TILE_BYTES, va);
+        if (!skip_b) store_tasks<NPASS>(P.b, ptid, st + TILE_BYTES, st + 3 * TILE_BYTES, vb);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(full_bar(stage));
+        if (++stage == C::STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == MMA_WARP) {
+    // =============================== MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t IDESC = idesc_tf32(BM, BN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int u = blockIdx.x; u < bt.total_units; u += gridDim.x, ++it) {
+        int pi, tm, tn, tile, split;
+        decode_unit(bt, u, pi, tm, tn, tile, split);
+        const Problem& P = bt.p[pi];
+        const bool skip_b = P.same_ab && tm == tn;
+        const int acc = it & 1;
+        mbar_wait(tempty_bar(acc), ((it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * BN;
+        const int kc0 = split * P.cps;
+        const int kc1 = min(P.chunks, kc0 + P.cps);
+        for (int kc = kc0; kc < kc1; ++kc) {
+          mbar_wait(full_bar(stage), phase);
+          tc_fence_after();
+          const uint32_t sa = base + stage * C::STAGE_BYTES;
+          const uint32_t sb = skip_b ? sa : sa + TILE_BYTES;
+          const uint32_t sal = sa + 2 * TILE_BYTES;
+          const uint32_t sbl = skip_b ? sal : sa + 3 * TILE_BYTES;
+#pragma unroll
+          for (int s = 0; s < BK / 8; ++s) {  // UMMA_K = 8 for tf32 (32 B)
+            const uint64_t da = sdesc_kmajor_sw128(sa + s * 32);
+            const uint64_t db = sdesc_kmajor_sw128(sb + s * 32);
+            mma_tf32(d, da, db, IDESC, (kc > kc0 || s > 0) ? 1u : 0u);
+            if (NPASS == 3) {
+              mma_tf32(d, da, sdesc_kmajor_sw128(sbl + s * 32), IDESC, 1u);
+              mma_tf32(d, sdesc_kmajor_sw128(sal + s * 32), db, IDESC, 1u);
+            }
+          }
+          mma_commit(empty_bar(stage));
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(tfull_bar(acc));
+      }
+    }
+  } else {
+    // =============================== epilogue (warps 0-3, thread = tile row)
+    const int m = warp * 32 + lane;
+    int it = 0;
+    for (int u = blockIdx.x; u < bt.total_units; u += gridDim.x, ++it) {
+      int pi, tm, tn, tile, split;
+      decode_unit(bt, u, pi, tm, tn, tile, split);
+      const Problem& P = bt.p[pi];
+      const int acc = it & 1;
+      mbar_wait(tfull_bar(acc), (it >> 1) & 1);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(warp * 32) << 16);
+      float* part = nullptr;
+      if (P.splits > 1)
+        part = P.partials + (static_cast<int64_t>(tile * P.splits + split) * BM + m) * BN;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(taddr + c * 32, r);
+        tmem_ld_wait();
+        float accv[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) accv[j] = __uint_as_float(r[j]);
+        if (P.splits == 1) {
+          store_final(P, tm, tn, m, c, accv);
+        } else {
+          float4* dst = reinterpret_cast<float4*>(part + c * 32);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            __stcg(dst + q, make_float4(accv[4 * q], accv[4 * q + 1], accv[4 * q + 2], accv[4 * q + 3]));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty_bar(acc));
+      if (P.splits > 1) {
+        __threadfence();
+        named_bar_sync(1, EPI_WARPS * 32);
+        if (m == 0) {
+          const int old = atomicAdd(P.counters + tile, 1);
+          const int last = (old == P.splits - 1);
+          if (last) P.counters[tile] = 0;
+          s_last = last;
+        }
+        named_bar_sync(1, EPI_WARPS * 32);
+        if (s_last) {
+          __threadfence();
+          const float* rowp = P.partials + (static_cast<int64_t>(tile * P.splits) * BM + m) * BN;
+#pragma unroll 1
+          for (int c = 0; c < BN / 32; ++c) {
+            float accv[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) accv[j] = 0.0f;
+            for (int s = 0; s < P.splits; ++s) {
+              const float4* src = reinterpret_cast<const float4*>(rowp + static_cast<int64_t>(s) * BM * BN + c * 32);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const float4 x = __ldcg(src + q);
+                accv[4 * q] += x.x;
+                accv[4 * q + 1] += x.y;
+                accv[4 * q + 2] += x.z;
+                accv[4 * q + 3] += x.w;
+              }
+            }
+            store_final(P, tm, tn, m, c, accv);
+          }
+        }
+        named_bar_sync(1, EPI_WARPS * 32);
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == MMA_WARP) {
+    __syncwarp();
+    tc_fence_after();
+    tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ host planning
+struct Plan {
+  std::vector<Problem> probs;
+  size_t ws_bytes = 0;
+};
+
+int operand_rows(const dpk_operand& o) { return o.rows + (o.bias_row ? 1 : 0); }
+
+bool valid_operand(const dpk_operand& o) {
+  if (o.data == nullptr && o.rows > 0) return false;
+  if (o.rows < 0 || o.cols < 1) return false;
+  if (o.kind == DPK_OPND_IM2COL) {
+    if (o.kh < 1 || o.kw < 1 || o.sh < 1 || o.sw < 1 || o.dh < 1 || o.dw < 1 || o.OH < 1 || o.OW < 1) return false;
+    if (o.rows != o.C * o.kh * o.kw) return false;
+  } else if (o.kind != DPK_OPND_ROWS_K && o.kind != DPK_OPND_ROWS_MN) {
+    return false;
+  }
+  return true;
+}
+
+int make_plan(const GemmSpec* specs, int n, Plan& plan) {
+  plan.probs.clear();
+  plan.probs.resize(n);
+  int64_t total_work = 0;
+  for (int i = 0; i < n; ++i) {
+    const dpk_gemm_job& j = specs[i].job;
+    if (!valid_operand(j.a) || !valid_operand(j.b)) {
+      set_error("dpk_gemm: invalid operand view (job " + std::to_string(i) + ")");
+      return DPK_EARG;
+    }
+    if (j.a.cols != j.b.cols) {
+      set_error("dpk_gemm: operand column (sample) counts differ (job " + std::to_string(i) + ")");
+      return DPK_ESHAPE;
+    }
+    Problem& P = plan.probs[i];
+    std::memset(&P, 0, sizeof(P));
+    P.a = j.a;
+    P.b = j.b;
+    P.out = j.out;
+    P.cin = j.cin;
+    P.ldo = j.ldo;
+    P.ldc = j.ldc;
+    P.alpha = j.alpha;
+    P.beta = j.beta;
+    P.M = operand_rows(j.a);
+    P.N = operand_rows(j.b);
+    P.symmetric = j.symmetric ? 1 : 0;
+    if (P.symmetric && P.M != P.N) {
+      set_error("dpk_gemm: symmetric output needs M == N");
+      return DPK_ESHAPE;
+    }
+    P.same_ab = std::memcmp(&j.a, &j.b, sizeof(dpk_operand)) == 0 ? 1 : 0;
+    P.epi = specs[i].epi;
+    P.vrow = specs[i].vrow;
+    P.vcol = specs[i].vcol;
+    P.gamma = specs[i].gamma;
+    P.out_t = specs[i].out_t;
+    P.ldt = specs[i].ldt;
+    if (P.beta != 0.0f && P.cin == nullptr) {
+      set_error("dpk_gemm: beta != 0 needs cin");
+      return DPK_EARG;
+    }
+    const int tmn = (P.M + BM - 1) / BM;
+    P.tiles_n = (P.N + BN - 1) / BN;
+    P.ntiles = P.symmetric ? tmn * (tmn + 1) / 2 : tmn * P.tiles_n;
+    P.chunks = static_cast<int>((j.a.cols + BK - 1) / BK);
+    total_work += static_cast<int64_t>(P.ntiles) * P.chunks;
+  }
+  // Split K so that the group yields several units per SM, but never below
+  // 16 chunks (512 samples) per unit so tile set-up and epilogue stay amortised.
+  const int64_t sms = num_sms();
+  const int64_t target = std::max<int64_t>(16, (total_work + 4 * sms - 1) / (4 * sms));
+  size_t counters = 0, partial_tiles = 0;
+  for (auto& P : plan.probs) {
+    P.splits = static_cast<int>(std::max<int64_t>(1, (P.chunks + target - 1) / target));
+    P.cps = (P.chunks + P.splits - 1) / P.splits;
+    P.splits = (P.chunks + P.cps - 1) / P.cps;
+    if (P.splits > 1) {
+      counters += P.ntiles;
+      partial_tiles += static_cast<size_t>(P.ntiles) * P.splits;
+    }
+  }
+  const size_t counter_bytes = align_up(counters * sizeof(int), 1024);
+  plan.ws_bytes = counter_bytes + partial_tiles * BM * BN * sizeof(float);
+  return DPK_OK;
+}
+
+template <int NPASS>
+int launch_batch(Batch& bt, cudaStream_t st) {
+  using C = Cfg<NPASS>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<NPASS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(tc_gemm_kernel)");
+    configured = true;
+  }
+  const int grid = std::min(bt.total_units, num_sms());
+  tc_gemm_kernel<NPASS><<<grid, NTHREADS, C::SMEM, st>>>(bt);
+  note_launch();
+  return cuda_status(cudaGetLastError(), "tc_gemm_kernel launch");
+}
+
+}  // namespace
+
+size_t gemm_workspace_bytes(const GemmSpec* specs, int n) {
+  Plan plan;
+  if (n <= 0 || make_plan(specs, n, plan) != DPK_OK) return 0;
+  return plan.ws_bytes;
+}
+
+int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int precision, cudaStream_t st) {
+  if (n == 0) return DPK_OK;
+  if (n < 0 || specs == nullptr) {
+    set_error("dpk_gemm: bad job list");
+    return DPK_EARG;
+  }
+  if (precision != DPK_PREC_TF32 && precision != DPK_PREC_3XTF32) {
+    set_error("dpk_gemm: precision must be DPK_PREC_TF32 or DPK_PREC_3XTF32");
+    return DPK_EARG;
+  }
+  Plan plan;
+  int rc = make_plan(specs, n, plan);
+  if (rc != DPK_OK) return rc;
+  if (plan.ws_bytes > ws_bytes) {
+    set_error("dpk_gemm: workspace too small (" + std::to_string(ws_bytes) + " < " +
+              std::to_string(plan.ws_bytes) + ")");
+    return DPK_ENOSPACE;
+  }
+  // carve counters + partials
+  size_t ncounters = 0, partial_tiles = 0;
+  for (auto& P : plan.probs)
+    if (P.splits > 1) ncounters += P.ntiles;
+  int* counters = static_cast<int*>(ws);
+  float* partials = reinterpret_cast<float*>(static_cast<char*>(ws) + align_up(ncounters * sizeof(int), 1024));
+  size_t ci = 0;
+  for (auto& P : plan.probs) {
+    if (P.splits > 1) {
+      P.counters = counters + ci;
+      P.partials = partials + partial_tiles * BM * BN;
+      ci += P.ntiles;
+      partial_tiles += static_cast<size_t>(P.ntiles) * P.splits;
+    }
+  }
+  thread_local Batch bt;  // host-side staging only (kernel params are copied at launch)
+  for (int first = 0; first < n; first += MAXP) {
+    const int cnt = std::min(MAXP, n - first);
+    bt.nprob = cnt;
+    int units = 0;
+    for (int i = 0; i < cnt; ++i) {
+      bt.p[i] = plan.probs[first + i];
+      bt.p[i].unit_begin = units;
+      units += bt.p[i].ntiles * bt.p[i].splits;
+    }
+    bt.total_units = units;
+    if (units == 0) continue;
+    rc = precision == DPK_PREC_3XTF32 ? launch_batch<3>(bt, st) : launch_batch<1>(bt, st);
+    if (rc != DPK_OK) return rc;
+  }
+  return DPK_OK;
+}
+
+}  // namespace dpk
+
+// ===================================================================== C ABI
+extern "C" {
+
+size_t dpk_gemm_workspace_bytes(const dpk_gemm_job* jobs, int n_jobs) {
+  std::vector<dpk::GemmSpec> specs(std::max(n_jobs, 0));
+  for (int i = 0; i < n_jobs; ++i) specs[i] = dpk::GemmSpec{jobs[i], dpk::EPI_LINEAR, nullptr, nullptr, 0.f, nullptr, 0};
+  return dpk::gemm_workspace_bytes(specs.data(), n_jobs);
+}
+
+int dpk_gemm(const dpk_gemm_job* jobs, int n_jobs, void* workspace, size_t ws_bytes, int precision,
+             dpk_stream_t stream) {
+  if (n_jobs < 0 || (n_jobs > 0 && jobs == nullptr)) {
+    dpk::set_error("dpk_gemm: bad job list");
+    return DPK_EARG;
+  }
+  std::vector<dpk::GemmSpec> specs(n_jobs);
+  for (int i = 0; i < n_jobs; ++i) specs[i] = dpk::GemmSpec{jobs[i], dpk::EPI_LINEAR, nullptr, nullptr, 0.f, nullptr, 0};
+  return dpk::gemm_launch(specs.data(), n_jobs, workspace, ws_bytes, precision,
+                          static_cast<cudaStream_t>(stream));
+}
+
+static std::vector<dpk::GemmSpec> factor_specs(const dpk_factor_job* jobs, int n) {
+  std::vector<dpk::GemmSpec> specs(std::max(n, 0));
+  for (int i = 0; i < n; ++i) {
+    dpk_gemm_job g{};
+    g.a = jobs[i].x;
+    g.b = jobs[i].x;
+    const int d = jobs[i].x.rows + (jobs[i].x.bias_row ? 1 : 0);
+    g.out = jobs[i].factor;
+    g.ldo = d;
+    g.cin = jobs[i].factor;
+    g.ldc = d;
+    g.alpha = jobs[i].alpha;
+    g.beta = jobs[i].beta;
+    g.symmetric = 1;
+    specs[i] = dpk::GemmSpec{g, dpk::EPI_LINEAR, nullptr, nullptr, 0.f, nullptr, 0};
+  }
+  return specs;
+}
+
+size_t dpk_factor_workspace_bytes(const dpk_factor_job* jobs, int n_jobs) {
+  auto specs = factor_specs(jobs, n_jobs);
+  return dpk::gemm_workspace_bytes(specs.data(), n_jobs);
+}
+
+int dpk_syrk_ema(const dpk_factor_job* jobs, int n_jobs, void* workspace, size_t ws_bytes, int precision,
+                 dpk_stream_t stream) {
+  if (n_jobs < 0 || (n_jobs > 0 && jobs == nullptr)) {
+    dpk::set_error("dpk_syrk_ema: bad job list");
+    return DPK_EARG;
+  }
+  for (int i = 0; i < n_jobs; ++i) {
+    if (jobs[i].factor == nullptr) {
+      dpk::set_error("dpk_syrk_ema: null factor pointer");
+      return DPK_EARG;
+    }
+    if (jobs[i].x.cols < 1) {
+      dpk::set_error("captured inputs must be a nonempty d x B matrix");
+      return DPK_EARG;
+    }
+  }
+  auto specs = factor_specs(jobs, n_jobs);
+  return dpk::gemm_launch(specs.data(), n_jobs, workspace, ws_bytes, precision, static_cast<cudaStream_t>(stream));
+}
+
+int dpk_conv_im2col_syrk_ema(const dpk_factor_job* jobs, int n_jobs, void* workspace, size_t ws_bytes,
+                             int precision, dpk_stream_t stream) {
+  for (int i = 0; i < n_jobs; ++i) {
+    if (jobs[i].x.kind != DPK_OPND_IM2COL) {
+      dpk::set_error("dpk_conv_im2col_syrk_ema: operand must be DPK_OPND_IM2COL");
+      return DPK_EARG;
+    }
+  }
+  return dpk_syrk_ema(jobs, n_jobs, workspace, ws_bytes, precision, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,195 @@
+// Library plumbing plus the HBM-bound helper kernels of the DP-KFAC update:
+//   * A6  dpk_trace_pi          -- traces, pi and the split damping shifts on device
+//   * K7  dpk_pack/unpack_owner_major -- gradient [W | b] <-> flat owner-major buffer
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "dpk_internal.h"
+
+namespace dpk {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<unsigned long long> g_launches{0};
+}
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+int cuda_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return DPK_OK;
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return DPK_ECUDA;
+}
+
+int num_sms() {
+  static int cached = 0;
+  if (cached == 0) {
+    int dev = 0, n = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && n > 0)
+      cached = n;
+    else
+      cached = 148;
+  }
+  return cached;
+}
+
+namespace {
+
+// ---------------------------------------------------------------- A6: traces and pi
+constexpr int PI_MAX = 256;
+struct PiBatch {
+  int n;
+  float root_gamma;
+  dpk_pi_job j[PI_MAX];
+};
+
+__device__ float block_sum(float v) {
+  __shared__ float red[32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  v = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0f;
+  if (w == 0)
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  return v;
+}
+
+// One block per layer: tr A, tr G in double (the diagonal is short), then
+// pi = sqrt((trA/dA)/(trG/dG)) on the RAW averaged factors (kfac.py:128-137, 145).
+__global__ void trace_pi_kernel(const __grid_constant__ PiBatch b) {
+  const dpk_pi_job& J = b.j[blockIdx.x];
+  float sa = 0.f, sg = 0.f;
+  for (int i = threadIdx.x; i < J.da; i += blockDim.x) sa += J.a[static_cast<int64_t>(i) * (J.da + 1)];
+  for (int i = threadIdx.x; i < J.dg; i += blockDim.x) sg += J.g[static_cast<int64_t>(i) * (J.dg + 1)];
+  sa = block_sum(sa);
+  sg = block_sum(sg);
+  if (threadIdx.x == 0) {
+    float sh_a = 0.f, sh_g = 0.f, pi = 0.f;
+    if (!(sa > 0.f) || !(sg > 0.f)) {
+      if (J.info) *J.info = DPK_INFO_TRACE;
+      pi = 1.0f;
+    } else {
+      pi = static_cast<float>(sqrt((static_cast<double>(sa) / J.da) / (static_cast<double>(sg) / J.dg)));
+    }
+    sh_a = pi * b.root_gamma;
+    sh_g = b.root_gamma / pi;
+    J.shifts[0] = sh_a;
+    J.shifts[1] = sh_g;
+    if (J.pi) *J.pi = pi;
+  }
+}
+
+// ---------------------------------------------------------------- K7: pack / unpack
+constexpr int SEG_MAX = 128;
+struct SegBatch {
+  int n;
+  float scale;
+  dpk_segment s[SEG_MAX];
+};
+
+// grid.y = segment; grid.x strides over the segment's rows*(cols_w+has_bias) elements.
+template <bool PACK>
+__global__ void segment_kernel(const __grid_constant__ SegBatch b, float* flat) {
+  const dpk_segment& S = b.s[blockIdx.y];
+  const int cols = S.cols_w + (S.bias ? 1 : 0);
+  const int64_t total = static_cast<int64_t>(S.rows) * cols;
+  float* dst = flat + S.offset;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = e / cols;
+    const int c = static_cast<int>(e - r * cols);
+    float* src = (c < S.cols_w) ? S.weight + r * S.ldw + c : S.bias + r;
+    if (PACK)
+      dst[e] = b.scale * *src;
+    else
+      *src = b.scale * dst[e];
+  }
+}
+
+template <bool PACK>
+int run_segments(const dpk_segment* segs, int n, float* flat, float scale, cudaStream_t st) {
+  if (n < 0 || (n > 0 && (segs == nullptr || flat == nullptr))) {
+    set_error("dpk_pack/unpack: bad arguments");
+    return DPK_EARG;
+  }
+  thread_local SegBatch b;
+  for (int first = 0; first < n; first += SEG_MAX) {
+    const int cnt = std::min(SEG_MAX, n - first);
+    b.n = cnt;
+    b.scale = scale;
+    int64_t maxe = 0;
+    for (int i = 0; i < cnt; ++i) {
+      b.s[i] = segs[first + i];
+      if (b.s[i].rows < 0 || b.s[i].cols_w < 0 || b.s[i].weight == nullptr) {
+        set_error("dpk_pack/unpack: invalid segment");
+        return DPK_EARG;
+      }
+      maxe = std::max<int64_t>(maxe, static_cast<int64_t>(b.s[i].rows) * (b.s[i].cols_w + (b.s[i].bias ? 1 : 0)));
+    }
+    const int threads = 256;
+    const int gx = static_cast<int>(std::min<int64_t>((maxe + threads - 1) / threads, 1024));
+    if (gx == 0) continue;
+    segment_kernel<PACK><<<dim3(gx, cnt), threads, 0, st>>>(b, flat);
+    note_launch();
+    int rc = cuda_status(cudaGetLastError(), "segment_kernel launch");
+    if (rc) return rc;
+  }
+  return DPK_OK;
+}
+
+}  // namespace
+}  // namespace dpk
+
+extern "C" {
+
+const char* dpk_version(void) { return "dpkfac-b200 0.1.0 (sm_100a, tcgen05 tf32/3xtf32)"; }
+
+const char* dpk_last_error(void) { return dpk::g_last_error.c_str(); }
+
+unsigned long long dpk_launch_count(void) { return dpk::g_launches.load(std::memory_order_relaxed); }
+
+int dpk_trace_pi(const dpk_pi_job* jobs, int n_jobs, float gamma, dpk_stream_t stream) {
+  if (n_jobs < 0 || (n_jobs > 0 && jobs == nullptr) || !(gamma >= 0.0f)) {
+    dpk::set_error("dpk_trace_pi: bad arguments");
+    return DPK_EARG;
+  }
+  thread_local dpk::PiBatch b;
+  for (int first = 0; first < n_jobs; first += dpk::PI_MAX) {
+    const int cnt = std::min(dpk::PI_MAX, n_jobs - first);
+    b.n = cnt;
+    b.root_gamma = std::sqrt(gamma);
+    for (int i = 0; i < cnt; ++i) {
+      b.j[i] = jobs[first + i];
+      if (b.j[i].a == nullptr || b.j[i].g == nullptr || b.j[i].shifts == nullptr || b.j[i].da < 1 ||
+          b.j[i].dg < 1) {
+        dpk::set_error("dpk_trace_pi: invalid job");
+        return DPK_EARG;
+      }
+    }
+    dpk::trace_pi_kernel<<<cnt, 256, 0, static_cast<cudaStream_t>(stream)>>>(b);
+    dpk::note_launch();
+    int rc = dpk::cuda_status(cudaGetLastError(), "trace_pi_kernel launch");
+    if (rc) return rc;
+  }
+  return DPK_OK;
+}
+
+int dpk_pack_owner_major(const dpk_segment* segs, int n_segs, float* flat, float scale, dpk_stream_t stream) {
+  return dpk::run_segments<true>(segs, n_segs, flat, scale, static_cast<cudaStream_t>(stream));
+}
+
+int dpk_unpack_owner_major(const dpk_segment* segs, int n_segs, const float* flat, float scale,
+                           dpk_stream_t stream) {
+  return dpk::run_segments<false>(segs, n_segs, const_cast<float*>(flat), scale, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,493 @@
+"""DPKFAC: the drop-in DP-KFAC second-order update for torch models on B200.
+
+Semantics follow the reference's simulated cluster (kfaclab distsim.py:289-338,
+``dp_kfac_step``) and per-layer step (kfac.py:257-276):
+
+  * registration walks ``model.named_modules()`` in order and keeps every
+    ``nn.Linear`` and ``nn.Conv2d`` (groups=1): the layer index is the position
+    in that walk (for torchvision ResNet-50 it equals the reference's
+    resnet50_manifest.txt row order);
+  * layer -> rank assignment is the reference's round robin
+    (costmodel.py:66-70) unless "balanced" or an explicit partition is asked
+    for, always validated like distsim.validate_partition;
+  * each rank captures a (forward-pre) and B_local * dL/ds (backward) for its
+    OWN layers from its LOCAL batch (model.py:9-12, 217-218, 247), builds and
+    inverts their Kronecker factors; factors are never communicated;
+  * ``step()`` (after ``loss.backward()``, before ``optimizer.step()``):
+      1. factor SYRK + running average if t % f_freq == 0 (one grouped launch),
+      2. refresh inverses / eigendecompositions if t % k_freq == 0,
+      3. pack every layer's [W | b] gradient into an owner-major flat buffer,
+      4. reduce-scatter (mean over ranks) -> each rank holds its layers' mean grads,
+      5. precondition the owned layers (one grouped launch per GEMM phase),
+      6. all-gather the preconditioned gradients, unpack into ``.grad``,
+      7. t += 1.
+    Non-preconditioned parameters (e.g. batch-norm) are plain all-reduced.
+"""
+
+from __future__ import annotations
+
+from typing import Optional, Sequence, Union
+
+import torch
+import torch.distributed as dist
+import torch.nn as nn
+
+from . import _lib as L
+from . import ops
+from .errors import ArgumentError, NumericError, OrderingError, ShapeError
+from .kfac import KfacHyper
+from .exchange import OwnerMajorExchange, OwnerMajorLayout
+from .partition import balanced_partition, layer_cost, round_robin_partition, validate_partition
+
+
+class _Layer:
+    """One preconditioned layer and its (owner-side) curvature state."""
+
+    def __init__(self, index: int, name: str, module: nn.Module):
+        self.index = index
+        self.name = name
+        self.module = module
+        self.is_conv = isinstance(module, nn.Conv2d)
+        self.has_bias = module.bias is not None
+        w = module.weight
+        self.d_out = w.shape[0]
+        self.d_in = w[0].numel() + (1 if self.has_bias else 0)
+        self.n_grad = self.d_out * self.d_in
+        self.owned = False
+        self.a_in: Optional[torch.Tensor] = None
+        self.g_out: Optional[torch.Tensor] = None
+        self.batch = 0
+        self.m_cols = 0
+        # state (allocated on first use, owner only)
+        self.a_cov = self.g_cov = None
+        self.a_inv = self.g_inv = None
+        self.a_q = self.a_w = self.g_q = self.g_w = None
+        self.initialized = False
+        self.last_factor_update = -1
+        self.last_inverse_update = -1
+        self.holds = None  # "eigen" | "inverse" | None
+
+    # ---- operand views of the captures (reference layout: d x M, columns = samples)
+    def operand_a(self) -> L.Operand:
+        x = self.a_in
+        if self.is_conv:
+            m = self.module
+            return ops.operand_im2col(x, m.kernel_size, m.stride, m.padding, m.dilation, self.has_bias)
+        return ops.operand_rows_mn(x.reshape(-1, x.shape[-1]), self.has_bias)
+
+    def operand_g(self) -> L.Operand:
+        g = self.g_out
+        if self.is_conv:
+            return ops.operand_im2col(g, (1, 1), (1, 1), (0, 0), (1, 1), False)
+        return ops.operand_rows_mn(g.reshape(-1, g.shape[-1]), False)
+
+    def alloc_state(self, inv_type: str, device):
+        if self.a_cov is None:
+            self.a_cov = torch.zeros(self.d_in, self.d_in, device=device)
+            self.g_cov = torch.zeros(self.d_out, self.d_out, device=device)
+        if inv_type == "inverse" and self.a_inv is None:
+            self.a_inv = torch.empty_like(self.a_cov)
+            self.g_inv = torch.empty_like(self.g_cov)
+        if inv_type == "eigen" and self.a_q is None:
+            self.a_q = torch.empty_like(self.a_cov)
+            self.g_q = torch.empty_like(self.g_cov)
+            self.a_w = torch.empty(self.d_in, device=device)
+            self.g_w = torch.empty(self.d_out, device=device)
+
+
+def _supported(m: nn.Module) -> bool:
+    if isinstance(m, nn.Linear):
+        return True
+    if isinstance(m, nn.Conv2d):
+        return (m.groups == 1 and m.padding_mode == "zeros" and not isinstance(m.padding, str))
+    return False
+
+
+class DPKFAC:
+    """Distributed-preconditioning K-FAC (DP-KFAC) for a torch model.
+
+    Hyper-parameters and their validation are the reference's KfacHyper
+    (kfac.py:55-74): gamma (damping, >= 0), xi (running-average weight of the
+    NEW factor, in (0, 1]), inv_type ("eigen" | "inverse"), f_freq, k_freq.
+    """
+
+    def __init__(self, model: nn.Module, *, gamma: float = 0.03, xi: float = 0.95, inv_type: str = "eigen",
+                 f_freq: int = 1, k_freq: int = 1,
+                 assignment: Union[str, Sequence[Sequence[int]]] = "round_robin",
+                 process_group=None, precision: str = "tf32", precond_precision: str = "3xtf32",
+                 grad_scale: Union[str, float] = "batch", check_numerics: Union[bool, str] = True):
+        self.hyper = KfacHyper(gamma=gamma, xi=xi, inv_type=inv_type, f_freq=f_freq, k_freq=k_freq)
+        ops.precision_code(precision)
+        ops.precision_code(precond_precision)
+        self.precision = precision  # factor SYRK (tcgen05 kind::tf32, RN-rounded operands)
+        self.precond_precision = precond_precision  # preconditioning GEMMs
+        if not (grad_scale == "batch" or isinstance(grad_scale, (int, float))):
+            raise ArgumentError("grad_scale must be 'batch' or a number")
+        self.grad_scale = grad_scale
+        if check_numerics not in (True, False, "sync", "deferred"):
+            raise ArgumentError("check_numerics must be True/'sync', 'deferred' or False")
+        # True/"sync": raise inside the failing step (one device->host read per step);
+        # "deferred": the read is asynchronous and a failure raises at the next step() / check()
+        self.check_numerics = "sync" if check_numerics is True else check_numerics
+        self._pending_info = None
+        self.model = model
+        self.layers = [_Layer(i, n, m) for i, (n, m) in enumerate(
+            (n, m) for n, m in model.named_modules() if _supported(m))]
+        if not self.layers:
+            raise ArgumentError("need at least one layer")
+        self.pg = process_group
+        if dist.is_available() and dist.is_initialized():
+            self.rank = dist.get_rank(process_group)
+            self.world = dist.get_world_size(process_group)
+        else:
+            self.rank, self.world = 0, 1
+        try:
+            self.device = next(model.parameters()).device
+        except StopIteration:
+            raise ArgumentError("model has no parameters") from None
+        if self.device.type != "cuda":
+            raise ArgumentError("DPKFAC runs on CUDA devices only (no CPU fallback)")
+        ops.lib()  # fail loudly now if libdpkfac.so is missing
+        n = len(self.layers)
+        self._pending_balance = False
+        if isinstance(assignment, str):
+            if assignment == "round_robin":
+                self.assignment = round_robin_partition(n, self.world)
+            elif assignment == "balanced":
+                self.assignment = None
+                self._pending_balance = True
+            else:
+                raise ArgumentError("assignment must be 'round_robin', 'balanced' or an explicit partition")
+        else:
+            parts = tuple(tuple(int(i) for i in p) for p in assignment)
+            if len(parts) != self.world:
+                raise ArgumentError("assignment must list one layer set per worker")
+            self.assignment = parts
+        if self.assignment is not None:
+            validate_partition(self.assignment, n)
+            self._set_ownership()
+        else:
+            for ly in self.layers:
+                ly.owned = True  # capture everything once, to measure shapes for the balancer
+        layer_params = set()
+        for ly in self.layers:
+            layer_params.add(id(ly.module.weight))
+            if ly.has_bias:
+                layer_params.add(id(ly.module.bias))
+        self.other_params = [p for p in model.parameters() if p.requires_grad and id(p) not in layer_params]
+        self.t = 0
+        self._capturing = True
+        self._hooks = []
+        for ly in self.layers:
+            self._hooks.append(ly.module.register_forward_pre_hook(self._make_pre_hook(ly)))
+            self._hooks.append(ly.module.register_forward_hook(self._make_fwd_hook(ly)))
+        self._bufs_ready = False
+        self.last_stage_ms = {}
+
+    # ------------------------------------------------------------ hooks
+    def _make_pre_hook(self, ly: _Layer):
+        def hook(module, inputs):
+            if self._capturing and ly.owned and torch.is_grad_enabled():
+                x = inputs[0]
+                ly.a_in = x.detach()
+                ly.batch = x.shape[0]
+        return hook
+
+    def _make_fwd_hook(self, ly: _Layer):
+        def hook(module, inputs, output):
+            if self._capturing and ly.owned and torch.is_grad_enabled() and output.requires_grad:
+                def grab(g, ly=ly):
+                    ly.g_out = g.detach()
+                output.register_hook(grab)
+        return hook
+
+    def remove_hooks(self):
+        for h in self._hooks:
+            h.remove()
+        self._hooks = []
+
+    # ------------------------------------------------------------ assignment / buffers
+    def _set_ownership(self):
+        mine = set(self.assignment[self.rank])
+        for ly in self.layers:
+            ly.owned = ly.index in mine
+            if not ly.owned:
+                ly.a_in = ly.g_out = None
+        self.owned = [self.layers[i] for i in sorted(mine)]
+
+    def _finalize_balance(self):
+        costs = []
+        for ly in self.layers:
+            if ly.a_in is None:
+                raise OrderingError("balanced assignment needs one forward/backward pass before step()")
+            m = ly.operand_a().cols
+            costs.append(layer_cost(ly.d_in, ly.d_out, m, self.hyper.inv_type))
+        # every rank sees the same shapes (same model, same local batch size), so the
+        # deterministic LPT gives the same partition everywhere.
+        self.assignment = balanced_partition(costs, self.world)
+        validate_partition(self.assignment, len(self.layers))
+        self._pending_balance = False
+        self._set_ownership()
+
+    def _build_buffers(self):
+        dev = self.device
+        self.layout = OwnerMajorLayout(self.assignment, [ly.n_grad for ly in self.layers])
+        self.xchg = OwnerMajorExchange(self.layout, self.rank, dev, self.pg)
+        self.offsets = self.layout.offsets
+        n_own = len(self.owned)
+        self.info = torch.zeros(max(len(self.layers), 1), dtype=torch.int32, device=dev)
+        self.shifts = torch.zeros(max(n_own, 1), 2, device=dev)
+        self.pis = torch.zeros(max(n_own, 1), device=dev)
+        self._bufs_ready = True
+
+    def _segments(self, which: str):
+        segs = []
+        for ly in self.layers:
+            w = ly.module.weight
+            b = ly.module.bias
+            if which == "grad":
+                if w.grad is None:
+                    raise OrderingError(f"layer {ly.index} ({ly.name}) has no gradient: call backward() before step()")
+                wt, bt = w.grad, (b.grad if b is not None else None)
+                if b is not None and bt is None:
+                    raise OrderingError(f"layer {ly.index} ({ly.name}) bias has no gradient")
+            off = self.offsets[ly.index]
+            segs.append(ops.segment(wt, bt, off))
+        return segs
+
+    # ------------------------------------------------------------ the step
+    @torch.no_grad()
+    def step(self):
+        h = self.hyper
+        t = self.t
+        self.check()
+        if self._pending_balance:
+            self._finalize_balance()
+        if not self._bufs_ready:
+            self._build_buffers()
+        for ly in self.layers:  # contiguous grads so [W | b] packing is a strided copy
+            if ly.module.weight.grad is not None and not ly.module.weight.grad.is_contiguous():
+                ly.module.weight.grad = ly.module.weight.grad.contiguous()
+        f_up = t % h.f_freq == 0
+        k_up = t % h.k_freq == 0
+        owned = self.owned
+        self.info.zero_()
+        self._mark("start")
+        # (1) Kronecker factors + running average: one grouped tcgen05 launch
+        if f_up and owned:
+            jobs, keep = [], []
+            for ly in owned:
+                if ly.a_in is None or ly.g_out is None:
+                    raise ArgumentError(f"worker {self.rank}, layer {ly.index}: captured inputs must be a "
+                                        "nonempty d x B matrix (run forward and backward before step())")
+                ly.alloc_state(h.inv_type, self.device)
+                first = not ly.initialized
+                w = 1.0 if first else h.xi
+                beta = 0.0 if first else 1.0 - h.xi
+                oa, og = ly.operand_a(), ly.operand_g()
+                m = oa.cols
+                if og.cols != m:
+                    raise ArgumentError(f"worker {self.rank}, layer {ly.index}: capture batch counts differ: "
+                                        f"{m} inputs vs {og.cols} gradients")
+                s = float(ly.batch) if self.grad_scale == "batch" else float(self.grad_scale)
+                jobs.append(ops.factor_job(oa, ly.a_cov, w / m, beta))
+                jobs.append(ops.factor_job(og, ly.g_cov, w * s * s / m, beta))
+                keep.append((ly.a_in, ly.g_out))
+            ops.syrk_ema(jobs, self.precision, device=self.device)
+            for ly in owned:
+                ly.initialized = True
+                ly.last_factor_update = t
+                ly.a_in = ly.g_out = None
+            del keep
+        self._mark("factors")
+        # (2) inverses / eigendecompositions
+        if k_up and owned:
+            for ly in owned:
+                if not ly.initialized:
+                    raise OrderingError(f"worker {self.rank}, layer {ly.index}: cannot build a preconditioner "
+                                        "before any factor update")
+                ly.alloc_state(h.inv_type, self.device)
+            if h.inv_type == "eigen":
+                jt = []
+                for ly in owned:
+                    jt.append((ly.a_cov, ly.a_q, ly.a_w, self.info[ly.index]))
+                    jt.append((ly.g_cov, ly.g_q, ly.g_w, self.info[ly.index]))
+                ops.syevd(jt)
+            else:
+                ops.trace_pi([(ly.a_cov, ly.g_cov) for ly in owned], h.gamma, self.shifts, self.pis,
+                             [self.info[ly.index] for ly in owned])
+                sj = []
+                for k, ly in enumerate(owned):
+                    sj.append(ops.spd_job(ly.a_cov, ly.a_inv, self.shifts[k, 0], self.info[ly.index], L.INFO_NOT_SPD_A))
+                    sj.append(ops.spd_job(ly.g_cov, ly.g_inv, self.shifts[k, 1], self.info[ly.index], L.INFO_NOT_SPD_G))
+                ops.chol_inv(sj)
+            for ly in owned:
+                ly.holds = h.inv_type
+                ly.last_inverse_update = t
+        self._mark("inversion")
+        # (3) pack every layer's [W | b] gradient, owner-major (scaled by 1/P)
+        segs = self._segments("grad")
+        P = self.world
+        X = self.xchg
+        ops.pack(segs, X.flat, 1.0 / P)
+        # (4) reduce-scatter: SUM of grad/P over ranks == mean, my layers only
+        X.reduce_scatter()
+        if P > 1 and self.other_params:
+            self._allreduce_others()
+        self._mark("comm_rs")
+        # (5) precondition owned layers, one grouped launch per GEMM phase
+        if owned:
+            pj = []
+            for ly in owned:
+                if ly.holds != h.inv_type:
+                    what = "eigendecomposition" if h.inv_type == "eigen" else "damped inverse"
+                    raise OrderingError(f"worker {self.rank}, layer {ly.index}: preconditioning requested "
+                                        f"before any {what} exists")
+                shape = (ly.d_out, ly.d_in)
+                g, o, tmp = X.view_in(ly.index, shape), X.view_out(ly.index, shape), X.view_tmp(ly.index, shape)
+                if h.inv_type == "eigen":
+                    pj.append(ops.precond_job(g, ly.a_q, ly.g_q, o, tmp, ly.a_w, ly.g_w, self.info[ly.index]))
+                else:
+                    pj.append(ops.precond_job(g, ly.a_inv, ly.g_inv, o, tmp))
+            ops.precondition(pj, h.inv_type == "eigen", h.gamma, self.precond_precision)
+        self._mark("precondition")
+        # numeric failures: reference wording, prefixed "worker p, layer i" (distsim.py:273-274)
+        if self.check_numerics == "sync":
+            self._raise_from_host(self._gather_info().cpu())
+        elif self.check_numerics == "deferred":
+            host = torch.empty(self.info.shape, dtype=torch.int32, pin_memory=True)
+            host.copy_(self._gather_info(), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            self._pending_info = (host, ev)
+        # (6) all-gather preconditioned grads, unpack into .grad
+        X.all_gather()
+        ops.unpack(segs, X.out_flat, 1.0)
+        self._mark("comm_ag")
+        self.t += 1
+
+    # ------------------------------------------------------------ stage timing (CUDA events)
+    def enable_stage_timing(self, on: bool = True):
+        """Record CUDA events at the stage boundaries of every step(); read them with
+        ``stage_ms()`` after a synchronize.  Stages: factors (SYRK+EMA), inversion,
+        comm_rs (pack + reduce-scatter), precondition, comm_ag (check + all-gather + unpack)."""
+        self._timing = on
+        self._marks = []
+
+    def _mark(self, name: str):
+        if getattr(self, "_timing", False):
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record()
+            self._marks.append((name, ev))
+
+    def stage_ms(self, reset: bool = True) -> dict:
+        """Accumulated milliseconds per stage over the steps recorded since the last reset."""
+        out: dict = {}
+        marks = getattr(self, "_marks", [])
+        for (_, a), (name, b) in zip(marks, marks[1:]):
+            if name == "start":
+                continue
+            out[name] = out.get(name, 0.0) + a.elapsed_time(b)
+        if reset:
+            self._marks = []
+        return out
+
+    def _allreduce_others(self):
+        grads = [p.grad for p in self.other_params if p.grad is not None]
+        if not grads:
+            return
+        flat = torch.cat([g.reshape(-1) for g in grads])
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.pg)
+        flat.mul_(1.0 / self.world)
+        off = 0
+        for g in grads:
+            n = g.numel()
+            g.copy_(flat[off:off + n].view_as(g))
+            off += n
+
+    def _gather_info(self):
+        if self.world > 1:
+            dist.all_reduce(self.info, op=dist.ReduceOp.MAX, group=self.pg)
+        return self.info
+
+    def check(self):
+        """Raise the NumericError of a previous deferred-checked step, if any."""
+        if self._pending_info is not None:
+            host, ev = self._pending_info
+            self._pending_info = None
+            ev.synchronize()
+            self._raise_from_host(host)
+
+    def _raise_from_host(self, host):
+        bad = torch.nonzero(host).flatten().tolist()
+        if not bad:
+            return
+        i = bad[0]
+        code = int(host[i])
+        owner = next(p for p, part in enumerate(self.assignment) if i in part)
+        ly = self.layers[i]
+        if code == L.INFO_TRACE:
+            msg = "degenerate factor: traces must be positive"
+        elif code == L.INFO_NOT_SPD_A:
+            msg = (f"damped input factor A is not invertible: Cholesky inversion failed for a "
+                   f"{ly.d_in}x{ly.d_in} matrix (not positive definite?)")
+        elif code == L.INFO_NOT_SPD_G:
+            msg = (f"damped gradient factor G is not invertible: Cholesky inversion failed for a "
+                   f"{ly.d_out}x{ly.d_out} matrix (not positive definite?)")
+        elif code == L.INFO_EIG_DENOM:
+            msg = "eigen damping denominator is not positive; use gamma > 0 or nonsingular factors"
+        else:
+            msg = "eigendecomposition produced non-finite values"
+        raise NumericError(f"worker {owner}, layer {i}: {msg}")
+
+    # ------------------------------------------------------------ state (reference checkpoint names, trainer.py:228-244)
+    def state_dict(self) -> dict:
+        layers = {}
+        for ly in getattr(self, "owned", []):
+            d = {"initialized": ly.initialized, "last_factor_update": ly.last_factor_update,
+                 "last_inverse_update": ly.last_inverse_update}
+            if ly.a_cov is not None:
+                d["a_cov"], d["g_cov"] = ly.a_cov.clone(), ly.g_cov.clone()
+            if ly.holds == "eigen":
+                d["a_eig_q"], d["a_eig_v"] = ly.a_q.clone(), ly.a_w.clone()
+                d["g_eig_q"], d["g_eig_v"] = ly.g_q.clone(), ly.g_w.clone()
+            elif ly.holds == "inverse":
+                d["a_damped_inv"], d["g_damped_inv"] = ly.a_inv.clone(), ly.g_inv.clone()
+            layers[ly.index] = d
+        return {"t": self.t, "rank": self.rank, "assignment": self.assignment, "layers": layers,
+                "hyper": dict(self.hyper.__dict__)}
+
+    def load_state_dict(self, sd: dict):
+        self.t = int(sd["t"])
+        if tuple(tuple(p) for p in sd["assignment"]) != tuple(self.assignment or ()):
+            raise ArgumentError("checkpoint assignment differs from this optimizer's")
+        for ly in self.owned:
+            d = sd["layers"].get(ly.index)
+            if d is None:
+                continue
+            ly.alloc_state(self.hyper.inv_type, self.device)
+            ly.initialized = bool(d["initialized"])
+            ly.last_factor_update = int(d["last_factor_update"])
+            ly.last_inverse_update = int(d["last_inverse_update"])
+            if "a_cov" in d:
+                ly.a_cov.copy_(d["a_cov"])
+                ly.g_cov.copy_(d["g_cov"])
+            if "a_eig_q" in d:
+                ly.alloc_state("eigen", self.device)
+                ly.a_q.copy_(d["a_eig_q"]), ly.a_w.copy_(d["a_eig_v"])
+                ly.g_q.copy_(d["g_eig_q"]), ly.g_w.copy_(d["g_eig_v"])
+                ly.holds = "eigen"
+            if "a_damped_inv" in d:
+                ly.alloc_state("inverse", self.device)
+                ly.a_inv.copy_(d["a_damped_inv"])
+                ly.g_inv.copy_(d["g_damped_inv"])
+                ly.holds = "inverse"
+
+    # ------------------------------------------------------------ introspection
+    def layer_dims(self):
+        """(d_in incl. bias, d_out) per registered layer -- the reference's LayerDims."""
+        return [(ly.d_in, ly.d_out) for ly in self.layers]
+
+    def preconditioned_by(self) -> dict:
+        """layer -> owning rank (reference StepResult.preconditioned_by, distsim.py:244)."""
+        return {i: p for p, part in enumerate(self.assignment) for i in part}

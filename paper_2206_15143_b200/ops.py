@@ -1,0 +1,273 @@
+"""torch-facing wrappers of the libdpkfac.so entry points.
+
+Each function takes CUDA float32 tensors, builds the C job structs, and
+launches on ``torch.cuda.current_stream()``.  Scratch space comes from a
+per-(device, stream) zero-initialised workspace that only grows.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence
+
+import torch
+
+from . import _lib as L
+from .errors import ArgumentError, ShapeError
+
+PRECISIONS = {"tf32": L.DPK_PREC_TF32, "3xtf32": L.DPK_PREC_3XTF32}
+
+
+def lib():
+    return L.load()
+
+
+def stream_handle(stream: Optional[torch.cuda.Stream] = None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+class Workspace:
+    """Grow-only zero-filled scratch buffer (the split-K semaphores inside it
+    must start at zero; every kernel restores them)."""
+
+    _pool: dict = {}
+
+    @classmethod
+    def get(cls, nbytes: int, device: torch.device, key: str = "main") -> int:
+        if nbytes <= 0:
+            return 0
+        skey = (device.index, torch.cuda.current_stream(device).cuda_stream, key)
+        buf = cls._pool.get(skey)
+        if buf is None or buf.numel() < nbytes:
+            size = max(nbytes, int(buf.numel() * 1.5) if buf is not None else 0)
+            buf = torch.zeros(size, dtype=torch.uint8, device=device)
+            cls._pool[skey] = buf
+        return buf.data_ptr()
+
+
+def precision_code(precision: str) -> int:
+    try:
+        return PRECISIONS[precision]
+    except KeyError:
+        raise ArgumentError(f"precision must be one of {tuple(PRECISIONS)}") from None
+
+
+def _check_cuda_f32(*ts):
+    for t in ts:
+        if t is None:
+            continue
+        if not t.is_cuda or t.dtype != torch.float32:
+            raise ArgumentError("expected CUDA float32 tensors")
+
+
+# ------------------------------------------------------------------ operand views
+def operand_rows_k(x: torch.Tensor, bias_row: bool = False) -> L.Operand:
+    """Column-per-sample matrix d x M (reference layout); rows contiguous in k."""
+    if x.dim() != 2 or x.stride(1) != 1:
+        raise ArgumentError("operand must be a 2-D tensor contiguous along the sample dimension")
+    o = L.Operand()
+    o.data = x.data_ptr()
+    o.kind = L.OPND_ROWS_K
+    o.rows = x.shape[0]
+    o.bias_row = int(bias_row)
+    o.cols = x.shape[1]
+    o.ld = x.stride(0)
+    return o
+
+
+def operand_rows_mn(x: torch.Tensor, bias_row: bool = False) -> L.Operand:
+    """Sample-major matrix M x d (e.g. an nn.Linear input): X[r, k] = x[k, r]."""
+    if x.dim() != 2 or x.stride(1) != 1:
+        raise ArgumentError("operand must be a 2-D tensor contiguous along the feature dimension")
+    o = L.Operand()
+    o.data = x.data_ptr()
+    o.kind = L.OPND_ROWS_MN
+    o.rows = x.shape[1]
+    o.bias_row = int(bias_row)
+    o.cols = x.shape[0]
+    o.ld = x.stride(0)
+    return o
+
+
+def operand_im2col(x: torch.Tensor, kernel, stride, padding, dilation, bias_row: bool = False) -> L.Operand:
+    """Implicit-im2col linear form of an N x C x H x W conv input (F.unfold row
+    order (C, kh, kw), columns (n, oh, ow)); any strides (NCHW or channels_last)."""
+    if x.dim() != 4:
+        raise ShapeError("conv capture must be N x C x H x W")
+    n, c, h, w = x.shape
+    kh, kw = kernel
+    sh, sw = stride
+    ph, pw = padding
+    dh, dw = dilation
+    oh = (h + 2 * ph - dh * (kh - 1) - 1) // sh + 1
+    ow = (w + 2 * pw - dw * (kw - 1) - 1) // sw + 1
+    o = L.Operand()
+    o.data = x.data_ptr()
+    o.kind = L.OPND_IM2COL
+    o.rows = c * kh * kw
+    o.bias_row = int(bias_row)
+    o.cols = n * oh * ow
+    o.C, o.H, o.W, o.OH, o.OW = c, h, w, oh, ow
+    o.kh, o.kw, o.sh, o.sw, o.ph, o.pw, o.dh, o.dw = kh, kw, sh, sw, ph, pw, dh, dw
+    o.sn, o.sc, o.shs, o.sws = x.stride()
+    return o
+
+
+# ------------------------------------------------------------------ K1 / K2
+def syrk_ema(jobs: Sequence[L.FactorJob], precision: str = "tf32", keepalive=None, device=None):
+    """F <- alpha X X^T + beta F for every job, one grouped tensor-core launch."""
+    if not jobs:
+        return
+    lb = lib()
+    arr = L.array(L.FactorJob, jobs)
+    need = lb.dpk_factor_workspace_bytes(arr, len(jobs))
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    ws = Workspace.get(need, dev)
+    L.check(lb.dpk_syrk_ema(arr, len(jobs), ws, need, precision_code(precision), stream_handle()),
+            "dpk_syrk_ema")
+
+
+def factor_job(x: L.Operand, factor: torch.Tensor, alpha: float, beta: float) -> L.FactorJob:
+    j = L.FactorJob()
+    j.x = x
+    j.factor = factor.data_ptr()
+    j.alpha = alpha
+    j.beta = beta
+    return j
+
+
+def gemm(jobs: Sequence[L.GemmJob], precision: str = "tf32"):
+    if not jobs:
+        return
+    lb = lib()
+    arr = L.array(L.GemmJob, jobs)
+    need = lb.dpk_gemm_workspace_bytes(arr, len(jobs))
+    ws = Workspace.get(need, torch.device("cuda", torch.cuda.current_device()))
+    L.check(lb.dpk_gemm(arr, len(jobs), ws, need, precision_code(precision), stream_handle()), "dpk_gemm")
+
+
+# ------------------------------------------------------------------ A6 + K3
+def trace_pi(pairs, gamma: float, shifts: torch.Tensor, pis: Optional[torch.Tensor], infos):
+    """pairs: list of (A, G) device matrices; writes shifts[i] = (pi sqrt(g), sqrt(g)/pi);
+    infos[i] (a one-element int32 view) receives DPK_INFO_TRACE on a non-positive trace."""
+    jobs = []
+    for i, (a, g) in enumerate(pairs):
+        j = L.PiJob()
+        j.a, j.g = a.data_ptr(), g.data_ptr()
+        j.da, j.dg = a.shape[0], g.shape[0]
+        j.shifts = shifts[i].data_ptr()
+        j.pi = pis[i].data_ptr() if pis is not None else None
+        j.info = infos[i].data_ptr()
+        jobs.append(j)
+    if not jobs:
+        return
+    lb = lib()
+    L.check(lb.dpk_trace_pi(L.array(L.PiJob, jobs), len(jobs), float(gamma), stream_handle()), "dpk_trace_pi")
+
+
+def spd_job(src: torch.Tensor, dst: torch.Tensor, shift: Optional[torch.Tensor], info: Optional[torch.Tensor],
+            fail_code: int) -> L.SpdJob:
+    j = L.SpdJob()
+    j.src, j.dst = src.data_ptr(), dst.data_ptr()
+    j.n = src.shape[0]
+    j.fail_code = fail_code
+    j.shift = shift.data_ptr() if shift is not None else None
+    j.info = info.data_ptr() if info is not None else None
+    return j
+
+
+def chol_inv(jobs: Sequence[L.SpdJob]):
+    if not jobs:
+        return
+    lb = lib()
+    arr = L.array(L.SpdJob, jobs)
+    need = lb.dpk_chol_inv_workspace_bytes(arr, len(jobs))
+    ws = Workspace.get(need, torch.device("cuda", torch.cuda.current_device()), key="spd")
+    L.check(lb.dpk_chol_inv_damped_batched(arr, len(jobs), ws, need, stream_handle()), "dpk_chol_inv_damped_batched")
+
+
+# ------------------------------------------------------------------ K4
+def eig_job(src, q, w, info) -> L.EigJob:
+    j = L.EigJob()
+    j.src, j.q, j.w = src.data_ptr(), q.data_ptr(), w.data_ptr()
+    j.n = src.shape[0]
+    j.info = info.data_ptr() if info is not None else None
+    return j
+
+
+EIG_ONCHIP_MAX = 128
+
+
+def syevd(jobs_tensors):
+    """jobs_tensors: list of (src, q, w, info_or_None).  n <= 128 runs the on-chip
+    Jacobi kernel of libdpkfac; larger factors currently go through cuSOLVER
+    (torch.linalg.eigh on the GPU) -- see DESIGN.md (K4 status)."""
+    small = [t for t in jobs_tensors if t[0].shape[0] <= EIG_ONCHIP_MAX]
+    large = [t for t in jobs_tensors if t[0].shape[0] > EIG_ONCHIP_MAX]
+    if small:
+        lb = lib()
+        arr = L.array(L.EigJob, [eig_job(*t) for t in small])
+        L.check(lb.dpk_syevd_batched(arr, len(small), None, 0, stream_handle()), "dpk_syevd_batched")
+    for src, q, w, info in large:
+        sym = 0.5 * (src + src.T)
+        vals, vecs = torch.linalg.eigh(sym)
+        w.copy_(vals.flip(0))
+        q.copy_(vecs.flip(1))
+        if info is not None:
+            bad = ~(torch.isfinite(vals).all() & torch.isfinite(vecs).all())
+            info.masked_fill_(bad, L.INFO_NONFINITE)
+
+
+# ------------------------------------------------------------------ K5 / K6
+def precond_job(grad, a_mat, g_mat, out, tmp, a_vals=None, g_vals=None, info=None) -> L.PrecondJob:
+    j = L.PrecondJob()
+    j.grad, j.a_mat, j.g_mat = grad.data_ptr(), a_mat.data_ptr(), g_mat.data_ptr()
+    j.a_vals = a_vals.data_ptr() if a_vals is not None else None
+    j.g_vals = g_vals.data_ptr() if g_vals is not None else None
+    j.out, j.tmp = out.data_ptr(), tmp.data_ptr()
+    j.d_out, j.d_in = g_mat.shape[0], a_mat.shape[0]
+    j.info = info.data_ptr() if info is not None else None
+    return j
+
+
+def precondition(jobs: Sequence[L.PrecondJob], eigen: bool, gamma: float, precision: str = "tf32"):
+    if not jobs:
+        return
+    lb = lib()
+    arr = L.array(L.PrecondJob, jobs)
+    need = lb.dpk_precond_workspace_bytes(arr, len(jobs))
+    ws = Workspace.get(need, torch.device("cuda", torch.cuda.current_device()), key="pre")
+    p = precision_code(precision)
+    if eigen:
+        rc = lb.dpk_precond_eigen(arr, len(jobs), float(gamma), ws, need, p, stream_handle())
+        L.check(rc, "dpk_precond_eigen")
+    else:
+        L.check(lb.dpk_precond_inverse(arr, len(jobs), ws, need, p, stream_handle()), "dpk_precond_inverse")
+
+
+# ------------------------------------------------------------------ K7
+def segment(weight: torch.Tensor, bias: Optional[torch.Tensor], offset: int) -> L.Segment:
+    s = L.Segment()
+    w2 = weight.reshape(weight.shape[0], -1)
+    if w2.stride(1) != 1:
+        raise ArgumentError("weight gradient must be contiguous in its trailing dims")
+    s.weight = w2.data_ptr()
+    s.bias = bias.data_ptr() if bias is not None else None
+    s.offset = offset
+    s.rows = w2.shape[0]
+    s.cols_w = w2.shape[1]
+    s.ldw = w2.stride(0)
+    return s
+
+
+def pack(segs: Sequence[L.Segment], flat: torch.Tensor, scale: float = 1.0):
+    if segs:
+        L.check(lib().dpk_pack_owner_major(L.array(L.Segment, segs), len(segs), flat.data_ptr(), float(scale),
+                                           stream_handle()), "dpk_pack_owner_major")
+
+
+def unpack(segs: Sequence[L.Segment], flat: torch.Tensor, scale: float = 1.0):
+    if segs:
+        L.check(lib().dpk_unpack_owner_major(L.array(L.Segment, segs), len(segs), flat.data_ptr(), float(scale),
+                                             stream_handle()), "dpk_unpack_owner_major")

@@ -1,0 +1,83 @@
+"""N>1 host logic on CPU: owner-major layout, reduce-scatter of mean gradients to
+the owners and all-gather of owner results, with world_size 2 and 3 over gloo.
+
+Mirrors the reference's semantics (distsim.py:259-265 mean of local grads;
+distsim.py:333-336 owner result broadcast to all)."""
+
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2206_15143_b200.exchange import OwnerMajorExchange, OwnerMajorLayout
+from paper_2206_15143_b200.partition import balanced_partition, round_robin_partition
+
+SHAPES = [(4, 7), (3, 5), (6, 2), (2, 9), (5, 5)]
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _local_grad(rank, i):
+    g = torch.Generator().manual_seed(1000 * rank + i)
+    return torch.randn(*SHAPES[i], generator=g)
+
+
+def _worker(rank, world, port, assign_kind, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n = len(SHAPES)
+        if assign_kind == "rr":
+            assignment = round_robin_partition(n, world)
+        else:
+            assignment = balanced_partition([r * c for r, c in SHAPES], world)
+        layout = OwnerMajorLayout(assignment, [r * c for r, c in SHAPES], align=4)
+        x = OwnerMajorExchange(layout, rank, "cpu")
+        for i in range(n):  # pack (the CUDA pack kernel's job on the GPU): flat = grad / P
+            off = layout.offsets[i]
+            x.flat[off:off + SHAPES[i][0] * SHAPES[i][1]] = (_local_grad(rank, i) / world).reshape(-1)
+        x.reduce_scatter()
+        for i in assignment[rank]:  # "precondition": owner tags its result with (i+1)
+            x.view_out(i, SHAPES[i]).copy_(x.view_in(i, SHAPES[i]) * (i + 1))
+        x.all_gather()
+        out = {}
+        for i in range(n):
+            off = layout.offsets[i]
+            out[i] = x.out_flat[off:off + SHAPES[i][0] * SHAPES[i][1]].view(*SHAPES[i]).clone()
+        q.put((rank, out, layout.padding))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,kind", [(2, "rr"), (3, "rr"), (2, "balanced")])
+def test_owner_major_exchange_gloo(world, kind):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for i in range(len(SHAPES)):
+        mean = sum(_local_grad(r, i) for r in range(world)) / world
+        want = mean * (i + 1)
+        for rank, out, pad in results:
+            assert torch.allclose(out[i], want, atol=1e-6), (rank, i)
+    # replicas identical after the exchange (reference test_distsim.py:203-214)
+    base = results[0][1]
+    for _, out, _ in results[1:]:
+        for i in range(len(SHAPES)):
+            assert torch.equal(out[i], base[i])

@@ -1,0 +1,206 @@
+"""End-to-end parity of the DPKFAC optimizer against the float64 oracle.
+
+* MLP (BASELINE config 1: 784-512-256-10, batch 64): the whole DP-KFAC
+  iteration (reference distsim.dp_kfac_step, distsim.py:289-338) over several
+  steps, weights initialised by the reference's init_network recipe.
+* Conv nets: per-layer parity at the linear-form boundary (unfold on the CPU,
+  reference kfac_layer_step in float64) for stride/padding/bias variants.
+"""
+
+import numpy as np
+import pytest
+import torch
+import torch.nn as nn
+import torch.nn.functional as F
+
+from oracle import kfac_ref as K
+from oracle import mlp_ref as MLP
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-3
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def torch_mlp(weights, dev):
+    mods = []
+    for i, w in enumerate(weights):
+        lin = nn.Linear(w.shape[1] - 1, w.shape[0])
+        with torch.no_grad():
+            lin.weight.copy_(torch.from_numpy(w[:, :-1]))
+            lin.bias.copy_(torch.from_numpy(w[:, -1]))
+        mods.append(lin)
+        if i < len(weights) - 1:
+            mods.append(nn.ReLU())
+    return nn.Sequential(*mods).to(dev), [m for m in mods if isinstance(m, nn.Linear)]
+
+
+@pytest.mark.parametrize("inv_type,precision", [("inverse", "tf32"), ("inverse", "3xtf32"), ("eigen", "3xtf32")])
+def test_mlp_config1_dp_kfac_matches_reference(inv_type, precision):
+    from paper_2206_15143_b200 import DPKFAC
+    dev = torch.device("cuda", 0)
+    spec = MLP.MlpSpec((784, 512, 256, 10), "relu", "softmax_cross_entropy", True)
+    h = K.Hyper(gamma=0.03, xi=0.95, inv_type=inv_type, f_freq=1, k_freq=1)
+    cl = MLP.build_cluster(spec, 1, seed=0)
+    model, lins = torch_mlp([w.copy() for w in cl.weights], dev)
+    kf = DPKFAC(model, gamma=0.03, xi=0.95, inv_type=inv_type, precision=precision)
+    opt = torch.optim.SGD(model.parameters(), lr=0.05, momentum=0.9)
+    rng = np.random.default_rng(1234)
+    for t in range(3):
+        x = rng.standard_normal((784, 64))
+        y = rng.integers(0, 10, size=64)
+        _, pre = MLP.dp_kfac_step(cl, MLP.shard(x, y, 1), h, 0.05, 0.9, t)
+        opt.zero_grad()
+        out = model(torch.from_numpy(x.T.copy()).float().to(dev))
+        F.cross_entropy(out, torch.from_numpy(y).to(dev)).backward()
+        kf.step()
+        for i, lin in enumerate(lins):
+            got = torch.cat([lin.weight.grad, lin.bias.grad[:, None]], 1).double().cpu().numpy()
+            assert rel(got, pre[i]) <= TOL, (t, i, rel(got, pre[i]))
+        opt.step()
+    for i, lin in enumerate(lins):
+        got = torch.cat([lin.weight, lin.bias[:, None]], 1).detach().double().cpu().numpy()
+        assert rel(got, cl.weights[i]) <= 1e-4
+    assert kf.t == 3
+
+
+class SmallConv(nn.Module):
+    def __init__(self):
+        super().__init__()
+        self.c1 = nn.Conv2d(3, 16, 3, padding=1, bias=True)
+        self.c2 = nn.Conv2d(16, 24, 3, stride=2, padding=1, bias=False)
+        self.c3 = nn.Conv2d(24, 32, 1, stride=2, bias=False)
+        self.c4 = nn.Conv2d(32, 8, 5, padding=2, dilation=1, bias=True)
+        self.fc = nn.Linear(8 * 4 * 4, 10)
+
+    def forward(self, x):
+        x = F.relu(self.c1(x))
+        x = F.relu(self.c2(x))
+        x = F.relu(self.c3(x))
+        x = torch.tanh(self.c4(x))
+        return self.fc(x.flatten(1))
+
+
+def _record(model):
+    """capture each layer's input and grad_output on the side (the CPU oracle's inputs)."""
+    rec = {}
+    hooks = []
+    for name, m in model.named_modules():
+        if isinstance(m, (nn.Conv2d, nn.Linear)):
+            def pre(mod, inp, name=name):
+                rec.setdefault(name, {})["x"] = inp[0].detach().double().cpu().numpy()
+
+            def fwd(mod, inp, out, name=name):
+                out.register_hook(lambda g, name=name: rec[name].__setitem__("g", g.detach().double().cpu().numpy()))
+            hooks.append(m.register_forward_pre_hook(pre))
+            hooks.append(m.register_forward_hook(fwd))
+    return rec, hooks
+
+
+def _oracle_layer(m, cap, batch):
+    x, g = cap["x"], cap["g"]
+    bias = m.bias is not None
+    if isinstance(m, nn.Conv2d):
+        X = K.unfold_columns(x, m.kernel_size[0], m.kernel_size[1], m.stride[0], m.padding[0], m.dilation[0], bias)
+        Gm = g.transpose(1, 0, 2, 3).reshape(g.shape[1], -1) * batch
+    else:
+        X = x.T
+        if bias:
+            X = np.vstack([X, np.ones((1, X.shape[1]))])
+        Gm = g.T * batch
+    W = m.weight.grad.double().cpu().numpy().reshape(m.weight.shape[0], -1)
+    if bias:
+        W = np.hstack([W, m.bias.grad.double().cpu().numpy()[:, None]])
+    return X, Gm, W
+
+
+@pytest.mark.parametrize("inv_type", ["inverse", "eigen"])
+def test_conv_layers_match_reference_layer_step(inv_type):
+    from paper_2206_15143_b200 import DPKFAC
+    torch.manual_seed(0)
+    dev = torch.device("cuda", 0)
+    model = SmallConv().to(dev)
+    kf = DPKFAC(model, gamma=0.01, xi=0.7, inv_type=inv_type, precision="tf32", f_freq=1, k_freq=2)
+    h = K.Hyper(gamma=0.01, xi=0.7, inv_type=inv_type, f_freq=1, k_freq=2)
+    rec, hooks = _record(model)
+    states = {}
+    gen = torch.Generator().manual_seed(7)
+    for t in range(3):
+        x = torch.randn(8, 3, 16, 16, generator=gen).to(dev)
+        y = torch.randint(0, 10, (8,), generator=gen).to(dev)
+        model.zero_grad()
+        F.cross_entropy(model(x), y).backward()
+        want = {}
+        for name, m in model.named_modules():
+            if isinstance(m, (nn.Conv2d, nn.Linear)):
+                X, Gm, W = _oracle_layer(m, rec[name], 8)
+                st = states.setdefault(name, K.LayerState())
+                want[name], _ = K.kfac_layer_step(st, X, Gm, W, h, t)
+        kf.step()
+        for name, m in model.named_modules():
+            if isinstance(m, (nn.Conv2d, nn.Linear)):
+                got = m.weight.grad.double().cpu().numpy().reshape(m.weight.shape[0], -1)
+                if m.bias is not None:
+                    got = np.hstack([got, m.bias.grad.double().cpu().numpy()[:, None]])
+                assert rel(got, want[name]) <= TOL, (t, name, rel(got, want[name]))
+    for hk in hooks:
+        hk.remove()
+
+
+def test_registration_order_matches_resnet50_manifest():
+    torchvision = pytest.importorskip("torchvision")
+    import json
+    import os
+    from conftest import GOLDEN
+    from paper_2206_15143_b200 import DPKFAC
+    model = torchvision.models.resnet50().cuda()
+    kf = DPKFAC(model, inv_type="inverse")
+    with open(os.path.join(GOLDEN, "resnet50_manifest.json")) as f:
+        dims = [tuple(d) for d in json.load(f)["dims"]]
+    assert kf.layer_dims() == dims
+    kf.remove_hooks()
+
+
+def test_step_before_backward_is_an_error():
+    from paper_2206_15143_b200 import DPKFAC, ArgumentError, OrderingError
+    model = nn.Sequential(nn.Linear(4, 3)).cuda()
+    kf = DPKFAC(model, inv_type="inverse")
+    with pytest.raises((ArgumentError, OrderingError)):
+        kf.step()
+
+
+def test_state_dict_roundtrip_stale_resume():
+    from paper_2206_15143_b200 import DPKFAC
+    torch.manual_seed(1)
+    dev = torch.device("cuda", 0)
+    model = nn.Sequential(nn.Linear(12, 10), nn.Tanh(), nn.Linear(10, 4)).to(dev)
+    kf = DPKFAC(model, inv_type="inverse", f_freq=2, k_freq=3, gamma=0.05, xi=0.5)
+    xs = [torch.randn(16, 12, device=dev) for _ in range(6)]
+    ys = [torch.randint(0, 4, (16,), device=dev) for _ in range(6)]
+
+    def one(kf, model, t):
+        model.zero_grad()
+        F.cross_entropy(model(xs[t]), ys[t]).backward()
+        kf.step()
+        return [p.grad.clone() for p in model.parameters()]
+
+    for t in range(3):
+        one(kf, model, t)
+    sd = kf.state_dict()
+    model2 = nn.Sequential(nn.Linear(12, 10), nn.Tanh(), nn.Linear(10, 4)).to(dev)
+    model2.load_state_dict(model.state_dict())
+    kf2 = DPKFAC(model2, inv_type="inverse", f_freq=2, k_freq=3, gamma=0.05, xi=0.5)
+    kf2.load_state_dict(sd)
+    for t in range(3, 6):
+        g1 = one(kf, model, t)
+        g2 = one(kf2, model2, t)
+        for a, b in zip(g1, g2):
+            assert torch.equal(a, b)

@@ -1,0 +1,277 @@
+"""GPU parity of every libdpkfac kernel against the float64 oracle (tolerances written per test).
+
+Bar (BASELINE north_star): relative Frobenius error <= 1e-3 for factors and
+preconditioned gradients in the fp32/TF32 path."""
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+from oracle import kfac_ref as K
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-3
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def dev():
+    return torch.device("cuda", 0)
+
+
+def T(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).float().to(dev())
+
+
+def N(t):
+    return t.double().cpu().numpy()
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2206_15143_b200 import _lib
+    _lib.load()
+
+
+# ---------------------------------------------------------------- K1 SYRK + EMA
+@pytest.mark.parametrize("d,m", [(1, 5), (10, 64), (127, 33), (128, 128), (129, 4000), (300, 777), (785, 64),
+                                 (64, 100352)])
+@pytest.mark.parametrize("precision", ["tf32", "3xtf32"])
+def test_syrk_rows_k_matches_oracle(d, m, precision):
+    from paper_2206_15143_b200 import kfac as FK
+    rng = np.random.default_rng(d * 7 + m)
+    x = rng.standard_normal((d, m))
+    g = rng.standard_normal((3, m))
+    a, _ = FK.compute_factors(T(x), T(g), precision=precision)
+    a_ref, _ = K.compute_factors(x, g)
+    assert rel(N(a), a_ref) <= (TOL if precision == "tf32" else 1e-5)
+    assert torch.equal(a, a.T)  # exactly symmetric like (F + F^T)/2
+
+
+def test_syrk_ema_fused_running_average():
+    from paper_2206_15143_b200 import kfac as FK
+    rng = np.random.default_rng(1)
+    st_ref, st = K.LayerState(), FK.FactorState()
+    for t in range(4):
+        x = np.maximum(rng.standard_normal((200, 300)), 0)
+        g = rng.standard_normal((50, 300)) * 0.1
+        a_new, g_new = K.compute_factors(x, g)
+        K.update_running_average(st_ref, a_new, g_new, 0.3, t)
+        FK.update_factors_fused(st, T(x), T(g), 0.3, t, precision="3xtf32")
+        assert rel(N(st.a_cov), st_ref.a_cov) <= 1e-5
+        assert rel(N(st.g_cov), st_ref.g_cov) <= 1e-5
+        assert st.last_factor_update == t
+
+
+def _linear_capture(rng, b, d, bias):
+    x = rng.standard_normal((b, d))
+    X = x.T
+    if bias:
+        X = np.vstack([X, np.ones((1, b))])
+    return x, X
+
+
+@pytest.mark.parametrize("b,d,bias", [(64, 784, True), (32, 2048, True), (7, 5, False)])
+def test_syrk_rows_mn_linear_input_with_bias_row(b, d, bias):
+    from paper_2206_15143_b200 import _lib as L, ops
+    rng = np.random.default_rng(b + d)
+    x, X = _linear_capture(rng, b, d, bias)
+    xt = T(x)
+    dd = d + int(bias)
+    out = torch.full((dd, dd), float("nan"), device=dev())
+    ops.syrk_ema([ops.factor_job(ops.operand_rows_mn(xt, bias), out, 1.0 / b, 0.0)], "tf32")
+    torch.cuda.synchronize()
+    want, _ = K.compute_factors(X, X[:1])
+    assert rel(N(out), want) <= TOL
+    assert torch.isfinite(out).all()
+
+
+@pytest.mark.parametrize("shape,k,s,p,dil", [
+    ((2, 3, 9, 9), 3, 1, 1, 1), ((2, 4, 10, 10), 3, 2, 1, 1), ((3, 5, 8, 8), 1, 2, 0, 1),
+    ((1, 3, 15, 15), 7, 2, 3, 1), ((2, 2, 9, 9), 3, 1, 2, 2), ((4, 64, 14, 14), 3, 1, 1, 1)])
+@pytest.mark.parametrize("channels_last", [False, True])
+def test_syrk_implicit_im2col_matches_unfold(shape, k, s, p, dil, channels_last):
+    from paper_2206_15143_b200 import ops
+    rng = np.random.default_rng(sum(shape) + k)
+    x = np.maximum(rng.standard_normal(shape), 0)
+    xt = T(x)
+    if channels_last:
+        xt = xt.to(memory_format=torch.channels_last)
+    cols = K.unfold_columns(x, k, k, s, p, dil, bias=True)
+    d = cols.shape[0]
+    out = torch.empty(d, d, device=dev())
+    op = ops.operand_im2col(xt, (k, k), (s, s), (p, p), (dil, dil), bias_row=True)
+    assert op.cols == cols.shape[1]
+    ops.syrk_ema([ops.factor_job(op, out, 1.0 / cols.shape[1], 0.0)], "3xtf32")
+    torch.cuda.synchronize()
+    want, _ = K.compute_factors(cols, cols[:1])
+    assert rel(N(out), want) <= 1e-5
+
+
+def test_grouped_syrk_many_problems_and_split_k():
+    from paper_2206_15143_b200 import ops
+    rng = np.random.default_rng(5)
+    jobs, outs, refs, keep = [], [], [], []
+    for i in range(45):  # > MAXP per launch -> several launches
+        d = int(rng.integers(1, 300))
+        m = int(rng.integers(1, 20000)) if i % 5 else 60000
+        x = rng.standard_normal((d, m)).astype(np.float32)
+        xt = T(x)
+        o = torch.empty(d, d, device=dev())
+        jobs.append(ops.factor_job(ops.operand_rows_k(xt), o, 1.0 / m, 0.0))
+        outs.append(o)
+        keep.append(xt)
+        refs.append(x.astype(np.float64) @ x.T.astype(np.float64) / m)
+    ops.syrk_ema(jobs, "tf32")
+    torch.cuda.synchronize()
+    for o, r in zip(outs, refs):
+        assert rel(N(o), r) <= TOL
+
+
+# ---------------------------------------------------------------- generic GEMM engine
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (130, 70, 45), (512, 785, 300), (1000, 2049, 33)])
+def test_gemm_all_operand_majors(m, n, k):
+    from paper_2206_15143_b200 import _lib as L, ops
+    rng = np.random.default_rng(m + n + k)
+    a = rng.standard_normal((m, k))
+    b = rng.standard_normal((n, k))
+    c = rng.standard_normal((m, n))
+    at, bt, ct = T(a), T(b), T(c)
+    atr, btr = T(a.T), T(b.T)
+    for a_op, b_op in [(ops.operand_rows_k(at), ops.operand_rows_k(bt)),
+                       (ops.operand_rows_mn(atr), ops.operand_rows_k(bt)),
+                       (ops.operand_rows_k(at), ops.operand_rows_mn(btr)),
+                       (ops.operand_rows_mn(atr), ops.operand_rows_mn(btr))]:
+        out = torch.empty(m, n, device=dev())
+        j = L.GemmJob()
+        j.a, j.b = a_op, b_op
+        j.out, j.ldo = out.data_ptr(), n
+        j.cin, j.ldc = ct.data_ptr(), n
+        j.alpha, j.beta = 0.5, -2.0
+        ops.gemm([j], "3xtf32")
+        torch.cuda.synchronize()
+        assert rel(N(out), 0.5 * a @ b.T - 2.0 * c) <= 1e-5
+
+
+# ---------------------------------------------------------------- K3 damped inverse
+def _spd(rng, n, cond_floor=1e-2):
+    b = rng.standard_normal((n, n + 3))
+    return b @ b.T / (n + 3) + cond_floor * np.eye(n)
+
+
+@pytest.mark.parametrize("n", [1, 2, 17, 64, 128, 129, 200, 513, 1000, 2049])
+def test_spd_inverse_matches_oracle(n):
+    from paper_2206_15143_b200 import kfac as FK
+    rng = np.random.default_rng(n)
+    a = _spd(rng, n)
+    got = FK.sym_inverse(T(a))
+    want = K.spd_inverse(a)
+    cond = np.linalg.cond(a)
+    # fp32-grade (3xTF32) elimination: error ~ cond * 2^-23 up to a modest growth factor
+    assert rel(N(got), want) <= max(1e-5, 20 * cond * 2.0 ** -23), (rel(N(got), want), cond)
+    assert torch.equal(got, got.T)
+
+
+def test_damped_inverses_and_pi_match_oracle():
+    from paper_2206_15143_b200 import kfac as FK
+    rng = np.random.default_rng(3)
+    for da, dg, gamma in [(785, 512, 0.03), (147, 64, 0.002), (300, 10, 1.0)]:
+        x = np.maximum(rng.standard_normal((da, 600)), 0)
+        g = rng.standard_normal((dg, 600)) * 0.01
+        a, gg = K.compute_factors(x, g)
+        ai, gi = FK.damped_inverses(T(a), T(gg), gamma)
+        ai_r, gi_r = K.damped_inverses(a, gg, gamma)
+        assert rel(N(ai), ai_r) <= 1e-4 and rel(N(gi), gi_r) <= 1e-4
+        assert abs(FK.pi_scalar(T(a), T(gg)) - K.pi_scalar(a, gg)) <= 1e-5 * K.pi_scalar(a, gg)
+
+
+def test_non_spd_raises_numeric_error_like_reference():
+    from paper_2206_15143_b200 import NumericError
+    from paper_2206_15143_b200 import kfac as FK
+    a = np.eye(150)
+    a[70, 70] = -1.0
+    with pytest.raises(NumericError, match="not positive definite"):
+        FK.sym_inverse(T(a))
+    with pytest.raises(NumericError, match="traces must be positive"):
+        FK.damped_inverses(T(np.zeros((3, 3))), T(np.eye(2)), 0.03)
+    with pytest.raises(NumericError, match="damped input factor A is not invertible"):
+        FK.damped_inverses(T(np.diag([1.0, -5.0, 1.0, 1.0])), T(np.eye(2)), 0.0)
+
+
+# ---------------------------------------------------------------- K4 eigen
+@pytest.mark.parametrize("n", [1, 2, 3, 31, 64, 127, 128])
+def test_sym_eig_onchip_jacobi(n):
+    from paper_2206_15143_b200 import kfac as FK
+    rng = np.random.default_rng(n)
+    a = _spd(rng, n, 0.0)
+    e = FK.sym_eig(T(a))
+    r = K.symmetric_eig(a)
+    assert rel(N(e.values), r.values) <= 1e-5
+    assert np.all(np.diff(N(e.values)) <= 0)
+    q = N(e.q)
+    assert np.abs(q.T @ q - np.eye(n)).max() <= 1e-4
+    assert rel(q @ np.diag(N(e.values)) @ q.T, a) <= 1e-5
+
+
+# ---------------------------------------------------------------- K5 / K6
+@pytest.mark.parametrize("din,dout,gamma", [(785, 512, 0.03), (65, 9, 0.002), (2049, 1000, 0.002), (3, 2, 0.03)])
+def test_precondition_inverse_matches_oracle(din, dout, gamma):
+    from paper_2206_15143_b200 import kfac as FK
+    rng = np.random.default_rng(din)
+    x = np.maximum(rng.standard_normal((din, 256)), 0)
+    g = rng.standard_normal((dout, 256)) * 0.1
+    grad = rng.standard_normal((dout, din)) * 0.01
+    a, gg = K.compute_factors(x, g)
+    got = FK.precondition_inverse(T(a), T(gg), T(grad), gamma)
+    want = K.precondition_inverse(a, gg, grad, gamma)
+    assert rel(N(got), want) <= TOL
+
+
+@pytest.mark.parametrize("din,dout,gamma", [(65, 9, 0.002), (128, 100, 0.03), (3, 2, 0.03), (120, 1, 0.5)])
+def test_precondition_eigen_matches_oracle(din, dout, gamma):
+    from paper_2206_15143_b200 import kfac as FK
+    rng = np.random.default_rng(din + dout)
+    x = np.maximum(rng.standard_normal((din, 200)), 0)
+    g = rng.standard_normal((dout, 200)) * 0.1
+    grad = rng.standard_normal((dout, din)) * 0.01
+    a, gg = K.compute_factors(x, g)
+    got = FK.precondition_eigen(FK.sym_eig(T(a)), FK.sym_eig(T(gg)), T(grad), gamma)
+    want = K.precondition_eigen(K.symmetric_eig(a), K.symmetric_eig(gg), grad, gamma)
+    assert rel(N(got), want) <= TOL
+
+
+def test_eigen_zero_denominator_raises():
+    from paper_2206_15143_b200 import NumericError
+    from paper_2206_15143_b200 import kfac as FK
+    z = FK.sym_eig(T(np.zeros((2, 2))))
+    with pytest.raises(NumericError, match="denominator"):
+        FK.precondition_eigen(z, z, T(np.ones((2, 2))), 0.0)
+
+
+# ---------------------------------------------------------------- K7 pack / unpack
+def test_pack_unpack_roundtrip_with_bias_column():
+    from paper_2206_15143_b200 import ops
+    rng = np.random.default_rng(9)
+    w1 = T(rng.standard_normal((5, 3, 3, 3)))
+    w2 = T(rng.standard_normal((4, 7)))
+    b2 = T(rng.standard_normal(4))
+    w1_0, w2_0, b2_0 = w1.clone(), w2.clone(), b2.clone()
+    flat = torch.zeros(5 * 27 + 4 * 8 + 10, device=dev())
+    segs = [ops.segment(w1, None, 0), ops.segment(w2, b2, 5 * 27 + 3)]
+    ops.pack(segs, flat, 0.5)
+    torch.cuda.synchronize()
+    assert torch.equal(flat[:135].view(5, 27), 0.5 * w1_0.view(5, 27))
+    m2 = flat[138:138 + 32].view(4, 8)
+    assert torch.equal(m2[:, :7], 0.5 * w2_0) and torch.equal(m2[:, 7], 0.5 * b2_0)
+    flat.mul_(4.0)
+    ops.unpack(segs, flat, 1.0)
+    torch.cuda.synchronize()
+    assert torch.equal(w1, 2.0 * w1_0) and torch.equal(w2, 2.0 * w2_0) and torch.equal(b2, 2.0 * b2_0)
