@@ -10,9 +10,9 @@
  * Conventions
  *   - All matrix / tensor pointers are DEVICE pointers owned by the caller
  *     (torch owns every byte; the library never allocates persistent memory).
- *     Scratch space is passed in explicitly as (workspace, bytes) and must be
- *     zero-filled once when first allocated (split-K semaphores live there and
- *     are restored to zero by every call).
+ *     Scratch space is passed in explicitly as (workspace, bytes); its size
+ *     comes from the matching *_workspace_bytes query and its content need not
+ *     be initialised (split-K semaphores in it are zeroed on the stream).
  *   - Matrices are row-major float32.  Factors are d x d and exactly symmetric.
  *   - Calls are asynchronous on the given stream and stateless, hence
  *     reentrant across streams.  No C++ exception crosses this boundary.

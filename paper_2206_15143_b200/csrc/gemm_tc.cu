@@ -630,6 +630,12 @@ int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int pre
       partial_tiles += static_cast<size_t>(P.ntiles) * P.splits;
     }
   }
+  // The split-K semaphores must start at zero.  Kernels restore them, but the
+  // caller's scratch may have held other data (e.g. the SPD recursion buffers).
+  if (ncounters > 0) {
+    rc = cuda_status(cudaMemsetAsync(counters, 0, ncounters * sizeof(int), st), "cudaMemsetAsync(counters)");
+    if (rc != DPK_OK) return rc;
+  }
   thread_local Batch bt;  // host-side staging only (kernel params are copied at launch)
   for (int first = 0; first < n; first += MAXP) {
     const int cnt = std::min(MAXP, n - first);

@@ -1,21 +1,24 @@
 // K3: batched damped SPD inverse  dst = (src + shift I)^-1   (reference
-// numerics.sym_inverse numerics.py:100-114 through kfac.damped_inverses
-// kfac.py:140-155).
+// numerics.sym_inverse numerics.py:100-114 -- cho_factor(lower) + cho_solve(I),
+// symmetrized -- through kfac.damped_inverses kfac.py:140-155).
 //
-// Small matrices (n <= 128) are inverted by one CTA each, fully staged in
-// shared memory, with the symmetric sweep: pivot k has value p_k = L_kk^2 (the
-// squared Cholesky diagonal of the leading block), so "p_k <= 0" is exactly the
-// condition under which the reference's cho_factor raises -- reported through
-// the info word.  Every update is applied symmetrically, so the result is
-// exactly symmetric like the reference's (inv + inv^T)/2.
+// Same method as the reference: Cholesky factor, then the inverse from the
+// factor (potrf -> trtri -> L^-T L^-1, LAPACK potri's route).
 //
-// Larger matrices use the recursive 2x2 block (Schur complement) form of the
-// same elimination, whose work is four tcgen05 3xTF32 GEMMs per level:
-//   X11 = A11^-1 (recurse)          Z = X11 A12
-//   S = A22 - A21 Z (symmetric)     X22 = S^-1 (recurse)
-//   X12 = -Z X22, X21 = X12^T       X11 = X11 - X12 Z^T (symmetric)
-// n^3 flops in total, like potrf+potri; the leaves are the shared-memory kernel.
-// All matrices of a call advance in lock-step rounds (<= 2 launches per round).
+// n <= 128: one CTA per matrix, everything in shared memory: right-looking
+//   Cholesky (a non-positive pivot is exactly where cho_factor raises ->
+//   info word), right-looking triangular inverse X = L^-1, then X^T X written
+//   as lower tiles + mirror, so the result is exactly symmetric.
+// n > 128: recursive 2x2 blocking whose off-diagonal work is tcgen05 3xTF32
+//   GEMMs (fp32-grade):
+//      L11, X11 = chol/trtri(A11)            (recurse; leaves = the smem kernel)
+//      L21 = A21 X11^T                       (TRSM via the triangular inverse)
+//      A22 <- A22 - L21 L21^T                (symmetric, lower tiles + mirror)
+//      L22, X22 = chol/trtri(A22)            (recurse)
+//      X21 = -X22 (L21 X11)
+//   and finally dst = X^T X (symmetric).  Leaves only need X = L^-1 of their
+//   diagonal block.  All matrices of a call advance in lock-step rounds of at
+//   most one leaf launch + one grouped GEMM launch.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -32,10 +35,15 @@ constexpr int LEAF_THREADS = 256;
 constexpr int LEAF_MAX = 256;
 
 struct LeafJob {
-  float* mat;
-  int64_t ld;
+  const float* src;    // input block (row stride lds)
+  float* dst;          // TRI: X = L^-1 block (lower, zeros above); FULL: the inverse
+  const float* shift;  // FULL mode: damping added to the diagonal (may be null)
+  int64_t lds;
+  int64_t ldd;
   int32_t n;
+  int32_t full;        // 1: whole matrix -> inverse; 0: diagonal block -> L^-1
   int32_t fail_code;
+  int32_t _pad;
   int32_t* info;
 };
 struct LeafBatch {
@@ -43,67 +51,89 @@ struct LeafBatch {
   LeafJob j[LEAF_MAX];
 };
 
-// In-place symmetric sweep on an n x n block (n <= 128) staged in smem;
-// writes +inverse back.  Full storage, 2 barriers per pivot.
 __global__ void __launch_bounds__(LEAF_THREADS) spd_leaf_kernel(const __grid_constant__ LeafBatch b) {
-  extern __shared__ float S[];
-  __shared__ float v[LEAF_N];
+  extern __shared__ float smem[];
   const LeafJob& J = b.j[blockIdx.x];
   const int n = J.n;
-  const int lds = n + 1;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  for (int i = ty; i < n; i += LEAF_THREADS / 32)
-    for (int j = tx; j < n; j += 32) S[i * lds + j] = J.mat[static_cast<int64_t>(i) * J.ld + j];
-  __syncthreads();
-  bool failed = false;
-  for (int k = 0; k < n; ++k) {
-    for (int j = threadIdx.x; j < n; j += LEAF_THREADS) v[j] = S[k * lds + j];
-    __syncthreads();
-    const float p = v[k];
-    if (!(p > 0.0f) || !isfinite(p)) {  // uniform across the block
-      failed = true;
-      break;
+  const int ld = n + 1;
+  float* S = smem;           // A -> L (lower)
+  float* X = smem + n * ld;  // L^-1 (lower)
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  constexpr int RY = LEAF_THREADS / 32;
+  const float sh = (J.full && J.shift) ? *J.shift : 0.0f;
+  for (int i = ty; i < n; i += RY)
+    for (int j = tx; j < n; j += 32) {
+      float a = J.src[static_cast<int64_t>(i) * J.lds + j];
+      if (i == j) a += sh;
+      S[i * ld + j] = a;
+      X[i * ld + j] = (i == j) ? 1.0f : 0.0f;
     }
-    const float r = 1.0f / p;
-    for (int i = ty; i < n; i += LEAF_THREADS / 32) {
-      const float vi = v[i];
-      for (int j = tx; j < n; j += 32) {
-        float* s = &S[i * lds + j];
-        if (i == k) {
-          *s = (j == k) ? -r : v[j] * r;
-        } else if (j == k) {
-          *s = vi * r;
-        } else {
-          *s -= (vi * v[j]) * r;
-        }
-      }
+  __syncthreads();
+  // ---- Cholesky (lower), right-looking
+  for (int k = 0; k < n; ++k) {
+    const float p = S[k * ld + k];
+    if (!(p > 0.0f) || !isfinite(p)) {  // uniform: every thread read the same pivot
+      if (tid == 0 && J.info) *J.info = J.fail_code;
+      return;
+    }
+    const float l = sqrtf(p);
+    const float inv = 1.0f / l;
+    __syncthreads();
+    for (int i = k + tid; i < n; i += LEAF_THREADS) S[i * ld + k] = (i == k) ? l : S[i * ld + k] * inv;
+    __syncthreads();
+    for (int i = k + 1 + ty; i < n; i += RY) {
+      const float lik = S[i * ld + k];
+      for (int j = k + 1 + tx; j <= i; j += 32) S[i * ld + j] -= lik * S[j * ld + k];
     }
     __syncthreads();
   }
-  if (failed) {
-    if (threadIdx.x == 0 && J.info) *J.info = J.fail_code;
+  // ---- X = L^-1 (lower), right-looking forward substitution on I
+  for (int k = 0; k < n; ++k) {
+    const float d = 1.0f / S[k * ld + k];
+    for (int j = tid; j <= k; j += LEAF_THREADS) X[k * ld + j] *= d;
+    __syncthreads();
+    for (int i = k + 1 + ty; i < n; i += RY) {
+      const float lik = S[i * ld + k];
+      for (int j = tx; j <= k; j += 32) X[i * ld + j] -= lik * X[k * ld + j];
+    }
+    __syncthreads();
+  }
+  if (!J.full) {
+    for (int i = ty; i < n; i += RY)
+      for (int j = tx; j < n; j += 32) J.dst[static_cast<int64_t>(i) * J.ldd + j] = (j <= i) ? X[i * ld + j] : 0.0f;
     return;
   }
-  for (int i = ty; i < n; i += LEAF_THREADS / 32)
-    for (int j = tx; j < n; j += 32) J.mat[static_cast<int64_t>(i) * J.ld + j] = -S[i * lds + j];
+  // ---- inverse = X^T X, lower entries computed once and mirrored
+  for (int i = ty; i < n; i += RY)
+    for (int j = tx; j <= i; j += 32) {
+      float acc = 0.0f;
+      for (int k = i; k < n; ++k) acc += X[k * ld + i] * X[k * ld + j];
+      J.dst[static_cast<int64_t>(i) * J.ldd + j] = acc;
+      J.dst[static_cast<int64_t>(j) * J.ldd + i] = acc;
+    }
 }
 
-// dst = src + shift * I (copy, then the recursion works in place on dst)
+// Aw = src + shift I for the blocked path
 constexpr int PREP_MAX = 256;
+struct PrepJob {
+  const float* src;
+  float* dst;
+  const float* shift;
+  int64_t n;
+};
 struct PrepBatch {
   int n;
-  dpk_spd_job j[PREP_MAX];
+  PrepJob j[PREP_MAX];
 };
 __global__ void prep_kernel(const __grid_constant__ PrepBatch b) {
-  const dpk_spd_job& J = b.j[blockIdx.y];
-  const int64_t total = static_cast<int64_t>(J.n) * J.n;
+  const PrepJob& J = b.j[blockIdx.y];
+  const int64_t total = J.n * J.n;
   const float sh = J.shift ? *J.shift : 0.0f;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t i = e / J.n;
-    const int64_t c = e - i * J.n;
     float x = J.src[e];
-    if (i == c) x += sh;
+    if (i == e - i * J.n) x += sh;
     J.dst[e] = x;
   }
 }
@@ -115,18 +145,23 @@ struct Op {
 };
 
 int split_point(int n) {
-  int n1 = ((n / 2 + 63) / 64) * 64;
+  const int n1 = ((n / 2 + 63) / 64) * 64;
   return std::min(n1, n - 1);
 }
 
-size_t recursion_ws_floats(int n) {
+size_t t_floats(int n) {  // largest n2 x n1 scratch over the recursion
   if (n <= LEAF_N) return 0;
   const int n1 = split_point(n), n2 = n - n1;
-  return static_cast<size_t>(n1) * n2 + std::max(recursion_ws_floats(n1), recursion_ws_floats(n2));
+  return std::max<size_t>(static_cast<size_t>(n1) * n2, std::max(t_floats(n1), t_floats(n2)));
+}
+
+size_t matrix_ws_floats(int n) {
+  if (n <= LEAF_N) return 0;
+  return 2 * static_cast<size_t>(n) * n + t_floats(n);  // L21 blocks, X = L^-1, T
 }
 
 GemmSpec spec(const dpk_operand& a, const dpk_operand& b, float* out, int64_t ldo, float alpha, float beta,
-              int symmetric, float* out_t = nullptr, int64_t ldt = 0) {
+              int symmetric) {
   GemmSpec s{};
   s.job.a = a;
   s.job.b = b;
@@ -138,62 +173,77 @@ GemmSpec spec(const dpk_operand& a, const dpk_operand& b, float* out, int64_t ld
   s.job.beta = beta;
   s.job.symmetric = symmetric;
   s.epi = EPI_LINEAR;
-  s.out_t = out_t;
-  s.ldt = ldt;
   return s;
 }
 
-void build_ops(float* A, int64_t ld, int n, float* ws, int fail_code, int32_t* info, std::vector<Op>& ops) {
+// Aw, Lb, Xb share the row stride ld; T has room for n2 x n1 floats.
+void build_ops(float* Aw, float* Lb, float* Xb, int64_t ld, int n, float* T, int fail_code, int32_t* info,
+               std::vector<Op>& ops) {
   if (n <= LEAF_N) {
     Op op{};
     op.leaf = true;
-    op.lj = LeafJob{A, ld, n, fail_code, info};
+    op.lj = LeafJob{Aw, Xb, nullptr, ld, ld, n, 0, fail_code, 0, info};
     ops.push_back(op);
     return;
   }
   const int n1 = split_point(n), n2 = n - n1;
-  float* A11 = A;
-  float* A12 = A + n1;
-  float* A21 = A + static_cast<int64_t>(n1) * ld;
-  float* A22 = A21 + n1;
-  float* Z = ws;  // n1 x n2
-  float* child = ws + static_cast<size_t>(n1) * n2;
-  build_ops(A11, ld, n1, child, fail_code, info, ops);
+  const int64_t o21 = static_cast<int64_t>(n1) * ld, o22 = o21 + n1;
+  build_ops(Aw, Lb, Xb, ld, n1, T, fail_code, info, ops);
   Op op{};
   op.leaf = false;
-  // Z = X11 A12
-  op.g = spec(rows_k(A11, n1, n1, ld), rows_mn(A12, n2, n1, ld), Z, n2, 1.0f, 0.0f, 0);
+  // L21 = A21 X11^T
+  op.g = spec(rows_k(Aw + o21, n2, n1, ld), rows_k(Xb, n1, n1, ld), Lb + o21, ld, 1.0f, 0.0f, 0);
   ops.push_back(op);
-  // A22 <- A22 - A21 Z   (Schur complement, symmetric)
-  op.g = spec(rows_k(A21, n2, n1, ld), rows_mn(Z, n2, n1, n2), A22, ld, -1.0f, 1.0f, 1);
+  // A22 <- A22 - L21 L21^T
+  op.g = spec(rows_k(Lb + o21, n2, n1, ld), rows_k(Lb + o21, n2, n1, ld), Aw + o22, ld, -1.0f, 1.0f, 1);
   ops.push_back(op);
-  build_ops(A22, ld, n2, child, fail_code, info, ops);
-  // X12 = -Z X22 ; X21 = X12^T
-  op.g = spec(rows_k(Z, n1, n2, n2), rows_k(A22, n2, n2, ld), A12, ld, -1.0f, 0.0f, 0, A21, ld);
+  build_ops(Aw + o22, Lb + o22, Xb + o22, ld, n2, T, fail_code, info, ops);
+  // T = L21 X11
+  op.g = spec(rows_k(Lb + o21, n2, n1, ld), rows_mn(Xb, n1, n1, ld), T, n1, 1.0f, 0.0f, 0);
   ops.push_back(op);
-  // X11 <- X11 - X12 Z^T  (= X11 + Z X22 Z^T, symmetric)
-  op.g = spec(rows_k(A12, n1, n2, ld), rows_k(Z, n1, n2, n2), A11, ld, -1.0f, 1.0f, 1);
+  // X21 = -X22 T
+  op.g = spec(rows_k(Xb + o22, n2, n2, ld), rows_mn(T, n1, n2, n1), Xb + o21, ld, -1.0f, 0.0f, 0);
   ops.push_back(op);
 }
 
 struct SpdPlan {
   std::vector<std::vector<Op>> lists;
+  std::vector<PrepJob> preps;
+  std::vector<float*> zero_x;
+  std::vector<size_t> zero_bytes;
   size_t rec_bytes = 0;
   size_t gemm_bytes = 0;
 };
 
-// float* base == nullptr: dry run for sizing (pointers are fake but sizes exact)
 void make_spd_plan(const dpk_spd_job* jobs, int n, char* base, SpdPlan& plan) {
   plan.lists.assign(n, {});
+  char* b = base ? base : reinterpret_cast<char*>(0x100000);
   size_t off = 0;
   for (int i = 0; i < n; ++i) {
-    const size_t fl = recursion_ws_floats(jobs[i].n);
-    float* ws = reinterpret_cast<float*>((base ? base : reinterpret_cast<char*>(0x100000)) + off);
-    build_ops(jobs[i].dst, jobs[i].n, jobs[i].n, ws, jobs[i].fail_code, jobs[i].info, plan.lists[i]);
-    off += align_up(fl * sizeof(float), 256);
+    const int m = jobs[i].n;
+    std::vector<Op>& ops = plan.lists[i];
+    if (m <= LEAF_N) {
+      Op op{};
+      op.leaf = true;
+      op.lj = LeafJob{jobs[i].src, jobs[i].dst, jobs[i].shift, m, m, m, 1, jobs[i].fail_code, 0, jobs[i].info};
+      ops.push_back(op);
+      continue;
+    }
+    float* Lb = reinterpret_cast<float*>(b + off);
+    float* Xb = Lb + static_cast<size_t>(m) * m;
+    float* T = Xb + static_cast<size_t>(m) * m;
+    off += align_up(matrix_ws_floats(m) * sizeof(float), 256);
+    plan.preps.push_back(PrepJob{jobs[i].src, jobs[i].dst, jobs[i].shift, m});
+    plan.zero_x.push_back(Xb);
+    plan.zero_bytes.push_back(static_cast<size_t>(m) * m * sizeof(float));
+    build_ops(jobs[i].dst, Lb, Xb, m, m, T, jobs[i].fail_code, jobs[i].info, ops);
+    Op op{};
+    op.leaf = false;
+    // dst = X^T X  (X lower triangular; symmetric output)
+    op.g = spec(rows_mn(Xb, m, m, m), rows_mn(Xb, m, m, m), jobs[i].dst, m, 1.0f, 0.0f, 1);
+    ops.push_back(op);
   }
   plan.rec_bytes = off;
-  // largest GEMM round
   std::vector<size_t> idx(n, 0);
   size_t worst = 0;
   for (;;) {
@@ -214,9 +264,9 @@ void make_spd_plan(const dpk_spd_job* jobs, int n, char* base, SpdPlan& plan) {
 
 int launch_leaves(std::vector<LeafJob>& leaves, cudaStream_t st) {
   static bool configured = false;
-  const int smem = LEAF_N * (LEAF_N + 1) * 4;
+  const int max_smem = 2 * LEAF_N * (LEAF_N + 1) * 4;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(spd_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(spd_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(spd_leaf_kernel)");
     configured = true;
   }
@@ -229,7 +279,7 @@ int launch_leaves(std::vector<LeafJob>& leaves, cudaStream_t st) {
       b.j[i] = leaves[first + i];
       maxn = std::max(maxn, b.j[i].n);
     }
-    spd_leaf_kernel<<<cnt, LEAF_THREADS, maxn * (maxn + 1) * 4, st>>>(b);
+    spd_leaf_kernel<<<cnt, LEAF_THREADS, 2 * maxn * (maxn + 1) * 4, st>>>(b);
     note_launch();
     int rc = cuda_status(cudaGetLastError(), "spd_leaf_kernel launch");
     if (rc) return rc;
@@ -268,15 +318,19 @@ int dpk_chol_inv_damped_batched(const dpk_spd_job* jobs, int n_jobs, void* works
     dpk::set_error("dpk_chol_inv_damped_batched: workspace too small");
     return DPK_ENOSPACE;
   }
-  // dst = src + shift I
+  dpk::SpdPlan plan;
+  char* base = static_cast<char*>(workspace);
+  dpk::make_spd_plan(jobs, n_jobs, base, plan);
+  char* gemm_ws = base + dpk::align_up(plan.rec_bytes, 1024);
+  // blocked path set-up: working copy with the damping, X = 0
   thread_local dpk::PrepBatch pb;
-  for (int first = 0; first < n_jobs; first += dpk::PREP_MAX) {
-    const int cnt = std::min(dpk::PREP_MAX, n_jobs - first);
+  for (size_t first = 0; first < plan.preps.size(); first += dpk::PREP_MAX) {
+    const int cnt = static_cast<int>(std::min<size_t>(dpk::PREP_MAX, plan.preps.size() - first));
     pb.n = cnt;
     int64_t maxe = 0;
     for (int i = 0; i < cnt; ++i) {
-      pb.j[i] = jobs[first + i];
-      maxe = std::max<int64_t>(maxe, static_cast<int64_t>(pb.j[i].n) * pb.j[i].n);
+      pb.j[i] = plan.preps[first + i];
+      maxe = std::max<int64_t>(maxe, pb.j[i].n * pb.j[i].n);
     }
     const int gx = static_cast<int>(std::min<int64_t>((maxe + 255) / 256, 2048));
     dpk::prep_kernel<<<dim3(gx, cnt), 256, 0, st>>>(pb);
@@ -284,10 +338,10 @@ int dpk_chol_inv_damped_batched(const dpk_spd_job* jobs, int n_jobs, void* works
     int rc = dpk::cuda_status(cudaGetLastError(), "prep_kernel launch");
     if (rc) return rc;
   }
-  dpk::SpdPlan plan;
-  char* base = static_cast<char*>(workspace);
-  dpk::make_spd_plan(jobs, n_jobs, base, plan);
-  char* gemm_ws = base + dpk::align_up(plan.rec_bytes, 1024);
+  for (size_t i = 0; i < plan.zero_x.size(); ++i) {
+    int rc = dpk::cuda_status(cudaMemsetAsync(plan.zero_x[i], 0, plan.zero_bytes[i], st), "cudaMemsetAsync");
+    if (rc) return rc;
+  }
   std::vector<size_t> idx(n_jobs, 0);
   for (;;) {
     std::vector<dpk::LeafJob> leaves;

@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(JAC_THREADS) jacobi_kernel(const __grid_consta
   __shared__ float dp_new[JAC_N / 2 + 1], dq_new[JAC_N / 2 + 1];
   __shared__ int pp[JAC_N / 2 + 1], qq[JAC_N / 2 + 1];
   __shared__ int rot_count;
+  __shared__ float fro2;
   __shared__ int rank_of[JAC_N];
   const dpk_eig_job& J = b.j[blockIdx.x];
   const int n = J.n;
@@ -60,7 +61,20 @@ __global__ void __launch_bounds__(JAC_THREADS) jacobi_kernel(const __grid_consta
     A[i * ld + c] = a;
     V[i * ld + c] = (i == c) ? 1.0f : 0.0f;
   }
+  if (threadIdx.x == 0) fro2 = 0.0f;
   __syncthreads();
+  {
+    float acc = 0.0f;
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+      const float a = A[(e / m) * ld + (e % m)];
+      acc += a * a;
+    }
+    atomicAdd(&fro2, acc);
+  }
+  __syncthreads();
+  // off-diagonal entries below ~eps*||A||_F are rounding noise of the other
+  // rotations; rotating them only re-injects noise (and never terminates)
+  const float abs_tol = 3e-8f * sqrtf(fro2);
   const int half = m / 2;
   for (int sweep = 0; sweep < MAX_SWEEPS && m > 1; ++sweep) {
     if (threadIdx.x == 0) rot_count = 0;
@@ -75,7 +89,7 @@ __global__ void __launch_bounds__(JAC_THREADS) jacobi_kernel(const __grid_consta
         const float apq = A[p * ld + q];
         const float app = A[p * ld + p], aqq = A[q * ld + q];
         float c = 1.f, si = 0.f;
-        if (fabsf(apq) > 2e-7f * sqrtf(fabsf(app * aqq)) && fabsf(apq) > 1e-36f) {
+        if (fabsf(apq) > 2e-7f * sqrtf(fabsf(app * aqq)) && fabsf(apq) > abs_tol && fabsf(apq) > 1e-36f) {
           // IEEE-rounded sqrt / division: c^2 + s^2 = 1 to 1/2 ulp with no bias
           // (rsqrtf's bias compounds over thousands of rotations into a visible
           // shrink of the spectrum)
