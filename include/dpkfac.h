@@ -21,8 +21,10 @@
  *     eigen denominator, non-finite values) are reported asynchronously through
  *     caller-provided device int32 "info" words: 0 = fine, >0 = failure code.
  *   - Precision: DPK_PREC_TF32 runs one tcgen05 kind::tf32 pass on
- *     round-to-nearest TF32 operands; DPK_PREC_3XTF32 splits every operand into
- *     hi + lo TF32 parts and accumulates hi*hi + hi*lo + lo*hi (fp32-grade).
+ *     round-to-nearest TF32 operands; DPK_PREC_TF32_TRUNC feeds the raw fp32
+ *     bits (the tensor core truncates to TF32, no conversion pass);
+ *     DPK_PREC_3XTF32 splits every operand into hi + lo TF32 parts and
+ *     accumulates hi*hi + hi*lo + lo*hi (fp32-grade).
  */
 #ifndef DPKFAC_H_
 #define DPKFAC_H_
@@ -44,7 +46,7 @@ enum {
   DPK_ENOSPACE = 4  /* workspace too small */
 };
 
-enum { DPK_PREC_TF32 = 1, DPK_PREC_3XTF32 = 3 };
+enum { DPK_PREC_TF32 = 1, DPK_PREC_TF32_TRUNC = 2, DPK_PREC_3XTF32 = 3 };
 
 /* info codes written to device info words */
 enum {
@@ -149,10 +151,12 @@ int dpk_trace_pi(const dpk_pi_job* jobs, int n_jobs, float gamma, dpk_stream_t s
 /* ------------------------------------------------------------------------
  * K3: batched damped SPD inverse  dst = (src + shift*I)^-1, symmetrized
  * (numerics.sym_inverse numerics.py:100-114 via kfac.damped_inverses
- * kfac.py:140-155).  Cholesky-based: n <= 128 runs one shared-memory CTA per
- * matrix (potrf + trtri + lauum); larger n run a blocked symmetric sweep whose
- * rank-64 updates are tcgen05 3xTF32 GEMMs.  On a non-positive pivot *info is
- * set to fail_code and dst is left undefined.  src and dst may not alias.
+ * kfac.py:140-155).  Same method as the reference (Cholesky factor, inverse from
+ * the factor): n <= 128 runs one shared-memory CTA per matrix (potrf, trtri,
+ * L^-T L^-1); larger n recurse on 2x2 blocks whose off-diagonal work (TRSM via
+ * the triangular inverse, Schur update, inverse assembly) runs as tcgen05
+ * 3xTF32 GEMMs.  On a non-positive pivot *info is set to fail_code and dst is
+ * left undefined.  src and dst may not alias.
  * ------------------------------------------------------------------------ */
 typedef struct dpk_spd_job {
   const float* src;

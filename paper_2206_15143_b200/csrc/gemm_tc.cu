@@ -5,25 +5,30 @@
 //
 // One persistent launch serves a whole group of problems (e.g. all Kronecker
 // factors of all owned layers).  Work units are (problem, 128x128 output tile,
-// K split).  Warp roles per CTA (416 threads, one CTA per SM):
+// K split).  Warp roles per CTA (12 warps, one CTA per SM):
 //   warps 0-3  epilogue: tcgen05.ld the TMEM accumulator (lane = tile row),
 //              apply alpha/beta (the fused running average) or the eigen
 //              divide, store, mirror lower tiles for symmetric outputs, and
 //              run the deterministic split-K fix-up (last split sums partials);
 //   warp 4     TMEM allocator + single-thread tcgen05.mma issuer;
-//   warps 5-12 producers: gather operand tiles straight from the torch
-//              tensors (row-major, column-major or implicit im2col of an
-//              NCHW conv input -- patches never touch HBM), round to TF32 (or
-//              split hi/lo for 3xTF32) and store them in the canonical
-//              K-major 128B-swizzled shared-memory layout the MMA reads.
-// Pipelines: smem stages full/empty (producers <-> MMA), two TMEM
-// accumulators full/empty (MMA <-> epilogue) so tile i's epilogue overlaps
-// tile i+1's MMAs.
+//   warp 5     TMA issuer: operands that TMA can address (row-major K-major,
+//              column-major MN-major, NCHW 1x1 "slab" captures as a 3-D map)
+//              are fetched with cp.async.bulk.tensor into 128B-swizzled
+//              stages, running ahead through the whole stage ring;
+//   warps 6-11 gather / convert: round TMA-landed tiles to TF32 in place (RN
+//              mode) or derive the 3xTF32 low parts; everything else -- implicit im2col
+//              of NCHW conv inputs (patches never touch HBM), bias rows,
+//              unaligned views -- is gathered by the warps with a one-chunk
+//              software pipeline and stored in the same canonical K-major
+//              SW128 layout.
+// Pipelines: smem stages (full / tma / empty barriers), two TMEM accumulators
+// full/empty (MMA <-> epilogue) so tile i's epilogue overlaps tile i+1's MMAs.
 //
 // Reference semantics reproduced (kfaclab 0.1.0): compute_factors
 // kfac.py:85-104 (symmetric A = X X^T / M), update_running_average
 // kfac.py:107-125 (alpha/beta epilogue), precondition_inverse / _eigen
 // kfac.py:165-191 (plain and eigen-divide epilogues).
+#include <cuda.h>  // CUtensorMap / enums only; the encoder is fetched through the runtime
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -43,14 +48,22 @@ constexpr int BK = 32;                       // fp32 elements per row of a stage
 constexpr int TILE_BYTES = BM * BK * 4;      // 16 KB
 constexpr int EPI_WARPS = 4;                 // warps 0..3 (one per TMEM lane quadrant)
 constexpr int MMA_WARP = 4;
-constexpr int PROD_WARP0 = 5;
-constexpr int PROD_WARPS = 8;
-constexpr int NPROD = PROD_WARPS * 32;
-constexpr int NTHREADS = (PROD_WARP0 + PROD_WARPS) * 32;  // 416
+constexpr int TMA_WARP = 5;                               // one elected thread issues all TMA loads
+constexpr int PROD_WARP0 = 6;
+constexpr int PROD_WARPS = 6;                             // 12 warps total -> up to 168 regs/thread
+constexpr int NPROD = PROD_WARPS * 32;                    // 192 gather / convert threads
+constexpr int TILE_TASKS = BM * (BK / 4);                 // (row, 16B chunk) tasks per operand tile
+constexpr int NTASK = (TILE_TASKS + NPROD - 1) / NPROD;   // 5 tasks per producer thread
+constexpr int NTHREADS = (PROD_WARP0 + PROD_WARPS) * 32;  // 384
 constexpr uint32_t TMEM_COLS = 2 * BN;                    // two accumulators
-constexpr int MAXP = 40;                                  // problems per launch (kernel params)
+constexpr int MAXP = 32;                                  // problems per launch (kernel params)
+static_assert(NPROD % 8 == 0, "im2col chunk sharing needs NPROD % 8 == 0");
 
-struct Problem {
+enum { TMA_NONE = 0, TMA_ROWS_K = 1, TMA_ROWS_MN = 2, TMA_SLAB = 3 };
+
+struct alignas(64) Problem {
+  CUtensorMap tmap_a;  // valid iff tma_a != TMA_NONE
+  CUtensorMap tmap_b;
   dpk_operand a;
   dpk_operand b;
   float* out;
@@ -69,6 +82,8 @@ struct Problem {
   int tiles_n, ntiles, splits;
   int chunks, cps;  // K chunks of 32, chunks per split
   int unit_begin;
+  int tma_a, tma_b;
+  int slab_cpn;     // TMA_SLAB: chunks per sample (K index = (sample, 32-pixel chunk))
 };
 
 struct Batch {
@@ -79,10 +94,10 @@ struct Batch {
 
 template <int NPASS>
 struct Cfg {
-  static constexpr int STAGES = NPASS == 1 ? 4 : 3;
+  static constexpr int STAGES = NPASS == 1 ? 6 : 3;
   static constexpr int OPS = NPASS == 1 ? 2 : 4;  // A, B (+ A_lo, B_lo)
   static constexpr int STAGE_BYTES = OPS * TILE_BYTES;
-  static constexpr int BAR_BYTES = 8 * (2 * STAGES + 4) + 16;
+  static constexpr int BAR_BYTES = 8 * (3 * STAGES + 4) + 16;
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + BAR_BYTES;
 };
 
@@ -107,38 +122,45 @@ __device__ __forceinline__ void decode_unit(const Batch& bt, int u, int& pi, int
   pi = p;
 }
 
-// ------------------------------------------------------------------ producer
+// ------------------------------------------------------------------ manual producer
 // A row task: one (row, 16-byte chunk) of a 128 x 32 stage tile.
 struct RowTask {
   int64_t off;  // element offset of the row inside the operand
-  int ih, iw;   // im2col filter offsets (i*dh, j*dw)
-  int flag;     // 0 zero row, 1 data row, 2 ones (bias) row
+  int packed;   // bits 0-1 flag (0 zero row, 1 data row, 2 ones/bias row),
+                // bits 2-16 im2col column offset j*dw, bits 17-31 row offset i*dh
+  __device__ __forceinline__ int flag() const { return packed & 3; }
+  __device__ __forceinline__ int iw() const { return (packed >> 2) & 0x7FFF; }
+  __device__ __forceinline__ int ih() const { return packed >> 17; }
 };
 
 __device__ __forceinline__ bool kfast(const dpk_operand& o) { return o.kind != DPK_OPND_ROWS_MN; }
 
-__device__ __forceinline__ void task_row_chunk(bool kf, int ptid, int j, int& row, int& chunk) {
+// task q = ptid + NPROD*j (q < TILE_TASKS).  k-fast: 8 lanes cover one 128 B row
+// segment; row-fast: consecutive lanes take consecutive rows (column-major sources).
+__device__ __forceinline__ bool task_row_chunk(bool kf, int ptid, int j, int& row, int& chunk) {
+  const int q = ptid + NPROD * j;
   if (kf) {
-    row = (ptid >> 3) + 32 * j;
-    chunk = ptid & 7;
+    row = q >> 3;
+    chunk = q & 7;
   } else {
-    row = ptid & 127;
-    chunk = (ptid >> 7) + 2 * j;
+    row = q & (BM - 1);
+    chunk = q >> 7;
   }
+  return q < TILE_TASKS;
 }
 
-__device__ __forceinline__ void setup_tasks(const dpk_operand& o, int row0, int ptid, RowTask (&t)[4]) {
+__device__ __forceinline__ void setup_tasks(const dpk_operand& o, int row0, int ptid, RowTask (&t)[NTASK]) {
   const bool kf = kfast(o);
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
+  for (int j = 0; j < NTASK; ++j) {
     int row, chunk;
-    task_row_chunk(kf, ptid, j, row, chunk);
+    const bool valid = task_row_chunk(kf, ptid, j, row, chunk);
     const int r = row0 + row;
     t[j].off = 0;
-    t[j].ih = 0;
-    t[j].iw = 0;
+    t[j].packed = 0;
+    if (!valid) continue;
     if (r < o.rows) {
-      t[j].flag = 1;
+      t[j].packed = 1;
       if (o.kind == DPK_OPND_ROWS_K) {
         t[j].off = static_cast<int64_t>(r) * o.ld;
       } else if (o.kind == DPK_OPND_ROWS_MN) {
@@ -149,23 +171,23 @@ __device__ __forceinline__ void setup_tasks(const dpk_operand& o, int row0, int 
         const int rem = r - c * kk;
         const int i = rem / o.kw;
         const int jj = rem - i * o.kw;
-        t[j].ih = i * o.dh;
-        t[j].iw = jj * o.dw;
-        t[j].off = static_cast<int64_t>(c) * o.sc + static_cast<int64_t>(t[j].ih) * o.shs +
-                   static_cast<int64_t>(t[j].iw) * o.sws;
+        const int ihd = i * o.dh, iwd = jj * o.dw;
+        t[j].packed = 1 | (iwd << 2) | (ihd << 17);
+        t[j].off = static_cast<int64_t>(c) * o.sc + static_cast<int64_t>(ihd) * o.shs +
+                   static_cast<int64_t>(iwd) * o.sws;
       }
     } else {
-      t[j].flag = (o.bias_row && r == o.rows) ? 2 : 0;
+      t[j].packed = (o.bias_row && r == o.rows) ? 2 : 0;
     }
   }
 }
 
-// Gather 4 operand tiles' worth of values for this thread and k-chunk kc.
-__device__ __forceinline__ void fetch_tasks(const dpk_operand& o, const RowTask (&t)[4], int ptid, int64_t k_base,
-                                            float4 (&v)[4]) {
+// Gather this thread's tasks of one operand for the k-chunk starting at k_base.
+__device__ __forceinline__ void fetch_tasks(const dpk_operand& o, const RowTask (&t)[NTASK], int ptid, int64_t k_base,
+                                            float4 (&v)[NTASK]) {
   const bool kf = kfast(o);
   if (o.kind == DPK_OPND_IM2COL) {
-    // all 4 tasks share the same chunk -> decompose its 4 sample columns once
+    // all tasks of this thread share one chunk (NPROD % 8 == 0) -> decompose its 4 sample columns once
     const int64_t k0 = k_base + 4 * (ptid & 7);
     const int ohw = o.OH * o.OW;
     int64_t kb[4];
@@ -192,18 +214,18 @@ __device__ __forceinline__ void fetch_tasks(const dpk_operand& o, const RowTask 
       }
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < NTASK; ++j) {
       float x[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         float val = 0.0f;
-        if (t[j].flag == 1) {
-          const int ih = ih0[e] + t[j].ih;
-          const int iw = iw0[e] + t[j].iw;
+        if (t[j].flag() == 1) {
+          const int ih = ih0[e] + t[j].ih();
+          const int iw = iw0[e] + t[j].iw();
           if (kv[e] && static_cast<unsigned>(ih) < static_cast<unsigned>(o.H) &&
               static_cast<unsigned>(iw) < static_cast<unsigned>(o.W))
             val = __ldg(o.data + kb[e] + t[j].off);
-        } else if (t[j].flag == 2) {
+        } else if (t[j].flag() == 2) {
           val = kv[e] ? 1.0f : 0.0f;
         }
         x[e] = val;
@@ -213,12 +235,12 @@ __device__ __forceinline__ void fetch_tasks(const dpk_operand& o, const RowTask 
     return;
   }
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
+  for (int j = 0; j < NTASK; ++j) {
     int row, chunk;
-    task_row_chunk(kf, ptid, j, row, chunk);
+    task_row_chunk(kf, ptid, j, row, chunk);  // invalid tasks carry flag 0 -> zeros
     const int64_t k0 = k_base + 4 * chunk;
     float x[4] = {0.f, 0.f, 0.f, 0.f};
-    if (t[j].flag == 1) {
+    if (t[j].flag() == 1) {
       if (o.kind == DPK_OPND_ROWS_K) {
         const float* p = o.data + t[j].off + k0;
         if (k0 + 3 < o.cols && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
@@ -237,7 +259,7 @@ __device__ __forceinline__ void fetch_tasks(const dpk_operand& o, const RowTask 
         for (int e = 0; e < 4; ++e)
           if (k0 + e < o.cols) x[e] = __ldg(o.data + (k0 + e) * o.ld + t[j].off);
       }
-    } else if (t[j].flag == 2) {
+    } else if (t[j].flag() == 2) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) x[e] = (k0 + e < o.cols) ? 1.0f : 0.0f;
     }
@@ -250,24 +272,62 @@ __device__ __forceinline__ uint32_t sw128_offset(int row, int chunk) {
   return static_cast<uint32_t>((row >> 3) * 1024 + (row & 7) * 128 + ((chunk ^ (row & 7)) << 4));
 }
 
-template <int NPASS>
+__device__ __forceinline__ uint32_t tf32_trunc_bits(float x) { return __float_as_uint(x) & 0xFFFFE000u; }
+
+template <int NPASS, bool RN>
 __device__ __forceinline__ void store_tasks(const dpk_operand& o, int ptid, uint8_t* tile, uint8_t* tile_lo,
-                                            const float4 (&v)[4]) {
+                                            const float4 (&v)[NTASK]) {
   const bool kf = kfast(o);
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
+  for (int j = 0; j < NTASK; ++j) {
     int row, chunk;
-    task_row_chunk(kf, ptid, j, row, chunk);
+    if (!task_row_chunk(kf, ptid, j, row, chunk)) continue;
     const uint32_t off = sw128_offset(row, chunk);
     const float x[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
     uint32_t hi[4], lo[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      hi[e] = to_tf32(x[e]);
-      if (NPASS == 3) lo[e] = to_tf32(x[e] - __uint_as_float(hi[e]));
+      if (NPASS == 3) {  // hi = what the tensor core reads (truncation), lo = exact remainder
+        hi[e] = __float_as_uint(x[e]);
+        lo[e] = __float_as_uint(x[e] - __uint_as_float(tf32_trunc_bits(x[e])));
+      } else {
+        hi[e] = RN ? to_tf32(x[e]) : __float_as_uint(x[e]);
+      }
     }
     *reinterpret_cast<uint4*>(tile + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
     if (NPASS == 3) *reinterpret_cast<uint4*>(tile_lo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+  }
+}
+
+// In-place pass over a TMA-filled tile (layout-agnostic, elementwise).
+template <int NPASS>
+__device__ __forceinline__ void convert_tile(uint8_t* tile, uint8_t* tile_lo, int ptid) {
+  uint4* t = reinterpret_cast<uint4*>(tile);
+  uint4* l = reinterpret_cast<uint4*>(tile_lo);
+  for (int i = ptid; i < TILE_BYTES / 16; i += NPROD) {
+    const uint4 v = t[i];
+    const float x[4] = {__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z), __uint_as_float(v.w)};
+    uint32_t r[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      r[e] = (NPASS == 3) ? __float_as_uint(x[e] - __uint_as_float(tf32_trunc_bits(x[e]))) : to_tf32(x[e]);
+    if (NPASS == 3)
+      l[i] = make_uint4(r[0], r[1], r[2], r[3]);
+    else
+      t[i] = make_uint4(r[0], r[1], r[2], r[3]);
+  }
+}
+
+__device__ __forceinline__ void issue_tma(int kind, const CUtensorMap* map, uint32_t dst, uint32_t bar, int row0, int kc,
+                                          int cpn) {
+  if (kind == TMA_ROWS_K) {
+    tma_load_2d(dst, map, bar, kc * BK, row0);
+  } else if (kind == TMA_ROWS_MN) {
+#pragma unroll
+    for (int b = 0; b < BM / 32; ++b) tma_load_2d(dst + b * 4096, map, bar, row0 + 32 * b, kc * BK);
+  } else {  // TMA_SLAB: dims {HW, C, N}
+    const int n = kc / cpn;
+    tma_load_3d(dst, map, bar, (kc - n * cpn) * BK, row0, n);
   }
 }
 
@@ -279,10 +339,11 @@ __device__ __forceinline__ void store_final(const Problem& P, int tm, int tn, in
   const int gn0 = tn * BN + c * 32;
   float vr = 0.f;
   if (P.epi == EPI_EIGDIV) vr = fmaxf(P.vrow[gm], 0.0f);
-#pragma unroll 4
+  const int jmax = min(32, min(P.N, diag ? gm + 1 : P.N) - gn0);  // columns to write
+#pragma unroll
   for (int j = 0; j < 32; ++j) {
     const int gn = gn0 + j;
-    if (gn >= P.N || (diag && gn > gm)) break;
+    if (j >= jmax) continue;  // predicated, keeps acc[] in registers
     float val = P.alpha * acc[j];
     if (P.epi == EPI_EIGDIV) {
       val = val / (vr * fmaxf(P.vcol[gn], 0.0f) + P.gamma);
@@ -295,9 +356,12 @@ __device__ __forceinline__ void store_final(const Problem& P, int tm, int tn, in
   }
 }
 
-template <int NPASS>
+template <int NPASS, bool RN>
 __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_constant__ Batch bt) {
   using C = Cfg<NPASS>;
+  // TMA'd tiles need a pass before the MMA only for the 3xTF32 low parts: in RN
+  // mode the tensor map's TFLOAT32 data type rounds during the copy itself.
+  constexpr bool CONVERT = (NPASS == 3);
   extern __shared__ uint8_t smem_raw[];
   __shared__ int s_last;
   const uint32_t raw = smem_u32(smem_raw);
@@ -306,9 +370,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   const uint32_t bars = base + C::STAGES * C::STAGE_BYTES;
   auto full_bar = [&](int s) { return bars + 8u * s; };
   auto empty_bar = [&](int s) { return bars + 8u * (C::STAGES + s); };
-  auto tfull_bar = [&](int a) { return bars + 8u * (2 * C::STAGES + a); };
-  auto tempty_bar = [&](int a) { return bars + 8u * (2 * C::STAGES + 2 + a); };
-  const uint32_t tmem_slot = bars + 8u * (2 * C::STAGES + 4);
+  auto tma_bar = [&](int s) { return bars + 8u * (2 * C::STAGES + s); };
+  auto tfull_bar = [&](int a) { return bars + 8u * (3 * C::STAGES + a); };
+  auto tempty_bar = [&](int a) { return bars + 8u * (3 * C::STAGES + 2 + a); };
+  const uint32_t tmem_slot = bars + 8u * (3 * C::STAGES + 4);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -317,6 +382,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(full_bar(s), PROD_WARPS);
       mbar_init(empty_bar(s), 1);
+      mbar_init(tma_bar(s), 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
@@ -330,8 +396,38 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   tc_fence_after();
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(gbase + (tmem_slot - base));
 
-  if (warp >= PROD_WARP0) {
-    // =============================== producers
+  if (warp == TMA_WARP) {
+    // =============================== TMA issuer: runs ahead through the stage ring
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < bt.total_units; u += gridDim.x) {
+        int pi, tm, tn, tile, split;
+        decode_unit(bt, u, pi, tm, tn, tile, split);
+        const Problem& P = bt.p[pi];
+        const bool skip_b = P.same_ab && tm == tn;
+        const bool tA = P.tma_a != TMA_NONE;
+        const bool tB = !skip_b && P.tma_b != TMA_NONE;
+        if (tA) tma_prefetch_desc(&P.tmap_a);
+        if (tB) tma_prefetch_desc(&P.tmap_b);
+        const int kc0 = split * P.cps;
+        const int kc1 = min(P.chunks, kc0 + P.cps);
+        for (int kc = kc0; kc < kc1; ++kc) {
+          mbar_wait(empty_bar(stage), phase ^ 1);
+          const uint32_t sst = base + stage * C::STAGE_BYTES;
+          // exactly one arrival per stage use; tx bytes only for TMA'd tiles
+          mbar_arrive_expect_tx(tma_bar(stage), (tA ? TILE_BYTES : 0) + (tB ? TILE_BYTES : 0));
+          if (tA) issue_tma(P.tma_a, &P.tmap_a, sst, tma_bar(stage), tm * BM, kc, P.slab_cpn);
+          if (tB) issue_tma(P.tma_b, &P.tmap_b, sst + TILE_BYTES, tma_bar(stage), tn * BN, kc, P.slab_cpn);
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp >= PROD_WARP0) {
+    // =============================== gather / convert warps
     const int ptid = threadIdx.x - PROD_WARP0 * 32;
     int stage = 0;
     uint32_t phase = 0;
@@ -340,20 +436,34 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
       decode_unit(bt, u, pi, tm, tn, tile, split);
       const Problem& P = bt.p[pi];
       const bool skip_b = P.same_ab && tm == tn;
-      RowTask ta[4], tb[4];
-      setup_tasks(P.a, tm * BM, ptid, ta);
-      if (!skip_b) setup_tasks(P.b, tn * BN, ptid, tb);
+      const bool tA = P.tma_a != TMA_NONE;
+      const bool tB = !skip_b && P.tma_b != TMA_NONE;
+      const bool mA = !tA;
+      const bool mB = !skip_b && !tB;
+      RowTask ta[NTASK], tb[NTASK];
+      if (mA) setup_tasks(P.a, tm * BM, ptid, ta);
+      if (mB) setup_tasks(P.b, tn * BN, ptid, tb);
       const int kc0 = split * P.cps;
       const int kc1 = min(P.chunks, kc0 + P.cps);
+      // manual operands: chunk kc+1's gathers are in flight while chunk kc is stored
+      float4 va[NTASK], vb[NTASK], na[NTASK], nb[NTASK];
+      if (mA) fetch_tasks(P.a, ta, ptid, static_cast<int64_t>(kc0) * BK, va);
+      if (mB) fetch_tasks(P.b, tb, ptid, static_cast<int64_t>(kc0) * BK, vb);
       for (int kc = kc0; kc < kc1; ++kc) {
-        float4 va[4], vb[4];
-        const int64_t kbase = static_cast<int64_t>(kc) * BK;
-        fetch_tasks(P.a, ta, ptid, kbase, va);
-        if (!skip_b) fetch_tasks(P.b, tb, ptid, kbase, vb);
+        if (kc + 1 < kc1) {
+          const int64_t knext = static_cast<int64_t>(kc + 1) * BK;
+          if (mA) fetch_tasks(P.a, ta, ptid, knext, na);
+          if (mB) fetch_tasks(P.b, tb, ptid, knext, nb);
+        }
         mbar_wait(empty_bar(stage), phase ^ 1);
         uint8_t* st = gbase + stage * C::STAGE_BYTES;
-        store_tasks<NPASS>(P.a, ptid, st, st + 2 * TILE_BYTES, va);
-        if (!skip_b) store_tasks<NPASS>(P.b, ptid, st + TILE_BYTES, st + 3 * TILE_BYTES, vb);
+        if (mA) store_tasks<NPASS, RN>(P.a, ptid, st, st + 2 * TILE_BYTES, va);
+        if (mB) store_tasks<NPASS, RN>(P.b, ptid, st + TILE_BYTES, st + 3 * TILE_BYTES, vb);
+        if (CONVERT && (tA || tB)) {
+          mbar_wait(tma_bar(stage), phase);
+          if (tA) convert_tile<NPASS>(st, st + 2 * TILE_BYTES, ptid);
+          if (tB) convert_tile<NPASS>(st + TILE_BYTES, st + 3 * TILE_BYTES, ptid);
+        }
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(full_bar(stage));
@@ -361,12 +471,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
           stage = 0;
           phase ^= 1;
         }
+#pragma unroll
+        for (int j = 0; j < NTASK; ++j) {
+          va[j] = na[j];
+          vb[j] = nb[j];
+        }
       }
     }
   } else if (warp == MMA_WARP) {
     // =============================== MMA issuer
     if (lane == 0) {
-      constexpr uint32_t IDESC = idesc_tf32(BM, BN);
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
@@ -375,6 +489,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         decode_unit(bt, u, pi, tm, tn, tile, split);
         const Problem& P = bt.p[pi];
         const bool skip_b = P.same_ab && tm == tn;
+        const int a_mn = P.tma_a == TMA_ROWS_MN;
+        const int b_mn = skip_b ? a_mn : (P.tma_b == TMA_ROWS_MN);
+        const uint32_t idesc = idesc_tf32(BM, BN, a_mn, b_mn);
         const int acc = it & 1;
         mbar_wait(tempty_bar(acc), ((it >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -383,19 +500,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         const int kc1 = min(P.chunks, kc0 + P.cps);
         for (int kc = kc0; kc < kc1; ++kc) {
           mbar_wait(full_bar(stage), phase);
+          mbar_wait(tma_bar(stage), phase);
           tc_fence_after();
           const uint32_t sa = base + stage * C::STAGE_BYTES;
           const uint32_t sb = skip_b ? sa : sa + TILE_BYTES;
           const uint32_t sal = sa + 2 * TILE_BYTES;
           const uint32_t sbl = skip_b ? sal : sa + 3 * TILE_BYTES;
 #pragma unroll
-          for (int s = 0; s < BK / 8; ++s) {  // UMMA_K = 8 for tf32 (32 B)
-            const uint64_t da = sdesc_kmajor_sw128(sa + s * 32);
-            const uint64_t db = sdesc_kmajor_sw128(sb + s * 32);
-            mma_tf32(d, da, db, IDESC, (kc > kc0 || s > 0) ? 1u : 0u);
+          for (int s = 0; s < BK / 8; ++s) {  // UMMA_K = 8 for tf32
+            // K-major: +32 B along the 128 B row; MN-major: next 8-row k group (+1024 B)
+            const uint32_t oa = a_mn ? s * 1024 : s * 32;
+            const uint32_t ob = b_mn ? s * 1024 : s * 32;
+            const uint64_t da = a_mn ? sdesc_mnmajor_sw128(sa + oa, 4096) : sdesc_kmajor_sw128(sa + oa);
+            const uint64_t db = b_mn ? sdesc_mnmajor_sw128(sb + ob, 4096) : sdesc_kmajor_sw128(sb + ob);
+            mma_tf32(d, da, db, idesc, (kc > kc0 || s > 0) ? 1u : 0u);
             if (NPASS == 3) {
-              mma_tf32(d, da, sdesc_kmajor_sw128(sbl + s * 32), IDESC, 1u);
-              mma_tf32(d, sdesc_kmajor_sw128(sal + s * 32), db, IDESC, 1u);
+              const uint64_t dbl = b_mn ? sdesc_mnmajor_sw128(sbl + ob, 4096) : sdesc_kmajor_sw128(sbl + ob);
+              const uint64_t dal = a_mn ? sdesc_mnmajor_sw128(sal + oa, 4096) : sdesc_kmajor_sw128(sal + oa);
+              mma_tf32(d, da, dbl, idesc, 1u);
+              mma_tf32(d, dal, db, idesc, 1u);
             }
           }
           mma_commit(empty_bar(stage));
@@ -487,6 +610,84 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   }
 }
 
+// ------------------------------------------------------------------ host: tensor maps
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encoder() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+bool tma_disabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DPK_DISABLE_TMA");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// tf32_rn: TMA rounds fp32 -> TF32 (nearest) in flight (TFLOAT32 data type);
+// otherwise raw fp32 bits land in shared memory (tensor core truncates).
+bool encode(CUtensorMap* m, int rank, const void* data, const cuuint64_t* dims, const cuuint64_t* strides,
+            const cuuint32_t* box, bool tf32_rn, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
+  EncodeTiledFn fn = encoder();
+  if (!fn) return false;
+  const cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, tf32_rn ? CU_TENSOR_MAP_DATA_TYPE_TFLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, const_cast<void*>(data), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// 2-D maps for row-major (K-major) / column-major (MN-major) operands.
+int plan_tma_2d(const dpk_operand& o, CUtensorMap* m, bool rn) {
+  if (tma_disabled() || o.bias_row || o.rows < 1 || !aligned16(o.data) || (o.ld * 4) % 16 != 0) return TMA_NONE;
+  if (o.kind == DPK_OPND_ROWS_K) {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(o.cols), static_cast<cuuint64_t>(o.rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(o.ld) * 4};
+    const cuuint32_t box[2] = {BK, BM};
+    return encode(m, 2, o.data, dims, strides, box, rn) ? TMA_ROWS_K : TMA_NONE;
+  }
+  if (o.kind == DPK_OPND_ROWS_MN) {
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(o.rows), static_cast<cuuint64_t>(o.cols)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(o.ld) * 4};
+    const cuuint32_t box[2] = {32, BK};
+    // MN-major tf32 must use the 32-byte-atom 128B swizzle (matches SWIZZLE_128B_BASE32B)
+    return encode(m, 2, o.data, dims, strides, box, rn, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ? TMA_ROWS_MN : TMA_NONE;
+  }
+  return TMA_NONE;
+}
+
+// NCHW 1x1/s1 capture (or any conv grad_output): per sample a contiguous C x HW
+// slab -> 3-D map {HW, C, N}; K is re-indexed as (sample, 32-pixel chunk).
+bool slab_eligible(const dpk_operand& o) {
+  return o.kind == DPK_OPND_IM2COL && !o.bias_row && o.kh == 1 && o.kw == 1 && o.sh == 1 && o.sw == 1 &&
+         o.ph == 0 && o.pw == 0 && o.OH == o.H && o.OW == o.W && o.sws == 1 && o.shs == o.W &&
+         aligned16(o.data) && (o.sc * 4) % 16 == 0 && (o.sn * 4) % 16 == 0 && !tma_disabled();
+}
+
+bool plan_tma_slab(const dpk_operand& o, CUtensorMap* m, bool rn) {
+  const int64_t hw = static_cast<int64_t>(o.H) * o.W;
+  const int64_t n = o.cols / hw;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(hw), static_cast<cuuint64_t>(o.C), static_cast<cuuint64_t>(n)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(o.sc) * 4, static_cast<cuuint64_t>(o.sn) * 4};
+  const cuuint32_t box[3] = {BK, BM, 1};
+  return encode(m, 3, o.data, dims, strides, box, rn);
+}
+
 // ------------------------------------------------------------------ host planning
 struct Plan {
   std::vector<Problem> probs;
@@ -507,7 +708,8 @@ bool valid_operand(const dpk_operand& o) {
   return true;
 }
 
-int make_plan(const GemmSpec* specs, int n, Plan& plan) {
+int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int precision = DPK_PREC_TF32) {
+  const bool rn = precision == DPK_PREC_TF32;
   plan.probs.clear();
   plan.probs.resize(n);
   int64_t total_work = 0;
@@ -522,7 +724,7 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan) {
       return DPK_ESHAPE;
     }
     Problem& P = plan.probs[i];
-    std::memset(&P, 0, sizeof(P));
+    std::memset(static_cast<void*>(&P), 0, sizeof(P));
     P.a = j.a;
     P.b = j.b;
     P.out = j.out;
@@ -553,6 +755,29 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan) {
     P.tiles_n = (P.N + BN - 1) / BN;
     P.ntiles = P.symmetric ? tmn * (tmn + 1) / 2 : tmn * P.tiles_n;
     P.chunks = static_cast<int>((j.a.cols + BK - 1) / BK);
+    if (P.same_ab && slab_eligible(j.a)) {
+      // SYRK over an NCHW slab: both operands through one 3-D map, K = (sample, chunk)
+      const int64_t hw = static_cast<int64_t>(j.a.H) * j.a.W;
+      P.slab_cpn = static_cast<int>((hw + BK - 1) / BK);
+      P.chunks = static_cast<int>((j.a.cols / hw) * P.slab_cpn);
+      if (with_maps) {
+        if (plan_tma_slab(j.a, &P.tmap_a, rn)) {
+          P.tmap_b = P.tmap_a;
+          P.tma_a = P.tma_b = TMA_SLAB;
+        } else {  // cannot happen for eligible views; fall back to the flat gather
+          P.slab_cpn = 0;
+          P.chunks = static_cast<int>((j.a.cols + BK - 1) / BK);
+        }
+      }
+    } else if (with_maps) {
+      P.tma_a = plan_tma_2d(j.a, &P.tmap_a, rn);
+      if (P.same_ab) {
+        P.tma_b = P.tma_a;
+        P.tmap_b = P.tmap_a;
+      } else {
+        P.tma_b = plan_tma_2d(j.b, &P.tmap_b, rn);
+      }
+    }
     total_work += static_cast<int64_t>(P.ntiles) * P.chunks;
   }
   // Split K so that the group yields several units per SM, but never below
@@ -574,17 +799,18 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan) {
   return DPK_OK;
 }
 
-template <int NPASS>
-int launch_batch(Batch& bt, cudaStream_t st) {
+template <int NPASS, bool RN>
+int launch_batch(const Batch& bt, cudaStream_t st) {
   using C = Cfg<NPASS>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(tc_gemm_kernel<NPASS>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaError_t e =
+        cudaFuncSetAttribute(tc_gemm_kernel<NPASS, RN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(tc_gemm_kernel)");
     configured = true;
   }
   const int grid = std::min(bt.total_units, num_sms());
-  tc_gemm_kernel<NPASS><<<grid, NTHREADS, C::SMEM, st>>>(bt);
+  tc_gemm_kernel<NPASS, RN><<<grid, NTHREADS, C::SMEM, st>>>(bt);
   note_launch();
   return cuda_status(cudaGetLastError(), "tc_gemm_kernel launch");
 }
@@ -593,7 +819,7 @@ int launch_batch(Batch& bt, cudaStream_t st) {
 
 size_t gemm_workspace_bytes(const GemmSpec* specs, int n) {
   Plan plan;
-  if (n <= 0 || make_plan(specs, n, plan) != DPK_OK) return 0;
+  if (n <= 0 || make_plan(specs, n, plan, false) != DPK_OK) return 0;
   return plan.ws_bytes;
 }
 
@@ -603,12 +829,12 @@ int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int pre
     set_error("dpk_gemm: bad job list");
     return DPK_EARG;
   }
-  if (precision != DPK_PREC_TF32 && precision != DPK_PREC_3XTF32) {
-    set_error("dpk_gemm: precision must be DPK_PREC_TF32 or DPK_PREC_3XTF32");
+  if (precision != DPK_PREC_TF32 && precision != DPK_PREC_TF32_TRUNC && precision != DPK_PREC_3XTF32) {
+    set_error("dpk_gemm: precision must be DPK_PREC_TF32, DPK_PREC_TF32_TRUNC or DPK_PREC_3XTF32");
     return DPK_EARG;
   }
   Plan plan;
-  int rc = make_plan(specs, n, plan);
+  int rc = make_plan(specs, n, plan, true, precision);
   if (rc != DPK_OK) return rc;
   if (plan.ws_bytes > ws_bytes) {
     set_error("dpk_gemm: workspace too small (" + std::to_string(ws_bytes) + " < " +
@@ -648,7 +874,12 @@ int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int pre
     }
     bt.total_units = units;
     if (units == 0) continue;
-    rc = precision == DPK_PREC_3XTF32 ? launch_batch<3>(bt, st) : launch_batch<1>(bt, st);
+    if (precision == DPK_PREC_3XTF32)
+      rc = launch_batch<3, false>(bt, st);
+    else if (precision == DPK_PREC_TF32_TRUNC)
+      rc = launch_batch<1, false>(bt, st);
+    else
+      rc = launch_batch<1, true>(bt, st);
     if (rc != DPK_OK) return rc;
   }
   return DPK_OK;

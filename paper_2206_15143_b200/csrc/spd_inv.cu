@@ -113,13 +113,15 @@ __global__ void __launch_bounds__(LEAF_THREADS) spd_leaf_kernel(const __grid_con
     }
 }
 
-// Aw = src + shift I for the blocked path
+// Aw = src + shift I for the blocked path; Aw rows are padded to ldw (a multiple
+// of 4 floats) so every recursion operand is a 16-byte aligned TMA view.
 constexpr int PREP_MAX = 256;
 struct PrepJob {
   const float* src;
   float* dst;
   const float* shift;
   int64_t n;
+  int64_t ldw;
 };
 struct PrepBatch {
   int n;
@@ -132,11 +134,14 @@ __global__ void prep_kernel(const __grid_constant__ PrepBatch b) {
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t i = e / J.n;
+    const int64_t c = e - i * J.n;
     float x = J.src[e];
-    if (i == e - i * J.n) x += sh;
-    J.dst[e] = x;
+    if (i == c) x += sh;
+    J.dst[i * J.ldw + c] = x;
   }
 }
+
+inline int64_t padded_ld(int n) { return (static_cast<int64_t>(n) + 3) / 4 * 4; }
 
 struct Op {
   bool leaf;
@@ -157,7 +162,8 @@ size_t t_floats(int n) {  // largest n2 x n1 scratch over the recursion
 
 size_t matrix_ws_floats(int n) {
   if (n <= LEAF_N) return 0;
-  return 2 * static_cast<size_t>(n) * n + t_floats(n);  // L21 blocks, X = L^-1, T
+  // working copy Aw, L21 blocks, X = L^-1 (all n x padded_ld), T scratch (+4 for alignment)
+  return 3 * static_cast<size_t>(n) * padded_ld(n) + t_floats(n) + 4;
 }
 
 GemmSpec spec(const dpk_operand& a, const dpk_operand& b, float* out, int64_t ldo, float alpha, float beta,
@@ -229,18 +235,21 @@ void make_spd_plan(const dpk_spd_job* jobs, int n, char* base, SpdPlan& plan) {
       ops.push_back(op);
       continue;
     }
-    float* Lb = reinterpret_cast<float*>(b + off);
-    float* Xb = Lb + static_cast<size_t>(m) * m;
-    float* T = Xb + static_cast<size_t>(m) * m;
+    const int64_t ldw = padded_ld(m);  // 16-byte rows -> TMA-addressable operands
+    const size_t blk = static_cast<size_t>(m) * ldw;
+    float* Aw = reinterpret_cast<float*>(b + off);
+    float* Lb = Aw + blk;
+    float* Xb = Lb + blk;
+    float* T = Xb + blk;
     off += align_up(matrix_ws_floats(m) * sizeof(float), 256);
-    plan.preps.push_back(PrepJob{jobs[i].src, jobs[i].dst, jobs[i].shift, m});
+    plan.preps.push_back(PrepJob{jobs[i].src, Aw, jobs[i].shift, m, ldw});
     plan.zero_x.push_back(Xb);
-    plan.zero_bytes.push_back(static_cast<size_t>(m) * m * sizeof(float));
-    build_ops(jobs[i].dst, Lb, Xb, m, m, T, jobs[i].fail_code, jobs[i].info, ops);
+    plan.zero_bytes.push_back(blk * sizeof(float));
+    build_ops(Aw, Lb, Xb, ldw, m, T, jobs[i].fail_code, jobs[i].info, ops);
     Op op{};
     op.leaf = false;
-    // dst = X^T X  (X lower triangular; symmetric output)
-    op.g = spec(rows_mn(Xb, m, m, m), rows_mn(Xb, m, m, m), jobs[i].dst, m, 1.0f, 0.0f, 1);
+    // dst = X^T X  (X lower triangular; symmetric output, written with the caller's ld = n)
+    op.g = spec(rows_mn(Xb, m, m, ldw), rows_mn(Xb, m, m, ldw), jobs[i].dst, m, 1.0f, 0.0f, 1);
     ops.push_back(op);
   }
   plan.rec_bytes = off;
