@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--gamma", type=float, default=0.002)
     ap.add_argument("--xi", type=float, default=0.95)      # reference default (kfac.py:61)
     ap.add_argument("--precision", default="tf32", choices=["tf32", "3xtf32"])
+    ap.add_argument("--nchw", action="store_true",
+                    help="keep the conv model NCHW (default: channels_last, the B200-native layout)")
     ap.add_argument("--assignment", default="round_robin")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -198,11 +200,18 @@ def run_ours(args, rank, world, local_rank):
     torch.manual_seed(0)
     model = ctor().to(dev)
     geom = BM.layer_geometry(model, shape, batch)
+    conv = len(shape) == 3
+    mf = torch.contiguous_format if (args.nchw or not conv) else torch.channels_last
+    if conv:
+        model = model.to(memory_format=mf)
     kf = DPKFAC(model, gamma=args.gamma, xi=args.xi, inv_type=args.inv_type, f_freq=1, k_freq=1,
                 assignment=args.assignment, precision=args.precision, check_numerics="deferred")
     opt = torch.optim.SGD(model.parameters(), lr=1e-3, momentum=0.9)
     gen = torch.Generator().manual_seed(1234 + rank)
-    x_host = torch.randn(batch, *shape, generator=gen).pin_memory()
+    x_host = torch.randn(batch, *shape, generator=gen)
+    if conv:
+        x_host = x_host.contiguous(memory_format=mf)
+    x_host = x_host.pin_memory()
     y_host = torch.randint(0, classes, (batch,), generator=gen).pin_memory()
     x = x_host.to(dev)
     y = y_host.to(dev)
@@ -352,7 +361,9 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": f"{args.model} DP-KFAC 2nd-order update, batch {batch}/GPU, "
                                    f"inv_type={args.inv_type}, gamma={args.gamma}, xi={args.xi}, F=K=1",
                        "model": args.model, "global_batch": batch * world, "parallelism": f"dp{world}",
-                       "assignment": args.assignment, "l2": "inputs (layer captures, >1.4 GB) larger than L2; no flush"},
+                       "assignment": args.assignment,
+                       "memory_format": "channels_last" if mf is torch.channels_last else "contiguous",
+                       "l2": "inputs (layer captures, >1.4 GB) larger than L2; no flush"},
             "stages_ms": stages, "stage_roofline": stage_roofline, "roofline": roofline,
             "cpu_baseline": cpu_baseline, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks.summary(),

@@ -65,8 +65,13 @@ enum {
 enum {
   DPK_OPND_ROWS_K = 0,  /* X[r,k] = data[r*ld + k]            (rows contiguous in k)   */
   DPK_OPND_ROWS_MN = 1, /* X[r,k] = data[k*ld + r]            (e.g. nn.Linear input B x d) */
-  DPK_OPND_IM2COL = 2   /* X[(c,i,j),(n,oh,ow)] = x[n, c, oh*sh-ph+i*dh, ow*sw-pw+j*dw] or 0:
+  DPK_OPND_IM2COL = 2,  /* X[(c,i,j),(n,oh,ow)] = x[n, c, oh*sh-ph+i*dh, ow*sw-pw+j*dw] or 0:
                            the implicit-im2col linear form of a Conv2d input (F.unfold order) */
+  DPK_OPND_IM2COL_TAPMAJOR = 3 /* same values, rows ordered (i, j, c) -- the channels-last
+                           weight order.  With an NHWC input (c contiguous, C % 32 == 0) the
+                           engine fetches it with TMA im2col loads; the factor is then a
+                           symmetric permutation of the (c,i,j) one and the gradient must
+                           be packed with dpk_segment.perm_khw. */
 };
 
 typedef struct dpk_operand {
@@ -104,9 +109,25 @@ typedef struct dpk_factor_job {
 size_t dpk_factor_workspace_bytes(const dpk_factor_job* jobs, int n_jobs);
 int dpk_syrk_ema(const dpk_factor_job* jobs, int n_jobs, void* workspace, size_t ws_bytes, int precision,
                  dpk_stream_t stream);
-/* K2 entry point: identical contract; every job's operand must be DPK_OPND_IM2COL. */
+/* K2 entry point: identical contract; every job's operand must be DPK_OPND_IM2COL or
+ * DPK_OPND_IM2COL_TAPMAJOR (the TMA-im2col form for channels-last inputs). */
 int dpk_conv_im2col_syrk_ema(const dpk_factor_job* jobs, int n_jobs, void* workspace, size_t ws_bytes,
                              int precision, dpk_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * Patch matrix for the conv A factor, sample-major:  out[k*ld + r] = X[r, k]
+ * (X = the operand's implicit-im2col view, bias ones row included), so the
+ * SYRK can stream it with 2-D TMA (MN-major) at full tensor-core rate.  With a
+ * channels-last input and DPK_OPND_IM2COL_TAPMAJOR rows every (pixel, tap) is
+ * one contiguous C-float copy.  ld >= rows + bias_row.
+ * ------------------------------------------------------------------------ */
+typedef struct dpk_im2col_job {
+  dpk_operand x; /* DPK_OPND_IM2COL or DPK_OPND_IM2COL_TAPMAJOR */
+  float* out;
+  int64_t ld;
+} dpk_im2col_job;
+
+int dpk_im2col_materialize(const dpk_im2col_job* jobs, int n_jobs, dpk_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * Grouped tensor-core GEMM used by preconditioning (and exposed for tests):
@@ -228,7 +249,8 @@ typedef struct dpk_segment {
   int32_t rows;
   int32_t cols_w;
   int64_t ldw;
-  int32_t perm_khw;  /* reserved (0) */
+  int32_t perm_khw;  /* 0: plain.  KH*KW: weight is rows x C x KH x KW (Conv2d) and the
+                        flat row is in (kh, kw, c) order, matching DPK_OPND_IM2COL_TAPMAJOR */
   int32_t _pad0;
 } dpk_segment;
 

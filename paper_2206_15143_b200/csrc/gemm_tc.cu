@@ -59,7 +59,11 @@ constexpr uint32_t TMEM_COLS = 2 * BN;                    // two accumulators
 constexpr int MAXP = 32;                                  // problems per launch (kernel params)
 static_assert(NPROD % 8 == 0, "im2col chunk sharing needs NPROD % 8 == 0");
 
-enum { TMA_NONE = 0, TMA_ROWS_K = 1, TMA_ROWS_MN = 2, TMA_SLAB = 3 };
+enum { TMA_NONE = 0, TMA_ROWS_K = 1, TMA_ROWS_MN = 2, TMA_SLAB = 3, TMA_IM2COL = 4 };
+
+__host__ __device__ __forceinline__ bool is_im2col(int kind) {
+  return kind == DPK_OPND_IM2COL || kind == DPK_OPND_IM2COL_TAPMAJOR;
+}
 
 struct alignas(64) Problem {
   CUtensorMap tmap_a;  // valid iff tma_a != TMA_NONE
@@ -70,8 +74,7 @@ struct alignas(64) Problem {
   const float* cin;
   const float* vrow;
   const float* vcol;
-  float* partials;
-  int* counters;
+  float* partials;  // split-K partial slots (ntiles * splits * BM * BN), splits > 1
   float* out_t;
   int64_t ldt;
   int64_t ldo;
@@ -107,8 +110,10 @@ __device__ __forceinline__ void decode_unit(const Batch& bt, int u, int& pi, int
   while (p + 1 < bt.nprob && bt.p[p + 1].unit_begin <= u) ++p;
   const Problem& P = bt.p[p];
   int local = u - P.unit_begin;
-  tile = local / P.splits;
-  split = local - tile * P.splits;
+  // split-major: CTAs of one wave take different tiles of the same K range, so
+  // each K slab of the operands is fetched from DRAM once and shared through L2
+  split = local / P.ntiles;
+  tile = local - split * P.ntiles;
   if (P.symmetric) {
     int r = static_cast<int>((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
     while ((r + 1) * (r + 2) / 2 <= tile) ++r;
@@ -166,11 +171,19 @@ __device__ __forceinline__ void setup_tasks(const dpk_operand& o, int row0, int 
       } else if (o.kind == DPK_OPND_ROWS_MN) {
         t[j].off = r;
       } else {
-        const int kk = o.kh * o.kw;
-        const int c = r / kk;
-        const int rem = r - c * kk;
-        const int i = rem / o.kw;
-        const int jj = rem - i * o.kw;
+        int c, i, jj;
+        if (o.kind == DPK_OPND_IM2COL) {  // rows (c, i, j): F.unfold / weight.view order
+          const int kk = o.kh * o.kw;
+          c = r / kk;
+          const int rem = r - c * kk;
+          i = rem / o.kw;
+          jj = rem - i * o.kw;
+        } else {  // TAPMAJOR rows (i, j, c): channels-last weight order
+          const int tap = r / o.C;
+          c = r - tap * o.C;
+          i = tap / o.kw;
+          jj = tap - i * o.kw;
+        }
         const int ihd = i * o.dh, iwd = jj * o.dw;
         t[j].packed = 1 | (iwd << 2) | (ihd << 17);
         t[j].off = static_cast<int64_t>(c) * o.sc + static_cast<int64_t>(ihd) * o.shs +
@@ -186,7 +199,7 @@ __device__ __forceinline__ void setup_tasks(const dpk_operand& o, int row0, int 
 __device__ __forceinline__ void fetch_tasks(const dpk_operand& o, const RowTask (&t)[NTASK], int ptid, int64_t k_base,
                                             float4 (&v)[NTASK]) {
   const bool kf = kfast(o);
-  if (o.kind == DPK_OPND_IM2COL) {
+  if (is_im2col(o.kind)) {
     // all tasks of this thread share one chunk (NPROD % 8 == 0) -> decompose its 4 sample columns once
     const int64_t k0 = k_base + 4 * (ptid & 7);
     const int ohw = o.OH * o.OW;
@@ -318,16 +331,42 @@ __device__ __forceinline__ void convert_tile(uint8_t* tile, uint8_t* tile_lo, in
   }
 }
 
-__device__ __forceinline__ void issue_tma(int kind, const CUtensorMap* map, uint32_t dst, uint32_t bar, int row0, int kc,
-                                          int cpn) {
+// Bytes one TMA'd operand tile delivers.  Box loads always count their full
+// (zero-filled) size; im2col tiles skip 32-row groups past the operand's rows
+// (those smem rows only feed accumulator rows the epilogue never stores).
+__device__ __forceinline__ uint32_t tma_tile_bytes(int kind, const dpk_operand& o, int row0) {
+  if (kind != TMA_IM2COL) return TILE_BYTES;
+  const int groups = min(BM / 32, (o.rows - row0 + 31) / 32);
+  return static_cast<uint32_t>(max(groups, 0)) * 4096u;
+}
+
+__device__ __forceinline__ void issue_tma(int kind, const CUtensorMap* map, const dpk_operand& o, uint32_t dst,
+                                          uint32_t bar, int row0, int kc, int cpn) {
   if (kind == TMA_ROWS_K) {
     tma_load_2d(dst, map, bar, kc * BK, row0);
   } else if (kind == TMA_ROWS_MN) {
 #pragma unroll
     for (int b = 0; b < BM / 32; ++b) tma_load_2d(dst + b * 4096, map, bar, row0 + 32 * b, kc * BK);
-  } else {  // TMA_SLAB: dims {HW, C, N}
+  } else if (kind == TMA_SLAB) {  // dims {HW, C, N}
     const int n = kc / cpn;
     tma_load_3d(dst, map, bar, (kc - n * cpn) * BK, row0, n);
+  } else {  // TMA_IM2COL: NHWC input, rows (i, j, c); a box = 32 output pixels x 32 channels
+    const int64_t k0 = static_cast<int64_t>(kc) * BK;
+    const int ohw = o.OH * o.OW;
+    const int n = static_cast<int>(k0 / ohw);
+    const int rem = static_cast<int>(k0 - static_cast<int64_t>(n) * ohw);
+    const int oh = rem / o.OW;
+    const int ow = rem - oh * o.OW;
+    const int w0 = ow * o.sw - o.pw, h0 = oh * o.sh - o.ph;
+    for (int b = 0; b < BM / 32; ++b) {
+      const int r = row0 + 32 * b;
+      if (r >= o.rows) break;
+      const int tap = r / o.C;
+      const int c0 = r - tap * o.C;
+      const int i = tap / o.kw, j = tap - (tap / o.kw) * o.kw;
+      tma_load_im2col_4d(dst + b * 4096, map, bar, c0, w0, h0, n, static_cast<uint16_t>(j * o.dw),
+                         static_cast<uint16_t>(i * o.dh));
+    }
   }
 }
 
@@ -363,7 +402,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   // mode the tensor map's TFLOAT32 data type rounds during the copy itself.
   constexpr bool CONVERT = (NPASS == 3);
   extern __shared__ uint8_t smem_raw[];
-  __shared__ int s_last;
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
@@ -412,13 +450,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         if (tB) tma_prefetch_desc(&P.tmap_b);
         const int kc0 = split * P.cps;
         const int kc1 = min(P.chunks, kc0 + P.cps);
+        const uint32_t bytes = (tA ? tma_tile_bytes(P.tma_a, P.a, tm * BM) : 0u) +
+                               (tB ? tma_tile_bytes(P.tma_b, P.b, tn * BN) : 0u);
         for (int kc = kc0; kc < kc1; ++kc) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t sst = base + stage * C::STAGE_BYTES;
           // exactly one arrival per stage use; tx bytes only for TMA'd tiles
-          mbar_arrive_expect_tx(tma_bar(stage), (tA ? TILE_BYTES : 0) + (tB ? TILE_BYTES : 0));
-          if (tA) issue_tma(P.tma_a, &P.tmap_a, sst, tma_bar(stage), tm * BM, kc, P.slab_cpn);
-          if (tB) issue_tma(P.tma_b, &P.tmap_b, sst + TILE_BYTES, tma_bar(stage), tn * BN, kc, P.slab_cpn);
+          mbar_arrive_expect_tx(tma_bar(stage), bytes);
+          if (tA) issue_tma(P.tma_a, &P.tmap_a, P.a, sst, tma_bar(stage), tm * BM, kc, P.slab_cpn);
+          if (tB) issue_tma(P.tma_b, &P.tmap_b, P.b, sst + TILE_BYTES, tma_bar(stage), tn * BN, kc, P.slab_cpn);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -489,8 +529,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         decode_unit(bt, u, pi, tm, tn, tile, split);
         const Problem& P = bt.p[pi];
         const bool skip_b = P.same_ab && tm == tn;
-        const int a_mn = P.tma_a == TMA_ROWS_MN;
-        const int b_mn = skip_b ? a_mn : (P.tma_b == TMA_ROWS_MN);
+        const int a_mn = P.tma_a == TMA_ROWS_MN || P.tma_a == TMA_IM2COL;
+        const int b_mn = skip_b ? a_mn : (P.tma_b == TMA_ROWS_MN || P.tma_b == TMA_IM2COL);
         const uint32_t idesc = idesc_tf32(BM, BN, a_mn, b_mn);
         const int acc = it & 1;
         mbar_wait(tempty_bar(acc), ((it >> 1) & 1) ^ 1);
@@ -564,40 +604,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
       }
       tc_fence_before();
       mbar_arrive(tempty_bar(acc));
-      if (P.splits > 1) {
-        __threadfence();
-        named_bar_sync(1, EPI_WARPS * 32);
-        if (m == 0) {
-          const int old = atomicAdd(P.counters + tile, 1);
-          const int last = (old == P.splits - 1);
-          if (last) P.counters[tile] = 0;
-          s_last = last;
-        }
-        named_bar_sync(1, EPI_WARPS * 32);
-        if (s_last) {
-          __threadfence();
-          const float* rowp = P.partials + (static_cast<int64_t>(tile * P.splits) * BM + m) * BN;
-#pragma unroll 1
-          for (int c = 0; c < BN / 32; ++c) {
-            float accv[32];
-#pragma unroll
-            for (int j = 0; j < 32; ++j) accv[j] = 0.0f;
-            for (int s = 0; s < P.splits; ++s) {
-              const float4* src = reinterpret_cast<const float4*>(rowp + static_cast<int64_t>(s) * BM * BN + c * 32);
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                const float4 x = __ldcg(src + q);
-                accv[4 * q] += x.x;
-                accv[4 * q + 1] += x.y;
-                accv[4 * q + 2] += x.z;
-                accv[4 * q + 3] += x.w;
-              }
-            }
-            store_final(P, tm, tn, m, c, accv);
-          }
-        }
-        named_bar_sync(1, EPI_WARPS * 32);
-      }
+      // split-K partials are summed (in split order, deterministic) and finished
+      // by splitk_reduce_kernel, spread over the whole GPU
     }
   }
 
@@ -607,6 +615,80 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
     __syncwarp();
     tc_fence_after();
     tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+// ------------------------------------------------------------------ split-K reduction
+// One CTA per (split tile, 8-row slab): 256 threads, each owns 4 consecutive
+// columns of one row, sums the partials in split order (deterministic) and
+// applies the same epilogue as the single-split path.
+constexpr int RED_MAX = 96;
+constexpr int RED_ROWS = 8;
+struct RedJob {
+  float* out;
+  const float* cin;
+  const float* vrow;
+  const float* vcol;
+  const float* partials;
+  float* out_t;
+  int64_t ldo, ldc, ldt;
+  float alpha, beta, gamma;
+  int M, N, symmetric, epi, tiles_n, splits;
+  int slab_begin;  // prefix over (tiles x BM/RED_ROWS) slabs
+};
+struct RedBatch {
+  int n;
+  int total;
+  RedJob j[RED_MAX];
+};
+
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constant__ RedBatch b) {
+  const int slab = blockIdx.x;
+  int p = 0;
+  while (p + 1 < b.n && b.j[p + 1].slab_begin <= slab) ++p;
+  const RedJob& J = b.j[p];
+  const int local = slab - J.slab_begin;
+  const int tile = local / (BM / RED_ROWS);
+  const int row = (local - tile * (BM / RED_ROWS)) * RED_ROWS + (threadIdx.x >> 5);
+  const int col = (threadIdx.x & 31) * 4;
+  int tm, tn;
+  if (J.symmetric) {
+    int r = static_cast<int>((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
+    while ((r + 1) * (r + 2) / 2 <= tile) ++r;
+    while (r * (r + 1) / 2 > tile) --r;
+    tm = r;
+    tn = tile - r * (r + 1) / 2;
+  } else {
+    tm = tile / J.tiles_n;
+    tn = tile - tm * J.tiles_n;
+  }
+  const int gm = tm * BM + row;
+  if (gm >= J.M) return;
+  const float* src = J.partials + (static_cast<int64_t>(tile) * J.splits * BM + row) * BN + col;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int s = 0; s < J.splits; ++s) {
+    const float4 x = __ldcg(reinterpret_cast<const float4*>(src + static_cast<int64_t>(s) * BM * BN));
+    acc.x += x.x;
+    acc.y += x.y;
+    acc.z += x.z;
+    acc.w += x.w;
+  }
+  const float a[4] = {acc.x, acc.y, acc.z, acc.w};
+  const bool diag = J.symmetric && tm == tn;
+  const float vr = (J.epi == EPI_EIGDIV) ? fmaxf(J.vrow[gm], 0.0f) : 0.0f;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int gn = tn * BN + col + e;
+    if (gn >= J.N || (diag && gn > gm)) continue;
+    float val = J.alpha * a[e];
+    if (J.epi == EPI_EIGDIV) {
+      val = val / (vr * fmaxf(J.vcol[gn], 0.0f) + J.gamma);
+    } else if (J.beta != 0.0f) {
+      val += J.beta * J.cin[gm * J.ldc + gn];
+    }
+    J.out[gm * J.ldo + gn] = val;
+    if (J.symmetric && gn != gm) J.out[static_cast<int64_t>(gn) * J.ldo + gm] = val;
+    if (J.out_t) J.out_t[static_cast<int64_t>(gn) * J.ldt + gm] = val;
   }
 }
 
@@ -688,6 +770,54 @@ bool plan_tma_slab(const dpk_operand& o, CUtensorMap* m, bool rn) {
   return encode(m, 3, o.data, dims, strides, box, rn);
 }
 
+// im2col-mode map over an NHWC conv input: dims {C, W, H, N}; the bounding box
+// (lower corner -pad, upper corner pad - dilation*(k-1)) spans exactly the
+// output pixels, traversed with the conv stride; a box is 32 output pixels x
+// 32 channels (one 128 B row per pixel), written in the MN-major tf32 layout.
+using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const int*, const int*, cuuint32_t, cuuint32_t,
+                                    const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeIm2colFn im2col_encoder() {
+  static EncodeIm2colFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeIm2colFn>(p);
+  }
+  return fn;
+}
+
+bool im2col_eligible(const dpk_operand& o) {
+  return o.kind == DPK_OPND_IM2COL_TAPMAJOR && !o.bias_row && !tma_disabled() && o.C % 32 == 0 && o.sc == 1 &&
+         aligned16(o.data) && (o.sws * 4) % 16 == 0 && (o.shs * 4) % 16 == 0 && (o.sn * 4) % 16 == 0 &&
+         o.pw <= 127 && o.ph <= 127 && o.pw - o.dw * (o.kw - 1) >= -128 && o.ph - o.dh * (o.kh - 1) >= -128 &&
+         o.sw <= 8 && o.sh <= 8 && o.dw * (o.kw - 1) < 65536 && o.dh * (o.kh - 1) < 65536;
+}
+
+bool plan_tma_im2col(const dpk_operand& o, CUtensorMap* m, bool rn) {
+  EncodeIm2colFn fn = im2col_encoder();
+  if (!fn) return false;
+  const int64_t n = o.cols / (static_cast<int64_t>(o.OH) * o.OW);
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(o.C), static_cast<cuuint64_t>(o.W),
+                              static_cast<cuuint64_t>(o.H), static_cast<cuuint64_t>(n)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(o.sws) * 4, static_cast<cuuint64_t>(o.shs) * 4,
+                                 static_cast<cuuint64_t>(o.sn) * 4};
+  const int lower[2] = {-o.pw, -o.ph};
+  const int upper[2] = {o.pw - o.dw * (o.kw - 1), o.ph - o.dh * (o.kh - 1)};
+  const cuuint32_t es[4] = {1, static_cast<cuuint32_t>(o.sw), static_cast<cuuint32_t>(o.sh), 1};
+  const CUresult r =
+      fn(m, rn ? CU_TENSOR_MAP_DATA_TYPE_TFLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(o.data),
+         dims, strides, lower, upper, 32, 32, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 // ------------------------------------------------------------------ host planning
 struct Plan {
   std::vector<Problem> probs;
@@ -699,7 +829,7 @@ int operand_rows(const dpk_operand& o) { return o.rows + (o.bias_row ? 1 : 0); }
 bool valid_operand(const dpk_operand& o) {
   if (o.data == nullptr && o.rows > 0) return false;
   if (o.rows < 0 || o.cols < 1) return false;
-  if (o.kind == DPK_OPND_IM2COL) {
+  if (is_im2col(o.kind)) {
     if (o.kh < 1 || o.kw < 1 || o.sh < 1 || o.sw < 1 || o.dh < 1 || o.dw < 1 || o.OH < 1 || o.OW < 1) return false;
     if (o.rows != o.C * o.kh * o.kw) return false;
   } else if (o.kind != DPK_OPND_ROWS_K && o.kind != DPK_OPND_ROWS_MN) {
@@ -770,33 +900,77 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
         }
       }
     } else if (with_maps) {
-      P.tma_a = plan_tma_2d(j.a, &P.tmap_a, rn);
+      auto plan_one = [&](const dpk_operand& o, CUtensorMap* m) -> int {
+        if (o.kind == DPK_OPND_IM2COL_TAPMAJOR)
+          return (im2col_eligible(o) && plan_tma_im2col(o, m, rn)) ? TMA_IM2COL : TMA_NONE;
+        return plan_tma_2d(o, m, rn);
+      };
+      P.tma_a = plan_one(j.a, &P.tmap_a);
       if (P.same_ab) {
         P.tma_b = P.tma_a;
         P.tmap_b = P.tmap_a;
       } else {
-        P.tma_b = plan_tma_2d(j.b, &P.tmap_b, rn);
+        P.tma_b = plan_one(j.b, &P.tmap_b);
       }
     }
     total_work += static_cast<int64_t>(P.ntiles) * P.chunks;
   }
-  // Split K so that the group yields several units per SM, but never below
-  // 16 chunks (512 samples) per unit so tile set-up and epilogue stay amortised.
+  // Split K so that the group yields ~3 units per SM, but never below 32 chunks
+  // (1024 samples) per unit so tile set-up and the partial round trip stay amortised.
   const int64_t sms = num_sms();
-  const int64_t target = std::max<int64_t>(16, (total_work + 4 * sms - 1) / (4 * sms));
-  size_t counters = 0, partial_tiles = 0;
+  const int64_t target = std::max<int64_t>(32, (total_work + 3 * sms - 1) / (3 * sms));
+  size_t partial_tiles = 0;
   for (auto& P : plan.probs) {
     P.splits = static_cast<int>(std::max<int64_t>(1, (P.chunks + target - 1) / target));
     P.cps = (P.chunks + P.splits - 1) / P.splits;
     P.splits = (P.chunks + P.cps - 1) / P.cps;
-    if (P.splits > 1) {
-      counters += P.ntiles;
-      partial_tiles += static_cast<size_t>(P.ntiles) * P.splits;
-    }
+    if (P.splits > 1) partial_tiles += static_cast<size_t>(P.ntiles) * P.splits;
   }
-  const size_t counter_bytes = align_up(counters * sizeof(int), 1024);
-  plan.ws_bytes = counter_bytes + partial_tiles * BM * BN * sizeof(float);
+  plan.ws_bytes = partial_tiles * BM * BN * sizeof(float);
   return DPK_OK;
+}
+
+int launch_reduce(const std::vector<Problem>& probs, cudaStream_t st) {
+  thread_local RedBatch rb;
+  rb.n = 0;
+  rb.total = 0;
+  auto flush = [&]() -> int {
+    if (rb.n == 0) return DPK_OK;
+    splitk_reduce_kernel<<<rb.total, 256, 0, st>>>(rb);
+    note_launch();
+    rb.n = 0;
+    rb.total = 0;
+    return cuda_status(cudaGetLastError(), "splitk_reduce_kernel launch");
+  };
+  for (const auto& P : probs) {
+    if (P.splits <= 1) continue;
+    if (rb.n == RED_MAX) {
+      int rc = flush();
+      if (rc) return rc;
+    }
+    RedJob& J = rb.j[rb.n++];
+    J.out = P.out;
+    J.cin = P.cin;
+    J.vrow = P.vrow;
+    J.vcol = P.vcol;
+    J.partials = P.partials;
+    J.out_t = P.out_t;
+    J.ldo = P.ldo;
+    J.ldc = P.ldc;
+    J.ldt = P.ldt;
+    J.alpha = P.alpha;
+    J.beta = P.beta;
+    J.gamma = P.gamma;
+    J.M = P.M;
+    J.N = P.N;
+    J.symmetric = P.symmetric;
+    J.epi = P.epi;
+    J.tiles_n = P.tiles_n;
+    J.splits = P.splits;
+    J.slab_begin = rb.total;
+    rb.total += P.ntiles * (BM / RED_ROWS);
+  }
+  return flush();
 }
 
 template <int NPASS, bool RN>
@@ -841,26 +1015,14 @@ int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int pre
               std::to_string(plan.ws_bytes) + ")");
     return DPK_ENOSPACE;
   }
-  // carve counters + partials
-  size_t ncounters = 0, partial_tiles = 0;
-  for (auto& P : plan.probs)
-    if (P.splits > 1) ncounters += P.ntiles;
-  int* counters = static_cast<int*>(ws);
-  float* partials = reinterpret_cast<float*>(static_cast<char*>(ws) + align_up(ncounters * sizeof(int), 1024));
-  size_t ci = 0;
+  // carve the split-K partial slots
+  size_t partial_tiles = 0;
+  float* partials = static_cast<float*>(ws);
   for (auto& P : plan.probs) {
     if (P.splits > 1) {
-      P.counters = counters + ci;
       P.partials = partials + partial_tiles * BM * BN;
-      ci += P.ntiles;
       partial_tiles += static_cast<size_t>(P.ntiles) * P.splits;
     }
-  }
-  // The split-K semaphores must start at zero.  Kernels restore them, but the
-  // caller's scratch may have held other data (e.g. the SPD recursion buffers).
-  if (ncounters > 0) {
-    rc = cuda_status(cudaMemsetAsync(counters, 0, ncounters * sizeof(int), st), "cudaMemsetAsync(counters)");
-    if (rc != DPK_OK) return rc;
   }
   thread_local Batch bt;  // host-side staging only (kernel params are copied at launch)
   for (int first = 0; first < n; first += MAXP) {
@@ -882,7 +1044,7 @@ int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int pre
       rc = launch_batch<1, true>(bt, st);
     if (rc != DPK_OK) return rc;
   }
-  return DPK_OK;
+  return launch_reduce(plan.probs, st);
 }
 
 }  // namespace dpk
@@ -955,8 +1117,8 @@ int dpk_syrk_ema(const dpk_factor_job* jobs, int n_jobs, void* workspace, size_t
 int dpk_conv_im2col_syrk_ema(const dpk_factor_job* jobs, int n_jobs, void* workspace, size_t ws_bytes,
                              int precision, dpk_stream_t stream) {
   for (int i = 0; i < n_jobs; ++i) {
-    if (jobs[i].x.kind != DPK_OPND_IM2COL) {
-      dpk::set_error("dpk_conv_im2col_syrk_ema: operand must be DPK_OPND_IM2COL");
+    if (!dpk::is_im2col(jobs[i].x.kind)) {
+      dpk::set_error("dpk_conv_im2col_syrk_ema: operand must be DPK_OPND_IM2COL or DPK_OPND_IM2COL_TAPMAJOR");
       return DPK_EARG;
     }
   }

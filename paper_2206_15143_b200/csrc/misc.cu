@@ -107,7 +107,13 @@ __global__ void segment_kernel(const __grid_constant__ SegBatch b, float* flat) 
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t r = e / cols;
     const int c = static_cast<int>(e - r * cols);
-    float* src = (c < S.cols_w) ? S.weight + r * S.ldw + c : S.bias + r;
+    int cw = c;
+    if (S.perm_khw > 0 && c < S.cols_w) {  // flat (kh, kw, ci) <- weight (ci, kh, kw)
+      const int cin = S.cols_w / S.perm_khw;
+      const int tap = c / cin;
+      cw = (c - tap * cin) * S.perm_khw + tap;
+    }
+    float* src = (c < S.cols_w) ? S.weight + r * S.ldw + cw : S.bias + r;
     if (PACK)
       dst[e] = b.scale * *src;
     else

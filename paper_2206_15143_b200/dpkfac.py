@@ -40,6 +40,11 @@ from .exchange import OwnerMajorExchange, OwnerMajorLayout
 from .partition import balanced_partition, layer_cost, round_robin_partition, validate_partition
 
 
+def _nhwc(t: torch.Tensor) -> bool:
+    """Dense channels-last 4-D tensor (and not simultaneously NCHW-contiguous)."""
+    return t.dim() == 4 and t.is_contiguous(memory_format=torch.channels_last) and not t.is_contiguous()
+
+
 class _Layer:
     """One preconditioned layer and its (owner-side) curvature state."""
 
@@ -66,20 +71,68 @@ class _Layer:
         self.last_factor_update = -1
         self.last_inverse_update = -1
         self.holds = None  # "eigen" | "inverse" | None
+        # Conv A-factor row order, fixed at registration from the weight's memory
+        # format so every rank packs gradients identically: True = (kh, kw, C)
+        # channels-last order (TMA im2col fetches it straight from an NHWC
+        # activation), False = the reference's (C, kh, kw) order.  1x1 kernels:
+        # both orders coincide, so False.
+        self.tap_major = bool(self.is_conv and w[0, 0].numel() > 1
+                              and w.is_contiguous(memory_format=torch.channels_last) and not w.is_contiguous())
+
+        self.patch: Optional[torch.Tensor] = None  # materialized patch matrix (M x ld), reused
 
     # ---- operand views of the captures (reference layout: d x M, columns = samples)
-    def operand_a(self) -> L.Operand:
+    def operand_a(self, im2col: str = "implicit"):
+        """-> (SYRK operand, (im2col operand, patch buffer) to materialize first, or None).
+
+        nn.Linear / 1x1-stride-1 captures are read in place (channels-last: a
+        sample-major [N*H*W, C] view streamed by 2-D TMA; NCHW: a 3-D slab map).
+        Other convs use the implicit-im2col view directly (``im2col="implicit"``:
+        TMA im2col mode for NHWC, in-kernel gather otherwise) or, by default, a
+        sample-major patch matrix written by one coalesced copy kernel and then
+        streamed by 2-D TMA (``im2col="materialize"``)."""
         x = self.a_in
-        if self.is_conv:
-            m = self.module
-            return ops.operand_im2col(x, m.kernel_size, m.stride, m.padding, m.dilation, self.has_bias)
-        return ops.operand_rows_mn(x.reshape(-1, x.shape[-1]), self.has_bias)
+        if not self.is_conv:
+            return ops.operand_rows_mn(x.reshape(-1, x.shape[-1]), self.has_bias), None
+        m = self.module
+        nhwc = _nhwc(x)
+        plain_1x1 = (m.kernel_size == (1, 1) and m.stride == (1, 1) and m.padding == (0, 0)
+                     and m.dilation == (1, 1) and not self.has_bias)
+        if plain_1x1 and nhwc:
+            return ops.operand_rows_mn(x.permute(0, 2, 3, 1).reshape(-1, x.shape[1])), None
+        tap = self.tap_major if m.kernel_size != (1, 1) else nhwc
+        op = ops.operand_im2col(x, m.kernel_size, m.stride, m.padding, m.dilation, self.has_bias, tap)
+        if im2col == "implicit" or (plain_1x1 and x.is_contiguous()):
+            return op, None
+        d = op.rows + op.bias_row
+        ld = (d + 3) // 4 * 4
+        if self.patch is None or self.patch.shape[0] < op.cols or self.patch.shape[1] != ld:
+            self.patch = torch.empty(op.cols, ld, device=x.device)
+        patch = self.patch[:op.cols]
+        return ops.operand_rows_mn(patch[:, :d]), (op, patch)
 
     def operand_g(self) -> L.Operand:
         g = self.g_out
         if self.is_conv:
+            if _nhwc(g):  # [N*H*W, C] sample-major view, no copy
+                return ops.operand_rows_mn(g.permute(0, 2, 3, 1).reshape(-1, g.shape[1]))
             return ops.operand_im2col(g, (1, 1), (1, 1), (0, 0), (1, 1), False)
         return ops.operand_rows_mn(g.reshape(-1, g.shape[-1]), False)
+
+    def a_perm(self) -> Optional[torch.Tensor]:
+        """Index map reference order -> held order of the A factor (None if identical):
+        a_reference = a_held[p][:, p]."""
+        if not self.tap_major:
+            return None
+        kh, kw = self.module.kernel_size
+        c = self.module.in_channels
+        ref = torch.arange(c * kh * kw).view(c, kh, kw)        # reference index of (c, i, j)
+        held = ref.permute(1, 2, 0).reshape(-1)                # held position t -> reference index
+        p = torch.empty_like(held)
+        p[held] = torch.arange(held.numel())                   # reference index -> held position
+        if self.has_bias:
+            p = torch.cat([p, torch.tensor([p.numel()])])
+        return p.to(self.a_cov.device if self.a_cov is not None else "cpu")
 
     def alloc_state(self, inv_type: str, device):
         if self.a_cov is None:
@@ -115,8 +168,12 @@ class DPKFAC:
                  f_freq: int = 1, k_freq: int = 1,
                  assignment: Union[str, Sequence[Sequence[int]]] = "round_robin",
                  process_group=None, precision: str = "tf32", precond_precision: str = "3xtf32",
-                 grad_scale: Union[str, float] = "batch", check_numerics: Union[bool, str] = True):
+                 grad_scale: Union[str, float] = "batch", check_numerics: Union[bool, str] = True,
+                 im2col: str = "materialize"):
         self.hyper = KfacHyper(gamma=gamma, xi=xi, inv_type=inv_type, f_freq=f_freq, k_freq=k_freq)
+        if im2col not in ("materialize", "implicit"):
+            raise ArgumentError("im2col must be 'materialize' or 'implicit'")
+        self.im2col = im2col
         ops.precision_code(precision)
         ops.precision_code(precond_precision)
         self.precision = precision  # factor SYRK (tcgen05 kind::tf32, RN-rounded operands)
@@ -220,7 +277,7 @@ class DPKFAC:
         for ly in self.layers:
             if ly.a_in is None:
                 raise OrderingError("balanced assignment needs one forward/backward pass before step()")
-            m = ly.operand_a().cols
+            m = ly.operand_a("implicit")[0].cols
             costs.append(layer_cost(ly.d_in, ly.d_out, m, self.hyper.inv_type))
         # every rank sees the same shapes (same model, same local batch size), so the
         # deterministic LPT gives the same partition everywhere.
@@ -252,7 +309,7 @@ class DPKFAC:
                 if b is not None and bt is None:
                     raise OrderingError(f"layer {ly.index} ({ly.name}) bias has no gradient")
             off = self.offsets[ly.index]
-            segs.append(ops.segment(wt, bt, off))
+            segs.append(ops.segment(wt, bt, off, tap_major=ly.tap_major))
         return segs
 
     # ------------------------------------------------------------ the step
@@ -265,9 +322,11 @@ class DPKFAC:
             self._finalize_balance()
         if not self._bufs_ready:
             self._build_buffers()
-        for ly in self.layers:  # contiguous grads so [W | b] packing is a strided copy
-            if ly.module.weight.grad is not None and not ly.module.weight.grad.is_contiguous():
-                ly.module.weight.grad = ly.module.weight.grad.contiguous()
+        for ly in self.layers:  # dense grads (NCHW or channels_last) so packing is a plain/permuted copy
+            gr = ly.module.weight.grad
+            if gr is not None and not gr.is_contiguous() and not (
+                    gr.dim() == 4 and gr.is_contiguous(memory_format=torch.channels_last)):
+                ly.module.weight.grad = gr.contiguous()
         f_up = t % h.f_freq == 0
         k_up = t % h.k_freq == 0
         owned = self.owned
@@ -275,7 +334,7 @@ class DPKFAC:
         self._mark("start")
         # (1) Kronecker factors + running average: one grouped tcgen05 launch
         if f_up and owned:
-            jobs, keep = [], []
+            jobs, keep, patches = [], [], []
             for ly in owned:
                 if ly.a_in is None or ly.g_out is None:
                     raise ArgumentError(f"worker {self.rank}, layer {ly.index}: captured inputs must be a "
@@ -284,7 +343,10 @@ class DPKFAC:
                 first = not ly.initialized
                 w = 1.0 if first else h.xi
                 beta = 0.0 if first else 1.0 - h.xi
-                oa, og = ly.operand_a(), ly.operand_g()
+                oa, pending = ly.operand_a(self.im2col)
+                og = ly.operand_g()
+                if pending is not None:
+                    patches.append(pending)
                 m = oa.cols
                 if og.cols != m:
                     raise ArgumentError(f"worker {self.rank}, layer {ly.index}: capture batch counts differ: "
@@ -293,6 +355,7 @@ class DPKFAC:
                 jobs.append(ops.factor_job(oa, ly.a_cov, w / m, beta))
                 jobs.append(ops.factor_job(og, ly.g_cov, w * s * s / m, beta))
                 keep.append((ly.a_in, ly.g_out))
+            ops.im2col_materialize(patches)  # one launch for every materialized conv
             ops.syrk_ema(jobs, self.precision, device=self.device)
             for ly in owned:
                 ly.initialized = True
@@ -442,17 +505,22 @@ class DPKFAC:
 
     # ------------------------------------------------------------ state (reference checkpoint names, trainer.py:228-244)
     def state_dict(self) -> dict:
+        """Per owned layer, the reference FactorState fields under trainer.py's names;
+        A-side matrices are always exported in the reference (C, kh, kw) row order."""
         layers = {}
         for ly in getattr(self, "owned", []):
             d = {"initialized": ly.initialized, "last_factor_update": ly.last_factor_update,
                  "last_inverse_update": ly.last_inverse_update}
+            p = ly.a_perm() if ly.a_cov is not None else None
+            sym = (lambda m: m[p][:, p].clone()) if p is not None else (lambda m: m.clone())
+            rows = (lambda m: m[p].clone()) if p is not None else (lambda m: m.clone())
             if ly.a_cov is not None:
-                d["a_cov"], d["g_cov"] = ly.a_cov.clone(), ly.g_cov.clone()
+                d["a_cov"], d["g_cov"] = sym(ly.a_cov), ly.g_cov.clone()
             if ly.holds == "eigen":
-                d["a_eig_q"], d["a_eig_v"] = ly.a_q.clone(), ly.a_w.clone()
+                d["a_eig_q"], d["a_eig_v"] = rows(ly.a_q), ly.a_w.clone()
                 d["g_eig_q"], d["g_eig_v"] = ly.g_q.clone(), ly.g_w.clone()
             elif ly.holds == "inverse":
-                d["a_damped_inv"], d["g_damped_inv"] = ly.a_inv.clone(), ly.g_inv.clone()
+                d["a_damped_inv"], d["g_damped_inv"] = sym(ly.a_inv), ly.g_inv.clone()
             layers[ly.index] = d
         return {"t": self.t, "rank": self.rank, "assignment": self.assignment, "layers": layers,
                 "hyper": dict(self.hyper.__dict__)}
@@ -469,17 +537,23 @@ class DPKFAC:
             ly.initialized = bool(d["initialized"])
             ly.last_factor_update = int(d["last_factor_update"])
             ly.last_inverse_update = int(d["last_inverse_update"])
+            p = ly.a_perm()
+            if p is not None:  # reference order -> held order
+                q = torch.empty_like(p)
+                q[p] = torch.arange(p.numel(), device=p.device)
+            sym = (lambda m: m.to(self.device)[q][:, q]) if p is not None else (lambda m: m)
+            rows = (lambda m: m.to(self.device)[q]) if p is not None else (lambda m: m)
             if "a_cov" in d:
-                ly.a_cov.copy_(d["a_cov"])
+                ly.a_cov.copy_(sym(d["a_cov"]))
                 ly.g_cov.copy_(d["g_cov"])
             if "a_eig_q" in d:
                 ly.alloc_state("eigen", self.device)
-                ly.a_q.copy_(d["a_eig_q"]), ly.a_w.copy_(d["a_eig_v"])
+                ly.a_q.copy_(rows(d["a_eig_q"])), ly.a_w.copy_(d["a_eig_v"])
                 ly.g_q.copy_(d["g_eig_q"]), ly.g_w.copy_(d["g_eig_v"])
                 ly.holds = "eigen"
             if "a_damped_inv" in d:
                 ly.alloc_state("inverse", self.device)
-                ly.a_inv.copy_(d["a_damped_inv"])
+                ly.a_inv.copy_(sym(d["a_damped_inv"]))
                 ly.g_inv.copy_(d["g_damped_inv"])
                 ly.holds = "inverse"
 

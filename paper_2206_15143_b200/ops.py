@@ -90,9 +90,12 @@ def operand_rows_mn(x: torch.Tensor, bias_row: bool = False) -> L.Operand:
     return o
 
 
-def operand_im2col(x: torch.Tensor, kernel, stride, padding, dilation, bias_row: bool = False) -> L.Operand:
+def operand_im2col(x: torch.Tensor, kernel, stride, padding, dilation, bias_row: bool = False,
+                   tap_major: bool = False) -> L.Operand:
     """Implicit-im2col linear form of an N x C x H x W conv input (F.unfold row
-    order (C, kh, kw), columns (n, oh, ow)); any strides (NCHW or channels_last)."""
+    order (C, kh, kw), columns (n, oh, ow)); any strides (NCHW or channels_last).
+    ``tap_major`` orders rows (kh, kw, C) instead -- the form the engine fetches
+    with TMA im2col loads from a channels-last input."""
     if x.dim() != 4:
         raise ShapeError("conv capture must be N x C x H x W")
     n, c, h, w = x.shape
@@ -104,7 +107,7 @@ def operand_im2col(x: torch.Tensor, kernel, stride, padding, dilation, bias_row:
     ow = (w + 2 * pw - dw * (kw - 1) - 1) // sw + 1
     o = L.Operand()
     o.data = x.data_ptr()
-    o.kind = L.OPND_IM2COL
+    o.kind = L.OPND_IM2COL_TAPMAJOR if tap_major else L.OPND_IM2COL
     o.rows = c * kh * kw
     o.bias_row = int(bias_row)
     o.cols = n * oh * ow
@@ -112,6 +115,21 @@ def operand_im2col(x: torch.Tensor, kernel, stride, padding, dilation, bias_row:
     o.kh, o.kw, o.sh, o.sw, o.ph, o.pw, o.dh, o.dw = kh, kw, sh, sw, ph, pw, dh, dw
     o.sn, o.sc, o.shs, o.sws = x.stride()
     return o
+
+
+def im2col_materialize(pairs):
+    """pairs: [(im2col operand, out tensor M x ld)] -> out[k, r] = X[r, k] (one launch)."""
+    if not pairs:
+        return
+    jobs = []
+    for op, out in pairs:
+        j = L.Im2colJob()
+        j.x = op
+        j.out = out.data_ptr()
+        j.ld = out.stride(0)
+        jobs.append(j)
+    L.check(lib().dpk_im2col_materialize(L.array(L.Im2colJob, jobs), len(jobs), stream_handle()),
+            "dpk_im2col_materialize")
 
 
 # ------------------------------------------------------------------ K1 / K2
@@ -247,17 +265,34 @@ def precondition(jobs: Sequence[L.PrecondJob], eigen: bool, gamma: float, precis
 
 
 # ------------------------------------------------------------------ K7
-def segment(weight: torch.Tensor, bias: Optional[torch.Tensor], offset: int) -> L.Segment:
+def segment(weight: torch.Tensor, bias: Optional[torch.Tensor], offset: int, tap_major: bool = False) -> L.Segment:
+    """[W | b] <-> flat.  ``tap_major`` puts a conv weight's columns in (kh, kw, C)
+    order: free for a channels-last gradient (that IS its memory order), a
+    gather (perm_khw) for a contiguous NCHW one.  The tensor must stay alive until
+    the launch that uses the segment has been enqueued."""
     s = L.Segment()
-    w2 = weight.reshape(weight.shape[0], -1)
-    if w2.stride(1) != 1:
-        raise ArgumentError("weight gradient must be contiguous in its trailing dims")
+    perm = 0
+    if tap_major and weight.dim() == 4 and weight.shape[2] * weight.shape[3] > 1:
+        if weight.is_contiguous(memory_format=torch.channels_last):
+            w2 = weight.permute(0, 2, 3, 1).reshape(weight.shape[0], -1)  # a view: (O, kh*kw*C)
+        elif weight.is_contiguous():
+            w2 = weight.reshape(weight.shape[0], -1)
+            perm = weight.shape[2] * weight.shape[3]
+        else:
+            raise ArgumentError("conv weight gradient must be contiguous (NCHW or channels_last)")
+    else:
+        if weight.dim() == 4 and not weight.is_contiguous():
+            raise ArgumentError("conv weight gradient must be NCHW-contiguous")
+        w2 = weight.reshape(weight.shape[0], -1)
+    if w2.stride(1) != 1 or w2.data_ptr() != weight.data_ptr():
+        raise ArgumentError("weight gradient must be a contiguous view")
     s.weight = w2.data_ptr()
     s.bias = bias.data_ptr() if bias is not None else None
     s.offset = offset
     s.rows = w2.shape[0]
     s.cols_w = w2.shape[1]
     s.ldw = w2.stride(0)
+    s.perm_khw = perm
     return s
 
 

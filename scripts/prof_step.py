@@ -21,15 +21,21 @@ ap.add_argument("--inv-type", default="inverse")
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--profiled", type=int, default=1)
 ap.add_argument("--precision", default="tf32")
+ap.add_argument("--nchw", action="store_true", help="keep the model NCHW (default: channels_last)")
 args = ap.parse_args()
 
 dev = torch.device("cuda", 0)
 ctor, batch, shape, classes = BM.WORKLOADS[args.model]
 torch.manual_seed(0)
 model = ctor().to(dev)
+mf = torch.contiguous_format if args.nchw else torch.channels_last
+if len(shape) == 3:
+    model = model.to(memory_format=mf)
 kf = DPKFAC(model, gamma=0.002, xi=0.95, inv_type=args.inv_type, precision=args.precision,
             check_numerics="deferred")
 x = torch.randn(batch, *shape, device=dev)
+if len(shape) == 3:
+    x = x.contiguous(memory_format=mf)
 y = torch.randint(0, classes, (batch,), device=dev)
 F.cross_entropy(model(x), y).backward()
 kf.step()

@@ -204,3 +204,60 @@ def test_state_dict_roundtrip_stale_resume():
         g2 = one(kf2, model2, t)
         for a, b in zip(g1, g2):
             assert torch.equal(a, b)
+
+
+class ClConv(nn.Module):
+    """Channels-last convs with C % 32 == 0 (TMA im2col path) plus a stem and an fc."""
+
+    def __init__(self):
+        super().__init__()
+        self.stem = nn.Conv2d(3, 32, 3, padding=1, bias=False)
+        self.c1 = nn.Conv2d(32, 64, 3, stride=2, padding=1, bias=False)
+        self.c2 = nn.Conv2d(64, 64, 3, padding=1, bias=False)
+        self.c3 = nn.Conv2d(64, 32, 1, bias=False)
+        self.fc = nn.Linear(32, 10)
+
+    def forward(self, x):
+        x = F.relu(self.stem(x))
+        x = F.relu(self.c1(x))
+        x = F.relu(self.c2(x))
+        x = F.relu(self.c3(x))
+        return self.fc(x.mean((2, 3)))
+
+
+@pytest.mark.parametrize("inv_type", ["inverse", "eigen"])
+def test_channels_last_model_tap_major_factors_match_reference(inv_type):
+    from paper_2206_15143_b200 import DPKFAC
+    torch.manual_seed(3)
+    dev = torch.device("cuda", 0)
+    model = ClConv().to(dev).to(memory_format=torch.channels_last)
+    kf = DPKFAC(model, gamma=0.01, xi=0.8, inv_type=inv_type, precision="tf32" if inv_type == "inverse" else "3xtf32", f_freq=1, k_freq=1)
+    assert kf.layers[1].tap_major and kf.layers[2].tap_major and not kf.layers[3].tap_major
+    h = K.Hyper(gamma=0.01, xi=0.8, inv_type=inv_type, f_freq=1, k_freq=1)
+    rec, hooks = _record(model)
+    states = {}
+    gen = torch.Generator().manual_seed(5)
+    for t in range(2):
+        x = torch.randn(8, 3, 16, 16, generator=gen).to(dev).to(memory_format=torch.channels_last)
+        y = torch.randint(0, 10, (8,), generator=gen).to(dev)
+        model.zero_grad()
+        F.cross_entropy(model(x), y).backward()
+        want = {}
+        for name, m in model.named_modules():
+            if isinstance(m, (nn.Conv2d, nn.Linear)):
+                X, Gm, W = _oracle_layer(m, rec[name], 8)
+                st = states.setdefault(name, K.LayerState())
+                want[name], _ = K.kfac_layer_step(st, X, Gm, W, h, t)
+        kf.step()
+        for name, m in model.named_modules():
+            if isinstance(m, (nn.Conv2d, nn.Linear)):
+                got = m.weight.grad.double().cpu().numpy().reshape(m.weight.shape[0], -1)
+                if m.bias is not None:
+                    got = np.hstack([got, m.bias.grad.double().cpu().numpy()[:, None]])
+                assert rel(got, want[name]) <= TOL, (t, name, rel(got, want[name]))
+    # exported factors are in the reference (C, kh, kw) order
+    sd = kf.state_dict()
+    for i, (name, m) in enumerate((n, m) for n, m in model.named_modules() if isinstance(m, (nn.Conv2d, nn.Linear))):
+        assert rel(sd["layers"][i]["a_cov"].double().cpu().numpy(), states[name].a_cov) <= TOL
+    for hk in hooks:
+        hk.remove()
