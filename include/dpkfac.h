@@ -263,6 +263,8 @@ const char* dpk_version(void);
 const char* dpk_last_error(void);
 /* number of kernels this library has launched in the process (bench evidence) */
 unsigned long long dpk_launch_count(void);
+/* debug: %globaltimer checkpoints (ns) of CTA 0 of the last GEMM launched with DPK_DEBUG_TS=1 */
+int dpk_debug_timestamps(unsigned long long* host16);
 
 #ifdef __cplusplus
 }

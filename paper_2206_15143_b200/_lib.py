@@ -99,6 +99,7 @@ _SIGNATURES = [
     ("dpk_version", C.c_char_p, []),
     ("dpk_last_error", C.c_char_p, []),
     ("dpk_launch_count", C.c_ulonglong, []),
+    ("dpk_debug_timestamps", C.c_int, [C.POINTER(C.c_ulonglong)]),
 ]
 
 EXPORTED = tuple(name for name, _, _ in _SIGNATURES)

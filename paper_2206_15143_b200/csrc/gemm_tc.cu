@@ -92,8 +92,19 @@ struct alignas(64) Problem {
 struct Batch {
   int nprob;
   int total_units;
+  int debug_ts;  // record %globaltimer checkpoints of CTA 0 (dpk_debug_timestamps)
   Problem p[MAXP];
 };
+
+__device__ unsigned long long g_dbg_ts[16];
+
+__device__ __forceinline__ void dbg_ts(const Batch& bt, int slot) {
+  if (bt.debug_ts && blockIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_dbg_ts[slot] = t;
+  }
+}
 
 template <int NPASS>
 struct Cfg {
@@ -101,7 +112,8 @@ struct Cfg {
   static constexpr int OPS = NPASS == 1 ? 2 : 4;  // A, B (+ A_lo, B_lo)
   static constexpr int STAGE_BYTES = OPS * TILE_BYTES;
   static constexpr int BAR_BYTES = 8 * (3 * STAGES + 4) + 16;
-  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + BAR_BYTES;
+  static constexpr int EPI_BYTES = EPI_WARPS * 32 * 33 * 4;  // per-warp 32x32 (+1 pad) staging
+  static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + BAR_BYTES + EPI_BYTES;
 };
 
 __device__ __forceinline__ void decode_unit(const Batch& bt, int u, int& pi, int& tm, int& tn, int& tile,
@@ -371,28 +383,135 @@ __device__ __forceinline__ void issue_tma(int kind, const CUtensorMap* map, cons
 }
 
 // ------------------------------------------------------------------ epilogue
-__device__ __forceinline__ void store_final(const Problem& P, int tm, int tn, int m, int c, const float (&acc)[32]) {
-  const int gm = tm * BM + m;
-  if (gm >= P.M) return;
-  const bool diag = P.symmetric && tm == tn;
-  const int gn0 = tn * BN + c * 32;
-  float vr = 0.f;
-  if (P.epi == EPI_EIGDIV) vr = fmaxf(P.vrow[gm], 0.0f);
-  const int jmax = min(32, min(P.N, diag ? gm + 1 : P.N) - gn0);  // columns to write
+// Problem fields live in the kernel parameter bank and are indexed by the
+// problem id, so every use is an indexed LDC; ptxas happily re-issues those in
+// the row loop (a constant-cache round trip per row).  Pin them in registers.
+__device__ __forceinline__ int pin(int v) {
+  asm volatile("mov.b32 %0, %0;" : "+r"(v));
+  return v;
+}
+__device__ __forceinline__ float pin(float v) {
+  asm volatile("mov.b32 %0, %0;" : "+f"(v));
+  return v;
+}
+template <class T>
+__device__ __forceinline__ T* pin(T* v) {
+  uint64_t x = reinterpret_cast<uint64_t>(v);
+  asm volatile("mov.b64 %0, %0;" : "+l"(x));
+  return reinterpret_cast<T*>(x);
+}
+__device__ __forceinline__ int64_t pin(int64_t v) {
+  asm volatile("mov.b64 %0, %0;" : "+l"(v));
+  return v;
+}
+
+struct Epi {
+  float* out;
+  const float* cin;
+  const float* vrow;
+  const float* vcol;
+  float* part;  // this unit's partial slot (split-K) or nullptr
+  float* out_t;
+  int64_t ldo, ldc, ldt;
+  float alpha, beta, gamma;
+  int M, N, symmetric, eigdiv;
+};
+
+__device__ __forceinline__ Epi load_epi(const Problem& P, int tile, int split) {
+  Epi e;
+  e.out = pin(P.out);
+  e.cin = pin(P.cin);
+  e.vrow = pin(P.vrow);
+  e.vcol = pin(P.vcol);
+  e.part = P.splits > 1 ? pin(P.partials + static_cast<int64_t>(tile * P.splits + split) * BM * BN) : nullptr;
+  e.out_t = pin(P.out_t);
+  e.ldo = pin(P.ldo);
+  e.ldc = pin(P.ldc);
+  e.ldt = pin(P.ldt);
+  e.alpha = pin(P.alpha);
+  e.beta = pin(P.beta);
+  e.gamma = pin(P.gamma);
+  e.M = pin(P.M);
+  e.N = pin(P.N);
+  e.symmetric = pin(P.symmetric);
+  e.eigdiv = pin(P.epi == EPI_EIGDIV ? 1 : 0);
+  return e;
+}
+
+// One warp's 32x32 accumulator block (rows warp*32.., columns c*32..) goes
+// through a padded smem transpose buffer so that every global access is a
+// 128 B coalesced row segment: the direct pass walks rows with lane = column,
+// the mirror / out_t pass walks columns with lane = row.
+__device__ __forceinline__ void store_chunk(const Epi& e, int tm, int tn, int warp, int lane, int c,
+                                            const uint32_t (&r)[32], float* T) {
 #pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const int gn = gn0 + j;
-    if (j >= jmax) continue;  // predicated, keeps acc[] in registers
-    float val = P.alpha * acc[j];
-    if (P.epi == EPI_EIGDIV) {
-      val = val / (vr * fmaxf(P.vcol[gn], 0.0f) + P.gamma);
-    } else if (P.beta != 0.0f) {
-      val += P.beta * P.cin[gm * P.ldc + gn];
-    }
-    P.out[gm * P.ldo + gn] = val;
-    if (P.symmetric && gn != gm) P.out[static_cast<int64_t>(gn) * P.ldo + gm] = val;
-    if (P.out_t) P.out_t[static_cast<int64_t>(gn) * P.ldt + gm] = val;
+  for (int j = 0; j < 32; ++j) T[lane * 33 + j] = __uint_as_float(r[j]);
+  __syncwarp();
+  const int row0 = warp * 32;
+  if (e.part) {
+    float* part = e.part + row0 * BN + c * 32 + lane;
+#pragma unroll 8
+    for (int rr = 0; rr < 32; ++rr) __stcg(part + rr * BN, T[rr * 33 + lane]);
+    __syncwarp();
+    return;
   }
+  const bool diag = e.symmetric && tm == tn;
+  const int gn = tn * BN + c * 32 + lane;
+  const int gm0 = tm * BM + row0;
+  const int nrows = min(32, e.M - gm0);
+  // row rr is written by this lane iff rr < nrows, gn < N and (not diag or gn <= gm)
+  const int rlo = diag ? max(0, gn - gm0) : 0;
+  const bool col_ok = gn < e.N;
+  float vc = 0.f;
+  if (e.eigdiv && col_ok) vc = fmaxf(__ldg(e.vcol + gn), 0.0f);
+  float* op = e.out + static_cast<int64_t>(gm0) * e.ldo + gn;
+  if (e.eigdiv) {
+#pragma unroll 8
+    for (int rr = 0; rr < 32; ++rr) {
+      if (col_ok && rr >= rlo && rr < nrows) {
+        const float val = e.alpha * T[rr * 33 + lane] / (fmaxf(__ldg(e.vrow + gm0 + rr), 0.0f) * vc + e.gamma);
+        __stcg(op + rr * e.ldo, val);
+        T[rr * 33 + lane] = val;
+      }
+    }
+  } else if (e.beta != 0.0f) {
+    const float* cp = e.cin + static_cast<int64_t>(gm0) * e.ldc + gn;
+#pragma unroll 8
+    for (int rr = 0; rr < 32; ++rr) {
+      if (col_ok && rr >= rlo && rr < nrows) {
+        const float val = e.alpha * T[rr * 33 + lane] + e.beta * __ldcg(cp + rr * e.ldc);
+        __stcg(op + rr * e.ldo, val);
+        T[rr * 33 + lane] = val;
+      }
+    }
+  } else {
+#pragma unroll 8
+    for (int rr = 0; rr < 32; ++rr) {
+      if (col_ok && rr >= rlo && rr < nrows) {
+        const float val = e.alpha * T[rr * 33 + lane];
+        __stcg(op + rr * e.ldo, val);
+        T[rr * 33 + lane] = val;
+      }
+    }
+  }
+  __syncwarp();
+  if (e.symmetric || e.out_t) {
+    const int gm = gm0 + lane;
+    const int gn0 = tn * BN + c * 32;
+    // columns written in the direct pass for this row: g < N and (not diag or g <= gm)
+    const int jend = lane < nrows ? min(32, min(e.N, diag ? gm + 1 : e.N) - gn0) : 0;
+    const bool mirror = e.symmetric != 0;
+#pragma unroll 8
+    for (int j = 0; j < 32; ++j) {
+      if (j < jend) {
+        const int g = gn0 + j;
+        const float val = T[lane * 33 + j];
+        if (mirror && g != gm) __stcg(e.out + static_cast<int64_t>(g) * e.ldo + gm, val);
+        if (e.out_t) __stcg(e.out_t + static_cast<int64_t>(g) * e.ldt + gm, val);
+      }
+    }
+  }
+  __syncwarp();
 }
 
 template <int NPASS, bool RN>
@@ -415,6 +534,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) dbg_ts(bt, 0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -433,6 +553,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(gbase + (tmem_slot - base));
+  if (threadIdx.x == 0) dbg_ts(bt, 1);
 
   if (warp == TMA_WARP) {
     // =============================== TMA issuer: runs ahead through the stage ring
@@ -465,6 +586,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
           }
         }
       }
+      dbg_ts(bt, 2);
     }
   } else if (warp >= PROD_WARP0) {
     // =============================== gather / convert warps
@@ -518,6 +640,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         }
       }
     }
+    if (ptid == 0) dbg_ts(bt, 3);
   } else if (warp == MMA_WARP) {
     // =============================== MMA issuer
     if (lane == 0) {
@@ -541,6 +664,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         for (int kc = kc0; kc < kc1; ++kc) {
           mbar_wait(full_bar(stage), phase);
           mbar_wait(tma_bar(stage), phase);
+          if (it == 0 && kc == kc0) dbg_ts(bt, 12);
           tc_fence_after();
           const uint32_t sa = base + stage * C::STAGE_BYTES;
           const uint32_t sb = skip_b ? sa : sa + TILE_BYTES;
@@ -569,10 +693,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         }
         mma_commit(tfull_bar(acc));
       }
+      dbg_ts(bt, 4);
     }
   } else {
     // =============================== epilogue (warps 0-3, thread = tile row)
     const int m = warp * 32 + lane;
+    float* T = reinterpret_cast<float*>(gbase + (bars - base) + C::BAR_BYTES) + warp * 32 * 33;
     int it = 0;
     for (int u = blockIdx.x; u < bt.total_units; u += gridDim.x, ++it) {
       int pi, tm, tn, tile, split;
@@ -580,41 +706,35 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
       const Problem& P = bt.p[pi];
       const int acc = it & 1;
       mbar_wait(tfull_bar(acc), (it >> 1) & 1);
+      if (it == 0 && threadIdx.x == 0) dbg_ts(bt, 9);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(warp * 32) << 16);
-      float* part = nullptr;
-      if (P.splits > 1)
-        part = P.partials + (static_cast<int64_t>(tile * P.splits + split) * BM + m) * BN;
+      const Epi e = load_epi(P, tile, split);
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
         tmem_ld32(taddr + c * 32, r);
         tmem_ld_wait();
-        float accv[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) accv[j] = __uint_as_float(r[j]);
-        if (P.splits == 1) {
-          store_final(P, tm, tn, m, c, accv);
-        } else {
-          float4* dst = reinterpret_cast<float4*>(part + c * 32);
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            __stcg(dst + q, make_float4(accv[4 * q], accv[4 * q + 1], accv[4 * q + 2], accv[4 * q + 3]));
-        }
+        if (it == 0 && c == 0 && threadIdx.x == 0) dbg_ts(bt, 10);
+        store_chunk(e, tm, tn, warp, lane, c, r, T);
+        if (it == 0 && c == 0 && threadIdx.x == 0) dbg_ts(bt, 11);
       }
       tc_fence_before();
       mbar_arrive(tempty_bar(acc));
       // split-K partials are summed (in split order, deterministic) and finished
       // by splitk_reduce_kernel, spread over the whole GPU
+      if (m == 0) dbg_ts(bt, 5 + (it > 0));
     }
   }
 
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) dbg_ts(bt, 7);
   if (warp == MMA_WARP) {
     __syncwarp();
     tc_fence_after();
     tmem_dealloc(tmem_base, TMEM_COLS);
+    if (lane == 0) dbg_ts(bt, 8);
   }
 }
 
@@ -991,6 +1111,15 @@ int launch_batch(const Batch& bt, cudaStream_t st) {
 
 }  // namespace
 
+bool debug_ts_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DPK_DEBUG_TS");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 size_t gemm_workspace_bytes(const GemmSpec* specs, int n) {
   Plan plan;
   if (n <= 0 || make_plan(specs, n, plan, false) != DPK_OK) return 0;
@@ -1035,6 +1164,7 @@ int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int pre
       units += bt.p[i].ntiles * bt.p[i].splits;
     }
     bt.total_units = units;
+    bt.debug_ts = debug_ts_enabled() ? 1 : 0;
     if (units == 0) continue;
     if (precision == DPK_PREC_3XTF32)
       rc = launch_batch<3, false>(bt, st);
@@ -1126,3 +1256,12 @@ int dpk_conv_im2col_syrk_ema(const dpk_factor_job* jobs, int n_jobs, void* works
 }
 
 }  // extern "C"
+
+// Debug: %globaltimer checkpoints (ns) of CTA 0 of the last GEMM launch made with
+// DPK_DEBUG_TS=1: start, set-up done, TMA done, gathers done, MMA done,
+// epilogue unit 0 / last unit done, final barrier, TMEM released.
+extern "C" int dpk_debug_timestamps(unsigned long long* host16) {
+  if (!host16) return DPK_EARG;
+  return dpk::cuda_status(cudaMemcpyFromSymbol(host16, dpk::g_dbg_ts, sizeof(unsigned long long) * 16),
+                          "cudaMemcpyFromSymbol");
+}
