@@ -31,7 +31,7 @@ namespace dpk {
 namespace {
 
 constexpr int LEAF_N = 128;
-constexpr int LEAF_THREADS = 256;
+constexpr int LEAF_THREADS = 256;  // 16 x 16 thread grid
 constexpr int LEAF_MAX = 256;
 
 struct LeafJob {
@@ -51,66 +51,141 @@ struct LeafBatch {
   LeafJob j[LEAF_MAX];
 };
 
-__global__ void __launch_bounds__(LEAF_THREADS) spd_leaf_kernel(const __grid_constant__ LeafBatch b) {
+// Register-resident leaf.  The (padded) N x N block, N = 16*NB, is spread over a
+// 16 x 16 thread grid with a stride-16 interleave: thread (ty, tx) owns rows
+// ty + 16r and columns tx + 16c (r, c < NB), so every broadcast vector read
+// below is bank-conflict free and the work stays balanced as the active
+// trailing block shrinks.  One fused sweep over k does both
+//   right-looking Cholesky      A[i][j] -= L[i][k] L[j][k]        (i, j > k)
+//   right-looking L^-1 (trtri)  X[i][:] -= L[i][k] X[k][:] / L[k][k]  (i > k)
+// with one __syncthreads per column (double-buffered column / row vectors).
+// Blocks that provably stay zero / untouched are skipped at compile time
+// (kb, r, c are all unrolled).  Padding rows/columns are the identity, so
+// pivots past n are 1 and the real n x n result is unaffected.
+template <int NB>
+__global__ void __launch_bounds__(LEAF_THREADS, 1) spd_leaf_kernel(const __grid_constant__ LeafBatch b) {
+  constexpr int N = 16 * NB;
+  constexpr int LDX = N + 1;
   extern __shared__ float smem[];
+  float* colb = smem;          // [2][N]  column k of the partially factored A
+  float* rowb = smem + 2 * N;  // [2][N]  row k of the partially solved X
+  float* Xs = smem + 4 * N;    // [N][N+1] X for the FULL-mode X^T X
   const LeafJob& J = b.j[blockIdx.x];
   const int n = J.n;
-  const int ld = n + 1;
-  float* S = smem;           // A -> L (lower)
-  float* X = smem + n * ld;  // L^-1 (lower)
-  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
-  constexpr int RY = LEAF_THREADS / 32;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
   const float sh = (J.full && J.shift) ? *J.shift : 0.0f;
-  for (int i = ty; i < n; i += RY)
-    for (int j = tx; j < n; j += 32) {
-      float a = J.src[static_cast<int64_t>(i) * J.lds + j];
-      if (i == j) a += sh;
-      S[i * ld + j] = a;
-      X[i * ld + j] = (i == j) ? 1.0f : 0.0f;
+  const float* src = J.src;
+  const int64_t lds = J.lds;
+  float a[NB][NB], x[NB][NB];
+#pragma unroll
+  for (int r = 0; r < NB; ++r)
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      const int i = ty + 16 * r, j = tx + 16 * c;
+      float v = (i == j) ? 1.0f : 0.0f;
+      if (i < n && j < n) v = src[static_cast<int64_t>(i) * lds + j] + ((i == j) ? sh : 0.0f);
+      a[r][c] = v;
+      x[r][c] = (i == j) ? 1.0f : 0.0f;
     }
-  __syncthreads();
-  // ---- Cholesky (lower), right-looking
-  for (int k = 0; k < n; ++k) {
-    const float p = S[k * ld + k];
-    if (!(p > 0.0f) || !isfinite(p)) {  // uniform: every thread read the same pivot
-      if (tid == 0 && J.info) *J.info = J.fail_code;
-      return;
+#pragma unroll
+  for (int kb = 0; kb < NB; ++kb) {
+#pragma unroll 1
+    for (int kk = 0; kk < 16; ++kk) {
+      const int k = 16 * kb + kk;
+      float* cb = colb + (k & 1) * N;
+      float* rb = rowb + (k & 1) * N;
+      if (tx == kk) {
+#pragma unroll
+        for (int r = kb; r < NB; ++r) cb[ty + 16 * r] = a[r][kb];
+      }
+      if (ty == kk) {
+#pragma unroll
+        for (int c = 0; c <= kb; ++c) rb[tx + 16 * c] = x[kb][c];
+      }
+      __syncthreads();
+      const float p = cb[k];
+      if (!(p > 0.0f) || !isfinite(p)) {  // uniform: every thread read the same pivot
+        if (tid == 0 && J.info) *J.info = J.fail_code;
+        return;
+      }
+      const float inv = 1.0f / sqrtf(p);
+      float lr[NB], lc[NB], xc[NB];
+#pragma unroll
+      for (int r = kb; r < NB; ++r) {
+        const int i = ty + 16 * r;
+        lr[r] = (i > k) ? cb[i] * inv : 0.0f;
+      }
+#pragma unroll
+      for (int c = kb; c < NB; ++c) {
+        const int j = tx + 16 * c;
+        lc[c] = (j > k) ? cb[j] * inv : 0.0f;
+      }
+#pragma unroll
+      for (int c = 0; c <= kb; ++c) xc[c] = rb[tx + 16 * c] * inv;
+#pragma unroll
+      for (int r = kb; r < NB; ++r) {
+#pragma unroll
+        for (int c = kb; c < NB; ++c) a[r][c] = fmaf(-lr[r], lc[c], a[r][c]);
+#pragma unroll
+        for (int c = 0; c <= kb; ++c) x[r][c] = fmaf(-lr[r], xc[c], x[r][c]);
+      }
+      if (ty == kk) {
+#pragma unroll
+        for (int c = 0; c <= kb; ++c) x[kb][c] = xc[c];
+      }
     }
-    const float l = sqrtf(p);
-    const float inv = 1.0f / l;
-    __syncthreads();
-    for (int i = k + tid; i < n; i += LEAF_THREADS) S[i * ld + k] = (i == k) ? l : S[i * ld + k] * inv;
-    __syncthreads();
-    for (int i = k + 1 + ty; i < n; i += RY) {
-      const float lik = S[i * ld + k];
-      for (int j = k + 1 + tx; j <= i; j += 32) S[i * ld + j] -= lik * S[j * ld + k];
-    }
-    __syncthreads();
   }
-  // ---- X = L^-1 (lower), right-looking forward substitution on I
-  for (int k = 0; k < n; ++k) {
-    const float d = 1.0f / S[k * ld + k];
-    for (int j = tid; j <= k; j += LEAF_THREADS) X[k * ld + j] *= d;
-    __syncthreads();
-    for (int i = k + 1 + ty; i < n; i += RY) {
-      const float lik = S[i * ld + k];
-      for (int j = tx; j <= k; j += 32) X[i * ld + j] -= lik * X[k * ld + j];
-    }
-    __syncthreads();
-  }
-  if (!J.full) {
-    for (int i = ty; i < n; i += RY)
-      for (int j = tx; j < n; j += 32) J.dst[static_cast<int64_t>(i) * J.ldd + j] = (j <= i) ? X[i * ld + j] : 0.0f;
+  float* dst = J.dst;
+  const int64_t ldd = J.ldd;
+  if (!J.full) {  // X = L^-1: exactly zero above the diagonal by construction
+#pragma unroll
+    for (int r = 0; r < NB; ++r)
+#pragma unroll
+      for (int c = 0; c < NB; ++c) {
+        const int i = ty + 16 * r, j = tx + 16 * c;
+        if (i < n && j < n) dst[static_cast<int64_t>(i) * ldd + j] = x[r][c];
+      }
     return;
   }
-  // ---- inverse = X^T X, lower entries computed once and mirrored
-  for (int i = ty; i < n; i += RY)
-    for (int j = tx; j <= i; j += 32) {
-      float acc = 0.0f;
-      for (int k = i; k < n; ++k) acc += X[k * ld + i] * X[k * ld + j];
-      J.dst[static_cast<int64_t>(i) * J.ldd + j] = acc;
-      J.dst[static_cast<int64_t>(j) * J.ldd + i] = acc;
+  // ---- inverse = X^T X  (X[k][i] == 0 for k < i: block kb only meets r, c <= kb)
+#pragma unroll
+  for (int r = 0; r < NB; ++r)
+#pragma unroll
+    for (int c = 0; c < NB; ++c) Xs[(ty + 16 * r) * LDX + tx + 16 * c] = x[r][c];
+  __syncthreads();
+  float acc[NB][NB];
+#pragma unroll
+  for (int r = 0; r < NB; ++r)
+#pragma unroll
+    for (int c = 0; c < NB; ++c) acc[r][c] = 0.0f;
+#pragma unroll
+  for (int kb = 0; kb < NB; ++kb) {
+#pragma unroll 4
+    for (int kk = 0; kk < 16; ++kk) {
+      const float* row = Xs + (16 * kb + kk) * LDX;
+      float xi[NB], xj[NB];
+#pragma unroll
+      for (int r = 0; r <= kb; ++r) xi[r] = row[ty + 16 * r];
+#pragma unroll
+      for (int c = 0; c <= kb; ++c) xj[c] = row[tx + 16 * c];
+#pragma unroll
+      for (int r = 0; r <= kb; ++r)
+#pragma unroll
+        for (int c = 0; c <= kb; ++c) acc[r][c] = fmaf(xi[r], xj[c], acc[r][c]);
     }
+  }
+#pragma unroll
+  for (int r = 0; r < NB; ++r)
+#pragma unroll
+    for (int c = 0; c < NB; ++c) {
+      const int i = ty + 16 * r, j = tx + 16 * c;
+      if (i < n && j < n) dst[static_cast<int64_t>(i) * ldd + j] = acc[r][c];
+    }
+}
+
+template <int NB>
+constexpr int leaf_smem_bytes() {
+  return (4 * 16 * NB + 16 * NB * (16 * NB + 1)) * 4;
 }
 
 // Aw = src + shift I for the blocked path; Aw rows are padded to ldw (a multiple
@@ -271,14 +346,21 @@ void make_spd_plan(const dpk_spd_job* jobs, int n, char* base, SpdPlan& plan) {
   plan.gemm_bytes = worst;
 }
 
-int launch_leaves(std::vector<LeafJob>& leaves, cudaStream_t st) {
+template <int NB>
+int launch_leaf_nb(const LeafBatch& b, int cnt, cudaStream_t st) {
   static bool configured = false;
-  const int max_smem = 2 * LEAF_N * (LEAF_N + 1) * 4;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(spd_leaf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+    cudaError_t e = cudaFuncSetAttribute(spd_leaf_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         leaf_smem_bytes<NB>());
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(spd_leaf_kernel)");
     configured = true;
   }
+  spd_leaf_kernel<NB><<<cnt, LEAF_THREADS, leaf_smem_bytes<NB>(), st>>>(b);
+  note_launch();
+  return cuda_status(cudaGetLastError(), "spd_leaf_kernel launch");
+}
+
+int launch_leaves(std::vector<LeafJob>& leaves, cudaStream_t st) {
   thread_local LeafBatch b;
   for (size_t first = 0; first < leaves.size(); first += LEAF_MAX) {
     const int cnt = static_cast<int>(std::min<size_t>(LEAF_MAX, leaves.size() - first));
@@ -288,9 +370,15 @@ int launch_leaves(std::vector<LeafJob>& leaves, cudaStream_t st) {
       b.j[i] = leaves[first + i];
       maxn = std::max(maxn, b.j[i].n);
     }
-    spd_leaf_kernel<<<cnt, LEAF_THREADS, 2 * maxn * (maxn + 1) * 4, st>>>(b);
-    note_launch();
-    int rc = cuda_status(cudaGetLastError(), "spd_leaf_kernel launch");
+    int rc;
+    if (maxn <= 16)
+      rc = launch_leaf_nb<1>(b, cnt, st);
+    else if (maxn <= 32)
+      rc = launch_leaf_nb<2>(b, cnt, st);
+    else if (maxn <= 64)
+      rc = launch_leaf_nb<4>(b, cnt, st);
+    else
+      rc = launch_leaf_nb<8>(b, cnt, st);
     if (rc) return rc;
   }
   return DPK_OK;
