@@ -12,6 +12,9 @@ namespace dpk {
 
 void set_error(const std::string& msg);
 void note_launch();  // counts every kernel this library launches (dpk_launch_count)
+void note_launches(unsigned long long n);  // graph replays: the kernels the graph holds
+unsigned long long launch_counter();
+void set_launch_counter(unsigned long long v);  // captures launch nothing: undo their counts
 int cuda_status(cudaError_t e, const char* what);
 int num_sms();
 
@@ -26,7 +29,14 @@ struct GemmSpec {
   float gamma;          // EIGDIV damping
   float* out_t;         // optional: also write out_t[n*ldt + m] = value (transposed copy)
   int64_t ldt;
+  // operand structure (TRI_*): a tile's K range is clipped to the chunks where
+  // both operands can be nonzero (triangular factors in the SPD recursion)
+  int tri_a = 0;
+  int tri_b = 0;
 };
+constexpr int TRI_NONE = 0;
+constexpr int TRI_LOWER = 1;  // op[r][k] == 0 for k > r
+constexpr int TRI_UPPER = 2;  // op[r][k] == 0 for k < r
 
 size_t gemm_workspace_bytes(const GemmSpec* specs, int n);
 int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int precision, cudaStream_t st);

@@ -87,6 +87,7 @@ struct alignas(64) Problem {
   int unit_begin;
   int tma_a, tma_b;
   int slab_cpn;     // TMA_SLAB: chunks per sample (K index = (sample, 32-pixel chunk))
+  int tri_a, tri_b; // TRI_*: per-tile K clipping for triangular operands
 };
 
 struct Batch {
@@ -137,6 +138,18 @@ __device__ __forceinline__ void decode_unit(const Batch& bt, int u, int& pi, int
     tn = tile - tm * P.tiles_n;
   }
   pi = p;
+}
+
+// K chunks [kc0, kc1) of one unit: the tile's structural range (triangular
+// operands) split into cps-chunk pieces.  May be empty for trailing splits.
+__device__ __forceinline__ void chunk_range(const Problem& P, int tm, int tn, int split, int& kc0, int& kc1) {
+  int lo = 0, hi = P.chunks;
+  if (P.tri_a == TRI_UPPER) lo = max(lo, tm * (BM / BK));
+  if (P.tri_b == TRI_UPPER) lo = max(lo, tn * (BN / BK));
+  if (P.tri_a == TRI_LOWER) hi = min(hi, (tm + 1) * (BM / BK));
+  if (P.tri_b == TRI_LOWER) hi = min(hi, (tn + 1) * (BN / BK));
+  kc0 = lo + split * P.cps;
+  kc1 = min(hi, kc0 + P.cps);
 }
 
 // ------------------------------------------------------------------ manual producer
@@ -405,6 +418,27 @@ __device__ __forceinline__ int64_t pin(int64_t v) {
   return v;
 }
 
+// plain weak global store (st.global.f32): no cache-scope strength, so the LSU
+// never has to order consecutive epilogue stores
+__device__ __forceinline__ void st_out(float* p, float v) {
+  asm volatile("st.global.f32 [%0], %1;" ::"l"(p), "f"(v) : "memory");
+}
+// predicated store: no branch / reconvergence point per element
+__device__ __forceinline__ void st_out_if(bool pred, float* p, float v) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.f32 [%0], %1;\n\t}\n" ::"l"(p), "f"(v),
+      "r"(static_cast<int>(pred))
+      : "memory");
+}
+__device__ __forceinline__ float ld_cg_if(bool pred, const float* p) {
+  float v = 0.0f;
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.global.cg.f32 %0, [%1];\n\t}\n"
+      : "+f"(v)
+      : "l"(p), "r"(static_cast<int>(pred)));
+  return v;
+}
+
 struct Epi {
   float* out;
   const float* cin;
@@ -441,17 +475,32 @@ __device__ __forceinline__ Epi load_epi(const Problem& P, int tile, int split) {
 // One warp's 32x32 accumulator block (rows warp*32.., columns c*32..) goes
 // through a padded smem transpose buffer so that every global access is a
 // 128 B coalesced row segment: the direct pass walks rows with lane = column,
-// the mirror / out_t pass walks columns with lane = row.
+// the mirror / out_t pass walks columns with lane = row.  Every phase first
+// pulls all 32 of its smem (and cin) values into registers, then issues the
+// 32 stores back to back -- no load waits behind a store.
+__device__ __forceinline__ void dbg_raw(bool on, int slot) {
+  if (on) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_dbg_ts[slot] = t;
+  }
+}
+
 __device__ __forceinline__ void store_chunk(const Epi& e, int tm, int tn, int warp, int lane, int c,
-                                            const uint32_t (&r)[32], float* T) {
+                                            const uint32_t (&r)[32], float* T, bool dbg = false) {
 #pragma unroll
   for (int j = 0; j < 32; ++j) T[lane * 33 + j] = __uint_as_float(r[j]);
   __syncwarp();
+  dbg_raw(dbg, 13);
+  float v[32];
+#pragma unroll
+  for (int rr = 0; rr < 32; ++rr) v[rr] = T[rr * 33 + lane];
+  dbg_raw(dbg, 14);
   const int row0 = warp * 32;
   if (e.part) {
     float* part = e.part + row0 * BN + c * 32 + lane;
-#pragma unroll 8
-    for (int rr = 0; rr < 32; ++rr) __stcg(part + rr * BN, T[rr * 33 + lane]);
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) st_out(part + rr * BN, v[rr]);
     __syncwarp();
     return;
   }
@@ -462,52 +511,60 @@ __device__ __forceinline__ void store_chunk(const Epi& e, int tm, int tn, int wa
   // row rr is written by this lane iff rr < nrows, gn < N and (not diag or gn <= gm)
   const int rlo = diag ? max(0, gn - gm0) : 0;
   const bool col_ok = gn < e.N;
-  float vc = 0.f;
-  if (e.eigdiv && col_ok) vc = fmaxf(__ldg(e.vcol + gn), 0.0f);
-  float* op = e.out + static_cast<int64_t>(gm0) * e.ldo + gn;
   if (e.eigdiv) {
-#pragma unroll 8
-    for (int rr = 0; rr < 32; ++rr) {
-      if (col_ok && rr >= rlo && rr < nrows) {
-        const float val = e.alpha * T[rr * 33 + lane] / (fmaxf(__ldg(e.vrow + gm0 + rr), 0.0f) * vc + e.gamma);
-        __stcg(op + rr * e.ldo, val);
-        T[rr * 33 + lane] = val;
-      }
-    }
+    const float vc = col_ok ? fmaxf(__ldg(e.vcol + gn), 0.0f) : 0.0f;
+    // lane rr holds row rr's eigenvalue (one coalesced load), broadcast by shuffle
+    const float vr_lane = lane < nrows ? fmaxf(__ldg(e.vrow + gm0 + lane), 0.0f) : 0.0f;
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) v[rr] = e.alpha * v[rr] / (__shfl_sync(0xffffffffu, vr_lane, rr) * vc + e.gamma);
   } else if (e.beta != 0.0f) {
     const float* cp = e.cin + static_cast<int64_t>(gm0) * e.ldc + gn;
-#pragma unroll 8
+    float cv[32];
+#pragma unroll
     for (int rr = 0; rr < 32; ++rr) {
-      if (col_ok && rr >= rlo && rr < nrows) {
-        const float val = e.alpha * T[rr * 33 + lane] + e.beta * __ldcg(cp + rr * e.ldc);
-        __stcg(op + rr * e.ldo, val);
-        T[rr * 33 + lane] = val;
-      }
+      cv[rr] = ld_cg_if(col_ok && rr >= rlo && rr < nrows, cp);
+      cp += e.ldc;
     }
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) v[rr] = fmaf(e.beta, cv[rr], e.alpha * v[rr]);
   } else {
-#pragma unroll 8
-    for (int rr = 0; rr < 32; ++rr) {
-      if (col_ok && rr >= rlo && rr < nrows) {
-        const float val = e.alpha * T[rr * 33 + lane];
-        __stcg(op + rr * e.ldo, val);
-        T[rr * 33 + lane] = val;
-      }
-    }
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) v[rr] *= e.alpha;
   }
-  __syncwarp();
+  float* op = e.out + static_cast<int64_t>(gm0) * e.ldo + gn;
+  dbg_raw(dbg, 15);
+#pragma unroll
+  for (int rr = 0; rr < 32; ++rr) {
+    st_out_if(col_ok && rr >= rlo && rr < nrows, op, v[rr]);
+    op += e.ldo;
+  }
+  dbg_raw(dbg, 12);
   if (e.symmetric || e.out_t) {
+    __syncwarp();  // every lane has read its column of T
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) T[rr * 33 + lane] = v[rr];
+    __syncwarp();
+    float w[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) w[j] = T[lane * 33 + j];
     const int gm = gm0 + lane;
     const int gn0 = tn * BN + c * 32;
     // columns written in the direct pass for this row: g < N and (not diag or g <= gm)
     const int jend = lane < nrows ? min(32, min(e.N, diag ? gm + 1 : e.N) - gn0) : 0;
-    const bool mirror = e.symmetric != 0;
-#pragma unroll 8
-    for (int j = 0; j < 32; ++j) {
-      if (j < jend) {
-        const int g = gn0 + j;
-        const float val = T[lane * 33 + j];
-        if (mirror && g != gm) __stcg(e.out + static_cast<int64_t>(g) * e.ldo + gm, val);
-        if (e.out_t) __stcg(e.out_t + static_cast<int64_t>(g) * e.ldt + gm, val);
+    if (e.symmetric) {
+      float* mp = e.out + static_cast<int64_t>(gn0) * e.ldo + gm;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        st_out_if(j < jend && gn0 + j != gm, mp, w[j]);
+        mp += e.ldo;
+      }
+    }
+    if (e.out_t) {
+      float* tp = e.out_t + static_cast<int64_t>(gn0) * e.ldt + gm;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        st_out_if(j < jend, tp, w[j]);
+        tp += e.ldt;
       }
     }
   }
@@ -569,8 +626,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         const bool tB = !skip_b && P.tma_b != TMA_NONE;
         if (tA) tma_prefetch_desc(&P.tmap_a);
         if (tB) tma_prefetch_desc(&P.tmap_b);
-        const int kc0 = split * P.cps;
-        const int kc1 = min(P.chunks, kc0 + P.cps);
+        int kc0, kc1;
+        chunk_range(P, tm, tn, split, kc0, kc1);
         const uint32_t bytes = (tA ? tma_tile_bytes(P.tma_a, P.a, tm * BM) : 0u) +
                                (tB ? tma_tile_bytes(P.tma_b, P.b, tn * BN) : 0u);
         for (int kc = kc0; kc < kc1; ++kc) {
@@ -605,8 +662,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
       RowTask ta[NTASK], tb[NTASK];
       if (mA) setup_tasks(P.a, tm * BM, ptid, ta);
       if (mB) setup_tasks(P.b, tn * BN, ptid, tb);
-      const int kc0 = split * P.cps;
-      const int kc1 = min(P.chunks, kc0 + P.cps);
+      int kc0, kc1;
+      chunk_range(P, tm, tn, split, kc0, kc1);
       // manual operands: chunk kc+1's gathers are in flight while chunk kc is stored
       float4 va[NTASK], vb[NTASK], na[NTASK], nb[NTASK];
       if (mA) fetch_tasks(P.a, ta, ptid, static_cast<int64_t>(kc0) * BK, va);
@@ -659,12 +716,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         mbar_wait(tempty_bar(acc), ((it >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * BN;
-        const int kc0 = split * P.cps;
-        const int kc1 = min(P.chunks, kc0 + P.cps);
+        int kc0, kc1;
+        chunk_range(P, tm, tn, split, kc0, kc1);
         for (int kc = kc0; kc < kc1; ++kc) {
           mbar_wait(full_bar(stage), phase);
           mbar_wait(tma_bar(stage), phase);
-          if (it == 0 && kc == kc0) dbg_ts(bt, 12);
+
           tc_fence_after();
           const uint32_t sa = base + stage * C::STAGE_BYTES;
           const uint32_t sb = skip_b ? sa : sa + TILE_BYTES;
@@ -710,13 +767,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(warp * 32) << 16);
       const Epi e = load_epi(P, tile, split);
+      int kc0, kc1;
+      chunk_range(P, tm, tn, split, kc0, kc1);
+      const bool empty = kc1 <= kc0;  // nothing accumulated: the tile's product is zero
 #pragma unroll 1
       for (int c = 0; c < BN / 32; ++c) {
         uint32_t r[32];
-        tmem_ld32(taddr + c * 32, r);
-        tmem_ld_wait();
+        if (empty) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) r[j] = 0u;
+        } else {
+          tmem_ld32(taddr + c * 32, r);
+          tmem_ld_wait();
+        }
         if (it == 0 && c == 0 && threadIdx.x == 0) dbg_ts(bt, 10);
-        store_chunk(e, tm, tn, warp, lane, c, r, T);
+        store_chunk(e, tm, tn, warp, lane, c, r, T, bt.debug_ts && blockIdx.x == 0 && it == 0 && c == 0 && threadIdx.x == 0);
         if (it == 0 && c == 0 && threadIdx.x == 0) dbg_ts(bt, 11);
       }
       tc_fence_before();
@@ -997,6 +1062,8 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
     P.gamma = specs[i].gamma;
     P.out_t = specs[i].out_t;
     P.ldt = specs[i].ldt;
+    P.tri_a = specs[i].tri_a;
+    P.tri_b = specs[i].tri_b;
     if (P.beta != 0.0f && P.cin == nullptr) {
       set_error("dpk_gemm: beta != 0 needs cin");
       return DPK_EARG;
@@ -1184,7 +1251,7 @@ extern "C" {
 
 size_t dpk_gemm_workspace_bytes(const dpk_gemm_job* jobs, int n_jobs) {
   std::vector<dpk::GemmSpec> specs(std::max(n_jobs, 0));
-  for (int i = 0; i < n_jobs; ++i) specs[i] = dpk::GemmSpec{jobs[i], dpk::EPI_LINEAR, nullptr, nullptr, 0.f, nullptr, 0};
+  for (int i = 0; i < n_jobs; ++i) specs[i] = dpk::GemmSpec{jobs[i], dpk::EPI_LINEAR, nullptr, nullptr, 0.f, nullptr, 0, 0, 0};
   return dpk::gemm_workspace_bytes(specs.data(), n_jobs);
 }
 
@@ -1195,7 +1262,7 @@ int dpk_gemm(const dpk_gemm_job* jobs, int n_jobs, void* workspace, size_t ws_by
     return DPK_EARG;
   }
   std::vector<dpk::GemmSpec> specs(n_jobs);
-  for (int i = 0; i < n_jobs; ++i) specs[i] = dpk::GemmSpec{jobs[i], dpk::EPI_LINEAR, nullptr, nullptr, 0.f, nullptr, 0};
+  for (int i = 0; i < n_jobs; ++i) specs[i] = dpk::GemmSpec{jobs[i], dpk::EPI_LINEAR, nullptr, nullptr, 0.f, nullptr, 0, 0, 0};
   return dpk::gemm_launch(specs.data(), n_jobs, workspace, ws_bytes, precision,
                           static_cast<cudaStream_t>(stream));
 }
@@ -1214,7 +1281,7 @@ static std::vector<dpk::GemmSpec> factor_specs(const dpk_factor_job* jobs, int n
     g.alpha = jobs[i].alpha;
     g.beta = jobs[i].beta;
     g.symmetric = 1;
-    specs[i] = dpk::GemmSpec{g, dpk::EPI_LINEAR, nullptr, nullptr, 0.f, nullptr, 0};
+    specs[i] = dpk::GemmSpec{g, dpk::EPI_LINEAR, nullptr, nullptr, 0.f, nullptr, 0, 0, 0};
   }
   return specs;
 }

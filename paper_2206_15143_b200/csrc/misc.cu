@@ -20,6 +20,9 @@ std::atomic<unsigned long long> g_launches{0};
 
 void set_error(const std::string& msg) { g_last_error = msg; }
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void note_launches(unsigned long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+unsigned long long launch_counter() { return g_launches.load(std::memory_order_relaxed); }
+void set_launch_counter(unsigned long long v) { g_launches.store(v, std::memory_order_relaxed); }
 
 int cuda_status(cudaError_t e, const char* what) {
   if (e == cudaSuccess) return DPK_OK;

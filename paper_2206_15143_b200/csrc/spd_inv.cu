@@ -23,6 +23,10 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "dpk_internal.h"
@@ -31,7 +35,7 @@ namespace dpk {
 namespace {
 
 constexpr int LEAF_N = 128;
-constexpr int LEAF_THREADS = 256;  // 16 x 16 thread grid
+constexpr int LEAF_THREADS = 512;  // 16 x 32 thread grid
 constexpr int LEAF_MAX = 256;
 
 struct LeafJob {
@@ -51,87 +55,152 @@ struct LeafBatch {
   LeafJob j[LEAF_MAX];
 };
 
-// Register-resident leaf.  The (padded) N x N block, N = 16*NB, is spread over a
-// 16 x 16 thread grid with a stride-16 interleave: thread (ty, tx) owns rows
-// ty + 16r and columns tx + 16c (r, c < NB), so every broadcast vector read
-// below is bank-conflict free and the work stays balanced as the active
-// trailing block shrinks.  One fused sweep over k does both
-//   right-looking Cholesky      A[i][j] -= L[i][k] L[j][k]        (i, j > k)
+// Register-resident leaf.  The (padded) N x N block, N = 16*RB, is spread over a
+// 16 x 32 grid of 512 threads with strided ownership: thread (ty, tx) owns rows
+// ty + 16r (r < RB) and columns tx + 32c (c < RB/2).  A warp is one ty and 32
+// consecutive tx, so column-vector reads are conflict-free and row-vector
+// reads are broadcasts; the work stays balanced as the trailing block shrinks.
+// One fused sweep does both
+//   right-looking Cholesky      A[i][j] -= L[i][k] L[j][k]            (i, j > k)
 //   right-looking L^-1 (trtri)  X[i][:] -= L[i][k] X[k][:] / L[k][k]  (i > k)
-// with one __syncthreads per column (double-buffered column / row vectors).
-// Blocks that provably stay zero / untouched are skipped at compile time
-// (kb, r, c are all unrolled).  Padding rows/columns are the identity, so
-// pivots past n are 1 and the real n x n result is unaffected.
-template <int NB>
+// four columns per __syncthreads: the owners publish columns k..k+3 of A and
+// rows k..k+3 of X (double-buffered), every thread factors the 4x4 pivot block
+// itself (identically) and applies the rank-4 updates to its registers.
+// Blocks that provably stay zero / untouched are skipped at compile time (the
+// 16-row block index kr is unrolled).  Padding rows/columns are the identity,
+// so pivots past n are 1 and the real n x n result is unaffected.
+template <int RB>
 __global__ void __launch_bounds__(LEAF_THREADS, 1) spd_leaf_kernel(const __grid_constant__ LeafBatch b) {
-  constexpr int N = 16 * NB;
+  constexpr int N = 16 * RB;
+  constexpr int CB = RB / 2;
   constexpr int LDX = N + 1;
   extern __shared__ float smem[];
-  float* colb = smem;          // [2][N]  column k of the partially factored A
-  float* rowb = smem + 2 * N;  // [2][N]  row k of the partially solved X
-  float* Xs = smem + 4 * N;    // [N][N+1] X for the FULL-mode X^T X
+  float* colb = smem;          // [2][4][N] columns k..k+3 of the partially factored A
+  float* rowb = smem + 8 * N;  // [2][4][N] rows k..k+3 of the partially solved X
+  float* Xs = smem + 16 * N;   // [N][N+1] X for the FULL-mode X^T X
   const LeafJob& J = b.j[blockIdx.x];
   const int n = J.n;
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
   const float sh = (J.full && J.shift) ? *J.shift : 0.0f;
   const float* src = J.src;
   const int64_t lds = J.lds;
-  float a[NB][NB], x[NB][NB];
+  float a[RB][CB], x[RB][CB];
+  // unconditional loads (padding reads element 0 and is replaced afterwards):
+  // all RB*CB loads are in flight together instead of one branch-guarded
+  // round trip each
 #pragma unroll
-  for (int r = 0; r < NB; ++r)
+  for (int r = 0; r < RB; ++r)
 #pragma unroll
-    for (int c = 0; c < NB; ++c) {
-      const int i = ty + 16 * r, j = tx + 16 * c;
-      float v = (i == j) ? 1.0f : 0.0f;
-      if (i < n && j < n) v = src[static_cast<int64_t>(i) * lds + j] + ((i == j) ? sh : 0.0f);
-      a[r][c] = v;
+    for (int c = 0; c < CB; ++c) {
+      const int i = ty + 16 * r, j = tx + 32 * c;
+      const bool in = i < n && j < n;
+      a[r][c] = __ldg(src + (in ? static_cast<int64_t>(i) * lds + j : 0));
+    }
+#pragma unroll
+  for (int r = 0; r < RB; ++r)
+#pragma unroll
+    for (int c = 0; c < CB; ++c) {
+      const int i = ty + 16 * r, j = tx + 32 * c;
+      const bool in = i < n && j < n;
+      a[r][c] = in ? a[r][c] + ((i == j) ? sh : 0.0f) : ((i == j) ? 1.0f : 0.0f);
       x[r][c] = (i == j) ? 1.0f : 0.0f;
     }
 #pragma unroll
-  for (int kb = 0; kb < NB; ++kb) {
+  for (int kr = 0; kr < RB; ++kr) {
+    const int kc = kr / 2;  // column block holding k (compile-time after unrolling)
 #pragma unroll 1
-    for (int kk = 0; kk < 16; ++kk) {
-      const int k = 16 * kb + kk;
-      float* cb = colb + (k & 1) * N;
-      float* rb = rowb + (k & 1) * N;
-      if (tx == kk) {
+    for (int kq = 0; kq < 4; ++kq) {
+      const int k = 16 * kr + 4 * kq;
+      float* cb = colb + (kq & 1) * 4 * N;  // group parity (4 groups per kr)
+      float* rb = rowb + (kq & 1) * 4 * N;
+      const int tcol = tx - (k & 31), trow = ty - (k & 15);
+      if (tcol >= 0 && tcol < 4) {
 #pragma unroll
-        for (int r = kb; r < NB; ++r) cb[ty + 16 * r] = a[r][kb];
+        for (int r = kr; r < RB; ++r) cb[tcol * N + ty + 16 * r] = a[r][kc];
       }
-      if (ty == kk) {
+      if (trow >= 0 && trow < 4) {
 #pragma unroll
-        for (int c = 0; c <= kb; ++c) rb[tx + 16 * c] = x[kb][c];
+        for (int c = 0; c <= kc; ++c) rb[trow * N + tx + 32 * c] = x[kr][c];
       }
       __syncthreads();
-      const float p = cb[k];
-      if (!(p > 0.0f) || !isfinite(p)) {  // uniform: every thread read the same pivot
+      const float p00 = cb[k], p10 = cb[k + 1], p20 = cb[k + 2], p30 = cb[k + 3];
+      const float p11 = cb[N + k + 1], p21 = cb[N + k + 2], p31 = cb[N + k + 3];
+      const float p22 = cb[2 * N + k + 2], p32 = cb[2 * N + k + 3];
+      const float p33 = cb[3 * N + k + 3];
+      const float d0 = p00;
+      const float i0 = 1.0f / sqrtf(d0);
+      const float l10 = p10 * i0, l20 = p20 * i0, l30 = p30 * i0;
+      const float d1 = p11 - l10 * l10;
+      const float i1 = 1.0f / sqrtf(d1);
+      const float l21 = (p21 - l20 * l10) * i1, l31 = (p31 - l30 * l10) * i1;
+      const float d2 = p22 - l20 * l20 - l21 * l21;
+      const float i2 = 1.0f / sqrtf(d2);
+      const float l32 = (p32 - l30 * l20 - l31 * l21) * i2;
+      const float d3 = p33 - l30 * l30 - l31 * l31 - l32 * l32;
+      const float i3 = 1.0f / sqrtf(d3);
+      const bool ok = (d0 > 0.0f) && (d1 > 0.0f) && (d2 > 0.0f) && (d3 > 0.0f) && isfinite(i0) && isfinite(i1) &&
+                      isfinite(i2) && isfinite(i3);
+      if (!ok) {  // uniform: every thread factored the same block
         if (tid == 0 && J.info) *J.info = J.fail_code;
         return;
       }
-      const float inv = 1.0f / sqrtf(p);
-      float lr[NB], lc[NB], xc[NB];
+      float lr[RB][4], lc[CB][4];
 #pragma unroll
-      for (int r = kb; r < NB; ++r) {
+      for (int r = kr; r < RB; ++r) {
         const int i = ty + 16 * r;
-        lr[r] = (i > k) ? cb[i] * inv : 0.0f;
+        const float v0 = cb[i] * i0;
+        const float v1 = (cb[N + i] - v0 * l10) * i1;
+        const float v2 = (cb[2 * N + i] - v0 * l20 - v1 * l21) * i2;
+        const float v3 = (cb[3 * N + i] - v0 * l30 - v1 * l31 - v2 * l32) * i3;
+        const bool on = i > k + 3;
+        lr[r][0] = on ? v0 : 0.0f;
+        lr[r][1] = on ? v1 : 0.0f;
+        lr[r][2] = on ? v2 : 0.0f;
+        lr[r][3] = on ? v3 : 0.0f;
       }
 #pragma unroll
-      for (int c = kb; c < NB; ++c) {
-        const int j = tx + 16 * c;
-        lc[c] = (j > k) ? cb[j] * inv : 0.0f;
+      for (int c = kc; c < CB; ++c) {
+        const int j = tx + 32 * c;
+        const float v0 = cb[j] * i0;
+        const float v1 = (cb[N + j] - v0 * l10) * i1;
+        const float v2 = (cb[2 * N + j] - v0 * l20 - v1 * l21) * i2;
+        const float v3 = (cb[3 * N + j] - v0 * l30 - v1 * l31 - v2 * l32) * i3;
+        const bool on = j > k + 3;
+        lc[c][0] = on ? v0 : 0.0f;
+        lc[c][1] = on ? v1 : 0.0f;
+        lc[c][2] = on ? v2 : 0.0f;
+        lc[c][3] = on ? v3 : 0.0f;
+      }
+      float xn[4][CB];  // finished X rows k..k+3, this thread's columns
+#pragma unroll
+      for (int c = 0; c <= kc; ++c) {
+        const int j = tx + 32 * c;
+        xn[0][c] = rb[j] * i0;
+        xn[1][c] = (rb[N + j] - l10 * xn[0][c]) * i1;
+        xn[2][c] = (rb[2 * N + j] - l20 * xn[0][c] - l21 * xn[1][c]) * i2;
+        xn[3][c] = (rb[3 * N + j] - l30 * xn[0][c] - l31 * xn[1][c] - l32 * xn[2][c]) * i3;
       }
 #pragma unroll
-      for (int c = 0; c <= kb; ++c) xc[c] = rb[tx + 16 * c] * inv;
+      for (int r = kr; r < RB; ++r) {
 #pragma unroll
-      for (int r = kb; r < NB; ++r) {
+        for (int c = kc; c < CB; ++c) {
+          float v = a[r][c];
 #pragma unroll
-        for (int c = kb; c < NB; ++c) a[r][c] = fmaf(-lr[r], lc[c], a[r][c]);
+          for (int t = 0; t < 4; ++t) v = fmaf(-lr[r][t], lc[c][t], v);
+          a[r][c] = v;
+        }
 #pragma unroll
-        for (int c = 0; c <= kb; ++c) x[r][c] = fmaf(-lr[r], xc[c], x[r][c]);
+        for (int c = 0; c <= kc; ++c) {
+          float v = x[r][c];
+#pragma unroll
+          for (int t = 0; t < 4; ++t) v = fmaf(-lr[r][t], xn[t][c], v);
+          x[r][c] = v;
+        }
       }
-      if (ty == kk) {
+      if (trow >= 0 && trow < 4) {
 #pragma unroll
-        for (int c = 0; c <= kb; ++c) x[kb][c] = xc[c];
+        for (int c = 0; c <= kc; ++c)
+          x[kr][c] = trow == 0 ? xn[0][c] : trow == 1 ? xn[1][c] : trow == 2 ? xn[2][c] : xn[3][c];
       }
     }
   }
@@ -139,53 +208,53 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) spd_leaf_kernel(const __grid_
   const int64_t ldd = J.ldd;
   if (!J.full) {  // X = L^-1: exactly zero above the diagonal by construction
 #pragma unroll
-    for (int r = 0; r < NB; ++r)
+    for (int r = 0; r < RB; ++r)
 #pragma unroll
-      for (int c = 0; c < NB; ++c) {
-        const int i = ty + 16 * r, j = tx + 16 * c;
+      for (int c = 0; c < CB; ++c) {
+        const int i = ty + 16 * r, j = tx + 32 * c;
         if (i < n && j < n) dst[static_cast<int64_t>(i) * ldd + j] = x[r][c];
       }
     return;
   }
-  // ---- inverse = X^T X  (X[k][i] == 0 for k < i: block kb only meets r, c <= kb)
+  // ---- inverse = X^T X  (X[k][i] == 0 for k < i: 16-row block kr meets r <= kr, c <= kr/2)
 #pragma unroll
-  for (int r = 0; r < NB; ++r)
+  for (int r = 0; r < RB; ++r)
 #pragma unroll
-    for (int c = 0; c < NB; ++c) Xs[(ty + 16 * r) * LDX + tx + 16 * c] = x[r][c];
+    for (int c = 0; c < CB; ++c) Xs[(ty + 16 * r) * LDX + tx + 32 * c] = x[r][c];
   __syncthreads();
-  float acc[NB][NB];
+  float acc[RB][CB];
 #pragma unroll
-  for (int r = 0; r < NB; ++r)
+  for (int r = 0; r < RB; ++r)
 #pragma unroll
-    for (int c = 0; c < NB; ++c) acc[r][c] = 0.0f;
+    for (int c = 0; c < CB; ++c) acc[r][c] = 0.0f;
 #pragma unroll
-  for (int kb = 0; kb < NB; ++kb) {
+  for (int kr = 0; kr < RB; ++kr) {
 #pragma unroll 4
     for (int kk = 0; kk < 16; ++kk) {
-      const float* row = Xs + (16 * kb + kk) * LDX;
-      float xi[NB], xj[NB];
+      const float* row = Xs + (16 * kr + kk) * LDX;
+      float xi[RB], xj[CB];
 #pragma unroll
-      for (int r = 0; r <= kb; ++r) xi[r] = row[ty + 16 * r];
+      for (int r = 0; r <= kr; ++r) xi[r] = row[ty + 16 * r];
 #pragma unroll
-      for (int c = 0; c <= kb; ++c) xj[c] = row[tx + 16 * c];
+      for (int c = 0; c <= kr / 2; ++c) xj[c] = row[tx + 32 * c];
 #pragma unroll
-      for (int r = 0; r <= kb; ++r)
+      for (int r = 0; r <= kr; ++r)
 #pragma unroll
-        for (int c = 0; c <= kb; ++c) acc[r][c] = fmaf(xi[r], xj[c], acc[r][c]);
+        for (int c = 0; c <= kr / 2; ++c) acc[r][c] = fmaf(xi[r], xj[c], acc[r][c]);
     }
   }
 #pragma unroll
-  for (int r = 0; r < NB; ++r)
+  for (int r = 0; r < RB; ++r)
 #pragma unroll
-    for (int c = 0; c < NB; ++c) {
-      const int i = ty + 16 * r, j = tx + 16 * c;
+    for (int c = 0; c < CB; ++c) {
+      const int i = ty + 16 * r, j = tx + 32 * c;
       if (i < n && j < n) dst[static_cast<int64_t>(i) * ldd + j] = acc[r][c];
     }
 }
 
-template <int NB>
+template <int RB>
 constexpr int leaf_smem_bytes() {
-  return (4 * 16 * NB + 16 * NB * (16 * NB + 1)) * 4;
+  return (16 * 16 * RB + 16 * RB * (16 * RB + 1)) * 4;
 }
 
 // Aw = src + shift I for the blocked path; Aw rows are padded to ldw (a multiple
@@ -274,16 +343,20 @@ void build_ops(float* Aw, float* Lb, float* Xb, int64_t ld, int n, float* T, int
   op.leaf = false;
   // L21 = A21 X11^T
   op.g = spec(rows_k(Aw + o21, n2, n1, ld), rows_k(Xb, n1, n1, ld), Lb + o21, ld, 1.0f, 0.0f, 0);
+  op.g.tri_b = TRI_LOWER;  // X11 lower: output column block j only needs k <= j
   ops.push_back(op);
+  op.g.tri_b = TRI_NONE;
   // A22 <- A22 - L21 L21^T
   op.g = spec(rows_k(Lb + o21, n2, n1, ld), rows_k(Lb + o21, n2, n1, ld), Aw + o22, ld, -1.0f, 1.0f, 1);
   ops.push_back(op);
   build_ops(Aw + o22, Lb + o22, Xb + o22, ld, n2, T, fail_code, info, ops);
   // T = L21 X11
   op.g = spec(rows_k(Lb + o21, n2, n1, ld), rows_mn(Xb, n1, n1, ld), T, n1, 1.0f, 0.0f, 0);
+  op.g.tri_b = TRI_UPPER;  // op view of X11 is X11^T: k >= j
   ops.push_back(op);
   // X21 = -X22 T
   op.g = spec(rows_k(Xb + o22, n2, n2, ld), rows_mn(T, n1, n2, n1), Xb + o21, ld, -1.0f, 0.0f, 0);
+  op.g.tri_a = TRI_LOWER;  // X22 lower: k <= i
   ops.push_back(op);
 }
 
@@ -325,6 +398,7 @@ void make_spd_plan(const dpk_spd_job* jobs, int n, char* base, SpdPlan& plan) {
     op.leaf = false;
     // dst = X^T X  (X lower triangular; symmetric output, written with the caller's ld = n)
     op.g = spec(rows_mn(Xb, m, m, ldw), rows_mn(Xb, m, m, ldw), jobs[i].dst, m, 1.0f, 0.0f, 1);
+    op.g.tri_a = op.g.tri_b = TRI_UPPER;  // (X^T X)[i][j] = sum over k >= max(i, j)
     ops.push_back(op);
   }
   plan.rec_bytes = off;
@@ -371,9 +445,7 @@ int launch_leaves(std::vector<LeafJob>& leaves, cudaStream_t st) {
       maxn = std::max(maxn, b.j[i].n);
     }
     int rc;
-    if (maxn <= 16)
-      rc = launch_leaf_nb<1>(b, cnt, st);
-    else if (maxn <= 32)
+    if (maxn <= 32)
       rc = launch_leaf_nb<2>(b, cnt, st);
     else if (maxn <= 64)
       rc = launch_leaf_nb<4>(b, cnt, st);
@@ -383,6 +455,37 @@ int launch_leaves(std::vector<LeafJob>& leaves, cudaStream_t st) {
   }
   return DPK_OK;
 }
+
+// DPK_SPD_TRACE=1: time every lock-step round with events and print a table
+// (diagnostics only; synchronises the stream at the end of the call).
+bool spd_trace() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("DPK_SPD_TRACE");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
+
+double spec_fma(const GemmSpec& g) {
+  const double M = g.job.a.rows, N = g.job.b.rows, K = static_cast<double>(g.job.a.cols);
+  double f = M * N * K;
+  if (g.job.symmetric) f *= 0.5;
+  if (g.tri_a) f *= 0.5;
+  if (g.tri_b) f *= (g.tri_a ? 2.0 / 3.0 : 0.5);
+  return f;
+}
+
+bool spd_graphs_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("DPK_SPD_GRAPH");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+int run_inverse(const dpk_spd_job* jobs, int n_jobs, void* workspace, cudaStream_t st, bool trace);
+int run_cached_graph(const dpk_spd_job* jobs, int n_jobs, void* workspace, size_t ws_bytes, cudaStream_t st);
 
 }  // namespace
 }  // namespace dpk
@@ -415,6 +518,23 @@ int dpk_chol_inv_damped_batched(const dpk_spd_job* jobs, int n_jobs, void* works
     dpk::set_error("dpk_chol_inv_damped_batched: workspace too small");
     return DPK_ENOSPACE;
   }
+  const bool trace = dpk::spd_trace();
+  if (!trace && dpk::spd_graphs_enabled()) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    int rc = dpk::cuda_status(cudaStreamIsCapturing(st, &cs), "cudaStreamIsCapturing");
+    if (rc) return rc;
+    // inside a caller's capture the launches simply join that graph
+    if (cs == cudaStreamCaptureStatusNone) return dpk::run_cached_graph(jobs, n_jobs, workspace, ws_bytes, st);
+  }
+  return dpk::run_inverse(jobs, n_jobs, workspace, st, trace);
+}
+
+}  // extern "C"
+
+namespace dpk {
+namespace {
+
+int run_inverse(const dpk_spd_job* jobs, int n_jobs, void* workspace, cudaStream_t st, bool trace) {
   dpk::SpdPlan plan;
   char* base = static_cast<char*>(workspace);
   dpk::make_spd_plan(jobs, n_jobs, base, plan);
@@ -440,6 +560,13 @@ int dpk_chol_inv_damped_batched(const dpk_spd_job* jobs, int n_jobs, void* works
     if (rc) return rc;
   }
   std::vector<size_t> idx(n_jobs, 0);
+  struct RoundRec {
+    cudaEvent_t e0, e1, e2;
+    int nleaf, maxn, ngemm;
+    double fma;
+    int bm, bn, bk;
+  };
+  std::vector<RoundRec> recs;
   for (;;) {
     std::vector<dpk::LeafJob> leaves;
     std::vector<dpk::GemmSpec> g;
@@ -455,16 +582,138 @@ int dpk_chol_inv_damped_batched(const dpk_spd_job* jobs, int n_jobs, void* works
       ++idx[i];
     }
     if (!any) break;
+    RoundRec rr{};
+    if (trace) {
+      cudaEventCreate(&rr.e0);
+      cudaEventCreate(&rr.e1);
+      cudaEventCreate(&rr.e2);
+      cudaEventRecord(rr.e0, st);
+      rr.nleaf = static_cast<int>(leaves.size());
+      for (auto& l : leaves) rr.maxn = std::max(rr.maxn, l.n);
+      rr.ngemm = static_cast<int>(g.size());
+      double best = -1;
+      for (auto& x : g) {
+        const double f = dpk::spec_fma(x);
+        rr.fma += f;
+        if (f > best) {
+          best = f;
+          rr.bm = x.job.a.rows;
+          rr.bn = x.job.b.rows;
+          rr.bk = static_cast<int>(x.job.a.cols);
+        }
+      }
+    }
     if (!leaves.empty()) {
       int rc = dpk::launch_leaves(leaves, st);
       if (rc) return rc;
     }
+    if (trace) cudaEventRecord(rr.e1, st);
     if (!g.empty()) {
       int rc = dpk::gemm_launch(g.data(), static_cast<int>(g.size()), gemm_ws, plan.gemm_bytes, DPK_PREC_3XTF32, st);
       if (rc) return rc;
     }
+    if (trace) {
+      cudaEventRecord(rr.e2, st);
+      recs.push_back(rr);
+    }
+  }
+  if (trace) {
+    cudaStreamSynchronize(st);
+    double tl = 0, tg = 0, tf = 0;
+    fprintf(stderr, "round  leaves(maxn)  leaf_us  gemms  gemm_us  GFMA  TF/s(useful)  largest MxNxK\n");
+    for (size_t i = 0; i < recs.size(); ++i) {
+      float a = 0, b = 0;
+      cudaEventElapsedTime(&a, recs[i].e0, recs[i].e1);
+      cudaEventElapsedTime(&b, recs[i].e1, recs[i].e2);
+      tl += a;
+      tg += b;
+      tf += recs[i].fma;
+      fprintf(stderr, "%5zu  %4d(%4d)  %8.1f  %5d  %8.1f  %7.3f  %6.1f  %dx%dx%d\n", i, recs[i].nleaf, recs[i].maxn,
+              a * 1e3, recs[i].ngemm, b * 1e3, recs[i].fma / 1e9, b > 0 ? 2 * recs[i].fma / (b * 1e9) : 0.0,
+              recs[i].bm, recs[i].bn, recs[i].bk);
+      cudaEventDestroy(recs[i].e0);
+      cudaEventDestroy(recs[i].e1);
+      cudaEventDestroy(recs[i].e2);
+    }
+    fprintf(stderr, "total: leaves %.3f ms, gemms %.3f ms, %.1f GFMA -> %.1f TF/s useful\n", tl, tg, tf / 1e9,
+            tg > 0 ? 2 * tf / (tg * 1e9) : 0.0);
   }
   return DPK_OK;
 }
 
-}  // extern "C"
+// Every training step inverts the same factor buffers with the same workspace,
+// so the ~200 launches of the lock-step recursion are captured once into a
+// CUDA graph (on a private stream) and replayed: host launch cost per round
+// disappears and the GPU runs the rounds back to back.  Keyed by the exact job
+// list + workspace + device; a small LRU bounds the cache.
+struct GraphEntry {
+  std::vector<char> key;
+  cudaGraphExec_t exec;
+  unsigned long long launches;
+  unsigned long long last_use;
+};
+
+int run_cached_graph(const dpk_spd_job* jobs, int n_jobs, void* workspace, size_t ws_bytes, cudaStream_t st) {
+  static std::mutex mu;
+  static std::vector<GraphEntry> cache;
+  static unsigned long long tick = 0;
+  static std::vector<cudaStream_t> cap_streams;
+  constexpr size_t CACHE_MAX = 8;
+  int dev = 0;
+  int rc = cuda_status(cudaGetDevice(&dev), "cudaGetDevice");
+  if (rc) return rc;
+  std::vector<char> key(sizeof(dpk_spd_job) * n_jobs + sizeof(void*) + sizeof(size_t) + sizeof(int));
+  char* k = key.data();
+  std::memcpy(k, jobs, sizeof(dpk_spd_job) * n_jobs);
+  k += sizeof(dpk_spd_job) * n_jobs;
+  std::memcpy(k, &workspace, sizeof(void*));
+  k += sizeof(void*);
+  std::memcpy(k, &ws_bytes, sizeof(size_t));
+  k += sizeof(size_t);
+  std::memcpy(k, &dev, sizeof(int));
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : cache) {
+    if (e.key == key) {
+      e.last_use = ++tick;
+      rc = cuda_status(cudaGraphLaunch(e.exec, st), "cudaGraphLaunch(spd inverse)");
+      if (!rc) note_launches(e.launches);
+      return rc;
+    }
+  }
+  if (static_cast<int>(cap_streams.size()) <= dev) cap_streams.resize(dev + 1, nullptr);
+  if (!cap_streams[dev]) {
+    rc = cuda_status(cudaStreamCreateWithFlags(&cap_streams[dev], cudaStreamNonBlocking), "cudaStreamCreate");
+    if (rc) return rc;
+  }
+  cudaStream_t cap = cap_streams[dev];
+  const unsigned long long before = launch_counter();
+  rc = cuda_status(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+  if (rc) return rc;
+  rc = run_inverse(jobs, n_jobs, workspace, cap, false);
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ee = cudaStreamEndCapture(cap, &graph);
+  const unsigned long long captured = launch_counter() - before;
+  set_launch_counter(before);
+  if (rc || ee != cudaSuccess) {
+    if (graph) cudaGraphDestroy(graph);
+    return rc ? rc : cuda_status(ee, "cudaStreamEndCapture");
+  }
+  cudaGraphExec_t exec = nullptr;
+  const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  rc = cuda_status(ie, "cudaGraphInstantiate(spd inverse)");
+  if (rc) return rc;
+  if (cache.size() >= CACHE_MAX) {
+    auto old = std::min_element(cache.begin(), cache.end(),
+                                [](const GraphEntry& a, const GraphEntry& b) { return a.last_use < b.last_use; });
+    cudaGraphExecDestroy(old->exec);
+    cache.erase(old);
+  }
+  cache.push_back(GraphEntry{std::move(key), exec, captured, ++tick});
+  rc = cuda_status(cudaGraphLaunch(exec, st), "cudaGraphLaunch(spd inverse)");
+  if (!rc) note_launches(captured);
+  return rc;
+}
+
+}  // namespace
+}  // namespace dpk

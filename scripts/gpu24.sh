@@ -1,0 +1,4 @@
+python scripts/leaf_one.py 128 3
+python scripts/leaf_one.py 64 3
+python scripts/leaf_one.py 128 3 && ncu --set full --clock-control none --import-source on -k regex:spd_leaf -s 3 -c 1 -o gpurun_out/prof_leaf python scripts/leaf_one.py 128 3 > gpurun_out/ncu24.log 2>&1
+echo rc=$?
