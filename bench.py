@@ -245,14 +245,20 @@ def run_ours(args, rank, world, local_rank):
     kf.enable_stage_timing(True)
     launches0 = lib.dpk_launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # DPK_PROFILE_TIMED=1: bracket exactly the timed steps for `ncu --profile-from-start off`
+    prof = os.environ.get("DPK_PROFILE_TIMED") == "1"
     with ClockSampler(local_rank) as clocks:
         sync_barrier()
+        if prof:
+            torch.cuda.cudart().cudaProfilerStart()
         start.record()
         for _ in range(args.steps):
             restore()
             kf.step()
         end.record()
         sync_barrier()
+        if prof:
+            torch.cuda.cudart().cudaProfilerStop()
     kf.check()
     launches = lib.dpk_launch_count() - launches0
     ms_local = start.elapsed_time(end) / args.steps
