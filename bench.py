@@ -296,7 +296,8 @@ def run_ours(args, rank, world, local_rank):
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get(dom)
+                t = json.load(f).get(dom)
+                traffic = t.get("bytes") if isinstance(t, dict) else t
         except (OSError, ValueError):
             traffic = None
     roofline = {"bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
