@@ -178,7 +178,7 @@ def run_reference(args, rank, world):
                                    "layers by the per-layer flop model; median over timed steps"},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ----------------------------------------------------------------- ours
@@ -375,11 +375,28 @@ def run_ours(args, rank, world, local_rank):
             "cpu_baseline": cpu_baseline, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks.summary(),
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     kf.remove_hooks()
 
 
+_JSON_OUT = None
+
+
+def emit(line):
+    """The one JSON result line, on the process's original stdout."""
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    # Keep stdout JSON-only: libraries (NCCL's version banner at communicator
+    # init, cuSOLVER/cuBLAS warnings) write to fd 1 directly, so fd 1 is pointed
+    # at stderr and the result line goes to a private copy of the original fd.
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

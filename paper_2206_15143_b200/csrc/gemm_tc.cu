@@ -68,6 +68,8 @@ __host__ __device__ __forceinline__ bool is_im2col(int kind) {
 struct alignas(64) Problem {
   CUtensorMap tmap_a;  // valid iff tma_a != TMA_NONE
   CUtensorMap tmap_b;
+  CUtensorMap tmap_alo;  // valid iff lo_a (3-pass: low-part shadow of A streamed by TMA)
+  CUtensorMap tmap_blo;
   dpk_operand a;
   dpk_operand b;
   float* out;
@@ -88,6 +90,8 @@ struct alignas(64) Problem {
   int tma_a, tma_b;
   int slab_cpn;     // TMA_SLAB: chunks per sample (K index = (sample, 32-pixel chunk))
   int tri_a, tri_b; // TRI_*: per-tile K clipping for triangular operands
+  int lo_a, lo_b;   // 3-pass: low parts arrive by TMA (no smem conversion)
+  int64_t out_lo;   // element offset of the output's low-part shadow (0 = none)
 };
 
 struct Batch {
@@ -96,6 +100,7 @@ struct Batch {
   int debug_ts;  // record %globaltimer checkpoints of CTA 0 (dpk_debug_timestamps)
   Problem p[MAXP];
 };
+static_assert(sizeof(Batch) <= 32764, "kernel parameter space is 32764 bytes");
 
 __device__ unsigned long long g_dbg_ts[16];
 
@@ -447,6 +452,7 @@ struct Epi {
   float* part;  // this unit's partial slot (split-K) or nullptr
   float* out_t;
   int64_t ldo, ldc, ldt;
+  int64_t out_lo;  // 0: no low-part shadow
   float alpha, beta, gamma;
   int M, N, symmetric, eigdiv;
 };
@@ -462,6 +468,7 @@ __device__ __forceinline__ Epi load_epi(const Problem& P, int tile, int split) {
   e.ldo = pin(P.ldo);
   e.ldc = pin(P.ldc);
   e.ldt = pin(P.ldt);
+  e.out_lo = pin(P.out_lo);
   e.alpha = pin(P.alpha);
   e.beta = pin(P.beta);
   e.gamma = pin(P.gamma);
@@ -538,6 +545,14 @@ __device__ __forceinline__ void store_chunk(const Epi& e, int tm, int tn, int wa
     st_out_if(col_ok && rr >= rlo && rr < nrows, op, v[rr]);
     op += e.ldo;
   }
+  if (e.out_lo) {
+    float* lp = e.out + e.out_lo + static_cast<int64_t>(gm0) * e.ldo + gn;
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) {
+      st_out_if(col_ok && rr >= rlo && rr < nrows, lp, v[rr] - __uint_as_float(tf32_trunc_bits(v[rr])));
+      lp += e.ldo;
+    }
+  }
   dbg_raw(dbg, 12);
   if (e.symmetric || e.out_t) {
     __syncwarp();  // every lane has read its column of T
@@ -557,6 +572,14 @@ __device__ __forceinline__ void store_chunk(const Epi& e, int tm, int tn, int wa
       for (int j = 0; j < 32; ++j) {
         st_out_if(j < jend && gn0 + j != gm, mp, w[j]);
         mp += e.ldo;
+      }
+      if (e.out_lo) {
+        float* lp = e.out + e.out_lo + static_cast<int64_t>(gn0) * e.ldo + gm;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          st_out_if(j < jend && gn0 + j != gm, lp, w[j] - __uint_as_float(tf32_trunc_bits(w[j])));
+          lp += e.ldo;
+        }
       }
     }
     if (e.out_t) {
@@ -624,12 +647,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         const bool skip_b = P.same_ab && tm == tn;
         const bool tA = P.tma_a != TMA_NONE;
         const bool tB = !skip_b && P.tma_b != TMA_NONE;
+        const bool lA = NPASS == 3 && P.lo_a;  // low parts streamed from a shadow
+        const bool lB = NPASS == 3 && !skip_b && P.lo_b;
         if (tA) tma_prefetch_desc(&P.tmap_a);
         if (tB) tma_prefetch_desc(&P.tmap_b);
         int kc0, kc1;
         chunk_range(P, tm, tn, split, kc0, kc1);
         const uint32_t bytes = (tA ? tma_tile_bytes(P.tma_a, P.a, tm * BM) : 0u) +
-                               (tB ? tma_tile_bytes(P.tma_b, P.b, tn * BN) : 0u);
+                               (tB ? tma_tile_bytes(P.tma_b, P.b, tn * BN) : 0u) + (lA ? TILE_BYTES : 0u) +
+                               (lB ? TILE_BYTES : 0u);
         for (int kc = kc0; kc < kc1; ++kc) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t sst = base + stage * C::STAGE_BYTES;
@@ -637,6 +663,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
           mbar_arrive_expect_tx(tma_bar(stage), bytes);
           if (tA) issue_tma(P.tma_a, &P.tmap_a, P.a, sst, tma_bar(stage), tm * BM, kc, P.slab_cpn);
           if (tB) issue_tma(P.tma_b, &P.tmap_b, P.b, sst + TILE_BYTES, tma_bar(stage), tn * BN, kc, P.slab_cpn);
+          if (lA) issue_tma(P.tma_a, &P.tmap_alo, P.a, sst + 2 * TILE_BYTES, tma_bar(stage), tm * BM, kc, 0);
+          if (lB) issue_tma(P.tma_b, &P.tmap_blo, P.b, sst + 3 * TILE_BYTES, tma_bar(stage), tn * BN, kc, 0);
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -659,6 +687,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
       const bool tB = !skip_b && P.tma_b != TMA_NONE;
       const bool mA = !tA;
       const bool mB = !skip_b && !tB;
+      const bool cA = tA && !P.lo_a;  // TMA'd tiles whose low part is computed here
+      const bool cB = tB && !P.lo_b;
       RowTask ta[NTASK], tb[NTASK];
       if (mA) setup_tasks(P.a, tm * BM, ptid, ta);
       if (mB) setup_tasks(P.b, tn * BN, ptid, tb);
@@ -678,10 +708,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         uint8_t* st = gbase + stage * C::STAGE_BYTES;
         if (mA) store_tasks<NPASS, RN>(P.a, ptid, st, st + 2 * TILE_BYTES, va);
         if (mB) store_tasks<NPASS, RN>(P.b, ptid, st + TILE_BYTES, st + 3 * TILE_BYTES, vb);
-        if (CONVERT && (tA || tB)) {
+        if (CONVERT && (cA || cB)) {
           mbar_wait(tma_bar(stage), phase);
-          if (tA) convert_tile<NPASS>(st, st + 2 * TILE_BYTES, ptid);
-          if (tB) convert_tile<NPASS>(st + TILE_BYTES, st + 3 * TILE_BYTES, ptid);
+          if (cA) convert_tile<NPASS>(st, st + 2 * TILE_BYTES, ptid);
+          if (cB) convert_tile<NPASS>(st + TILE_BYTES, st + 3 * TILE_BYTES, ptid);
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -817,6 +847,7 @@ struct RedJob {
   const float* partials;
   float* out_t;
   int64_t ldo, ldc, ldt;
+  int64_t out_lo;  // low-part shadow offset (0 = none)
   float alpha, beta, gamma;
   int M, N, symmetric, epi, tiles_n, splits;
   int slab_begin;  // prefix over (tiles x BM/RED_ROWS) slabs
@@ -874,6 +905,11 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
     J.out[gm * J.ldo + gn] = val;
     if (J.symmetric && gn != gm) J.out[static_cast<int64_t>(gn) * J.ldo + gm] = val;
     if (J.out_t) J.out_t[static_cast<int64_t>(gn) * J.ldt + gm] = val;
+    if (J.out_lo) {
+      const float lo = val - __uint_as_float(tf32_trunc_bits(val));
+      J.out[J.out_lo + gm * J.ldo + gn] = lo;
+      if (J.symmetric && gn != gm) J.out[J.out_lo + static_cast<int64_t>(gn) * J.ldo + gm] = lo;
+    }
   }
 }
 
@@ -1099,7 +1135,24 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
       } else {
         P.tma_b = plan_one(j.b, &P.tmap_b);
       }
+      if (precision == DPK_PREC_3XTF32) {
+        // low-part shadows: the same view shifted by a_lo / b_lo elements
+        auto plan_lo = [&](const dpk_operand& o, int kind, int64_t off, CUtensorMap* m) -> int {
+          if (off == 0 || (kind != TMA_ROWS_K && kind != TMA_ROWS_MN)) return 0;
+          dpk_operand lo = o;
+          lo.data = o.data + off;
+          return plan_tma_2d(lo, m, false) == kind ? 1 : 0;
+        };
+        P.lo_a = plan_lo(j.a, P.tma_a, specs[i].a_lo, &P.tmap_alo);
+        if (P.same_ab) {
+          P.lo_b = P.lo_a;
+          P.tmap_blo = P.tmap_alo;
+        } else {
+          P.lo_b = plan_lo(j.b, P.tma_b, specs[i].b_lo, &P.tmap_blo);
+        }
+      }
     }
+    P.out_lo = specs[i].out_lo;
     total_work += static_cast<int64_t>(P.ntiles) * P.chunks;
   }
   // Split K so that the group yields ~3 units per SM, but never below 32 chunks
@@ -1145,6 +1198,7 @@ int launch_reduce(const std::vector<Problem>& probs, cudaStream_t st) {
     J.ldo = P.ldo;
     J.ldc = P.ldc;
     J.ldt = P.ldt;
+    J.out_lo = P.out_lo;
     J.alpha = P.alpha;
     J.beta = P.beta;
     J.gamma = P.gamma;
