@@ -289,7 +289,7 @@ __global__ void prep_kernel(const __grid_constant__ PrepBatch b) {
     float x = J.src[e];
     if (i == c) x += sh;
     J.dst[i * J.ldw + c] = x;
-    J.dst[J.lo + i * J.ldw + c] = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    if (J.lo) J.dst[J.lo + i * J.ldw + c] = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
   }
 }
 
@@ -318,9 +318,11 @@ size_t region_floats(int n) {
   return (3 * static_cast<size_t>(n) * padded_ld(n) + t_floats(n) + 63) / 64 * 64;
 }
 
+bool spd_lo_enabled();
+
 size_t matrix_ws_floats(int n) {
   if (n <= LEAF_N) return 0;
-  return 2 * region_floats(n) + 4;
+  return (spd_lo_enabled() ? 2 : 1) * region_floats(n) + 4;
 }
 
 GemmSpec spec(const dpk_operand& a, const dpk_operand& b, float* out, int64_t ldo, float alpha, float beta,
@@ -342,7 +344,20 @@ GemmSpec spec(const dpk_operand& a, const dpk_operand& b, float* out, int64_t ld
 // Aw, Lb, Xb share the row stride ld; T has room for n2 x n1 floats.
 // every operand and output below lives in the work region; its 3xTF32 low part
 // is at +lo elements (written by prep / leaf / GEMM epilogues, read by TMA)
+// Streaming low parts doubles operand traffic; with 128x128 tiles the engine is
+// operand-delivery bound, so it measured slower than converting in smem (round
+// 1: 11.7 vs 10.4 ms/step).  Kept behind DPK_SPD_LO=1 for larger tiles.
+bool spd_lo_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("DPK_SPD_LO");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
+
 GemmSpec with_lo(GemmSpec g, int64_t lo, bool out_lo) {
+  if (!spd_lo_enabled()) return g;
   g.a_lo = lo;
   g.b_lo = lo;
   g.out_lo = out_lo ? lo : 0;
@@ -417,12 +432,15 @@ void make_spd_plan(const dpk_spd_job* jobs, int n, char* base, SpdPlan& plan) {
     float* T = Xb + blk;
     const int64_t lo = static_cast<int64_t>(region_floats(m));  // low-part shadow distance
     off += align_up(matrix_ws_floats(m) * sizeof(float), 256);
-    plan.preps.push_back(PrepJob{jobs[i].src, Aw, jobs[i].shift, m, ldw, lo});
+    const int64_t lo_used = spd_lo_enabled() ? lo : 0;
+    plan.preps.push_back(PrepJob{jobs[i].src, Aw, jobs[i].shift, m, ldw, lo_used});
     plan.zero_x.push_back(Xb);
     plan.zero_bytes.push_back(blk * sizeof(float));
-    plan.zero_x.push_back(Xb + lo);
-    plan.zero_bytes.push_back(blk * sizeof(float));
-    build_ops(Aw, Lb, Xb, ldw, m, T, jobs[i].fail_code, jobs[i].info, lo, ops);
+    if (lo_used) {
+      plan.zero_x.push_back(Xb + lo);
+      plan.zero_bytes.push_back(blk * sizeof(float));
+    }
+    build_ops(Aw, Lb, Xb, ldw, m, T, jobs[i].fail_code, jobs[i].info, lo_used, ops);
     Op op{};
     op.leaf = false;
     // dst = X^T X  (X lower triangular; symmetric output, written with the caller's ld = n)
