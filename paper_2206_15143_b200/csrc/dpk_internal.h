@@ -33,13 +33,6 @@ struct GemmSpec {
   // both operands can be nonzero (triangular factors in the SPD recursion)
   int tri_a = 0;
   int tri_b = 0;
-  // 3xTF32 low-part shadows (element offsets from the operand / output data;
-  // 0 = none): an operand with a shadow streams its low part by TMA instead of
-  // having it computed in shared memory, and an output with a shadow gets
-  // lo(v) = v - trunc_tf32(v) written beside v by the epilogue.
-  int64_t a_lo = 0;
-  int64_t b_lo = 0;
-  int64_t out_lo = 0;
 };
 constexpr int TRI_NONE = 0;
 constexpr int TRI_LOWER = 1;  // op[r][k] == 0 for k > r

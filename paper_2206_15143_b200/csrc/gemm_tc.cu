@@ -40,6 +40,7 @@
 #include "dpk_ptx.cuh"
 
 namespace dpk {
+bool debug_ts_enabled();
 namespace {
 
 constexpr int BM = 128;
@@ -55,7 +56,6 @@ constexpr int NPROD = PROD_WARPS * 32;                    // 192 gather / conver
 constexpr int TILE_TASKS = BM * (BK / 4);                 // (row, 16B chunk) tasks per operand tile
 constexpr int NTASK = (TILE_TASKS + NPROD - 1) / NPROD;   // 5 tasks per producer thread
 constexpr int NTHREADS = (PROD_WARP0 + PROD_WARPS) * 32;  // 384
-constexpr uint32_t TMEM_COLS = 2 * BN;                    // two accumulators
 constexpr int MAXP = 32;                                  // problems per launch (kernel params)
 static_assert(NPROD % 8 == 0, "im2col chunk sharing needs NPROD % 8 == 0");
 
@@ -68,8 +68,6 @@ __host__ __device__ __forceinline__ bool is_im2col(int kind) {
 struct alignas(64) Problem {
   CUtensorMap tmap_a;  // valid iff tma_a != TMA_NONE
   CUtensorMap tmap_b;
-  CUtensorMap tmap_alo;  // valid iff lo_a (3-pass: low-part shadow of A streamed by TMA)
-  CUtensorMap tmap_blo;
   dpk_operand a;
   dpk_operand b;
   float* out;
@@ -90,8 +88,6 @@ struct alignas(64) Problem {
   int tma_a, tma_b;
   int slab_cpn;     // TMA_SLAB: chunks per sample (K index = (sample, 32-pixel chunk))
   int tri_a, tri_b; // TRI_*: per-tile K clipping for triangular operands
-  int lo_a, lo_b;   // 3-pass: low parts arrive by TMA (no smem conversion)
-  int64_t out_lo;   // element offset of the output's low-part shadow (0 = none)
 };
 
 struct Batch {
@@ -147,12 +143,14 @@ __device__ __forceinline__ void decode_unit(const Batch& bt, int u, int& pi, int
 
 // K chunks [kc0, kc1) of one unit: the tile's structural range (triangular
 // operands) split into cps-chunk pieces.  May be empty for trailing splits.
+template <int CG>
 __device__ __forceinline__ void chunk_range(const Problem& P, int tm, int tn, int split, int& kc0, int& kc1) {
+  constexpr int TC = 128 * CG / BK;  // K chunks per unit tile edge
   int lo = 0, hi = P.chunks;
-  if (P.tri_a == TRI_UPPER) lo = max(lo, tm * (BM / BK));
-  if (P.tri_b == TRI_UPPER) lo = max(lo, tn * (BN / BK));
-  if (P.tri_a == TRI_LOWER) hi = min(hi, (tm + 1) * (BM / BK));
-  if (P.tri_b == TRI_LOWER) hi = min(hi, (tn + 1) * (BN / BK));
+  if (P.tri_a == TRI_UPPER) lo = max(lo, tm * TC);
+  if (P.tri_b == TRI_UPPER) lo = max(lo, tn * TC);
+  if (P.tri_a == TRI_LOWER) hi = min(hi, (tm + 1) * TC);
+  if (P.tri_b == TRI_LOWER) hi = min(hi, (tn + 1) * TC);
   kc0 = lo + split * P.cps;
   kc1 = min(hi, kc0 + P.cps);
 }
@@ -370,16 +368,27 @@ __device__ __forceinline__ uint32_t tma_tile_bytes(int kind, const dpk_operand& 
   return static_cast<uint32_t>(max(groups, 0)) * 4096u;
 }
 
+// PAIR: signal `bar` (possibly the peer CTA's, a shared::cluster address)
+template <bool PAIR = false>
 __device__ __forceinline__ void issue_tma(int kind, const CUtensorMap* map, const dpk_operand& o, uint32_t dst,
                                           uint32_t bar, int row0, int kc, int cpn) {
+  auto ld2 = [&](uint32_t d, int c0, int c1) {
+    if (PAIR)
+      tma_load_2d_pair(d, map, bar, c0, c1);
+    else
+      tma_load_2d(d, map, bar, c0, c1);
+  };
   if (kind == TMA_ROWS_K) {
-    tma_load_2d(dst, map, bar, kc * BK, row0);
+    ld2(dst, kc * BK, row0);
   } else if (kind == TMA_ROWS_MN) {
 #pragma unroll
-    for (int b = 0; b < BM / 32; ++b) tma_load_2d(dst + b * 4096, map, bar, row0 + 32 * b, kc * BK);
+    for (int b = 0; b < BM / 32; ++b) ld2(dst + b * 4096, row0 + 32 * b, kc * BK);
   } else if (kind == TMA_SLAB) {  // dims {HW, C, N}
     const int n = kc / cpn;
-    tma_load_3d(dst, map, bar, (kc - n * cpn) * BK, row0, n);
+    if (PAIR)
+      tma_load_3d_pair(dst, map, bar, (kc - n * cpn) * BK, row0, n);
+    else
+      tma_load_3d(dst, map, bar, (kc - n * cpn) * BK, row0, n);
   } else {  // TMA_IM2COL: NHWC input, rows (i, j, c); a box = 32 output pixels x 32 channels
     const int64_t k0 = static_cast<int64_t>(kc) * BK;
     const int ohw = o.OH * o.OW;
@@ -394,8 +403,12 @@ __device__ __forceinline__ void issue_tma(int kind, const CUtensorMap* map, cons
       const int tap = r / o.C;
       const int c0 = r - tap * o.C;
       const int i = tap / o.kw, j = tap - (tap / o.kw) * o.kw;
-      tma_load_im2col_4d(dst + b * 4096, map, bar, c0, w0, h0, n, static_cast<uint16_t>(j * o.dw),
-                         static_cast<uint16_t>(i * o.dh));
+      if (PAIR)
+        tma_load_im2col_4d_pair(dst + b * 4096, map, bar, c0, w0, h0, n, static_cast<uint16_t>(j * o.dw),
+                                static_cast<uint16_t>(i * o.dh));
+      else
+        tma_load_im2col_4d(dst + b * 4096, map, bar, c0, w0, h0, n, static_cast<uint16_t>(j * o.dw),
+                           static_cast<uint16_t>(i * o.dh));
     }
   }
 }
@@ -452,23 +465,24 @@ struct Epi {
   float* part;  // this unit's partial slot (split-K) or nullptr
   float* out_t;
   int64_t ldo, ldc, ldt;
-  int64_t out_lo;  // 0: no low-part shadow
   float alpha, beta, gamma;
   int M, N, symmetric, eigdiv;
 };
 
+// unit tiles are (128*CG) x (128*CG); each CTA of a pair owns 128 of its rows
+template <int CG>
 __device__ __forceinline__ Epi load_epi(const Problem& P, int tile, int split) {
+  constexpr int64_t UNIT = static_cast<int64_t>(128 * CG) * (128 * CG);
   Epi e;
   e.out = pin(P.out);
   e.cin = pin(P.cin);
   e.vrow = pin(P.vrow);
   e.vcol = pin(P.vcol);
-  e.part = P.splits > 1 ? pin(P.partials + static_cast<int64_t>(tile * P.splits + split) * BM * BN) : nullptr;
+  e.part = P.splits > 1 ? pin(P.partials + static_cast<int64_t>(tile * P.splits + split) * UNIT) : nullptr;
   e.out_t = pin(P.out_t);
   e.ldo = pin(P.ldo);
   e.ldc = pin(P.ldc);
   e.ldt = pin(P.ldt);
-  e.out_lo = pin(P.out_lo);
   e.alpha = pin(P.alpha);
   e.beta = pin(P.beta);
   e.gamma = pin(P.gamma);
@@ -493,8 +507,11 @@ __device__ __forceinline__ void dbg_raw(bool on, int slot) {
   }
 }
 
-__device__ __forceinline__ void store_chunk(const Epi& e, int tm, int tn, int warp, int lane, int c,
-                                            const uint32_t (&r)[32], float* T, bool dbg = false) {
+// gm0: global row of this warp's first row; gnc: global column of the chunk's
+// first column; part: the chunk's split-K partial (row 0, column 0) with row
+// stride pstride; diag: symmetric diagonal unit (store gn <= gm, mirror gn < gm).
+__device__ __forceinline__ void store_chunk(const Epi& e, bool diag, int gm0, int gnc, float* part, int pstride,
+                                            int lane, const uint32_t (&r)[32], float* T, bool dbg = false) {
 #pragma unroll
   for (int j = 0; j < 32; ++j) T[lane * 33 + j] = __uint_as_float(r[j]);
   __syncwarp();
@@ -503,17 +520,14 @@ __device__ __forceinline__ void store_chunk(const Epi& e, int tm, int tn, int wa
 #pragma unroll
   for (int rr = 0; rr < 32; ++rr) v[rr] = T[rr * 33 + lane];
   dbg_raw(dbg, 14);
-  const int row0 = warp * 32;
-  if (e.part) {
-    float* part = e.part + row0 * BN + c * 32 + lane;
+  if (part) {
+    float* pp = part + lane;
 #pragma unroll
-    for (int rr = 0; rr < 32; ++rr) st_out(part + rr * BN, v[rr]);
+    for (int rr = 0; rr < 32; ++rr) st_out(pp + rr * pstride, v[rr]);
     __syncwarp();
     return;
   }
-  const bool diag = e.symmetric && tm == tn;
-  const int gn = tn * BN + c * 32 + lane;
-  const int gm0 = tm * BM + row0;
+  const int gn = gnc + lane;
   const int nrows = min(32, e.M - gm0);
   // row rr is written by this lane iff rr < nrows, gn < N and (not diag or gn <= gm)
   const int rlo = diag ? max(0, gn - gm0) : 0;
@@ -545,14 +559,6 @@ __device__ __forceinline__ void store_chunk(const Epi& e, int tm, int tn, int wa
     st_out_if(col_ok && rr >= rlo && rr < nrows, op, v[rr]);
     op += e.ldo;
   }
-  if (e.out_lo) {
-    float* lp = e.out + e.out_lo + static_cast<int64_t>(gm0) * e.ldo + gn;
-#pragma unroll
-    for (int rr = 0; rr < 32; ++rr) {
-      st_out_if(col_ok && rr >= rlo && rr < nrows, lp, v[rr] - __uint_as_float(tf32_trunc_bits(v[rr])));
-      lp += e.ldo;
-    }
-  }
   dbg_raw(dbg, 12);
   if (e.symmetric || e.out_t) {
     __syncwarp();  // every lane has read its column of T
@@ -563,7 +569,7 @@ __device__ __forceinline__ void store_chunk(const Epi& e, int tm, int tn, int wa
 #pragma unroll
     for (int j = 0; j < 32; ++j) w[j] = T[lane * 33 + j];
     const int gm = gm0 + lane;
-    const int gn0 = tn * BN + c * 32;
+    const int gn0 = gnc;
     // columns written in the direct pass for this row: g < N and (not diag or g <= gm)
     const int jend = lane < nrows ? min(32, min(e.N, diag ? gm + 1 : e.N) - gn0) : 0;
     if (e.symmetric) {
@@ -572,14 +578,6 @@ __device__ __forceinline__ void store_chunk(const Epi& e, int tm, int tn, int wa
       for (int j = 0; j < 32; ++j) {
         st_out_if(j < jend && gn0 + j != gm, mp, w[j]);
         mp += e.ldo;
-      }
-      if (e.out_lo) {
-        float* lp = e.out + e.out_lo + static_cast<int64_t>(gn0) * e.ldo + gm;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          st_out_if(j < jend && gn0 + j != gm, lp, w[j] - __uint_as_float(tf32_trunc_bits(w[j])));
-          lp += e.ldo;
-        }
       }
     }
     if (e.out_t) {
@@ -594,9 +592,22 @@ __device__ __forceinline__ void store_chunk(const Epi& e, int tm, int tn, int wa
   __syncwarp();
 }
 
-template <int NPASS, bool RN>
+// CG = 1: one CTA per 128x128 unit tile, cta_group::1 MMAs (M=128, N=128).
+// CG = 2: a CTA pair (cluster of 2) per 256x256 unit tile, cta_group::2 MMAs
+// (M=256, N=256) issued by the leader: CTA r stages rows [128r, 128r+128) of
+// the tile's A rows and of its B rows (the pair's two B halves form N=256), so
+// each SM moves half the operand bytes per flop of the CG=1 tile and reads half
+// the shared memory per MMA -- the 1-SM tf32 MMA is otherwise shared-memory
+// bound (MMA operand reads + TMA writes > 128 B/clk).  Each CTA's TMEM holds its
+// 128 rows x 256 columns.  Producers of both CTAs arrive on the leader's full
+// barrier, both epilogues arrive on the leader's TMEM-empty barrier, and the
+// leader's commits multicast to both CTAs' stage-empty / TMEM-full barriers.
+template <int NPASS, bool RN, int CG>
 __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_constant__ Batch bt) {
   using C = Cfg<NPASS>;
+  constexpr int UT = 128 * CG;                  // unit tile edge (rows and columns)
+  constexpr uint32_t ACC_COLS = UT;             // TMEM columns per accumulator
+  constexpr uint32_t TMEM_N = 2 * ACC_COLS;     // two accumulators
   // TMA'd tiles need a pass before the MMA only for the 3xTF32 low parts: in RN
   // mode the tensor map's TFLOAT32 data type rounds during the copy itself.
   constexpr bool CONVERT = (NPASS == 3);
@@ -614,23 +625,35 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int half = static_cast<int>(rank) * 128;  // this CTA's row offset inside a unit tile
+  const int unit0 = (CG == 2) ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int ustep = (CG == 2) ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
   if (threadIdx.x == 0) dbg_ts(bt, 0);
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
-      mbar_init(full_bar(s), PROD_WARPS);
+      // CG=2: the leader's full barrier counts both CTAs' producers + its TMA thread
+      mbar_init(full_bar(s), CG == 2 ? 2 * PROD_WARPS + 1 : PROD_WARPS);
       mbar_init(empty_bar(s), 1);
       mbar_init(tma_bar(s), 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
-      mbar_init(tempty_bar(a), EPI_WARPS * 32);
+      mbar_init(tempty_bar(a), EPI_WARPS * 32 * CG);
     }
     mbar_fence_init();
   }
-  if (warp == MMA_WARP) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == MMA_WARP) {
+    if (CG == 2)
+      tmem_alloc2(tmem_slot, TMEM_N);
+    else
+      tmem_alloc(tmem_slot, TMEM_N);
+  }
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync_all();  // peer barriers initialised before any remote arrive / multicast
   tc_fence_after();
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(gbase + (tmem_slot - base));
   if (threadIdx.x == 0) dbg_ts(bt, 1);
@@ -640,31 +663,43 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < bt.total_units; u += gridDim.x) {
+      for (int u = unit0; u < bt.total_units; u += ustep) {
         int pi, tm, tn, tile, split;
         decode_unit(bt, u, pi, tm, tn, tile, split);
         const Problem& P = bt.p[pi];
         const bool skip_b = P.same_ab && tm == tn;
         const bool tA = P.tma_a != TMA_NONE;
         const bool tB = !skip_b && P.tma_b != TMA_NONE;
-        const bool lA = NPASS == 3 && P.lo_a;  // low parts streamed from a shadow
-        const bool lB = NPASS == 3 && !skip_b && P.lo_b;
         if (tA) tma_prefetch_desc(&P.tmap_a);
         if (tB) tma_prefetch_desc(&P.tmap_b);
         int kc0, kc1;
-        chunk_range(P, tm, tn, split, kc0, kc1);
-        const uint32_t bytes = (tA ? tma_tile_bytes(P.tma_a, P.a, tm * BM) : 0u) +
-                               (tB ? tma_tile_bytes(P.tma_b, P.b, tn * BN) : 0u) + (lA ? TILE_BYTES : 0u) +
-                               (lB ? TILE_BYTES : 0u);
+        chunk_range<CG>(P, tm, tn, split, kc0, kc1);
+        const int ra = tm * UT + half, rb = tn * UT + half;
+        auto tile_bytes = [&](int a_row, int b_row) -> uint32_t {
+          return (tA ? tma_tile_bytes(P.tma_a, P.a, a_row) : 0u) + (tB ? tma_tile_bytes(P.tma_b, P.b, b_row) : 0u);
+        };
+        const uint32_t bytes = tile_bytes(ra, rb);
+        // CG=2 without an smem conversion: both CTAs' loads complete directly on
+        // the leader's full barrier (cta_group::2 TMA), no producer hand-off
+        const bool conv = CONVERT && (tA || tB);
+        const bool direct = CG == 2 && !conv;
+        const uint32_t pair_bytes = direct ? bytes + tile_bytes(tm * UT + (128 - half), tn * UT + (128 - half)) : 0u;
         for (int kc = kc0; kc < kc1; ++kc) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t sst = base + stage * C::STAGE_BYTES;
-          // exactly one arrival per stage use; tx bytes only for TMA'd tiles
-          mbar_arrive_expect_tx(tma_bar(stage), bytes);
-          if (tA) issue_tma(P.tma_a, &P.tmap_a, P.a, sst, tma_bar(stage), tm * BM, kc, P.slab_cpn);
-          if (tB) issue_tma(P.tma_b, &P.tmap_b, P.b, sst + TILE_BYTES, tma_bar(stage), tn * BN, kc, P.slab_cpn);
-          if (lA) issue_tma(P.tma_a, &P.tmap_alo, P.a, sst + 2 * TILE_BYTES, tma_bar(stage), tm * BM, kc, 0);
-          if (lB) issue_tma(P.tma_b, &P.tmap_blo, P.b, sst + 3 * TILE_BYTES, tma_bar(stage), tn * BN, kc, 0);
+          if (direct) {
+            const uint32_t fb = leader ? full_bar(stage) : mapa_shared(full_bar(stage), 0);
+            mbar_arrive(tma_bar(stage));  // keeps the per-stage phase in step (no bytes)
+            if (leader) mbar_arrive_expect_tx(full_bar(stage), pair_bytes);
+            if (tA) issue_tma<true>(P.tma_a, &P.tmap_a, P.a, sst, fb, ra, kc, P.slab_cpn);
+            if (tB) issue_tma<true>(P.tma_b, &P.tmap_b, P.b, sst + TILE_BYTES, fb, rb, kc, P.slab_cpn);
+          } else {
+            // exactly one arrival per stage use; tx bytes only for TMA'd tiles
+            mbar_arrive_expect_tx(tma_bar(stage), bytes);
+            if (CG == 2 && leader) mbar_arrive(full_bar(stage));  // this thread's count on the pair barrier
+            if (tA) issue_tma(P.tma_a, &P.tmap_a, P.a, sst, tma_bar(stage), ra, kc, P.slab_cpn);
+            if (tB) issue_tma(P.tma_b, &P.tmap_b, P.b, sst + TILE_BYTES, tma_bar(stage), rb, kc, P.slab_cpn);
+          }
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
@@ -678,22 +713,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
     const int ptid = threadIdx.x - PROD_WARP0 * 32;
     int stage = 0;
     uint32_t phase = 0;
-    for (int u = blockIdx.x; u < bt.total_units; u += gridDim.x) {
+    for (int u = unit0; u < bt.total_units; u += ustep) {
       int pi, tm, tn, tile, split;
       decode_unit(bt, u, pi, tm, tn, tile, split);
       const Problem& P = bt.p[pi];
       const bool skip_b = P.same_ab && tm == tn;
       const bool tA = P.tma_a != TMA_NONE;
       const bool tB = !skip_b && P.tma_b != TMA_NONE;
-      const bool mA = !tA;
-      const bool mB = !skip_b && !tB;
-      const bool cA = tA && !P.lo_a;  // TMA'd tiles whose low part is computed here
-      const bool cB = tB && !P.lo_b;
+      const bool mA = CG == 1 && !tA;  // CG=2 problems are planned TMA-only
+      const bool mB = CG == 1 && !skip_b && !tB;
+      const bool cA = tA;  // 3-pass: TMA'd tiles get their low part computed here
+      const bool cB = tB;
       RowTask ta[NTASK], tb[NTASK];
-      if (mA) setup_tasks(P.a, tm * BM, ptid, ta);
-      if (mB) setup_tasks(P.b, tn * BN, ptid, tb);
+      if (mA) setup_tasks(P.a, tm * UT, ptid, ta);
+      if (mB) setup_tasks(P.b, tn * UT, ptid, tb);
       int kc0, kc1;
-      chunk_range(P, tm, tn, split, kc0, kc1);
+      chunk_range<CG>(P, tm, tn, split, kc0, kc1);
       // manual operands: chunk kc+1's gathers are in flight while chunk kc is stored
       float4 va[NTASK], vb[NTASK], na[NTASK], nb[NTASK];
       if (mA) fetch_tasks(P.a, ta, ptid, static_cast<int64_t>(kc0) * BK, va);
@@ -708,6 +743,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         uint8_t* st = gbase + stage * C::STAGE_BYTES;
         if (mA) store_tasks<NPASS, RN>(P.a, ptid, st, st + 2 * TILE_BYTES, va);
         if (mB) store_tasks<NPASS, RN>(P.b, ptid, st + TILE_BYTES, st + 3 * TILE_BYTES, vb);
+        // CG=2 with a conversion: the leader's MMA cannot see this CTA's TMA
+        // barrier, so the producers forward its completion with their arrival
+        // (without one, the loads signal the leader's full barrier directly)
         if (CONVERT && (cA || cB)) {
           mbar_wait(tma_bar(stage), phase);
           if (cA) convert_tile<NPASS>(st, st + 2 * TILE_BYTES, ptid);
@@ -715,7 +753,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(full_bar(stage));
+        if (lane == 0) {
+          if (CG == 2 && !leader)
+            mbar_arrive_remote(mapa_shared(full_bar(stage), 0));
+          else
+            mbar_arrive(full_bar(stage));
+        }
         if (++stage == C::STAGES) {
           stage = 0;
           phase ^= 1;
@@ -729,29 +772,35 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
     }
     if (ptid == 0) dbg_ts(bt, 3);
   } else if (warp == MMA_WARP) {
-    // =============================== MMA issuer
-    if (lane == 0) {
+    // =============================== MMA issuer (CG=2: the leader CTA only)
+    if (lane == 0 && leader) {
       int stage = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int u = blockIdx.x; u < bt.total_units; u += gridDim.x, ++it) {
+      for (int u = unit0; u < bt.total_units; u += ustep, ++it) {
         int pi, tm, tn, tile, split;
         decode_unit(bt, u, pi, tm, tn, tile, split);
         const Problem& P = bt.p[pi];
         const bool skip_b = P.same_ab && tm == tn;
         const int a_mn = P.tma_a == TMA_ROWS_MN || P.tma_a == TMA_IM2COL;
         const int b_mn = skip_b ? a_mn : (P.tma_b == TMA_ROWS_MN || P.tma_b == TMA_IM2COL);
-        const uint32_t idesc = idesc_tf32(BM, BN, a_mn, b_mn);
+        const uint32_t idesc = idesc_tf32(UT, UT, a_mn, b_mn);
         const int acc = it & 1;
-        mbar_wait(tempty_bar(acc), ((it >> 1) & 1) ^ 1);
+        if (CG == 2)
+          mbar_wait_cluster(tempty_bar(acc), ((it >> 1) & 1) ^ 1);
+        else
+          mbar_wait(tempty_bar(acc), ((it >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem_base + acc * BN;
+        const uint32_t d = tmem_base + acc * ACC_COLS;
         int kc0, kc1;
-        chunk_range(P, tm, tn, split, kc0, kc1);
+        chunk_range<CG>(P, tm, tn, split, kc0, kc1);
         for (int kc = kc0; kc < kc1; ++kc) {
-          mbar_wait(full_bar(stage), phase);
-          mbar_wait(tma_bar(stage), phase);
-
+          if (CG == 2) {
+            mbar_wait_cluster(full_bar(stage), phase);  // producers of both CTAs (TMA forwarded)
+          } else {
+            mbar_wait(full_bar(stage), phase);
+            mbar_wait(tma_bar(stage), phase);
+          }
           tc_fence_after();
           const uint32_t sa = base + stage * C::STAGE_BYTES;
           const uint32_t sb = skip_b ? sa : sa + TILE_BYTES;
@@ -764,30 +813,45 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
             const uint32_t ob = b_mn ? s * 1024 : s * 32;
             const uint64_t da = a_mn ? sdesc_mnmajor_sw128(sa + oa, 4096) : sdesc_kmajor_sw128(sa + oa);
             const uint64_t db = b_mn ? sdesc_mnmajor_sw128(sb + ob, 4096) : sdesc_kmajor_sw128(sb + ob);
-            mma_tf32(d, da, db, idesc, (kc > kc0 || s > 0) ? 1u : 0u);
+            const uint32_t accum = (kc > kc0 || s > 0) ? 1u : 0u;
+            if (CG == 2)
+              mma_tf32_pair(d, da, db, idesc, accum);
+            else
+              mma_tf32(d, da, db, idesc, accum);
             if (NPASS == 3) {
               const uint64_t dbl = b_mn ? sdesc_mnmajor_sw128(sbl + ob, 4096) : sdesc_kmajor_sw128(sbl + ob);
               const uint64_t dal = a_mn ? sdesc_mnmajor_sw128(sal + oa, 4096) : sdesc_kmajor_sw128(sal + oa);
-              mma_tf32(d, da, dbl, idesc, 1u);
-              mma_tf32(d, dal, db, idesc, 1u);
+              if (CG == 2) {
+                mma_tf32_pair(d, da, dbl, idesc, 1u);
+                mma_tf32_pair(d, dal, db, idesc, 1u);
+              } else {
+                mma_tf32(d, da, dbl, idesc, 1u);
+                mma_tf32(d, dal, db, idesc, 1u);
+              }
             }
           }
-          mma_commit(empty_bar(stage));
+          if (CG == 2)
+            mma_commit_pair(empty_bar(stage), 0x3);
+          else
+            mma_commit(empty_bar(stage));
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit(tfull_bar(acc));
+        if (CG == 2)
+          mma_commit_pair(tfull_bar(acc), 0x3);
+        else
+          mma_commit(tfull_bar(acc));
       }
       dbg_ts(bt, 4);
     }
-  } else {
+  } else if (warp < EPI_WARPS) {
     // =============================== epilogue (warps 0-3, thread = tile row)
     const int m = warp * 32 + lane;
     float* T = reinterpret_cast<float*>(gbase + (bars - base) + C::BAR_BYTES) + warp * 32 * 33;
     int it = 0;
-    for (int u = blockIdx.x; u < bt.total_units; u += gridDim.x, ++it) {
+    for (int u = unit0; u < bt.total_units; u += ustep, ++it) {
       int pi, tm, tn, tile, split;
       decode_unit(bt, u, pi, tm, tn, tile, split);
       const Problem& P = bt.p[pi];
@@ -795,13 +859,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
       mbar_wait(tfull_bar(acc), (it >> 1) & 1);
       if (it == 0 && threadIdx.x == 0) dbg_ts(bt, 9);
       tc_fence_after();
-      const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(warp * 32) << 16);
-      const Epi e = load_epi(P, tile, split);
+      const uint32_t taddr = tmem_base + acc * ACC_COLS + (static_cast<uint32_t>(warp * 32) << 16);
+      const Epi e = load_epi<CG>(P, tile, split);
       int kc0, kc1;
-      chunk_range(P, tm, tn, split, kc0, kc1);
+      chunk_range<CG>(P, tm, tn, split, kc0, kc1);
       const bool empty = kc1 <= kc0;  // nothing accumulated: the tile's product is zero
+      const bool diag = e.symmetric && tm == tn;
+      const int gm0 = tm * UT + half + warp * 32;
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
+      for (int c = 0; c < static_cast<int>(ACC_COLS) / 32; ++c) {
         uint32_t r[32];
         if (empty) {
 #pragma unroll
@@ -811,11 +877,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
           tmem_ld_wait();
         }
         if (it == 0 && c == 0 && threadIdx.x == 0) dbg_ts(bt, 10);
-        store_chunk(e, tm, tn, warp, lane, c, r, T, bt.debug_ts && blockIdx.x == 0 && it == 0 && c == 0 && threadIdx.x == 0);
+        float* part = e.part ? e.part + static_cast<int64_t>(half + warp * 32) * UT + c * 32 : nullptr;
+        store_chunk(e, diag, gm0, tn * UT + c * 32, part, UT, lane, r, T,
+                    bt.debug_ts && blockIdx.x == 0 && it == 0 && c == 0 && threadIdx.x == 0);
         if (it == 0 && c == 0 && threadIdx.x == 0) dbg_ts(bt, 11);
       }
       tc_fence_before();
-      mbar_arrive(tempty_bar(acc));
+      if (CG == 2 && !leader)
+        mbar_arrive_remote(mapa_shared(tempty_bar(acc), 0));
+      else
+        mbar_arrive(tempty_bar(acc));
       // split-K partials are summed (in split order, deterministic) and finished
       // by splitk_reduce_kernel, spread over the whole GPU
       if (m == 0) dbg_ts(bt, 5 + (it > 0));
@@ -824,11 +895,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
 
   tc_fence_before();
   __syncthreads();
+  if (CG == 2) cluster_sync_all();  // no CTA leaves while its pair may still signal it
   if (threadIdx.x == 0) dbg_ts(bt, 7);
   if (warp == MMA_WARP) {
     __syncwarp();
     tc_fence_after();
-    tmem_dealloc(tmem_base, TMEM_COLS);
+    if (CG == 2)
+      tmem_dealloc2(tmem_base, TMEM_N);
+    else
+      tmem_dealloc(tmem_base, TMEM_N);
     if (lane == 0) dbg_ts(bt, 8);
   }
 }
@@ -838,7 +913,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
 // columns of one row, sums the partials in split order (deterministic) and
 // applies the same epilogue as the single-split path.
 constexpr int RED_MAX = 96;
-constexpr int RED_ROWS = 8;
 struct RedJob {
   float* out;
   const float* cin;
@@ -847,10 +921,10 @@ struct RedJob {
   const float* partials;
   float* out_t;
   int64_t ldo, ldc, ldt;
-  int64_t out_lo;  // low-part shadow offset (0 = none)
   float alpha, beta, gamma;
   int M, N, symmetric, epi, tiles_n, splits;
-  int slab_begin;  // prefix over (tiles x BM/RED_ROWS) slabs
+  int ut;          // unit tile edge (128 or 256)
+  int slab_begin;  // prefix over (tiles x ut/rows-per-slab) slabs
 };
 struct RedBatch {
   int n;
@@ -858,15 +932,21 @@ struct RedBatch {
   RedJob j[RED_MAX];
 };
 
+// One CTA per (split tile, slab of 1024 elements): 256 threads x 4 consecutive
+// columns; a slab is 8 rows of a 128-wide tile or 4 rows of a 256-wide one.
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constant__ RedBatch b) {
   const int slab = blockIdx.x;
   int p = 0;
   while (p + 1 < b.n && b.j[p + 1].slab_begin <= slab) ++p;
   const RedJob& J = b.j[p];
+  const int ut = J.ut;
+  const int tpr = ut / 4;            // threads per row
+  const int rows_per_slab = 256 / tpr;
   const int local = slab - J.slab_begin;
-  const int tile = local / (BM / RED_ROWS);
-  const int row = (local - tile * (BM / RED_ROWS)) * RED_ROWS + (threadIdx.x >> 5);
-  const int col = (threadIdx.x & 31) * 4;
+  const int slabs_per_tile = ut / rows_per_slab;
+  const int tile = local / slabs_per_tile;
+  const int row = (local - tile * slabs_per_tile) * rows_per_slab + threadIdx.x / tpr;
+  const int col = (threadIdx.x % tpr) * 4;
   int tm, tn;
   if (J.symmetric) {
     int r = static_cast<int>((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
@@ -878,12 +958,13 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
     tm = tile / J.tiles_n;
     tn = tile - tm * J.tiles_n;
   }
-  const int gm = tm * BM + row;
+  const int gm = tm * ut + row;
   if (gm >= J.M) return;
-  const float* src = J.partials + (static_cast<int64_t>(tile) * J.splits * BM + row) * BN + col;
+  const int64_t unit = static_cast<int64_t>(ut) * ut;
+  const float* src = J.partials + static_cast<int64_t>(tile) * J.splits * unit + static_cast<int64_t>(row) * ut + col;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int s = 0; s < J.splits; ++s) {
-    const float4 x = __ldcg(reinterpret_cast<const float4*>(src + static_cast<int64_t>(s) * BM * BN));
+    const float4 x = __ldcg(reinterpret_cast<const float4*>(src + s * unit));
     acc.x += x.x;
     acc.y += x.y;
     acc.z += x.z;
@@ -894,7 +975,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
   const float vr = (J.epi == EPI_EIGDIV) ? fmaxf(J.vrow[gm], 0.0f) : 0.0f;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const int gn = tn * BN + col + e;
+    const int gn = tn * ut + col + e;
     if (gn >= J.N || (diag && gn > gm)) continue;
     float val = J.alpha * a[e];
     if (J.epi == EPI_EIGDIV) {
@@ -905,11 +986,6 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
     J.out[gm * J.ldo + gn] = val;
     if (J.symmetric && gn != gm) J.out[static_cast<int64_t>(gn) * J.ldo + gm] = val;
     if (J.out_t) J.out_t[static_cast<int64_t>(gn) * J.ldt + gm] = val;
-    if (J.out_lo) {
-      const float lo = val - __uint_as_float(tf32_trunc_bits(val));
-      J.out[J.out_lo + gm * J.ldo + gn] = lo;
-      if (J.symmetric && gn != gm) J.out[J.out_lo + static_cast<int64_t>(gn) * J.ldo + gm] = lo;
-    }
   }
 }
 
@@ -1043,6 +1119,7 @@ bool plan_tma_im2col(const dpk_operand& o, CUtensorMap* m, bool rn) {
 struct Plan {
   std::vector<Problem> probs;
   size_t ws_bytes = 0;
+  int cg = 1;
 };
 
 int operand_rows(const dpk_operand& o) { return o.rows + (o.bias_row ? 1 : 0); }
@@ -1059,8 +1136,10 @@ bool valid_operand(const dpk_operand& o) {
   return true;
 }
 
-int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int precision = DPK_PREC_TF32) {
+int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int precision = DPK_PREC_TF32, int cg = 1) {
   const bool rn = precision == DPK_PREC_TF32;
+  const int UT = 128 * cg;
+  plan.cg = cg;
   plan.probs.clear();
   plan.probs.resize(n);
   int64_t total_work = 0;
@@ -1104,8 +1183,8 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
       set_error("dpk_gemm: beta != 0 needs cin");
       return DPK_EARG;
     }
-    const int tmn = (P.M + BM - 1) / BM;
-    P.tiles_n = (P.N + BN - 1) / BN;
+    const int tmn = (P.M + UT - 1) / UT;
+    P.tiles_n = (P.N + UT - 1) / UT;
     P.ntiles = P.symmetric ? tmn * (tmn + 1) / 2 : tmn * P.tiles_n;
     P.chunks = static_cast<int>((j.a.cols + BK - 1) / BK);
     if (P.same_ab && slab_eligible(j.a)) {
@@ -1135,29 +1214,12 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
       } else {
         P.tma_b = plan_one(j.b, &P.tmap_b);
       }
-      if (precision == DPK_PREC_3XTF32) {
-        // low-part shadows: the same view shifted by a_lo / b_lo elements
-        auto plan_lo = [&](const dpk_operand& o, int kind, int64_t off, CUtensorMap* m) -> int {
-          if (off == 0 || (kind != TMA_ROWS_K && kind != TMA_ROWS_MN)) return 0;
-          dpk_operand lo = o;
-          lo.data = o.data + off;
-          return plan_tma_2d(lo, m, false) == kind ? 1 : 0;
-        };
-        P.lo_a = plan_lo(j.a, P.tma_a, specs[i].a_lo, &P.tmap_alo);
-        if (P.same_ab) {
-          P.lo_b = P.lo_a;
-          P.tmap_blo = P.tmap_alo;
-        } else {
-          P.lo_b = plan_lo(j.b, P.tma_b, specs[i].b_lo, &P.tmap_blo);
-        }
-      }
     }
-    P.out_lo = specs[i].out_lo;
     total_work += static_cast<int64_t>(P.ntiles) * P.chunks;
   }
   // Split K so that the group yields ~3 units per SM, but never below 32 chunks
   // (1024 samples) per unit so tile set-up and the partial round trip stay amortised.
-  const int64_t sms = num_sms();
+  const int64_t sms = num_sms() / cg;  // workers: CTAs or CTA pairs
   const int64_t target = std::max<int64_t>(32, (total_work + 3 * sms - 1) / (3 * sms));
   size_t partial_tiles = 0;
   for (auto& P : plan.probs) {
@@ -1166,11 +1228,60 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
     P.splits = (P.chunks + P.cps - 1) / P.cps;
     if (P.splits > 1) partial_tiles += static_cast<size_t>(P.ntiles) * P.splits;
   }
-  plan.ws_bytes = partial_tiles * BM * BN * sizeof(float);
+  plan.ws_bytes = partial_tiles * UT * UT * sizeof(float);
   return DPK_OK;
 }
 
-int launch_reduce(const std::vector<Problem>& probs, cudaStream_t st) {
+// CTA-pair (256x256 unit) eligibility, decided without encoding tensor maps so
+// the workspace query and the launch partition identically: every operand must
+// be TMA-addressable (CG=2 has no manual gather path) and both output edges
+// must exceed one 128 tile (smaller problems waste the 256-wide unit).
+bool tma_possible_2d(const dpk_operand& o) {
+  return !tma_disabled() && !o.bias_row && o.rows >= 1 && aligned16(o.data) && (o.ld * 4) % 16 == 0 &&
+         (o.kind == DPK_OPND_ROWS_K || o.kind == DPK_OPND_ROWS_MN);
+}
+
+bool cg2_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DPK_CG2");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+bool wants_cg2(const GemmSpec& g) {
+  if (!cg2_enabled()) return false;
+  const dpk_gemm_job& j = g.job;
+  if (operand_rows(j.a) <= 128 || operand_rows(j.b) <= 128) return false;
+  const bool same = std::memcmp(&j.a, &j.b, sizeof(dpk_operand)) == 0;
+  auto ok = [&](const dpk_operand& o) {
+    if (tma_possible_2d(o)) return true;
+    if (o.kind == DPK_OPND_IM2COL_TAPMAJOR) return im2col_eligible(o);
+    return false;
+  };
+  if (same && slab_eligible(j.a)) return true;
+  return ok(j.a) && (same || ok(j.b));
+}
+
+// Pairs only pay when the eligible problems give every pair work: a group whose
+// 256x256 units cannot fill the GPU (fewer units than SMs) runs as single CTAs,
+// where twice the CTAs share the same output (measured: the 2048/2304 Schur
+// rounds of the SPD recursion lose 30% as pairs, the 4608 products gain 30%).
+void partition_cg(const GemmSpec* specs, int n, std::vector<GemmSpec>& g1, std::vector<GemmSpec>& g2) {
+  g1.clear();
+  g2.clear();
+  int64_t units2 = 0;
+  for (int i = 0; i < n; ++i) {
+    if (!wants_cg2(specs[i])) continue;
+    const int64_t tm = (operand_rows(specs[i].job.a) + 255) / 256, tn = (operand_rows(specs[i].job.b) + 255) / 256;
+    units2 += specs[i].job.symmetric ? tm * (tm + 1) / 2 : tm * tn;
+  }
+  const bool pairs = units2 >= num_sms();
+  for (int i = 0; i < n; ++i) (pairs && wants_cg2(specs[i]) ? g2 : g1).push_back(specs[i]);
+}
+
+int launch_reduce(const std::vector<Problem>& probs, int ut, cudaStream_t st) {
   thread_local RedBatch rb;
   rb.n = 0;
   rb.total = 0;
@@ -1198,7 +1309,6 @@ int launch_reduce(const std::vector<Problem>& probs, cudaStream_t st) {
     J.ldo = P.ldo;
     J.ldc = P.ldc;
     J.ldt = P.ldt;
-    J.out_lo = P.out_lo;
     J.alpha = P.alpha;
     J.beta = P.beta;
     J.gamma = P.gamma;
@@ -1208,26 +1318,107 @@ int launch_reduce(const std::vector<Problem>& probs, cudaStream_t st) {
     J.epi = P.epi;
     J.tiles_n = P.tiles_n;
     J.splits = P.splits;
+    J.ut = ut;
     J.slab_begin = rb.total;
-    rb.total += P.ntiles * (BM / RED_ROWS);
+    rb.total += P.ntiles * (ut * ut / 1024);
   }
   return flush();
 }
 
-template <int NPASS, bool RN>
+template <int NPASS, bool RN, int CG>
 int launch_batch(const Batch& bt, cudaStream_t st) {
   using C = Cfg<NPASS>;
   static bool configured = false;
+  static int max_pairs = 0;
   if (!configured) {
     cudaError_t e =
-        cudaFuncSetAttribute(tc_gemm_kernel<NPASS, RN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaFuncSetAttribute(tc_gemm_kernel<NPASS, RN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(tc_gemm_kernel)");
+    if (CG == 2) {
+      cudaLaunchConfig_t q = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = 2;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      q.gridDim = dim3(2 * (num_sms() / 2), 1, 1);
+      q.blockDim = dim3(NTHREADS, 1, 1);
+      q.dynamicSmemBytes = C::SMEM;
+      q.attrs = at;
+      q.numAttrs = 1;
+      int clusters = 0;
+      e = cudaOccupancyMaxActiveClusters(&clusters, tc_gemm_kernel<NPASS, RN, CG>, &q);
+      if (e != cudaSuccess) return cuda_status(e, "cudaOccupancyMaxActiveClusters(tc_gemm_kernel)");
+      max_pairs = std::max(clusters, 1);
+    }
     configured = true;
   }
-  const int grid = std::min(bt.total_units, num_sms());
-  tc_gemm_kernel<NPASS, RN><<<grid, NTHREADS, C::SMEM, st>>>(bt);
+  if (CG == 1) {
+    const int grid = std::min(bt.total_units, num_sms());
+    tc_gemm_kernel<NPASS, RN, CG><<<grid, NTHREADS, C::SMEM, st>>>(bt);
+  } else {
+    const int pairs = std::min(bt.total_units, max_pairs);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(2 * pairs, 1, 1);
+    cfg.blockDim = dim3(NTHREADS, 1, 1);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<NPASS, RN, CG>, bt);
+    if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(tc_gemm_kernel, cluster 2)");
+  }
   note_launch();
   return cuda_status(cudaGetLastError(), "tc_gemm_kernel launch");
+}
+
+template <int CG>
+int launch_group(const Batch& bt, int precision, cudaStream_t st) {
+  if (precision == DPK_PREC_3XTF32) return launch_batch<3, false, CG>(bt, st);
+  if (precision == DPK_PREC_TF32_TRUNC) return launch_batch<1, false, CG>(bt, st);
+  return launch_batch<1, true, CG>(bt, st);
+}
+
+// One plan (all problems share the unit-tile size) -> grouped launches of up to
+// MAXP problems, then the split-K reduction.
+int run_plan(Plan& plan, void* ws, size_t ws_bytes, int precision, cudaStream_t st) {
+  if (plan.ws_bytes > ws_bytes) {
+    set_error("dpk_gemm: workspace too small (" + std::to_string(ws_bytes) + " < " +
+              std::to_string(plan.ws_bytes) + ")");
+    return DPK_ENOSPACE;
+  }
+  const int ut = 128 * plan.cg;
+  size_t partial_tiles = 0;
+  float* partials = static_cast<float*>(ws);
+  for (auto& P : plan.probs) {
+    if (P.splits > 1) {
+      P.partials = partials + partial_tiles * ut * ut;
+      partial_tiles += static_cast<size_t>(P.ntiles) * P.splits;
+    }
+  }
+  const int n = static_cast<int>(plan.probs.size());
+  thread_local Batch bt;  // host-side staging only (kernel params are copied at launch)
+  for (int first = 0; first < n; first += MAXP) {
+    const int cnt = std::min(MAXP, n - first);
+    bt.nprob = cnt;
+    int units = 0;
+    for (int i = 0; i < cnt; ++i) {
+      bt.p[i] = plan.probs[first + i];
+      bt.p[i].unit_begin = units;
+      units += bt.p[i].ntiles * bt.p[i].splits;
+    }
+    bt.total_units = units;
+    bt.debug_ts = debug_ts_enabled() ? 1 : 0;
+    if (units == 0) continue;
+    const int rc = plan.cg == 2 ? launch_group<2>(bt, precision, st) : launch_group<1>(bt, precision, st);
+    if (rc != DPK_OK) return rc;
+  }
+  return launch_reduce(plan.probs, ut, st);
 }
 
 }  // namespace
@@ -1242,9 +1433,16 @@ bool debug_ts_enabled() {
 }
 
 size_t gemm_workspace_bytes(const GemmSpec* specs, int n) {
+  if (n <= 0) return 0;
+  std::vector<GemmSpec> g1, g2;
+  partition_cg(specs, n, g1, g2);
+  size_t ws = 0;
   Plan plan;
-  if (n <= 0 || make_plan(specs, n, plan, false) != DPK_OK) return 0;
-  return plan.ws_bytes;
+  if (!g1.empty() && make_plan(g1.data(), static_cast<int>(g1.size()), plan, false, DPK_PREC_TF32, 1) == DPK_OK)
+    ws = std::max(ws, plan.ws_bytes);
+  if (!g2.empty() && make_plan(g2.data(), static_cast<int>(g2.size()), plan, false, DPK_PREC_TF32, 2) == DPK_OK)
+    ws = std::max(ws, plan.ws_bytes);
+  return ws;
 }
 
 int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int precision, cudaStream_t st) {
@@ -1257,45 +1455,30 @@ int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int pre
     set_error("dpk_gemm: precision must be DPK_PREC_TF32, DPK_PREC_TF32_TRUNC or DPK_PREC_3XTF32");
     return DPK_EARG;
   }
-  Plan plan;
-  int rc = make_plan(specs, n, plan, true, precision);
-  if (rc != DPK_OK) return rc;
-  if (plan.ws_bytes > ws_bytes) {
-    set_error("dpk_gemm: workspace too small (" + std::to_string(ws_bytes) + " < " +
-              std::to_string(plan.ws_bytes) + ")");
-    return DPK_ENOSPACE;
-  }
-  // carve the split-K partial slots
-  size_t partial_tiles = 0;
-  float* partials = static_cast<float*>(ws);
-  for (auto& P : plan.probs) {
-    if (P.splits > 1) {
-      P.partials = partials + partial_tiles * BM * BN;
-      partial_tiles += static_cast<size_t>(P.ntiles) * P.splits;
+  // big problems run on CTA pairs, the rest on single CTAs (two launches, same
+  // stream: the split-K workspace is reused in order)
+  std::vector<GemmSpec> g1, g2;
+  partition_cg(specs, n, g1, g2);
+  for (int cg = 2; cg >= 1; --cg) {
+    std::vector<GemmSpec>& g = cg == 2 ? g2 : g1;
+    if (g.empty()) continue;
+    Plan plan;
+    int rc = make_plan(g.data(), static_cast<int>(g.size()), plan, true, precision, cg);
+    if (rc != DPK_OK) return rc;
+    if (cg == 2) {
+      // a view the predicate accepted must have been TMA-planned; anything else
+      // (encode failure) is an internal inconsistency, not a silent fallback
+      for (const auto& P : plan.probs) {
+        if (P.tma_a == TMA_NONE || (!P.same_ab && P.tma_b == TMA_NONE)) {
+          set_error("dpk_gemm: CTA-pair problem without a TMA plan (tensor map encode failed)");
+          return DPK_ECUDA;
+        }
+      }
     }
-  }
-  thread_local Batch bt;  // host-side staging only (kernel params are copied at launch)
-  for (int first = 0; first < n; first += MAXP) {
-    const int cnt = std::min(MAXP, n - first);
-    bt.nprob = cnt;
-    int units = 0;
-    for (int i = 0; i < cnt; ++i) {
-      bt.p[i] = plan.probs[first + i];
-      bt.p[i].unit_begin = units;
-      units += bt.p[i].ntiles * bt.p[i].splits;
-    }
-    bt.total_units = units;
-    bt.debug_ts = debug_ts_enabled() ? 1 : 0;
-    if (units == 0) continue;
-    if (precision == DPK_PREC_3XTF32)
-      rc = launch_batch<3, false>(bt, st);
-    else if (precision == DPK_PREC_TF32_TRUNC)
-      rc = launch_batch<1, false>(bt, st);
-    else
-      rc = launch_batch<1, true>(bt, st);
+    rc = run_plan(plan, ws, ws_bytes, precision, st);
     if (rc != DPK_OK) return rc;
   }
-  return launch_reduce(plan.probs, st);
+  return DPK_OK;
 }
 
 }  // namespace dpk

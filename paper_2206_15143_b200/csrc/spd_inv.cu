@@ -49,7 +49,6 @@ struct LeafJob {
   int32_t fail_code;
   int32_t _pad;
   int32_t* info;
-  int64_t dst_lo;      // TRI mode: also write lo(X) = X - trunc_tf32(X) at dst + dst_lo (0 = no)
 };
 struct LeafBatch {
   int n;
@@ -208,17 +207,12 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) spd_leaf_kernel(const __grid_
   float* dst = J.dst;
   const int64_t ldd = J.ldd;
   if (!J.full) {  // X = L^-1: exactly zero above the diagonal by construction
-    const int64_t lo = J.dst_lo;
 #pragma unroll
     for (int r = 0; r < RB; ++r)
 #pragma unroll
       for (int c = 0; c < CB; ++c) {
         const int i = ty + 16 * r, j = tx + 32 * c;
-        if (i < n && j < n) {
-          const float v = x[r][c];
-          dst[static_cast<int64_t>(i) * ldd + j] = v;
-          if (lo) dst[lo + static_cast<int64_t>(i) * ldd + j] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
-        }
+        if (i < n && j < n) dst[static_cast<int64_t>(i) * ldd + j] = x[r][c];
       }
     return;
   }
@@ -272,7 +266,6 @@ struct PrepJob {
   const float* shift;
   int64_t n;
   int64_t ldw;
-  int64_t lo;  // low-part shadow offset of dst
 };
 struct PrepBatch {
   int n;
@@ -289,7 +282,6 @@ __global__ void prep_kernel(const __grid_constant__ PrepBatch b) {
     float x = J.src[e];
     if (i == c) x += sh;
     J.dst[i * J.ldw + c] = x;
-    if (J.lo) J.dst[J.lo + i * J.ldw + c] = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
   }
 }
 
@@ -312,17 +304,10 @@ size_t t_floats(int n) {  // largest n2 x n1 scratch over the recursion
   return std::max<size_t>(static_cast<size_t>(n1) * n2, std::max(t_floats(n1), t_floats(n2)));
 }
 
-// working copy Aw, L21 blocks, X = L^-1 (all n x padded_ld) and the T scratch,
-// followed at a fixed distance by their 3xTF32 low-part shadows
-size_t region_floats(int n) {
-  return (3 * static_cast<size_t>(n) * padded_ld(n) + t_floats(n) + 63) / 64 * 64;
-}
-
-bool spd_lo_enabled();
-
 size_t matrix_ws_floats(int n) {
   if (n <= LEAF_N) return 0;
-  return (spd_lo_enabled() ? 2 : 1) * region_floats(n) + 4;
+  // working copy Aw, L21 blocks, X = L^-1 (all n x padded_ld), T scratch (+4 for alignment)
+  return 3 * static_cast<size_t>(n) * padded_ld(n) + t_floats(n) + 4;
 }
 
 GemmSpec spec(const dpk_operand& a, const dpk_operand& b, float* out, int64_t ldo, float alpha, float beta,
@@ -344,60 +329,36 @@ GemmSpec spec(const dpk_operand& a, const dpk_operand& b, float* out, int64_t ld
 // Aw, Lb, Xb share the row stride ld; T has room for n2 x n1 floats.
 // every operand and output below lives in the work region; its 3xTF32 low part
 // is at +lo elements (written by prep / leaf / GEMM epilogues, read by TMA)
-// Streaming low parts doubles operand traffic; with 128x128 tiles the engine is
-// operand-delivery bound, so it measured slower than converting in smem (round
-// 1: 11.7 vs 10.4 ms/step).  Kept behind DPK_SPD_LO=1 for larger tiles.
-bool spd_lo_enabled() {
-  static int on = -1;
-  if (on < 0) {
-    const char* e = getenv("DPK_SPD_LO");
-    on = (e && e[0] == '1') ? 1 : 0;
-  }
-  return on == 1;
-}
-
-GemmSpec with_lo(GemmSpec g, int64_t lo, bool out_lo) {
-  if (!spd_lo_enabled()) return g;
-  g.a_lo = lo;
-  g.b_lo = lo;
-  g.out_lo = out_lo ? lo : 0;
-  return g;
-}
-
 void build_ops(float* Aw, float* Lb, float* Xb, int64_t ld, int n, float* T, int fail_code, int32_t* info,
-               int64_t lo, std::vector<Op>& ops) {
+               std::vector<Op>& ops) {
   if (n <= LEAF_N) {
     Op op{};
     op.leaf = true;
-    op.lj = LeafJob{Aw, Xb, nullptr, ld, ld, n, 0, fail_code, 0, info, lo};
+    op.lj = LeafJob{Aw, Xb, nullptr, ld, ld, n, 0, fail_code, 0, info};
     ops.push_back(op);
     return;
   }
   const int n1 = split_point(n), n2 = n - n1;
   const int64_t o21 = static_cast<int64_t>(n1) * ld, o22 = o21 + n1;
-  build_ops(Aw, Lb, Xb, ld, n1, T, fail_code, info, lo, ops);
+  build_ops(Aw, Lb, Xb, ld, n1, T, fail_code, info, ops);
   Op op{};
   op.leaf = false;
   // L21 = A21 X11^T
   op.g = spec(rows_k(Aw + o21, n2, n1, ld), rows_k(Xb, n1, n1, ld), Lb + o21, ld, 1.0f, 0.0f, 0);
   op.g.tri_b = TRI_LOWER;  // X11 lower: output column block j only needs k <= j
-  op.g = with_lo(op.g, lo, true);
   ops.push_back(op);
   op.g.tri_b = TRI_NONE;
   // A22 <- A22 - L21 L21^T
   op.g = spec(rows_k(Lb + o21, n2, n1, ld), rows_k(Lb + o21, n2, n1, ld), Aw + o22, ld, -1.0f, 1.0f, 1);
-  op.g = with_lo(op.g, lo, true);
   ops.push_back(op);
-  build_ops(Aw + o22, Lb + o22, Xb + o22, ld, n2, T, fail_code, info, lo, ops);
+  build_ops(Aw + o22, Lb + o22, Xb + o22, ld, n2, T, fail_code, info, ops);
   // T = L21 X11
   op.g = spec(rows_k(Lb + o21, n2, n1, ld), rows_mn(Xb, n1, n1, ld), T, n1, 1.0f, 0.0f, 0);
   op.g.tri_b = TRI_UPPER;  // op view of X11 is X11^T: k >= j
-  op.g = with_lo(op.g, lo, true);
   ops.push_back(op);
   // X21 = -X22 T
   op.g = spec(rows_k(Xb + o22, n2, n2, ld), rows_mn(T, n1, n2, n1), Xb + o21, ld, -1.0f, 0.0f, 0);
   op.g.tri_a = TRI_LOWER;  // X22 lower: k <= i
-  op.g = with_lo(op.g, lo, true);
   ops.push_back(op);
 }
 
@@ -420,7 +381,7 @@ void make_spd_plan(const dpk_spd_job* jobs, int n, char* base, SpdPlan& plan) {
     if (m <= LEAF_N) {
       Op op{};
       op.leaf = true;
-      op.lj = LeafJob{jobs[i].src, jobs[i].dst, jobs[i].shift, m, m, m, 1, jobs[i].fail_code, 0, jobs[i].info, 0};
+      op.lj = LeafJob{jobs[i].src, jobs[i].dst, jobs[i].shift, m, m, m, 1, jobs[i].fail_code, 0, jobs[i].info};
       ops.push_back(op);
       continue;
     }
@@ -430,23 +391,16 @@ void make_spd_plan(const dpk_spd_job* jobs, int n, char* base, SpdPlan& plan) {
     float* Lb = Aw + blk;
     float* Xb = Lb + blk;
     float* T = Xb + blk;
-    const int64_t lo = static_cast<int64_t>(region_floats(m));  // low-part shadow distance
     off += align_up(matrix_ws_floats(m) * sizeof(float), 256);
-    const int64_t lo_used = spd_lo_enabled() ? lo : 0;
-    plan.preps.push_back(PrepJob{jobs[i].src, Aw, jobs[i].shift, m, ldw, lo_used});
+    plan.preps.push_back(PrepJob{jobs[i].src, Aw, jobs[i].shift, m, ldw});
     plan.zero_x.push_back(Xb);
     plan.zero_bytes.push_back(blk * sizeof(float));
-    if (lo_used) {
-      plan.zero_x.push_back(Xb + lo);
-      plan.zero_bytes.push_back(blk * sizeof(float));
-    }
-    build_ops(Aw, Lb, Xb, ldw, m, T, jobs[i].fail_code, jobs[i].info, lo_used, ops);
+    build_ops(Aw, Lb, Xb, ldw, m, T, jobs[i].fail_code, jobs[i].info, ops);
     Op op{};
     op.leaf = false;
     // dst = X^T X  (X lower triangular; symmetric output, written with the caller's ld = n)
     op.g = spec(rows_mn(Xb, m, m, ldw), rows_mn(Xb, m, m, ldw), jobs[i].dst, m, 1.0f, 0.0f, 1);
     op.g.tri_a = op.g.tri_b = TRI_UPPER;  // (X^T X)[i][j] = sum over k >= max(i, j)
-    op.g = with_lo(op.g, lo, false);      // dst is the caller's: no shadow
     ops.push_back(op);
   }
   plan.rec_bytes = off;

@@ -1,0 +1,1 @@
+python scripts/gemm_probe.py
