@@ -33,6 +33,10 @@ struct GemmSpec {
   // both operands can be nonzero (triangular factors in the SPD recursion)
   int tri_a = 0;
   int tri_b = 0;
+  // symmetric jobs only: compute and store the lower tiles, no mirror (the
+  // upper triangle of the output is left as it was, or -- on diagonal tiles --
+  // receives the full product)
+  int lower_only = 0;
 };
 constexpr int TRI_NONE = 0;
 constexpr int TRI_LOWER = 1;  // op[r][k] == 0 for k > r

@@ -81,7 +81,7 @@ struct alignas(64) Problem {
   int64_t ldc;
   float alpha, beta, gamma;
   int M, N;
-  int symmetric, same_ab, epi;
+  int symmetric, same_ab, epi;  // symmetric: 1 lower tiles + mirror, 2 lower tiles only
   int tiles_n, ntiles, splits;
   int chunks, cps;  // K chunks of 32, chunks per split
   int unit_begin;
@@ -93,7 +93,9 @@ struct alignas(64) Problem {
 struct Batch {
   int nprob;
   int total_units;
-  int debug_ts;  // record %globaltimer checkpoints of CTA 0 (dpk_debug_timestamps)
+  int debug_ts;   // record %globaltimer checkpoints of CTA 0 (dpk_debug_timestamps)
+  int producers;  // 0: every operand tile arrives by TMA ready for the MMA (no gather /
+                  // conversion anywhere in the launch) -> warps 6-11 sit the launch out
   Problem p[MAXP];
 };
 static_assert(sizeof(Batch) <= 32764, "kernel parameter space is 32764 bytes");
@@ -560,7 +562,7 @@ __device__ __forceinline__ void store_chunk(const Epi& e, bool diag, int gm0, in
     op += e.ldo;
   }
   dbg_raw(dbg, 12);
-  if (e.symmetric || e.out_t) {
+  if (e.symmetric == 1 || e.out_t) {
     __syncwarp();  // every lane has read its column of T
 #pragma unroll
     for (int rr = 0; rr < 32; ++rr) T[rr * 33 + lane] = v[rr];
@@ -572,7 +574,7 @@ __device__ __forceinline__ void store_chunk(const Epi& e, bool diag, int gm0, in
     const int gn0 = gnc;
     // columns written in the direct pass for this row: g < N and (not diag or g <= gm)
     const int jend = lane < nrows ? min(32, min(e.N, diag ? gm + 1 : e.N) - gn0) : 0;
-    if (e.symmetric) {
+    if (e.symmetric == 1) {
       float* mp = e.out + static_cast<int64_t>(gn0) * e.ldo + gm;
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
@@ -632,10 +634,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   const int ustep = (CG == 2) ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
   if (threadIdx.x == 0) dbg_ts(bt, 0);
 
+  // full-barrier arrivals per stage use: every producer warp of the CTA (CG=2:
+  // of both CTAs) or, in producer-free launches, the TMA thread alone (CG=2: the
+  // leader's, whose expect_tx covers both CTAs' loads)
+  const bool prods = bt.producers != 0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
-      // CG=2: the leader's full barrier counts both CTAs' producers + its TMA thread
-      mbar_init(full_bar(s), CG == 2 ? 2 * PROD_WARPS + 1 : PROD_WARPS);
+      mbar_init(full_bar(s), prods ? CG * PROD_WARPS : 1);
       mbar_init(empty_bar(s), 1);
       mbar_init(tma_bar(s), 1);
     }
@@ -681,22 +686,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         const uint32_t bytes = tile_bytes(ra, rb);
         // CG=2 without an smem conversion: both CTAs' loads complete directly on
         // the leader's full barrier (cta_group::2 TMA), no producer hand-off
-        const bool conv = CONVERT && (tA || tB);
-        const bool direct = CG == 2 && !conv;
+        // CG=2 without producers: both CTAs' loads complete on the leader's full barrier
+        const bool direct = CG == 2 && !prods;
         const uint32_t pair_bytes = direct ? bytes + tile_bytes(tm * UT + (128 - half), tn * UT + (128 - half)) : 0u;
         for (int kc = kc0; kc < kc1; ++kc) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t sst = base + stage * C::STAGE_BYTES;
           if (direct) {
             const uint32_t fb = leader ? full_bar(stage) : mapa_shared(full_bar(stage), 0);
-            mbar_arrive(tma_bar(stage));  // keeps the per-stage phase in step (no bytes)
             if (leader) mbar_arrive_expect_tx(full_bar(stage), pair_bytes);
             if (tA) issue_tma<true>(P.tma_a, &P.tmap_a, P.a, sst, fb, ra, kc, P.slab_cpn);
             if (tB) issue_tma<true>(P.tma_b, &P.tmap_b, P.b, sst + TILE_BYTES, fb, rb, kc, P.slab_cpn);
           } else {
             // exactly one arrival per stage use; tx bytes only for TMA'd tiles
             mbar_arrive_expect_tx(tma_bar(stage), bytes);
-            if (CG == 2 && leader) mbar_arrive(full_bar(stage));  // this thread's count on the pair barrier
+            if (!prods) mbar_arrive(full_bar(stage));  // CG=1 producer-free: stands in for the producers
             if (tA) issue_tma(P.tma_a, &P.tmap_a, P.a, sst, tma_bar(stage), ra, kc, P.slab_cpn);
             if (tB) issue_tma(P.tma_b, &P.tmap_b, P.b, sst + TILE_BYTES, tma_bar(stage), rb, kc, P.slab_cpn);
           }
@@ -708,7 +712,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
       }
       dbg_ts(bt, 2);
     }
-  } else if (warp >= PROD_WARP0) {
+  } else if (warp >= PROD_WARP0 && prods) {
     // =============================== gather / convert warps
     const int ptid = threadIdx.x - PROD_WARP0 * 32;
     int stage = 0;
@@ -751,6 +755,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
           if (cA) convert_tile<NPASS>(st, st + 2 * TILE_BYTES, ptid);
           if (cB) convert_tile<NPASS>(st + TILE_BYTES, st + 3 * TILE_BYTES, ptid);
         }
+        // one arrival per producer warp (measured faster than a named barrier +
+        // a single elected arrival: the warps' cluster-scope releases overlap)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -864,7 +870,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
       int kc0, kc1;
       chunk_range<CG>(P, tm, tn, split, kc0, kc1);
       const bool empty = kc1 <= kc0;  // nothing accumulated: the tile's product is zero
-      const bool diag = e.symmetric && tm == tn;
+      const bool diag = e.symmetric == 1 && tm == tn;
       const int gm0 = tm * UT + half + warp * 32;
 #pragma unroll 1
       for (int c = 0; c < static_cast<int>(ACC_COLS) / 32; ++c) {
@@ -971,7 +977,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
     acc.w += x.w;
   }
   const float a[4] = {acc.x, acc.y, acc.z, acc.w};
-  const bool diag = J.symmetric && tm == tn;
+  const bool diag = J.symmetric == 1 && tm == tn;
   const float vr = (J.epi == EPI_EIGDIV) ? fmaxf(J.vrow[gm], 0.0f) : 0.0f;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
@@ -984,7 +990,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
       val += J.beta * J.cin[gm * J.ldc + gn];
     }
     J.out[gm * J.ldo + gn] = val;
-    if (J.symmetric && gn != gm) J.out[static_cast<int64_t>(gn) * J.ldo + gm] = val;
+    if (J.symmetric == 1 && gn != gm) J.out[static_cast<int64_t>(gn) * J.ldo + gm] = val;
     if (J.out_t) J.out_t[static_cast<int64_t>(gn) * J.ldt + gm] = val;
   }
 }
@@ -1165,7 +1171,7 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
     P.beta = j.beta;
     P.M = operand_rows(j.a);
     P.N = operand_rows(j.b);
-    P.symmetric = j.symmetric ? 1 : 0;
+    P.symmetric = j.symmetric ? (specs[i].lower_only ? 2 : 1) : 0;
     if (P.symmetric && P.M != P.N) {
       set_error("dpk_gemm: symmetric output needs M == N");
       return DPK_ESHAPE;
@@ -1414,6 +1420,10 @@ int run_plan(Plan& plan, void* ws, size_t ws_bytes, int precision, cudaStream_t 
     }
     bt.total_units = units;
     bt.debug_ts = debug_ts_enabled() ? 1 : 0;
+    // producer warps are needed for 3xTF32 low parts and for operands TMA cannot address
+    bt.producers = precision == DPK_PREC_3XTF32 ? 1 : 0;
+    for (int i = 0; i < cnt; ++i)
+      if (bt.p[i].tma_a == TMA_NONE || bt.p[i].tma_b == TMA_NONE) bt.producers = 1;
     if (units == 0) continue;
     const int rc = plan.cg == 2 ? launch_group<2>(bt, precision, st) : launch_group<1>(bt, precision, st);
     if (rc != DPK_OK) return rc;

@@ -257,12 +257,19 @@ constexpr int leaf_smem_bytes() {
   return (16 * 16 * RB + 16 * RB * (16 * RB + 1)) * 4;
 }
 
-// Aw = src + shift I for the blocked path; Aw rows are padded to ldw (a multiple
-// of 4 floats) so every recursion operand is a 16-byte aligned TMA view.
+// Blocked-path set-up, one warp per row i:  Aw[i][0..i] = src[i][0..i] (+ shift
+// on the diagonal) and X[i][i+1..n) = 0.  The recursion only ever reads the
+// lower triangle of Aw (A21 blocks, lower-only Schur updates, leaves factor
+// from the lower part), and every lower block of X is overwritten by a leaf or
+// an X21 product, so nothing else needs initialising.  Aw / X rows are padded to
+// ldw (a multiple of 4 floats) so every recursion operand is a 16-byte aligned
+// TMA view.
 constexpr int PREP_MAX = 256;
+constexpr int PREP_WARPS = 8;
 struct PrepJob {
   const float* src;
   float* dst;
+  float* x;
   const float* shift;
   int64_t n;
   int64_t ldw;
@@ -271,26 +278,32 @@ struct PrepBatch {
   int n;
   PrepJob j[PREP_MAX];
 };
-__global__ void prep_kernel(const __grid_constant__ PrepBatch b) {
+__global__ void __launch_bounds__(PREP_WARPS * 32) prep_kernel(const __grid_constant__ PrepBatch b) {
   const PrepJob& J = b.j[blockIdx.y];
-  const int64_t total = J.n * J.n;
+  const int n = static_cast<int>(J.n);
+  const int64_t ldw = J.ldw;
   const float sh = J.shift ? *J.shift : 0.0f;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t i = e / J.n;
-    const int64_t c = e - i * J.n;
-    float x = J.src[e];
-    if (i == c) x += sh;
-    J.dst[i * J.ldw + c] = x;
+  const int lane = threadIdx.x & 31;
+  for (int i = blockIdx.x * PREP_WARPS + (threadIdx.x >> 5); i < n; i += gridDim.x * PREP_WARPS) {
+    const float* srow = J.src + static_cast<int64_t>(i) * n;
+    float* arow = J.dst + static_cast<int64_t>(i) * ldw;
+    float* xrow = J.x + static_cast<int64_t>(i) * ldw;
+    for (int c = lane; c <= i; c += 32) {
+      const float v = __ldg(srow + c);
+      arow[c] = c == i ? v + sh : v;
+    }
+    for (int c = i + 1 + lane; c < n; c += 32) xrow[c] = 0.0f;
   }
 }
 
 inline int64_t padded_ld(int n) { return (static_cast<int64_t>(n) + 3) / 4 * 4; }
 
+// One lock-step round of one matrix: a leaf, or one or two independent GEMMs.
 struct Op {
   bool leaf;
   LeafJob lj;
-  GemmSpec g;
+  int ng;
+  GemmSpec g[2];
 };
 
 int split_point(int n) {
@@ -298,16 +311,10 @@ int split_point(int n) {
   return std::min(n1, n - 1);
 }
 
-size_t t_floats(int n) {  // largest n2 x n1 scratch over the recursion
-  if (n <= LEAF_N) return 0;
-  const int n1 = split_point(n), n2 = n - n1;
-  return std::max<size_t>(static_cast<size_t>(n1) * n2, std::max(t_floats(n1), t_floats(n2)));
-}
-
 size_t matrix_ws_floats(int n) {
   if (n <= LEAF_N) return 0;
-  // working copy Aw, L21 blocks, X = L^-1 (all n x padded_ld), T scratch (+4 for alignment)
-  return 3 * static_cast<size_t>(n) * padded_ld(n) + t_floats(n) + 4;
+  // working copy Aw, L blocks, X = L^-1 (all n x padded_ld; +4 for alignment)
+  return 3 * static_cast<size_t>(n) * padded_ld(n) + 4;
 }
 
 GemmSpec spec(const dpk_operand& a, const dpk_operand& b, float* out, int64_t ldo, float alpha, float beta,
@@ -326,10 +333,13 @@ GemmSpec spec(const dpk_operand& a, const dpk_operand& b, float* out, int64_t ld
   return s;
 }
 
-// Aw, Lb, Xb share the row stride ld; T has room for n2 x n1 floats.
-// every operand and output below lives in the work region; its 3xTF32 low part
-// is at +lo elements (written by prep / leaf / GEMM epilogues, read by TMA)
-void build_ops(float* Aw, float* Lb, float* Xb, int64_t ld, int n, float* T, int fail_code, int32_t* info,
+// Aw, Lb, Xb share the row stride ld.  Three GEMM rounds per recursion node:
+//   (a) L21 = A21 X11^T
+//   (b) A22 -= L21 L21^T (lower tiles only)   and   T^T = X11^T L21^T
+//   (c) X21 = -X22 T                               (after the A22 recursion)
+// T^T (n1 x n2) lives in the node's upper-right block of Lb: L is lower
+// triangular, and no descendant of either child touches that block.
+void build_ops(float* Aw, float* Lb, float* Xb, int64_t ld, int n, int fail_code, int32_t* info,
                std::vector<Op>& ops) {
   if (n <= LEAF_N) {
     Op op{};
@@ -340,33 +350,33 @@ void build_ops(float* Aw, float* Lb, float* Xb, int64_t ld, int n, float* T, int
   }
   const int n1 = split_point(n), n2 = n - n1;
   const int64_t o21 = static_cast<int64_t>(n1) * ld, o22 = o21 + n1;
-  build_ops(Aw, Lb, Xb, ld, n1, T, fail_code, info, ops);
+  float* Tt = Lb + n1;  // n1 x n2, row stride ld
+  build_ops(Aw, Lb, Xb, ld, n1, fail_code, info, ops);
   Op op{};
   op.leaf = false;
-  // L21 = A21 X11^T
-  op.g = spec(rows_k(Aw + o21, n2, n1, ld), rows_k(Xb, n1, n1, ld), Lb + o21, ld, 1.0f, 0.0f, 0);
-  op.g.tri_b = TRI_LOWER;  // X11 lower: output column block j only needs k <= j
+  op.ng = 1;
+  op.g[0] = spec(rows_k(Aw + o21, n2, n1, ld), rows_k(Xb, n1, n1, ld), Lb + o21, ld, 1.0f, 0.0f, 0);
+  op.g[0].tri_b = TRI_LOWER;  // X11 lower: output column block j only needs k <= j
   ops.push_back(op);
-  op.g.tri_b = TRI_NONE;
-  // A22 <- A22 - L21 L21^T
-  op.g = spec(rows_k(Lb + o21, n2, n1, ld), rows_k(Lb + o21, n2, n1, ld), Aw + o22, ld, -1.0f, 1.0f, 1);
+  op.ng = 2;
+  op.g[0] = spec(rows_k(Lb + o21, n2, n1, ld), rows_k(Lb + o21, n2, n1, ld), Aw + o22, ld, -1.0f, 1.0f, 1);
+  op.g[0].lower_only = 1;  // the recursion reads only the lower triangle of A22
+  // T^T[j][i] = sum_k X11[k][j] L21[i][k]: A = X11^T (rows_mn view), B = L21
+  op.g[1] = spec(rows_mn(Xb, n1, n1, ld), rows_k(Lb + o21, n2, n1, ld), Tt, ld, 1.0f, 0.0f, 0);
+  op.g[1].tri_a = TRI_UPPER;  // op view of X11 is X11^T: k >= j
   ops.push_back(op);
-  build_ops(Aw + o22, Lb + o22, Xb + o22, ld, n2, T, fail_code, info, ops);
-  // T = L21 X11
-  op.g = spec(rows_k(Lb + o21, n2, n1, ld), rows_mn(Xb, n1, n1, ld), T, n1, 1.0f, 0.0f, 0);
-  op.g.tri_b = TRI_UPPER;  // op view of X11 is X11^T: k >= j
-  ops.push_back(op);
-  // X21 = -X22 T
-  op.g = spec(rows_k(Xb + o22, n2, n2, ld), rows_mn(T, n1, n2, n1), Xb + o21, ld, -1.0f, 0.0f, 0);
-  op.g.tri_a = TRI_LOWER;  // X22 lower: k <= i
+  build_ops(Aw + o22, Lb + o22, Xb + o22, ld, n2, fail_code, info, ops);
+  op.ng = 1;
+  op.g[1] = GemmSpec{};
+  // X21 = -X22 T:  B[j][k] = T[k][j] = T^T[j][k]
+  op.g[0] = spec(rows_k(Xb + o22, n2, n2, ld), rows_k(Tt, n1, n2, ld), Xb + o21, ld, -1.0f, 0.0f, 0);
+  op.g[0].tri_a = TRI_LOWER;  // X22 lower: k <= i
   ops.push_back(op);
 }
 
 struct SpdPlan {
   std::vector<std::vector<Op>> lists;
   std::vector<PrepJob> preps;
-  std::vector<float*> zero_x;
-  std::vector<size_t> zero_bytes;
   size_t rec_bytes = 0;
   size_t gemm_bytes = 0;
 };
@@ -390,17 +400,15 @@ void make_spd_plan(const dpk_spd_job* jobs, int n, char* base, SpdPlan& plan) {
     float* Aw = reinterpret_cast<float*>(b + off);
     float* Lb = Aw + blk;
     float* Xb = Lb + blk;
-    float* T = Xb + blk;
     off += align_up(matrix_ws_floats(m) * sizeof(float), 256);
-    plan.preps.push_back(PrepJob{jobs[i].src, Aw, jobs[i].shift, m, ldw});
-    plan.zero_x.push_back(Xb);
-    plan.zero_bytes.push_back(blk * sizeof(float));
-    build_ops(Aw, Lb, Xb, ldw, m, T, jobs[i].fail_code, jobs[i].info, ops);
+    plan.preps.push_back(PrepJob{jobs[i].src, Aw, Xb, jobs[i].shift, m, ldw});
+    build_ops(Aw, Lb, Xb, ldw, m, jobs[i].fail_code, jobs[i].info, ops);
     Op op{};
     op.leaf = false;
+    op.ng = 1;
     // dst = X^T X  (X lower triangular; symmetric output, written with the caller's ld = n)
-    op.g = spec(rows_mn(Xb, m, m, ldw), rows_mn(Xb, m, m, ldw), jobs[i].dst, m, 1.0f, 0.0f, 1);
-    op.g.tri_a = op.g.tri_b = TRI_UPPER;  // (X^T X)[i][j] = sum over k >= max(i, j)
+    op.g[0] = spec(rows_mn(Xb, m, m, ldw), rows_mn(Xb, m, m, ldw), jobs[i].dst, m, 1.0f, 0.0f, 1);
+    op.g[0].tri_a = op.g[0].tri_b = TRI_UPPER;  // (X^T X)[i][j] = sum over k >= max(i, j)
     ops.push_back(op);
   }
   plan.rec_bytes = off;
@@ -413,7 +421,8 @@ void make_spd_plan(const dpk_spd_job* jobs, int n, char* base, SpdPlan& plan) {
       if (idx[i] >= plan.lists[i].size()) continue;
       any = true;
       const Op& op = plan.lists[i][idx[i]];
-      if (!op.leaf) g.push_back(op.g);
+      if (!op.leaf)
+        for (int q = 0; q < op.ng; ++q) g.push_back(op.g[q]);
       ++idx[i];
     }
     if (!any) break;
@@ -546,19 +555,15 @@ int run_inverse(const dpk_spd_job* jobs, int n_jobs, void* workspace, cudaStream
   for (size_t first = 0; first < plan.preps.size(); first += dpk::PREP_MAX) {
     const int cnt = static_cast<int>(std::min<size_t>(dpk::PREP_MAX, plan.preps.size() - first));
     pb.n = cnt;
-    int64_t maxe = 0;
+    int64_t maxn = 0;
     for (int i = 0; i < cnt; ++i) {
       pb.j[i] = plan.preps[first + i];
-      maxe = std::max<int64_t>(maxe, pb.j[i].n * pb.j[i].n);
+      maxn = std::max<int64_t>(maxn, pb.j[i].n);
     }
-    const int gx = static_cast<int>(std::min<int64_t>((maxe + 255) / 256, 2048));
-    dpk::prep_kernel<<<dim3(gx, cnt), 256, 0, st>>>(pb);
+    const int gx = static_cast<int>(std::min<int64_t>((maxn + dpk::PREP_WARPS - 1) / dpk::PREP_WARPS, 64));
+    dpk::prep_kernel<<<dim3(gx, cnt), dpk::PREP_WARPS * 32, 0, st>>>(pb);
     dpk::note_launch();
     int rc = dpk::cuda_status(cudaGetLastError(), "prep_kernel launch");
-    if (rc) return rc;
-  }
-  for (size_t i = 0; i < plan.zero_x.size(); ++i) {
-    int rc = dpk::cuda_status(cudaMemsetAsync(plan.zero_x[i], 0, plan.zero_bytes[i], st), "cudaMemsetAsync");
     if (rc) return rc;
   }
   std::vector<size_t> idx(n_jobs, 0);
@@ -580,7 +585,7 @@ int run_inverse(const dpk_spd_job* jobs, int n_jobs, void* workspace, cudaStream
       if (op.leaf)
         leaves.push_back(op.lj);
       else
-        g.push_back(op.g);
+        for (int q = 0; q < op.ng; ++q) g.push_back(op.g[q]);
       ++idx[i];
     }
     if (!any) break;

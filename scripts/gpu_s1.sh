@@ -1,0 +1,6 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+python -m pytest tests -m gpu -x -q 2>&1 | tail -15
+python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench=$?
+cat gpurun_out/bench.json
+python scripts/factor_breakdown.py > gpurun_out/fb.log 2>&1; tail -20 gpurun_out/fb.log

@@ -44,8 +44,11 @@ def main():
         syrk_case("rows_k", lambda: ops.operand_rows_k(x), d, m)
         syrk_case("rows_k", lambda: ops.operand_rows_k(x), d, m, "3xtf32")
     # sample-major (nn.Linear input)
-    x = torch.randn(65536, 1024, device=dev)
-    syrk_case("rows_mn", lambda: ops.operand_rows_mn(x), 1024, 65536)
+    for d, m in [(1024, 65536), (4608, 1568), (576, 100352), (2304, 6272), (1152, 25088)]:
+        x = torch.randn(m, d, device=dev)
+        syrk_case("rows_mn", lambda: ops.operand_rows_mn(x), d, m)
+        x = torch.randn(d, m, device=dev)
+        syrk_case("rows_k", lambda: ops.operand_rows_k(x), d, m)
     # implicit im2col, ResNet-50 shapes
     for (c, h, k, s, p) in [(64, 56, 3, 1, 1), (128, 28, 3, 1, 1), (256, 14, 3, 1, 1), (512, 7, 3, 1, 1),
                             (64, 56, 1, 1, 0), (3, 224, 7, 2, 3), (256, 56, 1, 2, 0)]:
