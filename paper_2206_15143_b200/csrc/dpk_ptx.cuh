@@ -250,6 +250,15 @@ __device__ __forceinline__ void tma_prefetch_desc(const void* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// Kernels launched with the PDL attribute (launch_k) may start while the previous
+// kernel in the stream is still running; every one of our kernels calls
+// pdl_wait() before its first global-memory access, which returns once the
+// previous grid has completed and its writes are visible.  pdl_trigger() lets
+// the next kernel start its own prologue early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Round-to-nearest (ties away) TF32; low 13 mantissa bits become zero.
 __device__ __forceinline__ uint32_t to_tf32(float x) {
   uint32_t r;

@@ -660,6 +660,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   __syncthreads();
   if (CG == 2) cluster_sync_all();  // peer barriers initialised before any remote arrive / multicast
   tc_fence_after();
+  // everything above overlaps the previous kernel's tail (PDL); from here on we
+  // read operands / cin and write outputs
+  pdl_wait();
+  pdl_trigger();
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(gbase + (tmem_slot - base));
   if (threadIdx.x == 0) dbg_ts(bt, 1);
 
@@ -941,6 +945,8 @@ struct RedBatch {
 // One CTA per (split tile, slab of 1024 elements): 256 threads x 4 consecutive
 // columns; a slab is 8 rows of a 128-wide tile or 4 rows of a 256-wide one.
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constant__ RedBatch b) {
+  pdl_wait();
+  pdl_trigger();
   const int slab = blockIdx.x;
   int p = 0;
   while (p + 1 < b.n && b.j[p + 1].slab_begin <= slab) ++p;
@@ -1293,11 +1299,11 @@ int launch_reduce(const std::vector<Problem>& probs, int ut, cudaStream_t st) {
   rb.total = 0;
   auto flush = [&]() -> int {
     if (rb.n == 0) return DPK_OK;
-    splitk_reduce_kernel<<<rb.total, 256, 0, st>>>(rb);
+    const cudaError_t e = launch_k(splitk_reduce_kernel, dim3(rb.total), dim3(256), 0, st, 1, rb);
     note_launch();
     rb.n = 0;
     rb.total = 0;
-    return cuda_status(cudaGetLastError(), "splitk_reduce_kernel launch");
+    return cuda_status(e, "splitk_reduce_kernel launch");
   };
   for (const auto& P : probs) {
     if (P.splits <= 1) continue;
@@ -1359,28 +1365,10 @@ int launch_batch(const Batch& bt, cudaStream_t st) {
     }
     configured = true;
   }
-  if (CG == 1) {
-    const int grid = std::min(bt.total_units, num_sms());
-    tc_gemm_kernel<NPASS, RN, CG><<<grid, NTHREADS, C::SMEM, st>>>(bt);
-  } else {
-    const int pairs = std::min(bt.total_units, max_pairs);
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(2 * pairs, 1, 1);
-    cfg.blockDim = dim3(NTHREADS, 1, 1);
-    cfg.dynamicSmemBytes = C::SMEM;
-    cfg.stream = st;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, tc_gemm_kernel<NPASS, RN, CG>, bt);
-    if (e != cudaSuccess) return cuda_status(e, "cudaLaunchKernelEx(tc_gemm_kernel, cluster 2)");
-  }
+  const int grid = CG == 1 ? std::min(bt.total_units, num_sms()) : 2 * std::min(bt.total_units, max_pairs);
+  const cudaError_t e = launch_k(tc_gemm_kernel<NPASS, RN, CG>, dim3(grid), dim3(NTHREADS), C::SMEM, st, CG, bt);
   note_launch();
-  return cuda_status(cudaGetLastError(), "tc_gemm_kernel launch");
+  return cuda_status(e, "tc_gemm_kernel launch");
 }
 
 template <int CG>

@@ -30,6 +30,17 @@ int cuda_status(cudaError_t e, const char* what) {
   return DPK_ECUDA;
 }
 
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    // off by default: measured slower on the SPD graph (early-launched CTAs hold
+    // SMs that concurrent streams' kernels could use); DPK_PDL=1 enables
+    const char* e = getenv("DPK_PDL");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 int num_sms() {
   static int cached = 0;
   if (cached == 0) {

@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "dpk_internal.h"
+#include "dpk_ptx.cuh"
 
 namespace dpk {
 namespace {
@@ -78,6 +79,8 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) spd_leaf_kernel(const __grid_
   float* colb = smem;          // [2][4][N] columns k..k+3 of the partially factored A
   float* rowb = smem + 8 * N;  // [2][4][N] rows k..k+3 of the partially solved X
   float* Xs = smem + 16 * N;   // [N][N+1] X for the FULL-mode X^T X
+  pdl_wait();
+  pdl_trigger();
   const LeafJob& J = b.j[blockIdx.x];
   const int n = J.n;
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
@@ -279,6 +282,8 @@ struct PrepBatch {
   PrepJob j[PREP_MAX];
 };
 __global__ void __launch_bounds__(PREP_WARPS * 32) prep_kernel(const __grid_constant__ PrepBatch b) {
+  pdl_wait();
+  pdl_trigger();
   const PrepJob& J = b.j[blockIdx.y];
   const int n = static_cast<int>(J.n);
   const int64_t ldw = J.ldw;
@@ -374,12 +379,39 @@ void build_ops(float* Aw, float* Lb, float* Xb, int64_t ld, int n, int fail_code
   ops.push_back(op);
 }
 
+// Matrices advance in lock-step rounds inside a group; groups are independent
+// chains on their own streams (forked from / joined to the caller's stream), so
+// the long recursion of the largest factors is not paced by -- and its rounds
+// are not split into several launches by -- the many mid-sized ones.
+constexpr int MAX_GROUPS = 6;
 struct SpdPlan {
   std::vector<std::vector<Op>> lists;
   std::vector<PrepJob> preps;
+  std::vector<std::vector<int>> groups;   // job indices; groups[0] = the largest factors
+  std::vector<size_t> group_ws;           // split-K workspace offset of each group
   size_t rec_bytes = 0;
-  size_t gemm_bytes = 0;
+  size_t gemm_bytes = 0;                  // sum over groups
 };
+
+// groups: distinct sizes in descending order, a new group whenever the size
+// drops below 0.6x the group's largest (ResNet-50: 4608 | 2304..2048 |
+// 1152..1000 | 576, 512 | 256 | 147, 128 and below); at most MAX_GROUPS.
+void make_groups(const dpk_spd_job* jobs, int n, SpdPlan& plan) {
+  std::vector<int> order(n);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return jobs[a].n > jobs[b].n; });
+  plan.groups.clear();
+  int gmax = 0;
+  for (int i : order) {
+    const int m = jobs[i].n;
+    if (plan.groups.empty() || (m * 10 < gmax * 6 && static_cast<int>(plan.groups.size()) < MAX_GROUPS)) {
+      plan.groups.emplace_back();
+      gmax = m;
+    }
+    plan.groups.back().push_back(i);
+  }
+  for (auto& g : plan.groups) std::sort(g.begin(), g.end());  // ascending layer order inside a group
+}
 
 void make_spd_plan(const dpk_spd_job* jobs, int n, char* base, SpdPlan& plan) {
   plan.lists.assign(n, {});
@@ -412,23 +444,30 @@ void make_spd_plan(const dpk_spd_job* jobs, int n, char* base, SpdPlan& plan) {
     ops.push_back(op);
   }
   plan.rec_bytes = off;
-  std::vector<size_t> idx(n, 0);
-  size_t worst = 0;
-  for (;;) {
-    std::vector<GemmSpec> g;
-    bool any = false;
-    for (int i = 0; i < n; ++i) {
-      if (idx[i] >= plan.lists[i].size()) continue;
-      any = true;
-      const Op& op = plan.lists[i][idx[i]];
-      if (!op.leaf)
-        for (int q = 0; q < op.ng; ++q) g.push_back(op.g[q]);
-      ++idx[i];
+  make_groups(jobs, n, plan);
+  plan.gemm_bytes = 0;
+  plan.group_ws.clear();
+  for (const auto& grp : plan.groups) {
+    std::vector<size_t> idx(grp.size(), 0);
+    size_t worst = 0;
+    for (;;) {
+      std::vector<GemmSpec> g;
+      bool any = false;
+      for (size_t q = 0; q < grp.size(); ++q) {
+        const auto& list = plan.lists[grp[q]];
+        if (idx[q] >= list.size()) continue;
+        any = true;
+        const Op& op = list[idx[q]];
+        if (!op.leaf)
+          for (int t = 0; t < op.ng; ++t) g.push_back(op.g[t]);
+        ++idx[q];
+      }
+      if (!any) break;
+      if (!g.empty()) worst = std::max(worst, gemm_workspace_bytes(g.data(), static_cast<int>(g.size())));
     }
-    if (!any) break;
-    if (!g.empty()) worst = std::max(worst, gemm_workspace_bytes(g.data(), static_cast<int>(g.size())));
+    plan.group_ws.push_back(plan.gemm_bytes);
+    plan.gemm_bytes += align_up(worst, 1024);
   }
-  plan.gemm_bytes = worst;
 }
 
 template <int NB>
@@ -440,9 +479,9 @@ int launch_leaf_nb(const LeafBatch& b, int cnt, cudaStream_t st) {
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(spd_leaf_kernel)");
     configured = true;
   }
-  spd_leaf_kernel<NB><<<cnt, LEAF_THREADS, leaf_smem_bytes<NB>(), st>>>(b);
+  const cudaError_t e = launch_k(spd_leaf_kernel<NB>, dim3(cnt), dim3(LEAF_THREADS), leaf_smem_bytes<NB>(), st, 1, b);
   note_launch();
-  return cuda_status(cudaGetLastError(), "spd_leaf_kernel launch");
+  return cuda_status(e, "spd_leaf_kernel launch");
 }
 
 int launch_leaves(std::vector<LeafJob>& leaves, cudaStream_t st) {
@@ -496,6 +535,44 @@ bool spd_graphs_enabled() {
   return on == 1;
 }
 int run_inverse(const dpk_spd_job* jobs, int n_jobs, void* workspace, cudaStream_t st, bool trace);
+int run_lockstep(const SpdPlan& plan, const std::vector<int>& grp, char* gemm_ws, size_t gemm_bytes,
+                 cudaStream_t st, bool trace);
+
+// per-device side streams (priority: group 0 -- the critical chain -- stays on
+// the caller's stream; side streams get lower priority) and fork/join events
+struct SideStreams {
+  cudaStream_t s[MAX_GROUPS] = {};
+  cudaEvent_t fork = nullptr;
+  cudaEvent_t join[MAX_GROUPS] = {};
+  int n = 0;
+};
+SideStreams& side_streams() {
+  static std::mutex mu;
+  static std::vector<SideStreams> per_dev;
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (static_cast<int>(per_dev.size()) <= dev) per_dev.resize(dev + 1);
+  return per_dev[dev];
+}
+int ensure_side_streams(int n) {
+  SideStreams& ss = side_streams();
+  if (!ss.fork) {
+    int rc = cuda_status(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming), "cudaEventCreate");
+    if (rc) return rc;
+  }
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  while (ss.n < n) {
+    int rc = cuda_status(cudaStreamCreateWithPriority(&ss.s[ss.n], cudaStreamNonBlocking, least),
+                         "cudaStreamCreateWithPriority");
+    if (rc) return rc;
+    rc = cuda_status(cudaEventCreateWithFlags(&ss.join[ss.n], cudaEventDisableTiming), "cudaEventCreate");
+    if (rc) return rc;
+    ++ss.n;
+  }
+  return DPK_OK;
+}
 int run_cached_graph(const dpk_spd_job* jobs, int n_jobs, void* workspace, size_t ws_bytes, cudaStream_t st);
 
 }  // namespace
@@ -561,12 +638,45 @@ int run_inverse(const dpk_spd_job* jobs, int n_jobs, void* workspace, cudaStream
       maxn = std::max<int64_t>(maxn, pb.j[i].n);
     }
     const int gx = static_cast<int>(std::min<int64_t>((maxn + dpk::PREP_WARPS - 1) / dpk::PREP_WARPS, 64));
-    dpk::prep_kernel<<<dim3(gx, cnt), dpk::PREP_WARPS * 32, 0, st>>>(pb);
+    const cudaError_t e = dpk::launch_k(dpk::prep_kernel, dim3(gx, cnt), dim3(dpk::PREP_WARPS * 32), 0, st, 1, pb);
     dpk::note_launch();
-    int rc = dpk::cuda_status(cudaGetLastError(), "prep_kernel launch");
+    int rc = dpk::cuda_status(e, "prep_kernel launch");
     if (rc) return rc;
   }
-  std::vector<size_t> idx(n_jobs, 0);
+  if (trace) {  // diagnostics: one lock-step chain over all matrices, rounds timed
+    std::vector<int> all(n_jobs);
+    for (int i = 0; i < n_jobs; ++i) all[i] = i;
+    return run_lockstep(plan, all, gemm_ws, plan.gemm_bytes, st, true);
+  }
+  const int ng = static_cast<int>(plan.groups.size());
+  if (ng == 1) return run_lockstep(plan, plan.groups[0], gemm_ws + plan.group_ws[0], plan.gemm_bytes, st, false);
+  int rc = ensure_side_streams(ng - 1);
+  if (rc) return rc;
+  SideStreams& ss = side_streams();
+  rc = cuda_status(cudaEventRecord(ss.fork, st), "cudaEventRecord(fork)");
+  if (rc) return rc;
+  for (int g = 1; g < ng; ++g) {
+    rc = cuda_status(cudaStreamWaitEvent(ss.s[g - 1], ss.fork, 0), "cudaStreamWaitEvent(fork)");
+    if (rc) return rc;
+  }
+  for (int g = 0; g < ng; ++g) {
+    const size_t off = plan.group_ws[g];
+    const size_t bytes = (g + 1 < ng ? plan.group_ws[g + 1] : plan.gemm_bytes) - off;
+    rc = run_lockstep(plan, plan.groups[g], gemm_ws + off, bytes, g == 0 ? st : ss.s[g - 1], false);
+    if (rc) return rc;
+  }
+  for (int g = 1; g < ng; ++g) {
+    rc = cuda_status(cudaEventRecord(ss.join[g - 1], ss.s[g - 1]), "cudaEventRecord(join)");
+    if (rc) return rc;
+    rc = cuda_status(cudaStreamWaitEvent(st, ss.join[g - 1], 0), "cudaStreamWaitEvent(join)");
+    if (rc) return rc;
+  }
+  return DPK_OK;
+}
+
+int run_lockstep(const SpdPlan& plan, const std::vector<int>& grp, char* gemm_ws, size_t gemm_bytes,
+                 cudaStream_t st, bool trace) {
+  std::vector<size_t> idx(grp.size(), 0);
   struct RoundRec {
     cudaEvent_t e0, e1, e2;
     int nleaf, maxn, ngemm;
@@ -578,15 +688,16 @@ int run_inverse(const dpk_spd_job* jobs, int n_jobs, void* workspace, cudaStream
     std::vector<dpk::LeafJob> leaves;
     std::vector<dpk::GemmSpec> g;
     bool any = false;
-    for (int i = 0; i < n_jobs; ++i) {
-      if (idx[i] >= plan.lists[i].size()) continue;
+    for (size_t q = 0; q < grp.size(); ++q) {
+      const auto& list = plan.lists[grp[q]];
+      if (idx[q] >= list.size()) continue;
       any = true;
-      const dpk::Op& op = plan.lists[i][idx[i]];
+      const dpk::Op& op = list[idx[q]];
       if (op.leaf)
         leaves.push_back(op.lj);
       else
-        for (int q = 0; q < op.ng; ++q) g.push_back(op.g[q]);
-      ++idx[i];
+        for (int t = 0; t < op.ng; ++t) g.push_back(op.g[t]);
+      ++idx[q];
     }
     if (!any) break;
     RoundRec rr{};
@@ -616,7 +727,7 @@ int run_inverse(const dpk_spd_job* jobs, int n_jobs, void* workspace, cudaStream
     }
     if (trace) cudaEventRecord(rr.e1, st);
     if (!g.empty()) {
-      int rc = dpk::gemm_launch(g.data(), static_cast<int>(g.size()), gemm_ws, plan.gemm_bytes, DPK_PREC_3XTF32, st);
+      int rc = dpk::gemm_launch(g.data(), static_cast<int>(g.size()), gemm_ws, gemm_bytes, DPK_PREC_3XTF32, st);
       if (rc) return rc;
     }
     if (trace) {

@@ -6,7 +6,7 @@ sys.path.insert(0, ROOT)
 import torch
 from paper_2206_15143_b200 import _lib as L, ops
 names = ["start", "setup", "tma_done", "gather_done", "mma_done", "epi_u0", "epi_last", "final_bar", "dealloc",
-         "epi_tfull", "epi_ld0", "epi_st0"]
+         "epi_tfull", "epi_ld0", "epi_st0", "c0_stores_done", "c0_sts", "c0_lds", "c0_pre_store"]
 lib = L.load()
 dev = torch.device("cuda", 0)
 for nprob, n, prec in [(1, 128, "tf32"), (1, 128, "3xtf32"), (32, 128, "3xtf32"), (84, 128, "3xtf32"), (84, 256, "3xtf32")]:
@@ -26,5 +26,5 @@ for nprob, n, prec in [(1, 128, "tf32"), (1, 128, "3xtf32"), (32, 128, "3xtf32")
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); g.replay(); e1.record(); torch.cuda.synchronize()
     buf = (C.c_ulonglong * 16)(); lib.dpk_debug_timestamps(buf); t0 = buf[0]
-    tl = {names[i]: round((buf[i] - t0) / 1000.0, 2) for i in range(12) if buf[i] >= t0}
+    tl = {names[i]: round((buf[i] - t0) / 1000.0, 2) for i in range(16) if buf[i] >= t0}
     print(f"{nprob:3d} x {n}^3 {prec}: {e0.elapsed_time(e1) / 20 * 1e3:.1f} us/launch (graph)  CTA0 {tl}", flush=True)
