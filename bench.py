@@ -242,7 +242,6 @@ def run_ours(args, rank, world, local_rank):
         kf.step()
     kf.check()
     sync_barrier()
-    kf.enable_stage_timing(True)
     launches0 = lib.dpk_launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     # DPK_PROFILE_TIMED=1: bracket exactly the timed steps for `ncu --profile-from-start off`
@@ -262,8 +261,27 @@ def run_ours(args, rank, world, local_rank):
     kf.check()
     launches = lib.dpk_launch_count() - launches0
     ms_local = start.elapsed_time(end) / args.steps
+    # per-stage split: the same steps with the stages serialized on one stream
+    # (the timed steps above overlap the largest layers' pipeline with the rest)
+    overlap = kf.overlap
+    kf.overlap = False
+    for _ in range(2):
+        restore()
+        kf.step()
+    sync_barrier()
+    kf.enable_stage_timing(True)
+    s1, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s1.record()
+    for _ in range(args.steps):
+        restore()
+        kf.step()
+    e1.record()
+    sync_barrier()
+    kf.check()
+    ms_serial = s1.elapsed_time(e1) / args.steps
     stages = {k: v / args.steps for k, v in kf.stage_ms().items()}
     kf.enable_stage_timing(False)
+    kf.overlap = overlap
     t = torch.tensor([ms_local], device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -371,6 +389,7 @@ def run_ours(args, rank, world, local_rank):
                        "assignment": args.assignment,
                        "memory_format": "channels_last" if mf is torch.channels_last else "contiguous",
                        "l2": "inputs (layer captures, >1.4 GB) larger than L2; no flush"},
+            "overlap": overlap, "ms_per_step_serialized": ms_serial,
             "stages_ms": stages, "stage_roofline": stage_roofline, "roofline": roofline,
             "cpu_baseline": cpu_baseline, "e2e": e2e, "gpu_launches": launches,
             "clocks": clocks.summary(),

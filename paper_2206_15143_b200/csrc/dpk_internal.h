@@ -5,7 +5,9 @@
 #include <cstddef>
 #include <cstdint>
 #include <string>
+#include <mutex>
 #include <utility>
+#include <vector>
 
 #include "../../include/dpkfac.h"
 
@@ -66,6 +68,57 @@ inline dpk_operand rows_mn(const float* p, int rows, int64_t cols, int64_t ld) {
 }
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Small LRU keyed by raw bytes: host-side plans (tensor maps, unit layouts,
+// workspace sizes) of launches that repeat every training step with the same
+// buffers are built once.  Not thread-safe by itself; callers hold `mu`.
+template <class V>
+struct LruCache {
+  struct Entry {
+    std::string key;
+    V value;
+    unsigned long long last;
+  };
+  std::mutex mu;
+  std::vector<Entry> entries;
+  unsigned long long tick = 0;
+  size_t cap = 64;
+  V* find(const std::string& k) {
+    for (auto& e : entries)
+      if (e.key == k) {
+        e.last = ++tick;
+        return &e.value;
+      }
+    return nullptr;
+  }
+  V* put(const std::string& k, V v) {
+    if (entries.size() >= cap) {
+      size_t old = 0;
+      for (size_t i = 1; i < entries.size(); ++i)
+        if (entries[i].last < entries[old].last) old = i;
+      entries.erase(entries.begin() + old);
+    }
+    entries.push_back(Entry{k, std::move(v), ++tick});
+    return &entries.back().value;
+  }
+};
+template <class T>
+inline void key_put(std::string& k, const T& v) {
+  k.append(reinterpret_cast<const char*>(&v), sizeof(T));
+}
+// every field of a GemmSpec (not its padding) -> cache key bytes
+inline void key_spec(std::string& k, const GemmSpec& g) {
+  key_put(k, g.job);
+  key_put(k, g.epi);
+  key_put(k, g.vrow);
+  key_put(k, g.vcol);
+  key_put(k, g.gamma);
+  key_put(k, g.out_t);
+  key_put(k, g.ldt);
+  key_put(k, g.tri_a);
+  key_put(k, g.tri_b);
+  key_put(k, g.lower_only);
+}
 
 // Kernel launch with optional programmatic dependent launch (DPK_PDL=1) and an
 // optional cluster dimension.  Kernels launched this way must call pdl_wait()

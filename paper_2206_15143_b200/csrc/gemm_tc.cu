@@ -59,7 +59,13 @@ constexpr int NTHREADS = (PROD_WARP0 + PROD_WARPS) * 32;  // 384
 constexpr int MAXP = 32;                                  // problems per launch (kernel params)
 static_assert(NPROD % 8 == 0, "im2col chunk sharing needs NPROD % 8 == 0");
 
-enum { TMA_NONE = 0, TMA_ROWS_K = 1, TMA_ROWS_MN = 2, TMA_SLAB = 3, TMA_IM2COL = 4 };
+// TMA_ROWS_MN3: MN-major operand whose row count is a multiple of 32, fetched as
+// ONE 3-D box {32 rows, 32 k, 4 row blocks} per 128-row tile instead of four
+// 2-D boxes (same shared-memory image)
+enum { TMA_NONE = 0, TMA_ROWS_K = 1, TMA_ROWS_MN = 2, TMA_SLAB = 3, TMA_IM2COL = 4, TMA_ROWS_MN3 = 5 };
+__host__ __device__ __forceinline__ bool tma_mn(int kind) {
+  return kind == TMA_ROWS_MN || kind == TMA_IM2COL || kind == TMA_ROWS_MN3;
+}
 
 __host__ __device__ __forceinline__ bool is_im2col(int kind) {
   return kind == DPK_OPND_IM2COL || kind == DPK_OPND_IM2COL_TAPMAJOR;
@@ -385,6 +391,11 @@ __device__ __forceinline__ void issue_tma(int kind, const CUtensorMap* map, cons
   } else if (kind == TMA_ROWS_MN) {
 #pragma unroll
     for (int b = 0; b < BM / 32; ++b) ld2(dst + b * 4096, row0 + 32 * b, kc * BK);
+  } else if (kind == TMA_ROWS_MN3) {  // dims {32, K, rows / 32}
+    if (PAIR)
+      tma_load_3d_pair(dst, map, bar, 0, kc * BK, row0 / 32);
+    else
+      tma_load_3d(dst, map, bar, 0, kc * BK, row0 / 32);
   } else if (kind == TMA_SLAB) {  // dims {HW, C, N}
     const int n = kc / cpn;
     if (PAIR)
@@ -792,8 +803,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         decode_unit(bt, u, pi, tm, tn, tile, split);
         const Problem& P = bt.p[pi];
         const bool skip_b = P.same_ab && tm == tn;
-        const int a_mn = P.tma_a == TMA_ROWS_MN || P.tma_a == TMA_IM2COL;
-        const int b_mn = skip_b ? a_mn : (P.tma_b == TMA_ROWS_MN || P.tma_b == TMA_IM2COL);
+        const int a_mn = tma_mn(P.tma_a);
+        const int b_mn = skip_b ? a_mn : tma_mn(P.tma_b);
         const uint32_t idesc = idesc_tf32(UT, UT, a_mn, b_mn);
         const int acc = it & 1;
         if (CG == 2)
@@ -934,7 +945,7 @@ struct RedJob {
   float alpha, beta, gamma;
   int M, N, symmetric, epi, tiles_n, splits;
   int ut;          // unit tile edge (128 or 256)
-  int slab_begin;  // prefix over (tiles x ut/rows-per-slab) slabs
+  int slab_begin;  // prefix over (tiles x (ut/32)^2) 32x32 blocks
 };
 struct RedBatch {
   int n;
@@ -942,23 +953,24 @@ struct RedBatch {
   RedJob j[RED_MAX];
 };
 
-// One CTA per (split tile, slab of 1024 elements): 256 threads x 4 consecutive
-// columns; a slab is 8 rows of a 128-wide tile or 4 rows of a 256-wide one.
+// One CTA per 32 x 32 block of a split unit tile: 256 threads, thread (ty, tx)
+// owns rows ty + 8q (q < 4) of column tx.  Partials are summed in split order
+// (deterministic), the single-split epilogue is applied, and every global
+// access is a 128-byte row segment: direct stores walk rows, the mirror /
+// transposed copies go through a padded shared-memory transpose.
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constant__ RedBatch b) {
   pdl_wait();
   pdl_trigger();
-  const int slab = blockIdx.x;
+  __shared__ float T[32][33];
+  const int blk = blockIdx.x;
   int p = 0;
-  while (p + 1 < b.n && b.j[p + 1].slab_begin <= slab) ++p;
+  while (p + 1 < b.n && b.j[p + 1].slab_begin <= blk) ++p;
   const RedJob& J = b.j[p];
   const int ut = J.ut;
-  const int tpr = ut / 4;            // threads per row
-  const int rows_per_slab = 256 / tpr;
-  const int local = slab - J.slab_begin;
-  const int slabs_per_tile = ut / rows_per_slab;
-  const int tile = local / slabs_per_tile;
-  const int row = (local - tile * slabs_per_tile) * rows_per_slab + threadIdx.x / tpr;
-  const int col = (threadIdx.x % tpr) * 4;
+  const int nb = ut / 32;  // 32-blocks per tile edge
+  const int local = blk - J.slab_begin;
+  const int tile = local / (nb * nb);
+  const int bi = (local - tile * nb * nb) / nb, bj = local % nb;
   int tm, tn;
   if (J.symmetric) {
     int r = static_cast<int>((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
@@ -970,34 +982,60 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
     tm = tile / J.tiles_n;
     tn = tile - tm * J.tiles_n;
   }
-  const int gm = tm * ut + row;
-  if (gm >= J.M) return;
-  const int64_t unit = static_cast<int64_t>(ut) * ut;
-  const float* src = J.partials + static_cast<int64_t>(tile) * J.splits * unit + static_cast<int64_t>(row) * ut + col;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int s = 0; s < J.splits; ++s) {
-    const float4 x = __ldcg(reinterpret_cast<const float4*>(src + s * unit));
-    acc.x += x.x;
-    acc.y += x.y;
-    acc.z += x.z;
-    acc.w += x.w;
-  }
-  const float a[4] = {acc.x, acc.y, acc.z, acc.w};
   const bool diag = J.symmetric == 1 && tm == tn;
-  const float vr = (J.epi == EPI_EIGDIV) ? fmaxf(J.vrow[gm], 0.0f) : 0.0f;
+  if (diag && bj > bi) return;  // block entirely above the diagonal: the mirror writes it
+  const int gm0 = tm * ut + bi * 32, gn0 = tn * ut + bj * 32;
+  if (gm0 >= J.M || gn0 >= J.N) return;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t unit = static_cast<int64_t>(ut) * ut;
+  const float* src = J.partials + static_cast<int64_t>(tile) * J.splits * unit +
+                     static_cast<int64_t>(bi * 32) * ut + bj * 32 + tx;
+  // 4 interleaved partial sums per element (splits s = 4t + u), so 16 loads are in
+  // flight per thread; combined in a fixed order (deterministic)
+  float acc4[4][4] = {};
+  int s = 0;
+  for (; s + 4 <= J.splits; s += 4) {
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const int gn = tn * ut + col + e;
-    if (gn >= J.N || (diag && gn > gm)) continue;
-    float val = J.alpha * a[e];
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc4[u][q] += __ldcg(src + (s + u) * unit + static_cast<int64_t>(ty + 8 * q) * ut);
+  }
+  for (; s < J.splits; ++s) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) acc4[0][q] += __ldcg(src + s * unit + static_cast<int64_t>(ty + 8 * q) * ut);
+  }
+  float acc[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) acc[q] = (acc4[0][q] + acc4[1][q]) + (acc4[2][q] + acc4[3][q]);
+  const int gn = gn0 + tx;
+  const float vc = (J.epi == EPI_EIGDIV && gn < J.N) ? fmaxf(J.vcol[gn], 0.0f) : 0.0f;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = ty + 8 * q;
+    const int gm = gm0 + r;
+    float val = J.alpha * acc[q];
+    const bool in = gm < J.M && gn < J.N;
     if (J.epi == EPI_EIGDIV) {
-      val = val / (vr * fmaxf(J.vcol[gn], 0.0f) + J.gamma);
-    } else if (J.beta != 0.0f) {
-      val += J.beta * J.cin[gm * J.ldc + gn];
+      val = in ? val / (fmaxf(J.vrow[gm], 0.0f) * vc + J.gamma) : 0.0f;
+    } else if (J.beta != 0.0f && in && !(diag && gn > gm)) {
+      val += J.beta * J.cin[static_cast<int64_t>(gm) * J.ldc + gn];
     }
-    J.out[gm * J.ldo + gn] = val;
-    if (J.symmetric == 1 && gn != gm) J.out[static_cast<int64_t>(gn) * J.ldo + gm] = val;
-    if (J.out_t) J.out_t[static_cast<int64_t>(gn) * J.ldt + gm] = val;
+    if (in && !(diag && gn > gm)) J.out[static_cast<int64_t>(gm) * J.ldo + gn] = val;
+    T[r][tx] = val;
+  }
+  if (J.symmetric != 1 && !J.out_t) return;
+  __syncthreads();
+  // transposed pass: element (row gm0 + tx, column gn0 + r) of the block goes to
+  // out[gn0 + r][gm0 + tx] (mirror, strictly lower elements) and out_t likewise
+  const int gmt = gm0 + tx;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = ty + 8 * q;
+    const int gnt = gn0 + r;
+    const float val = T[tx][r];
+    const bool in = gmt < J.M && gnt < J.N && !(diag && gnt > gmt);
+    if (J.symmetric == 1 && in && gnt != gmt) J.out[static_cast<int64_t>(gnt) * J.ldo + gmt] = val;
+    if (J.out_t && in) J.out_t[static_cast<int64_t>(gnt) * J.ldt + gmt] = val;
   }
 }
 
@@ -1029,6 +1067,15 @@ bool tma_disabled() {
   return v == 1;
 }
 
+bool mn3_disabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DPK_MN3");
+    v = (e && e[0] == '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 // tf32_rn: TMA rounds fp32 -> TF32 (nearest) in flight (TFLOAT32 data type);
@@ -1051,6 +1098,12 @@ int plan_tma_2d(const dpk_operand& o, CUtensorMap* m, bool rn) {
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(o.ld) * 4};
     const cuuint32_t box[2] = {BK, BM};
     return encode(m, 2, o.data, dims, strides, box, rn) ? TMA_ROWS_K : TMA_NONE;
+  }
+  if (o.kind == DPK_OPND_ROWS_MN && o.rows % 32 == 0 && !mn3_disabled()) {
+    const cuuint64_t dims[3] = {32, static_cast<cuuint64_t>(o.cols), static_cast<cuuint64_t>(o.rows / 32)};
+    const cuuint64_t strides[2] = {static_cast<cuuint64_t>(o.ld) * 4, 128};
+    const cuuint32_t box[3] = {32, BK, BM / 32};
+    if (encode(m, 3, o.data, dims, strides, box, rn, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)) return TMA_ROWS_MN3;
   }
   if (o.kind == DPK_OPND_ROWS_MN) {
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(o.rows), static_cast<cuuint64_t>(o.cols)};
@@ -1277,9 +1330,11 @@ bool wants_cg2(const GemmSpec& g) {
 }
 
 // Pairs only pay when the eligible problems give every pair work: a group whose
-// 256x256 units cannot fill the GPU (fewer units than SMs) runs as single CTAs,
-// where twice the CTAs share the same output (measured: the 2048/2304 Schur
-// rounds of the SPD recursion lose 30% as pairs, the 4608 products gain 30%).
+// 256x256 units -- counting the split-K pieces of at least 32 chunks that long-K
+// problems can be cut into -- cannot fill the GPU runs as single CTAs, where
+// twice the CTAs share the same output (measured: the 2048/2304 Schur rounds of
+// the SPD recursion lose 30% as pairs, the 4608 products gain 30%; a 576 x 100352
+// factor SYRK gains as pairs despite the 256-row padding).
 void partition_cg(const GemmSpec* specs, int n, std::vector<GemmSpec>& g1, std::vector<GemmSpec>& g2) {
   g1.clear();
   g2.clear();
@@ -1287,7 +1342,8 @@ void partition_cg(const GemmSpec* specs, int n, std::vector<GemmSpec>& g1, std::
   for (int i = 0; i < n; ++i) {
     if (!wants_cg2(specs[i])) continue;
     const int64_t tm = (operand_rows(specs[i].job.a) + 255) / 256, tn = (operand_rows(specs[i].job.b) + 255) / 256;
-    units2 += specs[i].job.symmetric ? tm * (tm + 1) / 2 : tm * tn;
+    const int64_t pieces = std::max<int64_t>(1, specs[i].job.a.cols / (32 * BK));
+    units2 += (specs[i].job.symmetric ? tm * (tm + 1) / 2 : tm * tn) * pieces;
   }
   const bool pairs = units2 >= num_sms();
   for (int i = 0; i < n; ++i) (pairs && wants_cg2(specs[i]) ? g2 : g1).push_back(specs[i]);
@@ -1430,8 +1486,34 @@ bool debug_ts_enabled() {
   return v == 1;
 }
 
+std::string specs_key(const GemmSpec* specs, int n, int precision) {
+  std::string k;
+  k.reserve(static_cast<size_t>(n) * (sizeof(GemmSpec) + 8) + 16);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  key_put(k, dev);
+  key_put(k, precision);
+  for (int i = 0; i < n; ++i) key_spec(k, specs[i]);
+  return k;
+}
+
+size_t gemm_workspace_bytes_uncached(const GemmSpec* specs, int n);
+
 size_t gemm_workspace_bytes(const GemmSpec* specs, int n) {
   if (n <= 0) return 0;
+  static LruCache<size_t> cache;
+  const std::string k = specs_key(specs, n, 0);
+  {
+    std::lock_guard<std::mutex> lock(cache.mu);
+    if (size_t* v = cache.find(k)) return *v;
+  }
+  const size_t ws = gemm_workspace_bytes_uncached(specs, n);
+  std::lock_guard<std::mutex> lock(cache.mu);
+  cache.put(k, ws);
+  return ws;
+}
+
+size_t gemm_workspace_bytes_uncached(const GemmSpec* specs, int n) {
   std::vector<GemmSpec> g1, g2;
   partition_cg(specs, n, g1, g2);
   size_t ws = 0;
@@ -1454,26 +1536,41 @@ int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int pre
     return DPK_EARG;
   }
   // big problems run on CTA pairs, the rest on single CTAs (two launches, same
-  // stream: the split-K workspace is reused in order)
-  std::vector<GemmSpec> g1, g2;
-  partition_cg(specs, n, g1, g2);
-  for (int cg = 2; cg >= 1; --cg) {
-    std::vector<GemmSpec>& g = cg == 2 ? g2 : g1;
-    if (g.empty()) continue;
-    Plan plan;
-    int rc = make_plan(g.data(), static_cast<int>(g.size()), plan, true, precision, cg);
-    if (rc != DPK_OK) return rc;
-    if (cg == 2) {
-      // a view the predicate accepted must have been TMA-planned; anything else
-      // (encode failure) is an internal inconsistency, not a silent fallback
-      for (const auto& P : plan.probs) {
-        if (P.tma_a == TMA_NONE || (!P.same_ab && P.tma_b == TMA_NONE)) {
-          set_error("dpk_gemm: CTA-pair problem without a TMA plan (tensor map encode failed)");
-          return DPK_ECUDA;
+  // stream: the split-K workspace is reused in order).  The plans (tensor maps
+  // included) of a job list seen before come from the cache.
+  static LruCache<std::vector<Plan>> cache;
+  const std::string key = specs_key(specs, n, precision);
+  std::vector<Plan> plans;
+  {
+    std::lock_guard<std::mutex> lock(cache.mu);
+    if (std::vector<Plan>* v = cache.find(key)) plans = *v;
+  }
+  if (plans.empty()) {
+    std::vector<GemmSpec> g1, g2;
+    partition_cg(specs, n, g1, g2);
+    for (int cg = 2; cg >= 1; --cg) {
+      std::vector<GemmSpec>& g = cg == 2 ? g2 : g1;
+      if (g.empty()) continue;
+      Plan plan;
+      int rc = make_plan(g.data(), static_cast<int>(g.size()), plan, true, precision, cg);
+      if (rc != DPK_OK) return rc;
+      if (cg == 2) {
+        // a view the predicate accepted must have been TMA-planned; anything else
+        // (encode failure) is an internal inconsistency, not a silent fallback
+        for (const auto& P : plan.probs) {
+          if (P.tma_a == TMA_NONE || (!P.same_ab && P.tma_b == TMA_NONE)) {
+            set_error("dpk_gemm: CTA-pair problem without a TMA plan (tensor map encode failed)");
+            return DPK_ECUDA;
+          }
         }
       }
+      plans.push_back(std::move(plan));
     }
-    rc = run_plan(plan, ws, ws_bytes, precision, st);
+    std::lock_guard<std::mutex> lock(cache.mu);
+    cache.put(key, plans);
+  }
+  for (Plan& plan : plans) {
+    const int rc = run_plan(plan, ws, ws_bytes, precision, st);
     if (rc != DPK_OK) return rc;
   }
   return DPK_OK;

@@ -64,21 +64,32 @@ struct LeafBatch {
 // One fused sweep does both
 //   right-looking Cholesky      A[i][j] -= L[i][k] L[j][k]            (i, j > k)
 //   right-looking L^-1 (trtri)  X[i][:] -= L[i][k] X[k][:] / L[k][k]  (i > k)
-// four columns per __syncthreads: the owners publish columns k..k+3 of A and
-// rows k..k+3 of X (double-buffered), every thread factors the 4x4 pivot block
-// itself (identically) and applies the rank-4 updates to its registers.
-// Blocks that provably stay zero / untouched are skipped at compile time (the
-// 16-row block index kr is unrolled).  Padding rows/columns are the identity,
-// so pivots past n are 1 and the real n x n result is unaffected.
+// four columns k..k+3 per step, in three phases separated by two barriers:
+//   1. the owners publish the raw columns k..k+3 of A and rows k..k+3 of X;
+//   2. thread i < N turns row i of the column panel into L[i][k..k+3] (forward
+//      substitution with the 4x4 pivot block, which each of these threads
+//      factors itself), thread N + j turns column j of the X rows into the
+//      finished X[k..k+3][j]; both are published (zero where they do not apply);
+//   3. every thread applies the rank-4 updates to its registers, reading the
+//      published L / X values as float4 broadcasts.
+// Only lower-triangle blocks of A are updated (blocks entirely above the
+// diagonal are skipped at compile time; the 16-row block index kr is
+// unrolled), so the upper triangle of the input is never read.  Padding
+// rows/columns are the identity, so pivots past n are 1 and the real n x n
+// result is unaffected.
 template <int RB>
 __global__ void __launch_bounds__(LEAF_THREADS, 1) spd_leaf_kernel(const __grid_constant__ LeafBatch b) {
   constexpr int N = 16 * RB;
-  constexpr int CB = RB / 2;
+  constexpr int CB = RB / 2 > 0 ? RB / 2 : 1;
   constexpr int LDX = N + 1;
   extern __shared__ float smem[];
-  float* colb = smem;          // [2][4][N] columns k..k+3 of the partially factored A
-  float* rowb = smem + 8 * N;  // [2][4][N] rows k..k+3 of the partially solved X
-  float* Xs = smem + 16 * N;   // [N][N+1] X for the FULL-mode X^T X
+  float4* colb = reinterpret_cast<float4*>(smem);  // [N] raw A[i][k..k+3]
+  float4* rowb = colb + N;                         // [N] raw X[k..k+3][j]
+  float4* lpan = rowb + N;                         // [N] L[i][k..k+3] (0 for i <= k+3)
+  float4* xrow = lpan + N;                         // [N] finished X[k..k+3][j] (0 for j > k+3)
+  float* Xs = smem + 16 * N;                       // [N][N+1] X for the FULL-mode X^T X
+  __shared__ int s_fail;
+  if (threadIdx.x == 0) s_fail = 0;
   pdl_wait();
   pdl_trigger();
   const LeafJob& J = b.j[blockIdx.x];
@@ -114,96 +125,100 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) spd_leaf_kernel(const __grid_
 #pragma unroll 1
     for (int kq = 0; kq < 4; ++kq) {
       const int k = 16 * kr + 4 * kq;
-      float* cb = colb + (kq & 1) * 4 * N;  // group parity (4 groups per kr)
-      float* rb = rowb + (kq & 1) * 4 * N;
+      // ---- phase 1: publish raw columns k..k+3 (rows >= 16 kr) and X rows k..k+3
       const int tcol = tx - (k & 31), trow = ty - (k & 15);
       if (tcol >= 0 && tcol < 4) {
+        float* cf = reinterpret_cast<float*>(colb);
 #pragma unroll
-        for (int r = kr; r < RB; ++r) cb[tcol * N + ty + 16 * r] = a[r][kc];
+        for (int r = kr; r < RB; ++r) cf[(ty + 16 * r) * 4 + tcol] = a[r][kc];
       }
       if (trow >= 0 && trow < 4) {
+        float* rf = reinterpret_cast<float*>(rowb);
 #pragma unroll
-        for (int c = 0; c <= kc; ++c) rb[trow * N + tx + 32 * c] = x[kr][c];
+        for (int c = 0; c <= kc; ++c) rf[(tx + 32 * c) * 4 + trow] = x[kr][c];
       }
       __syncthreads();
-      const float p00 = cb[k], p10 = cb[k + 1], p20 = cb[k + 2], p30 = cb[k + 3];
-      const float p11 = cb[N + k + 1], p21 = cb[N + k + 2], p31 = cb[N + k + 3];
-      const float p22 = cb[2 * N + k + 2], p32 = cb[2 * N + k + 3];
-      const float p33 = cb[3 * N + k + 3];
-      const float d0 = p00;
-      const float i0 = 1.0f / sqrtf(d0);
-      const float l10 = p10 * i0, l20 = p20 * i0, l30 = p30 * i0;
-      const float d1 = p11 - l10 * l10;
-      const float i1 = 1.0f / sqrtf(d1);
-      const float l21 = (p21 - l20 * l10) * i1, l31 = (p31 - l30 * l10) * i1;
-      const float d2 = p22 - l20 * l20 - l21 * l21;
-      const float i2 = 1.0f / sqrtf(d2);
-      const float l32 = (p32 - l30 * l20 - l31 * l21) * i2;
-      const float d3 = p33 - l30 * l30 - l31 * l31 - l32 * l32;
-      const float i3 = 1.0f / sqrtf(d3);
-      const bool ok = (d0 > 0.0f) && (d1 > 0.0f) && (d2 > 0.0f) && (d3 > 0.0f) && isfinite(i0) && isfinite(i1) &&
-                      isfinite(i2) && isfinite(i3);
-      if (!ok) {  // uniform: every thread factored the same block
+      // ---- phase 2: pivot block, L panel, finished X rows
+      if (tid < 2 * N) {
+        const float4 q0 = colb[k], q1 = colb[k + 1], q2 = colb[k + 2], q3 = colb[k + 3];
+        const float d0 = q0.x;
+        const float i0 = 1.0f / sqrtf(d0);
+        const float l10 = q1.x * i0, l20 = q2.x * i0, l30 = q3.x * i0;
+        const float d1 = q1.y - l10 * l10;
+        const float i1 = 1.0f / sqrtf(d1);
+        const float l21 = (q2.y - l20 * l10) * i1, l31 = (q3.y - l30 * l10) * i1;
+        const float d2 = q2.z - l20 * l20 - l21 * l21;
+        const float i2 = 1.0f / sqrtf(d2);
+        const float l32 = (q3.z - l30 * l20 - l31 * l21) * i2;
+        const float d3 = q3.w - l30 * l30 - l31 * l31 - l32 * l32;
+        const float i3 = 1.0f / sqrtf(d3);
+        const bool ok = (d0 > 0.0f) && (d1 > 0.0f) && (d2 > 0.0f) && (d3 > 0.0f) && isfinite(i0) && isfinite(i1) &&
+                        isfinite(i2) && isfinite(i3);
+        if (!ok && tid == 0) s_fail = 1;  // uniform: every phase-2 thread factored the same block
+        if (tid < N) {
+          const int i = tid;
+          const float4 v = colb[i];
+          float4 l = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (i > k + 3) {
+            l.x = v.x * i0;
+            l.y = (v.y - l.x * l10) * i1;
+            l.z = (v.z - l.x * l20 - l.y * l21) * i2;
+            l.w = (v.w - l.x * l30 - l.y * l31 - l.z * l32) * i3;
+          }
+          lpan[i] = l;
+        } else {
+          const int j = tid - N;
+          const float4 v = rowb[j];
+          float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (j <= k + 3) {
+            o.x = v.x * i0;
+            o.y = (v.y - l10 * o.x) * i1;
+            o.z = (v.z - l20 * o.x - l21 * o.y) * i2;
+            o.w = (v.w - l30 * o.x - l31 * o.y - l32 * o.z) * i3;
+          }
+          xrow[j] = o;
+        }
+      }
+      __syncthreads();
+      if (s_fail) {  // a non-positive pivot: exactly where cho_factor raises
         if (tid == 0 && J.info) *J.info = J.fail_code;
         return;
       }
-      float lr[RB][4], lc[CB][4];
+      // ---- phase 3: rank-4 updates (lower-triangle blocks of A; X columns <= k+3)
+      float4 lr[RB], lc[CB], xn[CB];
 #pragma unroll
-      for (int r = kr; r < RB; ++r) {
-        const int i = ty + 16 * r;
-        const float v0 = cb[i] * i0;
-        const float v1 = (cb[N + i] - v0 * l10) * i1;
-        const float v2 = (cb[2 * N + i] - v0 * l20 - v1 * l21) * i2;
-        const float v3 = (cb[3 * N + i] - v0 * l30 - v1 * l31 - v2 * l32) * i3;
-        const bool on = i > k + 3;
-        lr[r][0] = on ? v0 : 0.0f;
-        lr[r][1] = on ? v1 : 0.0f;
-        lr[r][2] = on ? v2 : 0.0f;
-        lr[r][3] = on ? v3 : 0.0f;
-      }
+      for (int r = kr; r < RB; ++r) lr[r] = lpan[ty + 16 * r];
 #pragma unroll
-      for (int c = kc; c < CB; ++c) {
-        const int j = tx + 32 * c;
-        const float v0 = cb[j] * i0;
-        const float v1 = (cb[N + j] - v0 * l10) * i1;
-        const float v2 = (cb[2 * N + j] - v0 * l20 - v1 * l21) * i2;
-        const float v3 = (cb[3 * N + j] - v0 * l30 - v1 * l31 - v2 * l32) * i3;
-        const bool on = j > k + 3;
-        lc[c][0] = on ? v0 : 0.0f;
-        lc[c][1] = on ? v1 : 0.0f;
-        lc[c][2] = on ? v2 : 0.0f;
-        lc[c][3] = on ? v3 : 0.0f;
-      }
-      float xn[4][CB];  // finished X rows k..k+3, this thread's columns
+      for (int c = kc; c < CB; ++c) lc[c] = lpan[tx + 32 * c];
 #pragma unroll
-      for (int c = 0; c <= kc; ++c) {
-        const int j = tx + 32 * c;
-        xn[0][c] = rb[j] * i0;
-        xn[1][c] = (rb[N + j] - l10 * xn[0][c]) * i1;
-        xn[2][c] = (rb[2 * N + j] - l20 * xn[0][c] - l21 * xn[1][c]) * i2;
-        xn[3][c] = (rb[3 * N + j] - l30 * xn[0][c] - l31 * xn[1][c] - l32 * xn[2][c]) * i3;
-      }
+      for (int c = 0; c <= kc; ++c) xn[c] = xrow[tx + 32 * c];
 #pragma unroll
       for (int r = kr; r < RB; ++r) {
 #pragma unroll
         for (int c = kc; c < CB; ++c) {
+          if (RB > 2 && r <= 2 * c - 1) continue;  // block entirely above the diagonal
           float v = a[r][c];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) v = fmaf(-lr[r][t], lc[c][t], v);
+          v = fmaf(-lr[r].x, lc[c].x, v);
+          v = fmaf(-lr[r].y, lc[c].y, v);
+          v = fmaf(-lr[r].z, lc[c].z, v);
+          v = fmaf(-lr[r].w, lc[c].w, v);
           a[r][c] = v;
         }
 #pragma unroll
         for (int c = 0; c <= kc; ++c) {
+          if (RB > 2 && r <= 2 * c - 1) continue;  // X is lower triangular
           float v = x[r][c];
-#pragma unroll
-          for (int t = 0; t < 4; ++t) v = fmaf(-lr[r][t], xn[t][c], v);
+          v = fmaf(-lr[r].x, xn[c].x, v);
+          v = fmaf(-lr[r].y, xn[c].y, v);
+          v = fmaf(-lr[r].z, xn[c].z, v);
+          v = fmaf(-lr[r].w, xn[c].w, v);
           x[r][c] = v;
         }
       }
       if (trow >= 0 && trow < 4) {
 #pragma unroll
         for (int c = 0; c <= kc; ++c)
-          x[kr][c] = trow == 0 ? xn[0][c] : trow == 1 ? xn[1][c] : trow == 2 ? xn[2][c] : xn[3][c];
+          x[kr][c] = trow == 0 ? xn[c].x : trow == 1 ? xn[c].y : trow == 2 ? xn[c].z : xn[c].w;
       }
     }
   }
@@ -257,7 +272,7 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) spd_leaf_kernel(const __grid_
 
 template <int RB>
 constexpr int leaf_smem_bytes() {
-  return (16 * 16 * RB + 16 * RB * (16 * RB + 1)) * 4;
+  return (16 * 16 * RB + 16 * RB * (16 * RB + 1)) * 4;  // 4 float4 panels of N + the X^T X copy
 }
 
 // Blocked-path set-up, one warp per row i:  Aw[i][0..i] = src[i][0..i] (+ shift
@@ -582,9 +597,23 @@ extern "C" {
 
 size_t dpk_chol_inv_workspace_bytes(const dpk_spd_job* jobs, int n_jobs) {
   if (n_jobs <= 0 || jobs == nullptr) return 0;
+  // depends only on the sizes (the plan is built against a dummy base) -> cache by sizes
+  static dpk::LruCache<size_t> cache;
+  std::string key;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dpk::key_put(key, dev);
+  for (int i = 0; i < n_jobs; ++i) dpk::key_put(key, jobs[i].n);
+  {
+    std::lock_guard<std::mutex> lock(cache.mu);
+    if (size_t* v = cache.find(key)) return *v;
+  }
   dpk::SpdPlan plan;
   dpk::make_spd_plan(jobs, n_jobs, nullptr, plan);
-  return dpk::align_up(plan.rec_bytes, 1024) + plan.gemm_bytes;
+  const size_t need = dpk::align_up(plan.rec_bytes, 1024) + plan.gemm_bytes;
+  std::lock_guard<std::mutex> lock(cache.mu);
+  cache.put(key, need);
+  return need;
 }
 
 int dpk_chol_inv_damped_batched(const dpk_spd_job* jobs, int n_jobs, void* workspace, size_t ws_bytes,

@@ -169,7 +169,7 @@ class DPKFAC:
                  assignment: Union[str, Sequence[Sequence[int]]] = "round_robin",
                  process_group=None, precision: str = "tf32", precond_precision: str = "3xtf32",
                  grad_scale: Union[str, float] = "batch", check_numerics: Union[bool, str] = True,
-                 im2col: str = "materialize"):
+                 im2col: str = "materialize", overlap: bool = True):
         self.hyper = KfacHyper(gamma=gamma, xi=xi, inv_type=inv_type, f_freq=f_freq, k_freq=k_freq)
         if im2col not in ("materialize", "implicit"):
             raise ArgumentError("im2col must be 'materialize' or 'implicit'")
@@ -184,7 +184,7 @@ class DPKFAC:
         if check_numerics not in (True, False, "sync", "deferred"):
             raise ArgumentError("check_numerics must be True/'sync', 'deferred' or False")
         # True/"sync": raise inside the failing step (one device->host read per step);
-        # "deferred": the read is asynchronous and a failure raises at the next step() / check()
+        # "deferred": the read is asynchronous and a failure raises at a later step() / check()
         self.check_numerics = "sync" if check_numerics is True else check_numerics
         self._pending_info = None
         self.model = model
@@ -240,6 +240,12 @@ class DPKFAC:
             self._hooks.append(ly.module.register_forward_hook(self._make_fwd_hook(ly)))
         self._bufs_ready = False
         self.last_stage_ms = {}
+        # overlap=True: the owned layers of the largest size class (whose inversion
+        # is a long, latency-bound chain of small launches) run their whole
+        # factor -> inverse -> precondition pipeline on a high-priority side
+        # stream while the other layers' throughput-bound work fills the GPU
+        self.overlap = bool(overlap)
+        self._side = None
 
     # ------------------------------------------------------------ hooks
     def _make_pre_hook(self, ly: _Layer):
@@ -271,6 +277,8 @@ class DPKFAC:
             if not ly.owned:
                 ly.a_in = ly.g_out = None
         self.owned = [self.layers[i] for i in sorted(mine)]
+        for k, ly in enumerate(self.owned):
+            ly.slot = k
 
     def _finalize_balance(self):
         costs = []
@@ -317,7 +325,7 @@ class DPKFAC:
     def step(self):
         h = self.hyper
         t = self.t
-        self.check()
+        self.check(block=False)
         if self._pending_balance:
             self._finalize_balance()
         if not self._bufs_ready:
@@ -331,62 +339,20 @@ class DPKFAC:
         k_up = t % h.k_freq == 0
         owned = self.owned
         self.info.zero_()
+        crit, rest = self._split_critical(owned)
+        main = torch.cuda.current_stream(self.device)
         self._mark("start")
+        if crit:
+            side = self._side_stream()
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                self._factor_stage(crit, t, f_up, side)
+                self._inverse_stage(crit, t, k_up)
         # (1) Kronecker factors + running average: one grouped tcgen05 launch
-        if f_up and owned:
-            jobs, keep, patches = [], [], []
-            for ly in owned:
-                if ly.a_in is None or ly.g_out is None:
-                    raise ArgumentError(f"worker {self.rank}, layer {ly.index}: captured inputs must be a "
-                                        "nonempty d x B matrix (run forward and backward before step())")
-                ly.alloc_state(h.inv_type, self.device)
-                first = not ly.initialized
-                w = 1.0 if first else h.xi
-                beta = 0.0 if first else 1.0 - h.xi
-                oa, pending = ly.operand_a(self.im2col)
-                og = ly.operand_g()
-                if pending is not None:
-                    patches.append(pending)
-                m = oa.cols
-                if og.cols != m:
-                    raise ArgumentError(f"worker {self.rank}, layer {ly.index}: capture batch counts differ: "
-                                        f"{m} inputs vs {og.cols} gradients")
-                s = float(ly.batch) if self.grad_scale == "batch" else float(self.grad_scale)
-                jobs.append(ops.factor_job(oa, ly.a_cov, w / m, beta))
-                jobs.append(ops.factor_job(og, ly.g_cov, w * s * s / m, beta))
-                keep.append((ly.a_in, ly.g_out))
-            ops.im2col_materialize(patches)  # one launch for every materialized conv
-            ops.syrk_ema(jobs, self.precision, device=self.device)
-            for ly in owned:
-                ly.initialized = True
-                ly.last_factor_update = t
-                ly.a_in = ly.g_out = None
-            del keep
+        self._factor_stage(rest, t, f_up, None)
         self._mark("factors")
         # (2) inverses / eigendecompositions
-        if k_up and owned:
-            for ly in owned:
-                if not ly.initialized:
-                    raise OrderingError(f"worker {self.rank}, layer {ly.index}: cannot build a preconditioner "
-                                        "before any factor update")
-                ly.alloc_state(h.inv_type, self.device)
-            if h.inv_type == "eigen":
-                jt = []
-                for ly in owned:
-                    jt.append((ly.a_cov, ly.a_q, ly.a_w, self.info[ly.index]))
-                    jt.append((ly.g_cov, ly.g_q, ly.g_w, self.info[ly.index]))
-                ops.syevd(jt)
-            else:
-                ops.trace_pi([(ly.a_cov, ly.g_cov) for ly in owned], h.gamma, self.shifts, self.pis,
-                             [self.info[ly.index] for ly in owned])
-                sj = []
-                for k, ly in enumerate(owned):
-                    sj.append(ops.spd_job(ly.a_cov, ly.a_inv, self.shifts[k, 0], self.info[ly.index], L.INFO_NOT_SPD_A))
-                    sj.append(ops.spd_job(ly.g_cov, ly.g_inv, self.shifts[k, 1], self.info[ly.index], L.INFO_NOT_SPD_G))
-                ops.chol_inv(sj)
-            for ly in owned:
-                ly.holds = h.inv_type
-                ly.last_inverse_update = t
+        self._inverse_stage(rest, t, k_up)
         self._mark("inversion")
         # (3) pack every layer's [W | b] gradient, owner-major (scaled by 1/P)
         segs = self._segments("grad")
@@ -399,25 +365,20 @@ class DPKFAC:
             self._allreduce_others()
         self._mark("comm_rs")
         # (5) precondition owned layers, one grouped launch per GEMM phase
-        if owned:
-            pj = []
-            for ly in owned:
-                if ly.holds != h.inv_type:
-                    what = "eigendecomposition" if h.inv_type == "eigen" else "damped inverse"
-                    raise OrderingError(f"worker {self.rank}, layer {ly.index}: preconditioning requested "
-                                        f"before any {what} exists")
-                shape = (ly.d_out, ly.d_in)
-                g, o, tmp = X.view_in(ly.index, shape), X.view_out(ly.index, shape), X.view_tmp(ly.index, shape)
-                if h.inv_type == "eigen":
-                    pj.append(ops.precond_job(g, ly.a_q, ly.g_q, o, tmp, ly.a_w, ly.g_w, self.info[ly.index]))
-                else:
-                    pj.append(ops.precond_job(g, ly.a_inv, ly.g_inv, o, tmp))
-            ops.precondition(pj, h.inv_type == "eigen", h.gamma, self.precond_precision)
+        if crit:
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                self._precondition_stage(crit)
+        self._precondition_stage(rest)
+        if crit:
+            main.wait_stream(side)
         self._mark("precondition")
         # numeric failures: reference wording, prefixed "worker p, layer i" (distsim.py:273-274)
         if self.check_numerics == "sync":
             self._raise_from_host(self._gather_info().cpu())
         elif self.check_numerics == "deferred":
+            if self._pending_info is not None:  # an unread older flag set: wait for it now
+                self.check()
             host = torch.empty(self.info.shape, dtype=torch.int32, pin_memory=True)
             host.copy_(self._gather_info(), non_blocking=True)
             ev = torch.cuda.Event()
@@ -428,6 +389,111 @@ class DPKFAC:
         ops.unpack(segs, X.out_flat, 1.0)
         self._mark("comm_ag")
         self.t += 1
+
+    # ------------------------------------------------------------ stages
+    def _side_stream(self):
+        if self._side is None:
+            self._side = torch.cuda.Stream(self.device, priority=-1)
+        return self._side
+
+    def _split_critical(self, owned):
+        """(critical, rest): the owned layers of the largest size class run on the
+        side stream when overlapping (a strict, non-empty subset only)."""
+        if not self.overlap or len(owned) < 2:
+            return [], owned
+        size = [max(ly.d_in, ly.d_out) for ly in owned]
+        big = max(size)
+        crit = [ly for ly, d in zip(owned, size) if 10 * d >= 6 * big]
+        if len(crit) == len(owned):
+            return [], owned
+        return crit, [ly for ly, d in zip(owned, size) if 10 * d < 6 * big]
+
+    def _factor_stage(self, layers, t, f_up, stream):
+        """A3 + A4 for ``layers`` on the current stream (captures were produced on
+        the main stream; ``stream`` set = keep them alive for it)."""
+        h = self.hyper
+        if not (f_up and layers):
+            return
+        jobs, patches = [], []
+        for ly in layers:
+            if ly.a_in is None or ly.g_out is None:
+                raise ArgumentError(f"worker {self.rank}, layer {ly.index}: captured inputs must be a "
+                                    "nonempty d x B matrix (run forward and backward before step())")
+            ly.alloc_state(h.inv_type, self.device)
+            first = not ly.initialized
+            w = 1.0 if first else h.xi
+            beta = 0.0 if first else 1.0 - h.xi
+            oa, pending = ly.operand_a(self.im2col)
+            og = ly.operand_g()
+            if pending is not None:
+                patches.append(pending)
+            m = oa.cols
+            if og.cols != m:
+                raise ArgumentError(f"worker {self.rank}, layer {ly.index}: capture batch counts differ: "
+                                    f"{m} inputs vs {og.cols} gradients")
+            s = float(ly.batch) if self.grad_scale == "batch" else float(self.grad_scale)
+            jobs.append(ops.factor_job(oa, ly.a_cov, w / m, beta))
+            jobs.append(ops.factor_job(og, ly.g_cov, w * s * s / m, beta))
+            if stream is not None:
+                ly.a_in.record_stream(stream)
+                ly.g_out.record_stream(stream)
+        ops.im2col_materialize(patches)  # one launch for every materialized conv
+        ops.syrk_ema(jobs, self.precision, device=self.device)
+        for ly in layers:
+            ly.initialized = True
+            ly.last_factor_update = t
+            ly.a_in = ly.g_out = None
+
+    def _inverse_stage(self, layers, t, k_up):
+        """A6-A9 for ``layers``: damped Cholesky inverses or eigendecompositions."""
+        h = self.hyper
+        if not (k_up and layers):
+            return
+        for ly in layers:
+            if not ly.initialized:
+                raise OrderingError(f"worker {self.rank}, layer {ly.index}: cannot build a preconditioner "
+                                    "before any factor update")
+            ly.alloc_state(h.inv_type, self.device)
+        if h.inv_type == "eigen":
+            jt = []
+            for ly in layers:
+                jt.append((ly.a_cov, ly.a_q, ly.a_w, self.info[ly.index]))
+                jt.append((ly.g_cov, ly.g_q, ly.g_w, self.info[ly.index]))
+            ops.syevd(jt)
+        else:
+            ops.trace_pi([(ly.a_cov, ly.g_cov) for ly in layers], h.gamma,
+                         [self.shifts[ly.slot] for ly in layers], [self.pis[ly.slot] for ly in layers],
+                         [self.info[ly.index] for ly in layers])
+            sj = []
+            for ly in layers:
+                sj.append(ops.spd_job(ly.a_cov, ly.a_inv, self.shifts[ly.slot, 0], self.info[ly.index],
+                                      L.INFO_NOT_SPD_A))
+                sj.append(ops.spd_job(ly.g_cov, ly.g_inv, self.shifts[ly.slot, 1], self.info[ly.index],
+                                      L.INFO_NOT_SPD_G))
+            ops.chol_inv(sj)
+        for ly in layers:
+            ly.holds = h.inv_type
+            ly.last_inverse_update = t
+
+    def _precondition_stage(self, layers):
+        """A10/A11 for ``layers`` on the reduce-scattered mean gradients."""
+        h = self.hyper
+        if not layers:
+            return
+        X = self.xchg
+        pj = []
+        for ly in layers:
+            if ly.holds != h.inv_type:
+                what = "eigendecomposition" if h.inv_type == "eigen" else "damped inverse"
+                raise OrderingError(f"worker {self.rank}, layer {ly.index}: preconditioning requested "
+                                    f"before any {what} exists")
+            shape = (ly.d_out, ly.d_in)
+            g, o, tmp = X.view_in(ly.index, shape), X.view_out(ly.index, shape), X.view_tmp(ly.index, shape)
+            if h.inv_type == "eigen":
+                pj.append(ops.precond_job(g, ly.a_q, ly.g_q, o, tmp, ly.a_w, ly.g_w, self.info[ly.index]))
+            else:
+                pj.append(ops.precond_job(g, ly.a_inv, ly.g_inv, o, tmp))
+        ops.precondition(pj, h.inv_type == "eigen", h.gamma, self.precond_precision)
 
     # ------------------------------------------------------------ stage timing (CUDA events)
     def enable_stage_timing(self, on: bool = True):
@@ -473,10 +539,16 @@ class DPKFAC:
             dist.all_reduce(self.info, op=dist.ReduceOp.MAX, group=self.pg)
         return self.info
 
-    def check(self):
-        """Raise the NumericError of a previous deferred-checked step, if any."""
+    def check(self, block: bool = True):
+        """Raise the NumericError of a previous deferred-checked step, if any.
+
+        ``block=False`` (what step() does) only looks at flags whose device->host
+        copy has already landed, so a deferred check never stalls the host
+        behind the GPU; an explicit ``check()`` waits for them."""
         if self._pending_info is not None:
             host, ev = self._pending_info
+            if not block and not ev.query():
+                return
             self._pending_info = None
             ev.synchronize()
             self._raise_from_host(host)
