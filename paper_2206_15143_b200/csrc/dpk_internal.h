@@ -46,6 +46,10 @@ constexpr int TRI_LOWER = 1;  // op[r][k] == 0 for k > r
 constexpr int TRI_UPPER = 2;  // op[r][k] == 0 for k < r
 
 size_t gemm_workspace_bytes(const GemmSpec* specs, int n);
+// CUDA-core latency path for groups of small problems (gemm_simt.cu)
+bool simt_eligible(const GemmSpec* specs, int n, int precision);
+double simt_fma_limit();
+int simt_gemm_launch(const GemmSpec* specs, int n, cudaStream_t st);
 int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int precision, cudaStream_t st);
 
 inline dpk_operand rows_k(const float* p, int rows, int64_t cols, int64_t ld) {

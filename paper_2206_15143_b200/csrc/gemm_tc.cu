@@ -1535,6 +1535,8 @@ int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int pre
     set_error("dpk_gemm: precision must be DPK_PREC_TF32, DPK_PREC_TF32_TRUNC or DPK_PREC_3XTF32");
     return DPK_EARG;
   }
+  // small 3xTF32 groups (deep SPD-recursion rounds): latency path on CUDA cores
+  if (simt_eligible(specs, n, precision)) return simt_gemm_launch(specs, n, st);
   // big problems run on CTA pairs, the rest on single CTAs (two launches, same
   // stream: the split-K workspace is reused in order).  The plans (tensor maps
   // included) of a job list seen before come from the cache.

@@ -22,79 +22,85 @@ struct I2cBatch {
   dpk_im2col_job j[I2C_MAX];
 };
 
-__device__ __forceinline__ void pixel_of(const dpk_operand& o, int64_t k, int& n, int& oh, int& ow) {
-  const int64_t ohw = static_cast<int64_t>(o.OH) * o.OW;
-  n = static_cast<int>(k / ohw);
-  const int rem = static_cast<int>(k - n * ohw);
-  oh = rem / o.OW;
-  ow = rem - oh * o.OW;
-}
+// One warp per output pixel k (patch row): (n, oh, ow) is decomposed once, then
+// the lanes stream the row's (tap, channel) entries.  32-bit index math only:
+// every per-tensor offset below is < 2^31 elements except the sample offset,
+// which is taken in 64 bits.
+constexpr int I2C_WARPS = 8;
 
 // vectorised: tap-major rows, channels contiguous, C % 4 == 0, 16-byte aligned rows
-__global__ void im2col_vec_kernel(const __grid_constant__ I2cBatch b) {
+__global__ void __launch_bounds__(I2C_WARPS * 32) im2col_vec_kernel(const __grid_constant__ I2cBatch b) {
   const dpk_im2col_job& J = b.j[blockIdx.y];
   const dpk_operand& o = J.x;
   const int c4n = o.C / 4;
   const int taps = o.kh * o.kw;
-  const int64_t per_pixel = static_cast<int64_t>(taps) * c4n;
-  const int64_t total = o.cols * per_pixel;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t k = e / per_pixel;
-    const int rem = static_cast<int>(e - k * per_pixel);
-    const int tap = rem / c4n;
-    const int c4 = rem - tap * c4n;
-    int n, oh, ow;
-    pixel_of(o, k, n, oh, ow);
-    const int i = tap / o.kw, j = tap - (tap / o.kw) * o.kw;
-    const int ih = oh * o.sh - o.ph + i * o.dh;
-    const int iw = ow * o.sw - o.pw + j * o.dw;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (static_cast<unsigned>(ih) < static_cast<unsigned>(o.H) && static_cast<unsigned>(iw) < static_cast<unsigned>(o.W))
-      v = __ldg(reinterpret_cast<const float4*>(o.data + n * o.sn + static_cast<int64_t>(ih) * o.shs +
-                                                static_cast<int64_t>(iw) * o.sws) + c4);
-    *reinterpret_cast<float4*>(J.out + k * J.ld + static_cast<int64_t>(tap) * o.C + 4 * c4) = v;
-    if (o.bias_row && rem == 0) J.out[k * J.ld + o.rows] = 1.0f;
+  const int per_pixel = taps * c4n;
+  const int lane = threadIdx.x & 31;
+  const int ohw = o.OH * o.OW;
+  const int64_t npix = o.cols;
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * I2C_WARPS + (threadIdx.x >> 5); k < npix;
+       k += static_cast<int64_t>(gridDim.x) * I2C_WARPS) {
+    const int n = static_cast<int>(k / ohw);
+    const int rem = static_cast<int>(k - static_cast<int64_t>(n) * ohw);
+    const int oh = rem / o.OW, ow = rem - (rem / o.OW) * o.OW;
+    const int ih0 = oh * o.sh - o.ph, iw0 = ow * o.sw - o.pw;
+    const float* base = o.data + static_cast<int64_t>(n) * o.sn;
+    float4* out = reinterpret_cast<float4*>(J.out + k * J.ld);
+    for (int e = lane; e < per_pixel; e += 32) {
+      const int tap = e / c4n;
+      const int c4 = e - tap * c4n;
+      const int i = tap / o.kw, j = tap - (tap / o.kw) * o.kw;
+      const int ih = ih0 + i * o.dh, iw = iw0 + j * o.dw;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (static_cast<unsigned>(ih) < static_cast<unsigned>(o.H) && static_cast<unsigned>(iw) < static_cast<unsigned>(o.W))
+        v = __ldg(reinterpret_cast<const float4*>(base + static_cast<int64_t>(ih) * o.shs +
+                                                  static_cast<int64_t>(iw) * o.sws) + c4);
+      out[e] = v;  // tap * C + 4 * c4 == 4 * e
+    }
+    if (o.bias_row && lane == 0) J.out[k * J.ld + o.rows] = 1.0f;
   }
 }
 
 // generic: any strides, either row order
-__global__ void im2col_scalar_kernel(const __grid_constant__ I2cBatch b) {
+__global__ void __launch_bounds__(I2C_WARPS * 32) im2col_scalar_kernel(const __grid_constant__ I2cBatch b) {
   const dpk_im2col_job& J = b.j[blockIdx.y];
   const dpk_operand& o = J.x;
   const int d = o.rows + (o.bias_row ? 1 : 0);
-  const int64_t total = o.cols * d;
   const int kk = o.kh * o.kw;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t k = e / d;
-    const int r = static_cast<int>(e - k * d);
-    float v;
-    if (r == o.rows) {
-      v = 1.0f;
-    } else {
-      int c, i, j;
-      if (o.kind == DPK_OPND_IM2COL) {
-        c = r / kk;
-        const int t = r - c * kk;
-        i = t / o.kw;
-        j = t - i * o.kw;
-      } else {
-        const int t = r / o.C;
-        c = r - t * o.C;
-        i = t / o.kw;
-        j = t - i * o.kw;
+  const int lane = threadIdx.x & 31;
+  const int ohw = o.OH * o.OW;
+  for (int64_t k = static_cast<int64_t>(blockIdx.x) * I2C_WARPS + (threadIdx.x >> 5); k < o.cols;
+       k += static_cast<int64_t>(gridDim.x) * I2C_WARPS) {
+    const int n = static_cast<int>(k / ohw);
+    const int rem = static_cast<int>(k - static_cast<int64_t>(n) * ohw);
+    const int oh = rem / o.OW, ow = rem - (rem / o.OW) * o.OW;
+    const int ih0 = oh * o.sh - o.ph, iw0 = ow * o.sw - o.pw;
+    const float* base = o.data + static_cast<int64_t>(n) * o.sn;
+    float* out = J.out + k * J.ld;
+    for (int r = lane; r < d; r += 32) {
+      float v = 1.0f;  // the bias row
+      if (r < o.rows) {
+        int c, i, j;
+        if (o.kind == DPK_OPND_IM2COL) {
+          c = r / kk;
+          const int t = r - c * kk;
+          i = t / o.kw;
+          j = t - i * o.kw;
+        } else {
+          const int t = r / o.C;
+          c = r - t * o.C;
+          i = t / o.kw;
+          j = t - i * o.kw;
+        }
+        const int ih = ih0 + i * o.dh, iw = iw0 + j * o.dw;
+        v = 0.0f;
+        if (static_cast<unsigned>(ih) < static_cast<unsigned>(o.H) &&
+            static_cast<unsigned>(iw) < static_cast<unsigned>(o.W))
+          v = __ldg(base + static_cast<int64_t>(c) * o.sc + static_cast<int64_t>(ih) * o.shs +
+                    static_cast<int64_t>(iw) * o.sws);
       }
-      int n, oh, ow;
-      pixel_of(o, k, n, oh, ow);
-      const int ih = oh * o.sh - o.ph + i * o.dh;
-      const int iw = ow * o.sw - o.pw + j * o.dw;
-      v = 0.0f;
-      if (static_cast<unsigned>(ih) < static_cast<unsigned>(o.H) && static_cast<unsigned>(iw) < static_cast<unsigned>(o.W))
-        v = __ldg(o.data + n * o.sn + static_cast<int64_t>(c) * o.sc + static_cast<int64_t>(ih) * o.shs +
-                  static_cast<int64_t>(iw) * o.sws);
+      out[r] = v;
     }
-    J.out[k * J.ld + r] = v;
   }
 }
 
@@ -120,11 +126,12 @@ extern "C" int dpk_im2col_materialize(const dpk_im2col_job* jobs, int n_jobs, dp
   int64_t vmax = 0, smax = 0;
   auto flush = [&](dpk::I2cBatch& b, int64_t maxe, bool vec) -> int {
     if (b.n == 0) return DPK_OK;
-    const int gx = static_cast<int>(std::min<int64_t>((maxe + 255) / 256, 4096));
+    // maxe = the largest job's pixel count: one warp per pixel, grid-strided
+    const int gx = static_cast<int>(std::min<int64_t>((maxe + dpk::I2C_WARPS - 1) / dpk::I2C_WARPS, 2048));
     if (vec)
-      dpk::im2col_vec_kernel<<<dim3(gx, b.n), 256, 0, st>>>(b);
+      dpk::im2col_vec_kernel<<<dim3(gx, b.n), dpk::I2C_WARPS * 32, 0, st>>>(b);
     else
-      dpk::im2col_scalar_kernel<<<dim3(gx, b.n), 256, 0, st>>>(b);
+      dpk::im2col_scalar_kernel<<<dim3(gx, b.n), dpk::I2C_WARPS * 32, 0, st>>>(b);
     dpk::note_launch();
     b.n = 0;
     return dpk::cuda_status(cudaGetLastError(), "im2col kernel launch");
@@ -144,7 +151,7 @@ extern "C" int dpk_im2col_materialize(const dpk_im2col_job* jobs, int n_jobs, dp
         vmax = 0;
       }
       vb.j[vb.n++] = j;
-      vmax = std::max<int64_t>(vmax, o.cols * o.kh * o.kw * (o.C / 4));
+      vmax = std::max<int64_t>(vmax, o.cols);
     } else {
       if (sb.n == dpk::I2C_MAX) {
         int rc = flush(sb, smax, false);
@@ -152,7 +159,7 @@ extern "C" int dpk_im2col_materialize(const dpk_im2col_job* jobs, int n_jobs, dp
         smax = 0;
       }
       sb.j[sb.n++] = j;
-      smax = std::max<int64_t>(smax, o.cols * (o.rows + (o.bias_row ? 1 : 0)));
+      smax = std::max<int64_t>(smax, o.cols);
     }
   }
   int rc = flush(vb, vmax, true);

@@ -1,0 +1,7 @@
+python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+python scripts/spd_bench.py 2>/dev/null
+SPD_ONLY=4608 python scripts/spd_bench.py 2>/dev/null | head -1
+DPK_SIMT_FMA=0 SPD_ONLY=4608 python scripts/spd_bench.py 2>/dev/null| head -1
+DPK_SIMT_FMA=4e8 SPD_ONLY=4608 python scripts/spd_bench.py 2>/dev/null| head -1
+DPK_SIMT_FMA=4e7 SPD_ONLY=4608 python scripts/spd_bench.py 2>/dev/null| head -1
+python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['ms_per_step_serialized'], d['stages_ms'])"

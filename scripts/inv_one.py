@@ -7,6 +7,7 @@ from paper_2206_15143_b200 import ops
 dev = torch.device("cuda", 0)
 man = json.load(open(os.path.join(ROOT, "tests/golden/resnet50_manifest.json")))
 dims = [d for a, g in man["dims"] for d in (a, g)]
+if os.environ.get("SPD_ONLY"): dims = [d for d in dims if d == int(os.environ["SPD_ONLY"])]
 torch.manual_seed(0)
 jobs, keep = [], []
 for d in dims:
