@@ -192,6 +192,26 @@ size_t dpk_chol_inv_workspace_bytes(const dpk_spd_job* jobs, int n_jobs);
 int dpk_chol_inv_damped_batched(const dpk_spd_job* jobs, int n_jobs, void* workspace, size_t ws_bytes,
                                 dpk_stream_t stream);
 
+/* K3, factored form (same method, one product fewer): dst = X = L^-1 where
+ * L L^T = src + shift I, lower triangular with zeros above the diagonal, row
+ * stride ldd = round_up(n, 4), dst 16-byte aligned.  The damped inverse of
+ * kfac.damped_inverses (kfac.py:140-155) is X^T X; the DP-KFAC optimizer keeps
+ * X and applies it with dpk_precond_factored, so the final X^T X product of
+ * potri (a third of the inversion's flops) is never formed on the hot path. */
+typedef struct dpk_spd_factor_job {
+  const float* src;
+  float* dst;
+  int64_t ldd;
+  int32_t n;
+  int32_t fail_code;
+  const float* shift;
+  int32_t* info;
+} dpk_spd_factor_job;
+
+size_t dpk_chol_factor_inv_workspace_bytes(const dpk_spd_factor_job* jobs, int n_jobs);
+int dpk_chol_factor_inv_batched(const dpk_spd_factor_job* jobs, int n_jobs, void* workspace, size_t ws_bytes,
+                                dpk_stream_t stream);
+
 /* ------------------------------------------------------------------------
  * K5: inverse-mode preconditioning out = G_inv @ grad @ A_inv (kfac.py:251-254).
  * tmp is a d_out x d_in scratch matrix per job.
@@ -212,6 +232,26 @@ typedef struct dpk_precond_job {
 size_t dpk_precond_workspace_bytes(const dpk_precond_job* jobs, int n_jobs);
 int dpk_precond_inverse(const dpk_precond_job* jobs, int n_jobs, void* workspace, size_t ws_bytes,
                         int precision, dpk_stream_t stream);
+/* K5, factored inverses (apply_preconditioner kfac.py:244-254 with
+ * G_inv = X_G^T X_G, A_inv = X_A^T X_A from dpk_chol_factor_inv_batched):
+ *   out = X_G^T (X_G (grad X_A^T) X_A)   -- four triangular-clipped GEMM phases,
+ * the same flops as G_inv @ grad @ A_inv.  tmp: d_out x d_in scratch. */
+typedef struct dpk_precond_factor_job {
+  const float* grad;  /* d_out x d_in */
+  const float* xa;    /* d_in x d_in lower triangular, row stride ldxa */
+  const float* xg;    /* d_out x d_out lower triangular, row stride ldxg */
+  float* out;         /* d_out x d_in */
+  float* tmp;         /* d_out x d_in scratch */
+  int64_t ldxa;
+  int64_t ldxg;
+  int32_t d_out;
+  int32_t d_in;
+} dpk_precond_factor_job;
+
+size_t dpk_precond_factor_workspace_bytes(const dpk_precond_factor_job* jobs, int n_jobs);
+int dpk_precond_factored(const dpk_precond_factor_job* jobs, int n_jobs, void* workspace, size_t ws_bytes,
+                         int precision, dpk_stream_t stream);
+
 /* K6: eigen-mode preconditioning (kfac.py:174-191):
  *   out = Q_G ((Q_G^T grad Q_A) / (max(v_G,0) max(v_A,0)^T + gamma)) Q_A^T */
 int dpk_precond_eigen(const dpk_precond_job* jobs, int n_jobs, float gamma, void* workspace, size_t ws_bytes,

@@ -60,6 +60,17 @@ class SpdJob(C.Structure):
                 ("shift", C.c_void_p), ("info", C.c_void_p)]
 
 
+class SpdFactorJob(C.Structure):
+    _fields_ = [("src", C.c_void_p), ("dst", C.c_void_p), ("ldd", C.c_int64), ("n", C.c_int32),
+                ("fail_code", C.c_int32), ("shift", C.c_void_p), ("info", C.c_void_p)]
+
+
+class PrecondFactorJob(C.Structure):
+    _fields_ = [("grad", C.c_void_p), ("xa", C.c_void_p), ("xg", C.c_void_p), ("out", C.c_void_p),
+                ("tmp", C.c_void_p), ("ldxa", C.c_int64), ("ldxg", C.c_int64),
+                ("d_out", C.c_int32), ("d_in", C.c_int32)]
+
+
 class PrecondJob(C.Structure):
     _fields_ = [("grad", C.c_void_p), ("a_mat", C.c_void_p), ("g_mat", C.c_void_p),
                 ("a_vals", C.c_void_p), ("g_vals", C.c_void_p), ("out", C.c_void_p), ("tmp", C.c_void_p),
@@ -89,6 +100,10 @@ _SIGNATURES = [
     ("dpk_trace_pi", C.c_int, [C.POINTER(PiJob), C.c_int, C.c_float, _P]),
     ("dpk_chol_inv_workspace_bytes", C.c_size_t, [C.POINTER(SpdJob), C.c_int]),
     ("dpk_chol_inv_damped_batched", C.c_int, [C.POINTER(SpdJob), C.c_int, _P, C.c_size_t, _P]),
+    ("dpk_chol_factor_inv_workspace_bytes", C.c_size_t, [C.POINTER(SpdFactorJob), C.c_int]),
+    ("dpk_chol_factor_inv_batched", C.c_int, [C.POINTER(SpdFactorJob), C.c_int, _P, C.c_size_t, _P]),
+    ("dpk_precond_factor_workspace_bytes", C.c_size_t, [C.POINTER(PrecondFactorJob), C.c_int]),
+    ("dpk_precond_factored", C.c_int, [C.POINTER(PrecondFactorJob), C.c_int, _P, C.c_size_t, C.c_int, _P]),
     ("dpk_precond_workspace_bytes", C.c_size_t, [C.POINTER(PrecondJob), C.c_int]),
     ("dpk_precond_inverse", C.c_int, [C.POINTER(PrecondJob), C.c_int, _P, C.c_size_t, C.c_int, _P]),
     ("dpk_precond_eigen", C.c_int, [C.POINTER(PrecondJob), C.c_int, C.c_float, _P, C.c_size_t, C.c_int, _P]),

@@ -1076,6 +1076,15 @@ bool mn3_disabled() {
   return v == 1;
 }
 
+int units_per_cta() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("DPK_UNITS_PER_CTA");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 // tf32_rn: TMA rounds fp32 -> TF32 (nearest) in flight (TFLOAT32 data type);
@@ -1421,7 +1430,13 @@ int launch_batch(const Batch& bt, cudaStream_t st) {
     }
     configured = true;
   }
-  const int grid = CG == 1 ? std::min(bt.total_units, num_sms()) : 2 * std::min(bt.total_units, max_pairs);
+  // persistent CTAs (CTA pairs) walk the units round-robin; DPK_UNITS_PER_CTA
+  // caps how many units one CTA takes, so long launches hand SMs back to the
+  // block scheduler (and to higher-priority streams) between units
+  const int workers = CG == 1 ? num_sms() : max_pairs;
+  const int upc = units_per_cta();
+  const int want = upc > 0 ? std::max(workers, (bt.total_units + upc - 1) / upc) : workers;
+  const int grid = CG == 1 ? std::min(bt.total_units, want) : 2 * std::min(bt.total_units, want);
   const cudaError_t e = launch_k(tc_gemm_kernel<NPASS, RN, CG>, dim3(grid), dim3(NTHREADS), C::SMEM, st, CG, bt);
   note_launch();
   return cuda_status(e, "tc_gemm_kernel launch");

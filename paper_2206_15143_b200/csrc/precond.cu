@@ -65,6 +65,39 @@ void eigen_phases(const dpk_precond_job* J, int n, float gamma, Specs (&p)[4]) {
   }
 }
 
+// out = X_G^T (X_G (grad X_A^T) X_A), phases alternating between tmp and out
+void factored_phases(const dpk_precond_factor_job* J, int n, Specs (&p)[4]) {
+  for (int i = 0; i < n; ++i) {
+    const int o = J[i].d_out, d = J[i].d_in;
+    // P1 = grad X_A^T -> tmp:  B[j][k] = X_A[j][k], zero for k > j
+    GemmSpec s = lin(rows_k(J[i].grad, o, d, d), rows_k(J[i].xa, d, d, J[i].ldxa), J[i].tmp, d);
+    s.tri_b = TRI_LOWER;
+    p[0].push_back(s);
+    // P2 = P1 X_A -> out:  B[j][k] = X_A[k][j], zero for k < j
+    s = lin(rows_k(J[i].tmp, o, d, d), rows_mn(J[i].xa, d, d, J[i].ldxa), J[i].out, d);
+    s.tri_b = TRI_UPPER;
+    p[1].push_back(s);
+    // P3 = X_G P2 -> tmp:  A = X_G (zero for k > i), B[j][k] = P2[k][j]
+    s = lin(rows_k(J[i].xg, o, o, J[i].ldxg), rows_mn(J[i].out, d, o, d), J[i].tmp, d);
+    s.tri_a = TRI_LOWER;
+    p[2].push_back(s);
+    // out = X_G^T P3:  A[i][k] = X_G[k][i] (zero for k < i), B[j][k] = P3[k][j]
+    s = lin(rows_mn(J[i].xg, o, o, J[i].ldxg), rows_mn(J[i].tmp, d, o, d), J[i].out, d);
+    s.tri_a = TRI_UPPER;
+    p[3].push_back(s);
+  }
+}
+
+bool check_factor_jobs(const dpk_precond_factor_job* jobs, int n) {
+  if (n < 0 || (n > 0 && jobs == nullptr)) return false;
+  for (int i = 0; i < n; ++i) {
+    const dpk_precond_factor_job& j = jobs[i];
+    if (j.d_out < 1 || j.d_in < 1 || !j.grad || !j.xa || !j.xg || !j.out || !j.tmp) return false;
+    if (j.ldxa < j.d_in || j.ldxg < j.d_out || j.out == j.grad || j.tmp == j.grad || j.out == j.tmp) return false;
+  }
+  return true;
+}
+
 // min over the clamped outer product + gamma = max(min v_G,0) * max(min v_A,0) + gamma
 // (values are descending, so the minimum is the last entry).
 constexpr int DEN_MAX = 512;
@@ -112,6 +145,32 @@ int dpk_precond_inverse(const dpk_precond_job* jobs, int n_jobs, void* workspace
   int rc = dpk::gemm_launch(p1.data(), n_jobs, workspace, ws_bytes, precision, st);
   if (rc) return rc;
   return dpk::gemm_launch(p2.data(), n_jobs, workspace, ws_bytes, precision, st);
+}
+
+size_t dpk_precond_factor_workspace_bytes(const dpk_precond_factor_job* jobs, int n_jobs) {
+  if (!dpk::check_factor_jobs(jobs, n_jobs) || n_jobs == 0) return 0;
+  dpk::Specs p[4];
+  dpk::factored_phases(jobs, n_jobs, p);
+  size_t w = 0;
+  for (auto& s : p) w = std::max(w, dpk::gemm_workspace_bytes(s.data(), static_cast<int>(s.size())));
+  return w;
+}
+
+int dpk_precond_factored(const dpk_precond_factor_job* jobs, int n_jobs, void* workspace, size_t ws_bytes,
+                         int precision, dpk_stream_t stream) {
+  if (!dpk::check_factor_jobs(jobs, n_jobs)) {
+    dpk::set_error("dpk_precond_factored: invalid job list");
+    return DPK_EARG;
+  }
+  if (n_jobs == 0) return DPK_OK;
+  dpk::Specs p[4];
+  dpk::factored_phases(jobs, n_jobs, p);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (auto& s : p) {
+    int rc = dpk::gemm_launch(s.data(), n_jobs, workspace, ws_bytes, precision, st);
+    if (rc) return rc;
+  }
+  return DPK_OK;
 }
 
 int dpk_precond_eigen(const dpk_precond_job* jobs, int n_jobs, float gamma, void* workspace, size_t ws_bytes,

@@ -46,7 +46,7 @@ struct LeafJob {
   int64_t lds;
   int64_t ldd;
   int32_t n;
-  int32_t full;        // 1: whole matrix -> inverse; 0: diagonal block -> L^-1
+  int32_t full;        // 1: whole matrix -> inverse; 0: diagonal block -> L^-1; 2: whole matrix -> L^-1
   int32_t fail_code;
   int32_t _pad;
   int32_t* info;
@@ -77,17 +77,21 @@ struct LeafBatch {
 // unrolled), so the upper triangle of the input is never read.  Padding
 // rows/columns are the identity, so pivots past n are 1 and the real n x n
 // result is unaffected.
-template <int RB>
+#ifdef DPK_LEAF_PROF
+__device__ unsigned long long g_leaf_prof[12];
+#endif
+template <int RB, int W>
 __global__ void __launch_bounds__(LEAF_THREADS, 1) spd_leaf_kernel(const __grid_constant__ LeafBatch b) {
   constexpr int N = 16 * RB;
   constexpr int CB = RB / 2 > 0 ? RB / 2 : 1;
   constexpr int LDX = N + 1;
+  constexpr int W4 = W / 4;  // float4s per published panel row
   extern __shared__ float smem[];
-  float4* colb = reinterpret_cast<float4*>(smem);  // [N] raw A[i][k..k+3]
-  float4* rowb = colb + N;                         // [N] raw X[k..k+3][j]
-  float4* lpan = rowb + N;                         // [N] L[i][k..k+3] (0 for i <= k+3)
-  float4* xrow = lpan + N;                         // [N] finished X[k..k+3][j] (0 for j > k+3)
-  float* Xs = smem + 16 * N;                       // [N][N+1] X for the FULL-mode X^T X
+  float4* colb = reinterpret_cast<float4*>(smem);  // [N][W/4] raw A[i][k..k+W)
+  float4* rowb = colb + N * W4;                    // [N][W/4] raw X[k..k+W)[j]
+  float4* lpan = rowb + N * W4;                    // [N][W/4] L[i][k..k+W) (0 for i < k+W)
+  float4* xrow = lpan + N * W4;                    // [N][W/4] finished X[k..k+W)[j] (0 for j >= k+W)
+  float* Xs = smem + 4 * N * W;                    // [N][N+1] X for the FULL-mode X^T X
   __shared__ int s_fail;
   if (threadIdx.x == 0) s_fail = 0;
   pdl_wait();
@@ -123,108 +127,150 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) spd_leaf_kernel(const __grid_
   for (int kr = 0; kr < RB; ++kr) {
     const int kc = kr / 2;  // column block holding k (compile-time after unrolling)
 #pragma unroll 1
-    for (int kq = 0; kq < 4; ++kq) {
-      const int k = 16 * kr + 4 * kq;
-      // ---- phase 1: publish raw columns k..k+3 (rows >= 16 kr) and X rows k..k+3
+    for (int kq = 0; kq < 16 / W; ++kq) {
+      const int k = 16 * kr + W * kq;
+#ifdef DPK_LEAF_PROF
+      long long c0 = clock64();
+#endif
+      // ---- phase 1: publish raw columns k..k+W-1 (rows >= 16 kr) and X rows k..k+W-1
       const int tcol = tx - (k & 31), trow = ty - (k & 15);
-      if (tcol >= 0 && tcol < 4) {
+      if (tcol >= 0 && tcol < W) {
         float* cf = reinterpret_cast<float*>(colb);
 #pragma unroll
-        for (int r = kr; r < RB; ++r) cf[(ty + 16 * r) * 4 + tcol] = a[r][kc];
+        for (int r = kr; r < RB; ++r) cf[(ty + 16 * r) * W + tcol] = a[r][kc];
       }
-      if (trow >= 0 && trow < 4) {
+      if (trow >= 0 && trow < W) {
         float* rf = reinterpret_cast<float*>(rowb);
 #pragma unroll
-        for (int c = 0; c <= kc; ++c) rf[(tx + 32 * c) * 4 + trow] = x[kr][c];
+        for (int c = 0; c <= kc; ++c) rf[(tx + 32 * c) * W + trow] = x[kr][c];
       }
+#ifdef DPK_LEAF_PROF
+      long long c1 = clock64();
+#endif
       __syncthreads();
-      // ---- phase 2: pivot block, L panel, finished X rows
+#ifdef DPK_LEAF_PROF
+      long long c2 = clock64();
+#endif
+      // ---- phase 2: pivot block (each worker factors it itself), L panel rows,
+      // finished X rows
       if (tid < 2 * N) {
-        const float4 q0 = colb[k], q1 = colb[k + 1], q2 = colb[k + 2], q3 = colb[k + 3];
-        const float d0 = q0.x;
-        const float i0 = 1.0f / sqrtf(d0);
-        const float l10 = q1.x * i0, l20 = q2.x * i0, l30 = q3.x * i0;
-        const float d1 = q1.y - l10 * l10;
-        const float i1 = 1.0f / sqrtf(d1);
-        const float l21 = (q2.y - l20 * l10) * i1, l31 = (q3.y - l30 * l10) * i1;
-        const float d2 = q2.z - l20 * l20 - l21 * l21;
-        const float i2 = 1.0f / sqrtf(d2);
-        const float l32 = (q3.z - l30 * l20 - l31 * l21) * i2;
-        const float d3 = q3.w - l30 * l30 - l31 * l31 - l32 * l32;
-        const float i3 = 1.0f / sqrtf(d3);
-        const bool ok = (d0 > 0.0f) && (d1 > 0.0f) && (d2 > 0.0f) && (d3 > 0.0f) && isfinite(i0) && isfinite(i1) &&
-                        isfinite(i2) && isfinite(i3);
-        if (!ok && tid == 0) s_fail = 1;  // uniform: every phase-2 thread factored the same block
-        if (tid < N) {
-          const int i = tid;
-          const float4 v = colb[i];
-          float4 l = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (i > k + 3) {
-            l.x = v.x * i0;
-            l.y = (v.y - l.x * l10) * i1;
-            l.z = (v.z - l.x * l20 - l.y * l21) * i2;
-            l.w = (v.w - l.x * l30 - l.y * l31 - l.z * l32) * i3;
+        const float* cf = reinterpret_cast<const float*>(colb);
+        float L[W][W], inv[W];
+        bool ok = true;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+          float d = cf[(k + j) * W + j];
+#pragma unroll
+          for (int t = 0; t < j; ++t) d = fmaf(-L[j][t], L[j][t], d);
+          inv[j] = rsqrtf(d);
+          ok = ok && d > 0.0f && isfinite(inv[j]);
+#pragma unroll
+          for (int m = j + 1; m < W; ++m) {
+            float v = cf[(k + m) * W + j];
+#pragma unroll
+            for (int t = 0; t < j; ++t) v = fmaf(-L[m][t], L[j][t], v);
+            L[m][j] = v * inv[j];
           }
-          lpan[i] = l;
-        } else {
-          const int j = tid - N;
-          const float4 v = rowb[j];
-          float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (j <= k + 3) {
-            o.x = v.x * i0;
-            o.y = (v.y - l10 * o.x) * i1;
-            o.z = (v.z - l20 * o.x - l21 * o.y) * i2;
-            o.w = (v.w - l30 * o.x - l31 * o.y - l32 * o.z) * i3;
-          }
-          xrow[j] = o;
         }
+        if (!ok && tid == 0) s_fail = 1;  // uniform: every phase-2 thread factored the same block
+        const int row = tid < N ? tid : tid - N;
+        float v[W];
+        const float4* srcp = (tid < N ? colb : rowb) + row * W4;
+#pragma unroll
+        for (int q = 0; q < W4; ++q) {
+          const float4 t4 = srcp[q];
+          v[4 * q] = t4.x;
+          v[4 * q + 1] = t4.y;
+          v[4 * q + 2] = t4.z;
+          v[4 * q + 3] = t4.w;
+        }
+        float o[W];
+        // row i of the panel (i >= k+W): forward substitution against L^T;
+        // column j of the X rows (j < k+W): forward substitution against L
+        const bool live = tid < N ? row >= k + W : row < k + W;
+#pragma unroll
+        for (int t = 0; t < W; ++t) {
+          float y = v[t];
+#pragma unroll
+          for (int u = 0; u < t; ++u) y = fmaf(-o[u], L[t][u], y);
+          o[t] = y * inv[t];
+        }
+        float4* dstp = (tid < N ? lpan : xrow) + row * W4;
+#pragma unroll
+        for (int q = 0; q < W4; ++q)
+          dstp[q] = live ? make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3])
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
       }
+#ifdef DPK_LEAF_PROF
+      long long c3 = clock64();
+#endif
       __syncthreads();
+#ifdef DPK_LEAF_PROF
+      long long c4 = clock64();
+#endif
       if (s_fail) {  // a non-positive pivot: exactly where cho_factor raises
         if (tid == 0 && J.info) *J.info = J.fail_code;
         return;
       }
-      // ---- phase 3: rank-4 updates (lower-triangle blocks of A; X columns <= k+3)
-      float4 lr[RB], lc[CB], xn[CB];
-#pragma unroll
-      for (int r = kr; r < RB; ++r) lr[r] = lpan[ty + 16 * r];
-#pragma unroll
-      for (int c = kc; c < CB; ++c) lc[c] = lpan[tx + 32 * c];
-#pragma unroll
-      for (int c = 0; c <= kc; ++c) xn[c] = xrow[tx + 32 * c];
+      // ---- phase 3: rank-W updates (lower-triangle blocks of A; X columns < k+W)
 #pragma unroll
       for (int r = kr; r < RB; ++r) {
+        float lr[W];
+#pragma unroll
+        for (int q = 0; q < W4; ++q) {
+          const float4 t4 = lpan[(ty + 16 * r) * W4 + q];
+          lr[4 * q] = t4.x;
+          lr[4 * q + 1] = t4.y;
+          lr[4 * q + 2] = t4.z;
+          lr[4 * q + 3] = t4.w;
+        }
 #pragma unroll
         for (int c = kc; c < CB; ++c) {
           if (RB > 2 && r <= 2 * c - 1) continue;  // block entirely above the diagonal
           float v = a[r][c];
-          v = fmaf(-lr[r].x, lc[c].x, v);
-          v = fmaf(-lr[r].y, lc[c].y, v);
-          v = fmaf(-lr[r].z, lc[c].z, v);
-          v = fmaf(-lr[r].w, lc[c].w, v);
+#pragma unroll
+          for (int q = 0; q < W4; ++q) {
+            const float4 t4 = lpan[(tx + 32 * c) * W4 + q];
+            v = fmaf(-lr[4 * q], t4.x, v);
+            v = fmaf(-lr[4 * q + 1], t4.y, v);
+            v = fmaf(-lr[4 * q + 2], t4.z, v);
+            v = fmaf(-lr[4 * q + 3], t4.w, v);
+          }
           a[r][c] = v;
         }
 #pragma unroll
         for (int c = 0; c <= kc; ++c) {
           if (RB > 2 && r <= 2 * c - 1) continue;  // X is lower triangular
           float v = x[r][c];
-          v = fmaf(-lr[r].x, xn[c].x, v);
-          v = fmaf(-lr[r].y, xn[c].y, v);
-          v = fmaf(-lr[r].z, xn[c].z, v);
-          v = fmaf(-lr[r].w, xn[c].w, v);
+#pragma unroll
+          for (int q = 0; q < W4; ++q) {
+            const float4 t4 = xrow[(tx + 32 * c) * W4 + q];
+            v = fmaf(-lr[4 * q], t4.x, v);
+            v = fmaf(-lr[4 * q + 1], t4.y, v);
+            v = fmaf(-lr[4 * q + 2], t4.z, v);
+            v = fmaf(-lr[4 * q + 3], t4.w, v);
+          }
           x[r][c] = v;
         }
       }
-      if (trow >= 0 && trow < 4) {
+#ifdef DPK_LEAF_PROF
+      long long c5 = clock64();
+      if (blockIdx.x == 0 && (tid == 0 || tid == 511)) {
+        unsigned long long* g = g_leaf_prof + (tid ? 6 : 0);
+        atomicAdd(g + 0, c1 - c0); atomicAdd(g + 1, c2 - c1); atomicAdd(g + 2, c3 - c2);
+        atomicAdd(g + 3, c4 - c3); atomicAdd(g + 4, c5 - c4); atomicAdd(g + 5, 1ull);
+      }
+#endif
+      if (trow >= 0 && trow < W) {  // rows k..k+W-1 of X are final
+        const float* xf = reinterpret_cast<const float*>(xrow);
 #pragma unroll
-        for (int c = 0; c <= kc; ++c)
-          x[kr][c] = trow == 0 ? xn[c].x : trow == 1 ? xn[c].y : trow == 2 ? xn[c].z : xn[c].w;
+        for (int c = 0; c <= kc; ++c) x[kr][c] = xf[(tx + 32 * c) * W + trow];
       }
     }
   }
   float* dst = J.dst;
   const int64_t ldd = J.ldd;
-  if (!J.full) {  // X = L^-1: exactly zero above the diagonal by construction
+  if (J.full != 1) {  // X = L^-1: exactly zero above the diagonal by construction
 #pragma unroll
     for (int r = 0; r < RB; ++r)
 #pragma unroll
@@ -270,9 +316,17 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) spd_leaf_kernel(const __grid_
     }
 }
 
-template <int RB>
+template <int RB, int W>
 constexpr int leaf_smem_bytes() {
-  return (16 * 16 * RB + 16 * RB * (16 * RB + 1)) * 4;  // 4 float4 panels of N + the X^T X copy
+  return (4 * 16 * RB * W + 16 * RB * (16 * RB + 1)) * 4;  // 4 panels of N x W + the X^T X copy
+}
+int leaf_width() {  // columns per sweep step (DPK_LEAF_W=4 or 8)
+  static int w = -1;
+  if (w < 0) {
+    const char* e = getenv("DPK_LEAF_W");
+    w = (e && e[0] == '4') ? 4 : 8;
+  }
+  return w;
 }
 
 // Blocked-path set-up, one warp per row i:  Aw[i][0..i] = src[i][0..i] (+ shift
@@ -331,10 +385,11 @@ int split_point(int n) {
   return std::min(n1, n - 1);
 }
 
-size_t matrix_ws_floats(int n) {
+size_t matrix_ws_floats(int n, bool factor) {
   if (n <= LEAF_N) return 0;
-  // working copy Aw, L blocks, X = L^-1 (all n x padded_ld; +4 for alignment)
-  return 3 * static_cast<size_t>(n) * padded_ld(n) + 4;
+  // working copy Aw, L blocks, X = L^-1 (all n x padded_ld; +4 for alignment);
+  // factor mode writes X straight into the caller's dst
+  return (factor ? 2 : 3) * static_cast<size_t>(n) * padded_ld(n) + 4;
 }
 
 GemmSpec spec(const dpk_operand& a, const dpk_operand& b, float* out, int64_t ldo, float alpha, float beta,
@@ -399,6 +454,21 @@ void build_ops(float* Aw, float* Lb, float* Xb, int64_t ld, int n, int fail_code
 // the long recursion of the largest factors is not paced by -- and its rounds
 // are not split into several launches by -- the many mid-sized ones.
 constexpr int MAX_GROUPS = 6;
+// One factor of a batched call, either public job kind:
+//   factor == 0: dst (ldd = n) = (src + shift I)^-1          (dpk_chol_inv_damped_batched)
+//   factor == 1: dst (ldd = round_up(n, 4)) = L^-1, L L^T = src + shift I
+//                (dpk_chol_factor_inv_batched: the recursion's X, written in place)
+struct SpdReq {
+  const float* src;
+  float* dst;
+  int64_t ldd;
+  int32_t n;
+  int32_t fail_code;
+  const float* shift;
+  int32_t* info;
+  int32_t factor;
+  int32_t _pad;
+};
 struct SpdPlan {
   std::vector<std::vector<Op>> lists;
   std::vector<PrepJob> preps;
@@ -411,7 +481,7 @@ struct SpdPlan {
 // groups: distinct sizes in descending order, a new group whenever the size
 // drops below 0.6x the group's largest (ResNet-50: 4608 | 2304..2048 |
 // 1152..1000 | 576, 512 | 256 | 147, 128 and below); at most MAX_GROUPS.
-void make_groups(const dpk_spd_job* jobs, int n, SpdPlan& plan) {
+void make_groups(const SpdReq* jobs, int n, SpdPlan& plan) {
   std::vector<int> order(n);
   for (int i = 0; i < n; ++i) order[i] = i;
   std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return jobs[a].n > jobs[b].n; });
@@ -428,7 +498,7 @@ void make_groups(const dpk_spd_job* jobs, int n, SpdPlan& plan) {
   for (auto& g : plan.groups) std::sort(g.begin(), g.end());  // ascending layer order inside a group
 }
 
-void make_spd_plan(const dpk_spd_job* jobs, int n, char* base, SpdPlan& plan) {
+void make_spd_plan(const SpdReq* jobs, int n, char* base, SpdPlan& plan) {
   plan.lists.assign(n, {});
   char* b = base ? base : reinterpret_cast<char*>(0x100000);
   size_t off = 0;
@@ -438,18 +508,22 @@ void make_spd_plan(const dpk_spd_job* jobs, int n, char* base, SpdPlan& plan) {
     if (m <= LEAF_N) {
       Op op{};
       op.leaf = true;
-      op.lj = LeafJob{jobs[i].src, jobs[i].dst, jobs[i].shift, m, m, m, 1, jobs[i].fail_code, 0, jobs[i].info};
+      op.lj = LeafJob{jobs[i].src, jobs[i].dst,     jobs[i].shift, m,
+                      jobs[i].ldd, m,            jobs[i].factor ? 2 : 1, jobs[i].fail_code,
+                      0,           jobs[i].info};
       ops.push_back(op);
       continue;
     }
     const int64_t ldw = padded_ld(m);  // 16-byte rows -> TMA-addressable operands
     const size_t blk = static_cast<size_t>(m) * ldw;
+    const bool factor = jobs[i].factor != 0;
     float* Aw = reinterpret_cast<float*>(b + off);
     float* Lb = Aw + blk;
-    float* Xb = Lb + blk;
-    off += align_up(matrix_ws_floats(m) * sizeof(float), 256);
+    float* Xb = factor ? jobs[i].dst : Lb + blk;
+    off += align_up(matrix_ws_floats(m, factor) * sizeof(float), 256);
     plan.preps.push_back(PrepJob{jobs[i].src, Aw, Xb, jobs[i].shift, m, ldw});
     build_ops(Aw, Lb, Xb, ldw, m, jobs[i].fail_code, jobs[i].info, ops);
+    if (factor) continue;  // X is the result
     Op op{};
     op.leaf = false;
     op.ng = 1;
@@ -485,18 +559,24 @@ void make_spd_plan(const dpk_spd_job* jobs, int n, char* base, SpdPlan& plan) {
   }
 }
 
-template <int NB>
+template <int NB, int W>
 int launch_leaf_nb(const LeafBatch& b, int cnt, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(spd_leaf_kernel<NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         leaf_smem_bytes<NB>());
+    cudaError_t e = cudaFuncSetAttribute(spd_leaf_kernel<NB, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         leaf_smem_bytes<NB, W>());
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(spd_leaf_kernel)");
     configured = true;
   }
-  const cudaError_t e = launch_k(spd_leaf_kernel<NB>, dim3(cnt), dim3(LEAF_THREADS), leaf_smem_bytes<NB>(), st, 1, b);
+  const cudaError_t e = launch_k(spd_leaf_kernel<NB, W>, dim3(cnt), dim3(LEAF_THREADS), leaf_smem_bytes<NB, W>(),
+                                 st, 1, b);
   note_launch();
   return cuda_status(e, "spd_leaf_kernel launch");
+}
+
+template <int NB>
+int launch_leaf_w(const LeafBatch& b, int cnt, cudaStream_t st) {
+  return leaf_width() == 4 ? launch_leaf_nb<NB, 4>(b, cnt, st) : launch_leaf_nb<NB, 8>(b, cnt, st);
 }
 
 int launch_leaves(std::vector<LeafJob>& leaves, cudaStream_t st) {
@@ -511,11 +591,11 @@ int launch_leaves(std::vector<LeafJob>& leaves, cudaStream_t st) {
     }
     int rc;
     if (maxn <= 32)
-      rc = launch_leaf_nb<2>(b, cnt, st);
+      rc = launch_leaf_w<2>(b, cnt, st);
     else if (maxn <= 64)
-      rc = launch_leaf_nb<4>(b, cnt, st);
+      rc = launch_leaf_w<4>(b, cnt, st);
     else
-      rc = launch_leaf_nb<8>(b, cnt, st);
+      rc = launch_leaf_w<8>(b, cnt, st);
     if (rc) return rc;
   }
   return DPK_OK;
@@ -549,7 +629,7 @@ bool spd_graphs_enabled() {
   }
   return on == 1;
 }
-int run_inverse(const dpk_spd_job* jobs, int n_jobs, void* workspace, cudaStream_t st, bool trace);
+int run_inverse(const SpdReq* jobs, int n_jobs, void* workspace, cudaStream_t st, bool trace);
 int run_lockstep(const SpdPlan& plan, const std::vector<int>& grp, char* gemm_ws, size_t gemm_bytes,
                  cudaStream_t st, bool trace);
 
@@ -588,7 +668,81 @@ int ensure_side_streams(int n) {
   }
   return DPK_OK;
 }
-int run_cached_graph(const dpk_spd_job* jobs, int n_jobs, void* workspace, size_t ws_bytes, cudaStream_t st);
+int run_cached_graph(const SpdReq* jobs, int n_jobs, void* workspace, size_t ws_bytes, cudaStream_t st);
+
+}  // namespace
+}  // namespace dpk
+
+
+namespace dpk {
+namespace {
+
+size_t spd_workspace_bytes(const std::vector<SpdReq>& r) {
+  const int n_jobs = static_cast<int>(r.size());
+  if (n_jobs <= 0) return 0;
+  // depends only on the sizes and modes (the plan is built against a dummy base)
+  static LruCache<size_t> cache;
+  std::string key;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  key_put(key, dev);
+  for (const auto& q : r) {
+    key_put(key, q.n);
+    key_put(key, q.factor);
+  }
+  {
+    std::lock_guard<std::mutex> lock(cache.mu);
+    if (size_t* v = cache.find(key)) return *v;
+  }
+  SpdPlan plan;
+  make_spd_plan(r.data(), n_jobs, nullptr, plan);
+  const size_t need = align_up(plan.rec_bytes, 1024) + plan.gemm_bytes;
+  std::lock_guard<std::mutex> lock(cache.mu);
+  cache.put(key, need);
+  return need;
+}
+
+int spd_run(const std::vector<SpdReq>& r, void* workspace, size_t ws_bytes, cudaStream_t st, const char* who) {
+  const int n_jobs = static_cast<int>(r.size());
+  if (n_jobs == 0) return DPK_OK;
+  for (const auto& q : r) {
+    if (q.n < 1 || q.src == nullptr || q.dst == nullptr || q.src == q.dst) {
+      set_error(std::string(who) + ": invalid job (n >= 1, distinct src/dst required)");
+      return DPK_EARG;
+    }
+    if (q.factor && (q.ldd != padded_ld(q.n) || (reinterpret_cast<uintptr_t>(q.dst) & 15) != 0)) {
+      set_error(std::string(who) + ": dst must be 16-byte aligned with row stride round_up(n, 4)");
+      return DPK_EARG;
+    }
+  }
+  const size_t need = spd_workspace_bytes(r);
+  if (need > ws_bytes || (need > 0 && workspace == nullptr)) {
+    set_error(std::string(who) + ": workspace too small");
+    return DPK_ENOSPACE;
+  }
+  const bool trace = spd_trace();
+  if (!trace && spd_graphs_enabled()) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    int rc = cuda_status(cudaStreamIsCapturing(st, &cs), "cudaStreamIsCapturing");
+    if (rc) return rc;
+    // inside a caller's capture the launches simply join that graph
+    if (cs == cudaStreamCaptureStatusNone) return run_cached_graph(r.data(), n_jobs, workspace, ws_bytes, st);
+  }
+  return run_inverse(r.data(), n_jobs, workspace, st, trace);
+}
+
+std::vector<SpdReq> reqs_of(const dpk_spd_job* jobs, int n) {
+  std::vector<SpdReq> r(std::max(n, 0));
+  for (int i = 0; i < n; ++i)
+    r[i] = SpdReq{jobs[i].src, jobs[i].dst, jobs[i].n, jobs[i].n, jobs[i].fail_code, jobs[i].shift, jobs[i].info, 0, 0};
+  return r;
+}
+std::vector<SpdReq> reqs_of(const dpk_spd_factor_job* jobs, int n) {
+  std::vector<SpdReq> r(std::max(n, 0));
+  for (int i = 0; i < n; ++i)
+    r[i] = SpdReq{jobs[i].src, jobs[i].dst, jobs[i].ldd, jobs[i].n, jobs[i].fail_code, jobs[i].shift, jobs[i].info, 1, 0};
+  return r;
+}
 
 }  // namespace
 }  // namespace dpk
@@ -597,61 +751,47 @@ extern "C" {
 
 size_t dpk_chol_inv_workspace_bytes(const dpk_spd_job* jobs, int n_jobs) {
   if (n_jobs <= 0 || jobs == nullptr) return 0;
-  // depends only on the sizes (the plan is built against a dummy base) -> cache by sizes
-  static dpk::LruCache<size_t> cache;
-  std::string key;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  dpk::key_put(key, dev);
-  for (int i = 0; i < n_jobs; ++i) dpk::key_put(key, jobs[i].n);
-  {
-    std::lock_guard<std::mutex> lock(cache.mu);
-    if (size_t* v = cache.find(key)) return *v;
-  }
-  dpk::SpdPlan plan;
-  dpk::make_spd_plan(jobs, n_jobs, nullptr, plan);
-  const size_t need = dpk::align_up(plan.rec_bytes, 1024) + plan.gemm_bytes;
-  std::lock_guard<std::mutex> lock(cache.mu);
-  cache.put(key, need);
-  return need;
+  return dpk::spd_workspace_bytes(dpk::reqs_of(jobs, n_jobs));
 }
 
 int dpk_chol_inv_damped_batched(const dpk_spd_job* jobs, int n_jobs, void* workspace, size_t ws_bytes,
                                 dpk_stream_t stream) {
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (n_jobs == 0) return DPK_OK;
   if (n_jobs < 0 || jobs == nullptr) {
     dpk::set_error("dpk_chol_inv_damped_batched: bad job list");
     return DPK_EARG;
   }
-  for (int i = 0; i < n_jobs; ++i) {
-    if (jobs[i].n < 1 || jobs[i].src == nullptr || jobs[i].dst == nullptr || jobs[i].src == jobs[i].dst) {
-      dpk::set_error("dpk_chol_inv_damped_batched: invalid job (n >= 1, distinct src/dst required)");
-      return DPK_EARG;
-    }
-  }
-  const size_t need = dpk_chol_inv_workspace_bytes(jobs, n_jobs);
-  if (need > ws_bytes || (need > 0 && workspace == nullptr)) {
-    dpk::set_error("dpk_chol_inv_damped_batched: workspace too small");
-    return DPK_ENOSPACE;
-  }
-  const bool trace = dpk::spd_trace();
-  if (!trace && dpk::spd_graphs_enabled()) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    int rc = dpk::cuda_status(cudaStreamIsCapturing(st, &cs), "cudaStreamIsCapturing");
-    if (rc) return rc;
-    // inside a caller's capture the launches simply join that graph
-    if (cs == cudaStreamCaptureStatusNone) return dpk::run_cached_graph(jobs, n_jobs, workspace, ws_bytes, st);
-  }
-  return dpk::run_inverse(jobs, n_jobs, workspace, st, trace);
+  return dpk::spd_run(dpk::reqs_of(jobs, n_jobs), workspace, ws_bytes, static_cast<cudaStream_t>(stream),
+                      "dpk_chol_inv_damped_batched");
 }
 
+size_t dpk_chol_factor_inv_workspace_bytes(const dpk_spd_factor_job* jobs, int n_jobs) {
+  if (n_jobs <= 0 || jobs == nullptr) return 0;
+  return dpk::spd_workspace_bytes(dpk::reqs_of(jobs, n_jobs));
+}
+
+int dpk_chol_factor_inv_batched(const dpk_spd_factor_job* jobs, int n_jobs, void* workspace, size_t ws_bytes,
+                                dpk_stream_t stream) {
+  if (n_jobs == 0) return DPK_OK;
+  if (n_jobs < 0 || jobs == nullptr) {
+    dpk::set_error("dpk_chol_factor_inv_batched: bad job list");
+    return DPK_EARG;
+  }
+  return dpk::spd_run(dpk::reqs_of(jobs, n_jobs), workspace, ws_bytes, static_cast<cudaStream_t>(stream),
+                      "dpk_chol_factor_inv_batched");
+}
+
+#ifdef DPK_LEAF_PROF
+int dpk_leaf_prof(unsigned long long* out12) {
+  return dpk::cuda_status(cudaMemcpyFromSymbol(out12, dpk::g_leaf_prof, 12 * 8), "leaf prof");
+}
+#endif
 }  // extern "C"
 
 namespace dpk {
 namespace {
 
-int run_inverse(const dpk_spd_job* jobs, int n_jobs, void* workspace, cudaStream_t st, bool trace) {
+int run_inverse(const SpdReq* jobs, int n_jobs, void* workspace, cudaStream_t st, bool trace) {
   dpk::SpdPlan plan;
   char* base = static_cast<char*>(workspace);
   dpk::make_spd_plan(jobs, n_jobs, base, plan);
@@ -800,7 +940,7 @@ struct GraphEntry {
   unsigned long long last_use;
 };
 
-int run_cached_graph(const dpk_spd_job* jobs, int n_jobs, void* workspace, size_t ws_bytes, cudaStream_t st) {
+int run_cached_graph(const SpdReq* jobs, int n_jobs, void* workspace, size_t ws_bytes, cudaStream_t st) {
   static std::mutex mu;
   static std::vector<GraphEntry> cache;
   static unsigned long long tick = 0;
@@ -809,10 +949,10 @@ int run_cached_graph(const dpk_spd_job* jobs, int n_jobs, void* workspace, size_
   int dev = 0;
   int rc = cuda_status(cudaGetDevice(&dev), "cudaGetDevice");
   if (rc) return rc;
-  std::vector<char> key(sizeof(dpk_spd_job) * n_jobs + sizeof(void*) + sizeof(size_t) + sizeof(int));
+  std::vector<char> key(sizeof(SpdReq) * n_jobs + sizeof(void*) + sizeof(size_t) + sizeof(int));
   char* k = key.data();
-  std::memcpy(k, jobs, sizeof(dpk_spd_job) * n_jobs);
-  k += sizeof(dpk_spd_job) * n_jobs;
+  std::memcpy(k, jobs, sizeof(SpdReq) * n_jobs);
+  k += sizeof(SpdReq) * n_jobs;
   std::memcpy(k, &workspace, sizeof(void*));
   k += sizeof(void*);
   std::memcpy(k, &ws_bytes, sizeof(size_t));

@@ -65,7 +65,9 @@ class _Layer:
         self.m_cols = 0
         # state (allocated on first use, owner only)
         self.a_cov = self.g_cov = None
-        self.a_inv = self.g_inv = None
+        # inverse mode holds the damped inverses in factored form, A_inv = X_A^T X_A
+        # with X_A = L_A^-1 lower triangular (rows padded to a multiple of 4)
+        self.a_x = self.g_x = None
         self.a_q = self.a_w = self.g_q = self.g_w = None
         self.initialized = False
         self.last_factor_update = -1
@@ -138,14 +140,29 @@ class _Layer:
         if self.a_cov is None:
             self.a_cov = torch.zeros(self.d_in, self.d_in, device=device)
             self.g_cov = torch.zeros(self.d_out, self.d_out, device=device)
-        if inv_type == "inverse" and self.a_inv is None:
-            self.a_inv = torch.empty_like(self.a_cov)
-            self.g_inv = torch.empty_like(self.g_cov)
+        if inv_type == "inverse" and self.a_x is None:
+            self.a_x = torch.zeros(self.d_in, ops.factor_ld(self.d_in), device=device)[:, :self.d_in]
+            self.g_x = torch.zeros(self.d_out, ops.factor_ld(self.d_out), device=device)[:, :self.d_out]
         if inv_type == "eigen" and self.a_q is None:
             self.a_q = torch.empty_like(self.a_cov)
             self.g_q = torch.empty_like(self.g_cov)
             self.a_w = torch.empty(self.d_in, device=device)
             self.g_w = torch.empty(self.d_out, device=device)
+
+
+def _gram(x: torch.Tensor) -> torch.Tensor:
+    """X^T X in float64 (export only): the damped inverse held as its factor X."""
+    xd = x.double()
+    return (xd.T @ xd).float()
+
+
+def _factor_of_inverse(inv: torch.Tensor) -> torch.Tensor:
+    """X with X^T X = inv, X lower triangular (import of a checkpoint that only
+    carries the explicit inverse): inv^-1 = L L^T, X = L^-1."""
+    a = torch.linalg.inv(inv.double())
+    lo = torch.linalg.cholesky(0.5 * (a + a.T))
+    eye = torch.eye(lo.shape[0], dtype=lo.dtype, device=lo.device)
+    return torch.linalg.solve_triangular(lo, eye, upper=False).float()
 
 
 def _supported(m: nn.Module) -> bool:
@@ -466,11 +483,11 @@ class DPKFAC:
                          [self.info[ly.index] for ly in layers])
             sj = []
             for ly in layers:
-                sj.append(ops.spd_job(ly.a_cov, ly.a_inv, self.shifts[ly.slot, 0], self.info[ly.index],
-                                      L.INFO_NOT_SPD_A))
-                sj.append(ops.spd_job(ly.g_cov, ly.g_inv, self.shifts[ly.slot, 1], self.info[ly.index],
-                                      L.INFO_NOT_SPD_G))
-            ops.chol_inv(sj)
+                sj.append(ops.spd_factor_job(ly.a_cov, ly.a_x, self.shifts[ly.slot, 0], self.info[ly.index],
+                                             L.INFO_NOT_SPD_A))
+                sj.append(ops.spd_factor_job(ly.g_cov, ly.g_x, self.shifts[ly.slot, 1], self.info[ly.index],
+                                             L.INFO_NOT_SPD_G))
+            ops.chol_factor_inv(sj)
         for ly in layers:
             ly.holds = h.inv_type
             ly.last_inverse_update = t
@@ -492,8 +509,11 @@ class DPKFAC:
             if h.inv_type == "eigen":
                 pj.append(ops.precond_job(g, ly.a_q, ly.g_q, o, tmp, ly.a_w, ly.g_w, self.info[ly.index]))
             else:
-                pj.append(ops.precond_job(g, ly.a_inv, ly.g_inv, o, tmp))
-        ops.precondition(pj, h.inv_type == "eigen", h.gamma, self.precond_precision)
+                pj.append(ops.precond_factor_job(g, ly.a_x, ly.g_x, o, tmp))
+        if h.inv_type == "eigen":
+            ops.precondition(pj, True, h.gamma, self.precond_precision)
+        else:
+            ops.precondition_factored(pj, self.precond_precision)
 
     # ------------------------------------------------------------ stage timing (CUDA events)
     def enable_stage_timing(self, on: bool = True):
@@ -592,7 +612,9 @@ class DPKFAC:
                 d["a_eig_q"], d["a_eig_v"] = rows(ly.a_q), ly.a_w.clone()
                 d["g_eig_q"], d["g_eig_v"] = ly.g_q.clone(), ly.g_w.clone()
             elif ly.holds == "inverse":
-                d["a_damped_inv"], d["g_damped_inv"] = sym(ly.a_inv), ly.g_inv.clone()
+                # the reference's explicit damped inverses, formed from the held factors
+                d["a_damped_inv"], d["g_damped_inv"] = sym(_gram(ly.a_x)), _gram(ly.g_x)
+                d["a_inv_factor"], d["g_inv_factor"] = ly.a_x.clone(), ly.g_x.clone()
             layers[ly.index] = d
         return {"t": self.t, "rank": self.rank, "assignment": self.assignment, "layers": layers,
                 "hyper": dict(self.hyper.__dict__)}
@@ -625,8 +647,12 @@ class DPKFAC:
                 ly.holds = "eigen"
             if "a_damped_inv" in d:
                 ly.alloc_state("inverse", self.device)
-                ly.a_inv.copy_(sym(d["a_damped_inv"]))
-                ly.g_inv.copy_(d["g_damped_inv"])
+                if "a_inv_factor" in d:  # held order already
+                    ly.a_x.copy_(d["a_inv_factor"])
+                    ly.g_x.copy_(d["g_inv_factor"])
+                else:
+                    ly.a_x.copy_(_factor_of_inverse(sym(d["a_damped_inv"]).to(self.device)))
+                    ly.g_x.copy_(_factor_of_inverse(d["g_damped_inv"].to(self.device)))
                 ly.holds = "inverse"
 
     # ------------------------------------------------------------ introspection

@@ -205,6 +205,58 @@ def chol_inv(jobs: Sequence[L.SpdJob]):
     L.check(lb.dpk_chol_inv_damped_batched(arr, len(jobs), ws, need, stream_handle()), "dpk_chol_inv_damped_batched")
 
 
+def factor_ld(n: int) -> int:
+    """Row stride of a factored inverse X = L^-1 (16-byte aligned rows)."""
+    return (n + 3) // 4 * 4
+
+
+def spd_factor_job(src: torch.Tensor, dst: torch.Tensor, shift: Optional[torch.Tensor],
+                   info: Optional[torch.Tensor], fail_code: int) -> L.SpdFactorJob:
+    n = src.shape[0]
+    if dst.dim() != 2 or dst.shape[0] != n or dst.stride(0) != factor_ld(n) or dst.stride(1) != 1:
+        raise ShapeError("factored inverse needs an n x round_up(n, 4) row-major buffer")
+    j = L.SpdFactorJob()
+    j.src, j.dst = src.data_ptr(), dst.data_ptr()
+    j.ldd = dst.stride(0)
+    j.n = n
+    j.fail_code = fail_code
+    j.shift = shift.data_ptr() if shift is not None else None
+    j.info = info.data_ptr() if info is not None else None
+    return j
+
+
+def chol_factor_inv(jobs: Sequence[L.SpdFactorJob]):
+    """dst = X = L^-1 with L L^T = src + shift I (the damped inverse is X^T X)."""
+    if not jobs:
+        return
+    lb = lib()
+    arr = L.array(L.SpdFactorJob, jobs)
+    need = lb.dpk_chol_factor_inv_workspace_bytes(arr, len(jobs))
+    ws = Workspace.get(need, torch.device("cuda", torch.cuda.current_device()), key="spd")
+    L.check(lb.dpk_chol_factor_inv_batched(arr, len(jobs), ws, need, stream_handle()), "dpk_chol_factor_inv_batched")
+
+
+def precond_factor_job(grad, xa, xg, out, tmp) -> L.PrecondFactorJob:
+    j = L.PrecondFactorJob()
+    j.grad, j.xa, j.xg = grad.data_ptr(), xa.data_ptr(), xg.data_ptr()
+    j.out, j.tmp = out.data_ptr(), tmp.data_ptr()
+    j.ldxa, j.ldxg = xa.stride(0), xg.stride(0)
+    j.d_out, j.d_in = xg.shape[0], xa.shape[0]
+    return j
+
+
+def precondition_factored(jobs: Sequence[L.PrecondFactorJob], precision: str = "3xtf32"):
+    """out = X_G^T X_G grad X_A^T X_A  (= G_inv grad A_inv) for every job."""
+    if not jobs:
+        return
+    lb = lib()
+    arr = L.array(L.PrecondFactorJob, jobs)
+    need = lb.dpk_precond_factor_workspace_bytes(arr, len(jobs))
+    ws = Workspace.get(need, torch.device("cuda", torch.cuda.current_device()), key="pre")
+    L.check(lb.dpk_precond_factored(arr, len(jobs), ws, need, precision_code(precision), stream_handle()),
+            "dpk_precond_factored")
+
+
 # ------------------------------------------------------------------ K4
 def eig_job(src, q, w, info) -> L.EigJob:
     j = L.EigJob()

@@ -195,6 +195,58 @@ def test_spd_inverse_rank_deficient_factor_plus_damping(d, m, shift):
     assert rel(N(got), want) <= max(1e-4, 20 * cond * 2.0 ** -23), (rel(N(got), want), cond)
 
 
+@pytest.mark.parametrize("n,shift", [(1, 0.5), (37, 0.0), (128, 0.01), (129, 0.02), (513, 0.01), (2049, 0.045),
+                                     (4608, 0.045)])
+def test_factored_spd_inverse_matches_oracle(n, shift):
+    """dpk_chol_factor_inv_batched: X = L^-1 of (A + shift I), lower triangular; X^T X
+    is the reference's damped inverse (numerics.sym_inverse of the damped factor)."""
+    from paper_2206_15143_b200 import _lib as L, ops
+    rng = np.random.default_rng(n + 7)
+    m = max(n // 3, 4)
+    x = np.maximum(rng.standard_normal((n, m)), 0)
+    a = x @ x.T / m + (0.05 if shift == 0.0 else 0.0) * np.eye(n)
+    src = T(a)
+    dst = torch.full((n, ops.factor_ld(n)), float("nan"), device=dev())[:, :n]
+    sh = torch.tensor([shift], device=dev())
+    info = torch.zeros(1, dtype=torch.int32, device=dev())
+    ops.chol_factor_inv([ops.spd_factor_job(src, dst, sh, info, L.INFO_NOT_SPD_A)])
+    torch.cuda.synchronize()
+    assert int(info.item()) == 0
+    X = N(dst)
+    assert np.all(X[np.triu_indices(n, 1)] == 0.0)  # exactly lower triangular
+    want = K.spd_inverse(a + shift * np.eye(n))
+    cond = np.linalg.cond(a + shift * np.eye(n))
+    assert rel(X.T @ X, want) <= max(1e-4, 20 * cond * 2.0 ** -23), (rel(X.T @ X, want), cond)
+
+
+@pytest.mark.parametrize("din,dout,gamma", [(785, 512, 0.03), (65, 9, 0.002), (2049, 1000, 0.002), (3, 2, 0.03),
+                                            (4608, 512, 0.002)])
+def test_precondition_factored_matches_oracle(din, dout, gamma):
+    """dpk_precond_factored with the factors of dpk_chol_factor_inv_batched equals the
+    reference's G_inv @ grad @ A_inv (kfac.precondition_inverse, kfac.py:165-171)."""
+    from paper_2206_15143_b200 import _lib as L, ops
+    rng = np.random.default_rng(din * 3 + dout)
+    x = np.maximum(rng.standard_normal((din, 256)), 0)
+    g = rng.standard_normal((dout, 256)) * 0.1
+    grad = rng.standard_normal((dout, din)) * 0.01
+    a, gg = K.compute_factors(x, g)
+    pi = K.pi_scalar(a, gg)
+    sa, sg = pi * np.sqrt(gamma), np.sqrt(gamma) / pi
+    xa = torch.zeros(din, ops.factor_ld(din), device=dev())[:, :din]
+    xg = torch.zeros(dout, ops.factor_ld(dout), device=dev())[:, :dout]
+    shifts = torch.tensor([sa, sg], device=dev(), dtype=torch.float32)
+    info = torch.zeros(1, dtype=torch.int32, device=dev())
+    ta, tg = T(a), T(gg)  # keep the sources alive: the jobs hold raw pointers
+    ops.chol_factor_inv([ops.spd_factor_job(ta, xa, shifts[0], info, L.INFO_NOT_SPD_A),
+                         ops.spd_factor_job(tg, xg, shifts[1], info, L.INFO_NOT_SPD_G)])
+    gr, out, tmp = T(grad), torch.empty(dout, din, device=dev()), torch.empty(dout, din, device=dev())
+    ops.precondition_factored([ops.precond_factor_job(gr, xa, xg, out, tmp)], "3xtf32")
+    torch.cuda.synchronize()
+    assert int(info.item()) == 0
+    want = K.precondition_inverse(a, gg, grad, gamma)
+    assert rel(N(out), want) <= TOL, rel(N(out), want)
+
+
 def test_damped_inverses_and_pi_match_oracle():
     from paper_2206_15143_b200 import kfac as FK
     rng = np.random.default_rng(3)
