@@ -94,6 +94,8 @@ struct alignas(64) Problem {
   int tma_a, tma_b;
   int slab_cpn;     // TMA_SLAB: chunks per sample (K index = (sample, 32-pixel chunk))
   int tri_a, tri_b; // TRI_*: per-tile K clipping for triangular operands
+  int order;        // tile visiting order (non-symmetric): 0 row-major, 1 row-major reversed,
+                    // 2 column-major, 3 column-major reversed -- heaviest K ranges first
 };
 
 struct Batch {
@@ -135,7 +137,17 @@ __device__ __forceinline__ void decode_unit(const Batch& bt, int u, int& pi, int
   // split-major: CTAs of one wave take different tiles of the same K range, so
   // each K slab of the operands is fetched from DRAM once and shared through L2
   split = local / P.ntiles;
-  tile = local - split * P.ntiles;
+  const int v = local - split * P.ntiles;  // visiting position -> canonical (row-major) tile index
+  if (P.order == 0 || P.symmetric) {
+    tile = v;
+  } else if (P.order == 1) {
+    tile = P.ntiles - 1 - v;
+  } else {
+    const int tiles_m = P.ntiles / P.tiles_n;
+    const int w = P.order == 3 ? P.ntiles - 1 - v : v;
+    const int cn = w / tiles_m;
+    tile = (w - cn * tiles_m) * P.tiles_n + cn;
+  }
   if (P.symmetric) {
     int r = static_cast<int>((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
     while ((r + 1) * (r + 2) / 2 <= tile) ++r;
@@ -1253,6 +1265,9 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
     P.ldt = specs[i].ldt;
     P.tri_a = specs[i].tri_a;
     P.tri_b = specs[i].tri_b;
+    // K clipping makes tile cost grow along one tile index: visit the heavy
+    // tiles first so the static round-robin schedule ends on light ones
+    P.order = P.tri_a == TRI_LOWER ? 1 : P.tri_b == TRI_LOWER ? 3 : P.tri_b == TRI_UPPER ? 2 : 0;
     if (P.beta != 0.0f && P.cin == nullptr) {
       set_error("dpk_gemm: beta != 0 needs cin");
       return DPK_EARG;

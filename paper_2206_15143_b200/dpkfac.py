@@ -257,10 +257,10 @@ class DPKFAC:
             self._hooks.append(ly.module.register_forward_hook(self._make_fwd_hook(ly)))
         self._bufs_ready = False
         self.last_stage_ms = {}
-        # overlap=True: the owned layers of the largest size class (whose inversion
+        # overlap=True: the owned layers of the larger size classes (whose inversion
         # is a long, latency-bound chain of small launches) run their whole
-        # factor -> inverse -> precondition pipeline on a high-priority side
-        # stream while the other layers' throughput-bound work fills the GPU
+        # factor -> inverse -> precondition pipeline on higher-priority side
+        # streams while the other layers' throughput-bound work fills the GPU
         self.overlap = bool(overlap)
         self._side = None
 
@@ -356,21 +356,20 @@ class DPKFAC:
         k_up = t % h.k_freq == 0
         owned = self.owned
         self.info.zero_()
-        crit, rest = self._split_critical(owned)
+        classes = self._size_classes(owned)
+        sides, rest = classes[:-1], classes[-1]
         main = torch.cuda.current_stream(self.device)
         self._mark("start")
-        if crit:
-            side = self._side_stream()
-            side.wait_stream(main)
-            with torch.cuda.stream(side):
-                self._factor_stage(crit, t, f_up, side)
-                self._inverse_stage(crit, t, k_up)
-        # (1) Kronecker factors + running average: one grouped tcgen05 launch
-        self._factor_stage(rest, t, f_up, None)
-        self._mark("factors")
-        # (2) inverses / eigendecompositions
-        self._inverse_stage(rest, t, k_up)
-        self._mark("inversion")
+        # the larger size classes (long, latency-bound inversion chains) run their
+        # factor -> inverse pipeline on higher-priority side streams from the
+        # start of the step; the last class runs on the caller's stream
+        streams = self._side_streams(len(sides))
+        ev0 = main.record_event()
+        for cls, st in zip(sides, streams):
+            st.wait_event(ev0)
+            with torch.cuda.stream(st):
+                self._factor_stage(cls, t, f_up, st)
+                self._inverse_stage(cls, t, k_up)
         # (3) pack every layer's [W | b] gradient, owner-major (scaled by 1/P)
         segs = self._segments("grad")
         P = self.world
@@ -381,14 +380,21 @@ class DPKFAC:
         if P > 1 and self.other_params:
             self._allreduce_others()
         self._mark("comm_rs")
+        ev_rs = main.record_event()
+        for cls, st in zip(sides, streams):
+            st.wait_event(ev_rs)
+            with torch.cuda.stream(st):
+                self._precondition_stage(cls)
+        # (1) Kronecker factors + running average: one grouped tcgen05 launch
+        self._factor_stage(rest, t, f_up, None)
+        self._mark("factors")
+        # (2) inverses / eigendecompositions
+        self._inverse_stage(rest, t, k_up)
+        self._mark("inversion")
         # (5) precondition owned layers, one grouped launch per GEMM phase
-        if crit:
-            side.wait_stream(main)
-            with torch.cuda.stream(side):
-                self._precondition_stage(crit)
         self._precondition_stage(rest)
-        if crit:
-            main.wait_stream(side)
+        for st in streams:
+            main.wait_stream(st)
         self._mark("precondition")
         # numeric failures: reference wording, prefixed "worker p, layer i" (distsim.py:273-274)
         if self.check_numerics == "sync":
@@ -408,22 +414,29 @@ class DPKFAC:
         self.t += 1
 
     # ------------------------------------------------------------ stages
-    def _side_stream(self):
+    def _side_streams(self, n):
         if self._side is None:
-            self._side = torch.cuda.Stream(self.device, priority=-1)
-        return self._side
+            self._side = []
+        while len(self._side) < n:  # class 0 (largest factors) gets the highest priority
+            self._side.append(torch.cuda.Stream(self.device, priority=-1 - (len(self._side) == 0)))
+        return self._side[:n]
 
-    def _split_critical(self, owned):
-        """(critical, rest): the owned layers of the largest size class run on the
-        side stream when overlapping (a strict, non-empty subset only)."""
+    def _size_classes(self, owned):
+        """Owned layers grouped by factor size (max(d_in, d_out)), largest class
+        first: a new class whenever the size drops below 0.6x the class's largest,
+        at most three.  Without overlap (or with a single class) everything is one
+        class on the caller's stream."""
         if not self.overlap or len(owned) < 2:
-            return [], owned
-        size = [max(ly.d_in, ly.d_out) for ly in owned]
-        big = max(size)
-        crit = [ly for ly, d in zip(owned, size) if 10 * d >= 6 * big]
-        if len(crit) == len(owned):
-            return [], owned
-        return crit, [ly for ly, d in zip(owned, size) if 10 * d < 6 * big]
+            return [owned]
+        order = sorted(owned, key=lambda ly: -max(ly.d_in, ly.d_out))
+        classes, top = [], None
+        for ly in order:
+            d = max(ly.d_in, ly.d_out)
+            if top is None or (10 * d < 6 * top and len(classes) < 3):
+                classes.append([])
+                top = d
+            classes[-1].append(ly)
+        return [sorted(c, key=lambda ly: ly.index) for c in classes]
 
     def _factor_stage(self, layers, t, f_up, stream):
         """A3 + A4 for ``layers`` on the current stream (captures were produced on

@@ -19,13 +19,13 @@ def mark(name):
 orig_f, orig_i, orig_p = kf._factor_stage, kf._inverse_stage, kf._precondition_stage
 def wrap(fn, tag):
     def g(layers, *a):
-        who = "crit" if layers and layers[0] in crit else "rest"
+        who = f"class{next((i for i, c in enumerate(classes) if layers and layers[0] in c), -1)}"
         mark(f"{who}:{tag}:begin"); r = fn(layers, *a); mark(f"{who}:{tag}:end"); return r
     return g
 kf._factor_stage = wrap(orig_f, "factors"); kf._inverse_stage = wrap(orig_i, "inverse"); kf._precondition_stage = wrap(orig_p, "precond")
 for it in range(4):
     F.cross_entropy(model(x), y).backward()
-    crit, rest = kf._split_critical(kf.owned) if hasattr(kf, "owned") else ([], [])
+    classes = kf._size_classes(kf.owned) if hasattr(kf, "owned") else [[]]
     torch.cuda.synchronize()
     ev.clear()
     mark("start")
@@ -35,4 +35,4 @@ for it in range(4):
 t0 = ev[0][1]
 for name, e in ev:
     print(f"{t0.elapsed_time(e):8.3f} ms  {name}")
-print("crit layers:", [ly.index for ly in crit])
+print("classes:", [[ly.index for ly in c] for c in classes])
