@@ -1088,6 +1088,15 @@ bool mn3_disabled() {
   return v == 1;
 }
 
+int grid_cap() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("DPK_GRID_CAP");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
 int units_per_cta() {
   static int v = -2;
   if (v == -2) {
@@ -1448,7 +1457,9 @@ int launch_batch(const Batch& bt, cudaStream_t st) {
   // persistent CTAs (CTA pairs) walk the units round-robin; DPK_UNITS_PER_CTA
   // caps how many units one CTA takes, so long launches hand SMs back to the
   // block scheduler (and to higher-priority streams) between units
-  const int workers = CG == 1 ? num_sms() : max_pairs;
+  const int cap = grid_cap();  // experiment: leave SMs to concurrent streams
+  const int workers = cap > 0 ? std::max(1, std::min(CG == 1 ? num_sms() : max_pairs, cap / CG))
+                              : (CG == 1 ? num_sms() : max_pairs);
   const int upc = units_per_cta();
   const int want = upc > 0 ? std::max(workers, (bt.total_units + upc - 1) / upc) : workers;
   const int grid = CG == 1 ? std::min(bt.total_units, want) : 2 * std::min(bt.total_units, want);

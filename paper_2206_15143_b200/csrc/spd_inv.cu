@@ -212,45 +212,60 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) spd_leaf_kernel(const __grid_
         if (tid == 0 && J.info) *J.info = J.fail_code;
         return;
       }
-      // ---- phase 3: rank-W updates (lower-triangle blocks of A; X columns < k+W)
+      // ---- phase 3: rank-W updates (lower-triangle blocks of A; X columns < k+W).
+      // Column-outer: each thread's column vectors (lane-distinct, 4 smem wavefronts
+      // per float4) are loaded once per step; the row vectors are warp-uniform
+      // broadcasts (1 wavefront) and are re-read per column block.
 #pragma unroll
-      for (int r = kr; r < RB; ++r) {
-        float lr[W];
+      for (int c = 0; c < CB; ++c) {
+        const bool acol = c >= kc;   // A columns >= k (compile-time per kr, c)
+        const bool xcol = c <= kc;   // X columns <= k+W-1
+        float cv[W];
 #pragma unroll
         for (int q = 0; q < W4; ++q) {
-          const float4 t4 = lpan[(ty + 16 * r) * W4 + q];
-          lr[4 * q] = t4.x;
-          lr[4 * q + 1] = t4.y;
-          lr[4 * q + 2] = t4.z;
-          lr[4 * q + 3] = t4.w;
+          const float4 t4 = acol && !xcol ? lpan[(tx + 32 * c) * W4 + q] : xcol && !acol ? xrow[(tx + 32 * c) * W4 + q]
+                                                                                         : lpan[(tx + 32 * c) * W4 + q];
+          cv[4 * q] = t4.x;
+          cv[4 * q + 1] = t4.y;
+          cv[4 * q + 2] = t4.z;
+          cv[4 * q + 3] = t4.w;
         }
-#pragma unroll
-        for (int c = kc; c < CB; ++c) {
-          if (RB > 2 && r <= 2 * c - 1) continue;  // block entirely above the diagonal
-          float v = a[r][c];
-#pragma unroll
-          for (int q = 0; q < W4; ++q) {
-            const float4 t4 = lpan[(tx + 32 * c) * W4 + q];
-            v = fmaf(-lr[4 * q], t4.x, v);
-            v = fmaf(-lr[4 * q + 1], t4.y, v);
-            v = fmaf(-lr[4 * q + 2], t4.z, v);
-            v = fmaf(-lr[4 * q + 3], t4.w, v);
-          }
-          a[r][c] = v;
-        }
-#pragma unroll
-        for (int c = 0; c <= kc; ++c) {
-          if (RB > 2 && r <= 2 * c - 1) continue;  // X is lower triangular
-          float v = x[r][c];
+        float xv[W];
+        if (acol && xcol) {  // c == kc: both an A and an X column block
 #pragma unroll
           for (int q = 0; q < W4; ++q) {
             const float4 t4 = xrow[(tx + 32 * c) * W4 + q];
-            v = fmaf(-lr[4 * q], t4.x, v);
-            v = fmaf(-lr[4 * q + 1], t4.y, v);
-            v = fmaf(-lr[4 * q + 2], t4.z, v);
-            v = fmaf(-lr[4 * q + 3], t4.w, v);
+            xv[4 * q] = t4.x;
+            xv[4 * q + 1] = t4.y;
+            xv[4 * q + 2] = t4.z;
+            xv[4 * q + 3] = t4.w;
           }
-          x[r][c] = v;
+        }
+#pragma unroll
+        for (int r = kr; r < RB; ++r) {
+          if (RB > 2 && r <= 2 * c - 1) continue;  // block entirely above the diagonal
+          float lr[W];
+#pragma unroll
+          for (int q = 0; q < W4; ++q) {
+            const float4 t4 = lpan[(ty + 16 * r) * W4 + q];
+            lr[4 * q] = t4.x;
+            lr[4 * q + 1] = t4.y;
+            lr[4 * q + 2] = t4.z;
+            lr[4 * q + 3] = t4.w;
+          }
+          if (acol) {
+            float v = a[r][c];
+#pragma unroll
+            for (int t = 0; t < W; ++t) v = fmaf(-lr[t], cv[t], v);
+            a[r][c] = v;
+          }
+          if (xcol) {
+            const float* xs = acol ? xv : cv;
+            float v = x[r][c];
+#pragma unroll
+            for (int t = 0; t < W; ++t) v = fmaf(-lr[t], xs[t], v);
+            x[r][c] = v;
+          }
         }
       }
 #ifdef DPK_LEAF_PROF
@@ -320,11 +335,11 @@ template <int RB, int W>
 constexpr int leaf_smem_bytes() {
   return (4 * 16 * RB * W + 16 * RB * (16 * RB + 1)) * 4;  // 4 panels of N x W + the X^T X copy
 }
-int leaf_width() {  // columns per sweep step (DPK_LEAF_W=4 or 8)
+int leaf_width() {  // columns per sweep step (DPK_LEAF_W=4 default, or 8)
   static int w = -1;
   if (w < 0) {
     const char* e = getenv("DPK_LEAF_W");
-    w = (e && e[0] == '4') ? 4 : 8;
+    w = (e && e[0] == '8') ? 8 : 4;
   }
   return w;
 }
