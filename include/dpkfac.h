@@ -12,7 +12,8 @@
  *     (torch owns every byte; the library never allocates persistent memory).
  *     Scratch space is passed in explicitly as (workspace, bytes); its size
  *     comes from the matching *_workspace_bytes query and its content need not
- *     be initialised (split-K semaphores in it are zeroed on the stream).
+ *     be initialised (the GEMM engine's tile-scheduler counters at its start are
+ *     cleared on the stream by each call).
  *   - Matrices are row-major float32.  Factors are d x d and exactly symmetric.
  *   - Calls are asynchronous on the given stream and stateless, hence
  *     reentrant across streams.  No C++ exception crosses this boundary.

@@ -50,7 +50,12 @@ size_t gemm_workspace_bytes(const GemmSpec* specs, int n);
 bool simt_eligible(const GemmSpec* specs, int n, int precision);
 double simt_fma_limit();
 int simt_gemm_launch(const GemmSpec* specs, int n, cudaStream_t st);
-int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int precision, cudaStream_t st);
+// zero_counters: clear the scheduler counters at the workspace start first (callers
+// that issue several launches on one workspace/stream clear once; every kernel
+// leaves them zero)
+int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int precision, cudaStream_t st,
+                bool zero_counters = true);
+constexpr size_t GEMM_SCHED_BYTES = 256;
 
 inline dpk_operand rows_k(const float* p, int rows, int64_t cols, int64_t ld) {
   dpk_operand o{};

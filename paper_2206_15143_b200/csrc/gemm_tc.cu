@@ -57,6 +57,7 @@ constexpr int TILE_TASKS = BM * (BK / 4);                 // (row, 16B chunk) ta
 constexpr int NTASK = (TILE_TASKS + NPROD - 1) / NPROD;   // 5 tasks per producer thread
 constexpr int NTHREADS = (PROD_WARP0 + PROD_WARPS) * 32;  // 384
 constexpr int MAXP = 32;                                  // problems per launch (kernel params)
+constexpr size_t SCHED_BYTES = GEMM_SCHED_BYTES;          // scheduler counters at the workspace start
 static_assert(NPROD % 8 == 0, "im2col chunk sharing needs NPROD % 8 == 0");
 
 // TMA_ROWS_MN3: MN-major operand whose row count is a multiple of 32, fetched as
@@ -104,6 +105,8 @@ struct Batch {
   int debug_ts;   // record %globaltimer checkpoints of CTA 0 (dpk_debug_timestamps)
   int producers;  // 0: every operand tile arrives by TMA ready for the MMA (no gather /
                   // conversion anywhere in the launch) -> warps 6-11 sit the launch out
+  int dynamic;    // 1: units handed out by an atomic counter (sched[0]); 0: static round robin
+  int* sched;     // [0] next unit, [1] finished workers (the last one resets both)
   Problem p[MAXP];
 };
 static_assert(sizeof(Batch) <= 32764, "kernel parameter space is 32764 bytes");
@@ -123,7 +126,8 @@ struct Cfg {
   static constexpr int STAGES = NPASS == 1 ? 6 : 3;
   static constexpr int OPS = NPASS == 1 ? 2 : 4;  // A, B (+ A_lo, B_lo)
   static constexpr int STAGE_BYTES = OPS * TILE_BYTES;
-  static constexpr int BAR_BYTES = 8 * (3 * STAGES + 4) + 16;
+  static constexpr int NSLOT = 4;  // unit-id ring between the scheduler thread and the roles
+  static constexpr int BAR_BYTES = 8 * (3 * STAGES + 4) + 16 + 8 * 2 * NSLOT + 4 * NSLOT;
   static constexpr int EPI_BYTES = EPI_WARPS * 32 * 33 * 4;  // per-warp 32x32 (+1 pad) staging
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + BAR_BYTES + EPI_BYTES;
 };
@@ -647,6 +651,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   auto tfull_bar = [&](int a) { return bars + 8u * (3 * C::STAGES + a); };
   auto tempty_bar = [&](int a) { return bars + 8u * (3 * C::STAGES + 2 + a); };
   const uint32_t tmem_slot = bars + 8u * (3 * C::STAGES + 4);
+  // unit ring: the scheduler (CG=1 / leader TMA thread) publishes unit ids, every
+  // looping role reads them in order; -1 ends the launch
+  const uint32_t rbase = tmem_slot + 16u;
+  auto rfull_bar = [&](int q) { return rbase + 8u * q; };
+  auto rempty_bar = [&](int q) { return rbase + 8u * (C::NSLOT + q); };
+  const uint32_t ring_ids = rbase + 16u * C::NSLOT;
+  volatile int* ring = reinterpret_cast<volatile int*>(gbase + (ring_ids - base));
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -655,6 +666,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   const int half = static_cast<int>(rank) * 128;  // this CTA's row offset inside a unit tile
   const int unit0 = (CG == 2) ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
   const int ustep = (CG == 2) ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+  const bool prods_ = bt.producers != 0;
+  // ring consumers per CTA: MMA thread (CG=1 / leader) or the peer's TMA thread,
+  // 4 epilogue warps, the producer warps when they run
+  const int consumers = 1 + EPI_WARPS + (prods_ ? PROD_WARPS : 0);
   if (threadIdx.x == 0) dbg_ts(bt, 0);
 
   // full-barrier arrivals per stage use: every producer warp of the CTA (CG=2:
@@ -670,6 +685,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull_bar(a), 1);
       mbar_init(tempty_bar(a), EPI_WARPS * 32 * CG);
+    }
+    for (int q = 0; q < C::NSLOT; ++q) {
+      mbar_init(rfull_bar(q), 1);
+      mbar_init(rempty_bar(q), consumers * CG);  // CG=2: both CTAs' consumers, on the leader
     }
     mbar_fence_init();
   }
@@ -689,13 +708,64 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   pdl_trigger();
   const uint32_t tmem_base = *reinterpret_cast<volatile uint32_t*>(gbase + (tmem_slot - base));
   if (threadIdx.x == 0) dbg_ts(bt, 1);
+  // scheduler side (CG=1, or the leader's TMA thread): next unit id, -1 when done
+  auto sched_next = [&](int it) -> int {
+    int u = bt.dynamic ? atomicAdd(bt.sched, 1) : unit0 + it * ustep;
+    return u < bt.total_units ? u : -1;
+  };
+  auto ring_publish = [&](int it, int u) {
+    const int q = it % C::NSLOT;
+    const uint32_t par = static_cast<uint32_t>((it / C::NSLOT) & 1);
+    if (CG == 2)
+      mbar_wait_cluster(rempty_bar(q), par ^ 1);
+    else
+      mbar_wait(rempty_bar(q), par ^ 1);
+    ring[q] = u;
+    if (CG == 2) {
+      st_shared_cluster_s32(mapa_shared(ring_ids + 4u * q, 1), u);
+      mbar_arrive(rfull_bar(q));
+      mbar_arrive_remote(mapa_shared(rfull_bar(q), 1));
+    } else {
+      mbar_arrive(rfull_bar(q));
+    }
+  };
+  // consumer side: every thread of the calling warp reads; `arrive` = this
+  // thread releases the slot for its role (one per warp / role)
+  auto ring_take = [&](int it, bool arrive) -> int {
+    const int q = it % C::NSLOT;
+    const uint32_t par = static_cast<uint32_t>((it / C::NSLOT) & 1);
+    if (CG == 2 && !leader)
+      mbar_wait_cluster(rfull_bar(q), par);
+    else
+      mbar_wait(rfull_bar(q), par);
+    const int u = ring[q];
+    if (arrive) {
+      if (CG == 2 && !leader)
+        mbar_arrive_remote(mapa_shared(rempty_bar(q), 0));
+      else
+        mbar_arrive(rempty_bar(q));
+    }
+    return u;
+  };
 
   if (warp == TMA_WARP) {
     // =============================== TMA issuer: runs ahead through the stage ring
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = unit0; u < bt.total_units; u += ustep) {
+      // the next unit id is drawn one unit ahead, so the atomic's round trip
+      // overlaps this unit's load issue
+      int u_next = (CG == 1 || leader) ? sched_next(0) : 0;
+      for (int it = 0;; ++it) {
+        int u;
+        if (CG == 1 || leader) {
+          u = u_next;
+          ring_publish(it, u);
+          if (u >= 0) u_next = sched_next(it + 1);
+        } else {
+          u = ring_take(it, true);
+        }
+        if (u < 0) break;
         int pi, tm, tn, tile, split;
         decode_unit(bt, u, pi, tm, tn, tile, split);
         const Problem& P = bt.p[pi];
@@ -744,7 +814,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
     const int ptid = threadIdx.x - PROD_WARP0 * 32;
     int stage = 0;
     uint32_t phase = 0;
-    for (int u = unit0; u < bt.total_units; u += ustep) {
+    for (int it = 0;; ++it) {
+      const int u = ring_take(it, lane == 0);
+      __syncwarp();
+      if (u < 0) break;
       int pi, tm, tn, tile, split;
       decode_unit(bt, u, pi, tm, tn, tile, split);
       const Problem& P = bt.p[pi];
@@ -809,8 +882,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
     if (lane == 0 && leader) {
       int stage = 0;
       uint32_t phase = 0;
-      int it = 0;
-      for (int u = unit0; u < bt.total_units; u += ustep, ++it) {
+      for (int it = 0;; ++it) {
+        const int u = ring_take(it, true);
+        if (u < 0) break;
         int pi, tm, tn, tile, split;
         decode_unit(bt, u, pi, tm, tn, tile, split);
         const Problem& P = bt.p[pi];
@@ -883,8 +957,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
     // =============================== epilogue (warps 0-3, thread = tile row)
     const int m = warp * 32 + lane;
     float* T = reinterpret_cast<float*>(gbase + (bars - base) + C::BAR_BYTES) + warp * 32 * 33;
-    int it = 0;
-    for (int u = unit0; u < bt.total_units; u += ustep, ++it) {
+    for (int it = 0;; ++it) {
+      const int u = ring_take(it, lane == 0);
+      __syncwarp();
+      if (u < 0) break;
       int pi, tm, tn, tile, split;
       decode_unit(bt, u, pi, tm, tn, tile, split);
       const Problem& P = bt.p[pi];
@@ -930,6 +1006,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   __syncthreads();
   if (CG == 2) cluster_sync_all();  // no CTA leaves while its pair may still signal it
   if (threadIdx.x == 0) dbg_ts(bt, 7);
+  // dynamic schedule: the last worker to finish resets the counters for the next
+  // launch on this stream (every worker has drawn its final, out-of-range id)
+  if (bt.dynamic && threadIdx.x == 0 && (CG == 1 || leader)) {
+    __threadfence();
+    if (atomicAdd(bt.sched + 1, 1) == static_cast<int>(gridDim.x) / CG - 1) {
+      bt.sched[0] = 0;
+      bt.sched[1] = 0;
+      __threadfence();
+    }
+  }
   if (warp == MMA_WARP) {
     __syncwarp();
     tc_fence_after();
@@ -1084,6 +1170,15 @@ bool mn3_disabled() {
   if (v < 0) {
     const char* e = getenv("DPK_MN3");
     v = (e && e[0] == '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+bool dynamic_schedule() {  // DPK_DYN=0: static round-robin units
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DPK_DYN");
+    v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
 }
@@ -1326,7 +1421,7 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
     P.splits = (P.chunks + P.cps - 1) / P.cps;
     if (P.splits > 1) partial_tiles += static_cast<size_t>(P.ntiles) * P.splits;
   }
-  plan.ws_bytes = partial_tiles * UT * UT * sizeof(float);
+  plan.ws_bytes = SCHED_BYTES + partial_tiles * UT * UT * sizeof(float);
   return DPK_OK;
 }
 
@@ -1478,14 +1573,16 @@ int launch_group(const Batch& bt, int precision, cudaStream_t st) {
 // One plan (all problems share the unit-tile size) -> grouped launches of up to
 // MAXP problems, then the split-K reduction.
 int run_plan(Plan& plan, void* ws, size_t ws_bytes, int precision, cudaStream_t st) {
-  if (plan.ws_bytes > ws_bytes) {
+  if (plan.ws_bytes > ws_bytes || ws == nullptr) {
     set_error("dpk_gemm: workspace too small (" + std::to_string(ws_bytes) + " < " +
               std::to_string(plan.ws_bytes) + ")");
     return DPK_ENOSPACE;
   }
   const int ut = 128 * plan.cg;
   size_t partial_tiles = 0;
-  float* partials = static_cast<float*>(ws);
+  // workspace: [scheduler counters | split-K partials]
+  int* sched = static_cast<int*>(ws);
+  float* partials = reinterpret_cast<float*>(static_cast<char*>(ws) + SCHED_BYTES);
   for (auto& P : plan.probs) {
     if (P.splits > 1) {
       P.partials = partials + partial_tiles * ut * ut;
@@ -1505,6 +1602,8 @@ int run_plan(Plan& plan, void* ws, size_t ws_bytes, int precision, cudaStream_t 
     }
     bt.total_units = units;
     bt.debug_ts = debug_ts_enabled() ? 1 : 0;
+    bt.sched = sched;
+    bt.dynamic = dynamic_schedule() ? 1 : 0;
     // producer warps are needed for 3xTF32 low parts and for operands TMA cannot address
     bt.producers = precision == DPK_PREC_3XTF32 ? 1 : 0;
     for (int i = 0; i < cnt; ++i)
@@ -1566,7 +1665,8 @@ size_t gemm_workspace_bytes_uncached(const GemmSpec* specs, int n) {
   return ws;
 }
 
-int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int precision, cudaStream_t st) {
+int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int precision, cudaStream_t st,
+                bool zero_counters) {
   if (n == 0) return DPK_OK;
   if (n < 0 || specs == nullptr) {
     set_error("dpk_gemm: bad job list");
@@ -1578,6 +1678,10 @@ int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int pre
   }
   // small 3xTF32 groups (deep SPD-recursion rounds): latency path on CUDA cores
   if (simt_eligible(specs, n, precision)) return simt_gemm_launch(specs, n, st);
+  if (zero_counters && ws != nullptr && ws_bytes >= SCHED_BYTES) {
+    const int rc = cuda_status(cudaMemsetAsync(ws, 0, SCHED_BYTES, st), "cudaMemsetAsync(scheduler counters)");
+    if (rc) return rc;
+  }
   // big problems run on CTA pairs, the rest on single CTAs (two launches, same
   // stream: the split-K workspace is reused in order).  The plans (tensor maps
   // included) of a job list seen before come from the cache.

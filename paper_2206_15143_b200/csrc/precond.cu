@@ -144,7 +144,7 @@ int dpk_precond_inverse(const dpk_precond_job* jobs, int n_jobs, void* workspace
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int rc = dpk::gemm_launch(p1.data(), n_jobs, workspace, ws_bytes, precision, st);
   if (rc) return rc;
-  return dpk::gemm_launch(p2.data(), n_jobs, workspace, ws_bytes, precision, st);
+  return dpk::gemm_launch(p2.data(), n_jobs, workspace, ws_bytes, precision, st, false);
 }
 
 size_t dpk_precond_factor_workspace_bytes(const dpk_precond_factor_job* jobs, int n_jobs) {
@@ -166,9 +166,11 @@ int dpk_precond_factored(const dpk_precond_factor_job* jobs, int n_jobs, void* w
   dpk::Specs p[4];
   dpk::factored_phases(jobs, n_jobs, p);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  bool first = true;
   for (auto& s : p) {
-    int rc = dpk::gemm_launch(s.data(), n_jobs, workspace, ws_bytes, precision, st);
+    int rc = dpk::gemm_launch(s.data(), n_jobs, workspace, ws_bytes, precision, st, first);
     if (rc) return rc;
+    first = false;
   }
   return DPK_OK;
 }
@@ -200,9 +202,11 @@ int dpk_precond_eigen(const dpk_precond_job* jobs, int n_jobs, float gamma, void
   }
   dpk::Specs p[4];
   dpk::eigen_phases(jobs, n_jobs, gamma, p);
+  bool first = true;
   for (auto& s : p) {
-    int rc = dpk::gemm_launch(s.data(), n_jobs, workspace, ws_bytes, precision, st);
+    int rc = dpk::gemm_launch(s.data(), n_jobs, workspace, ws_bytes, precision, st, first);
     if (rc) return rc;
+    first = false;
   }
   return DPK_OK;
 }

@@ -861,6 +861,7 @@ int run_inverse(const SpdReq* jobs, int n_jobs, void* workspace, cudaStream_t st
 int run_lockstep(const SpdPlan& plan, const std::vector<int>& grp, char* gemm_ws, size_t gemm_bytes,
                  cudaStream_t st, bool trace) {
   std::vector<size_t> idx(grp.size(), 0);
+  bool counters_zeroed = false;
   struct RoundRec {
     cudaEvent_t e0, e1, e2;
     int nleaf, maxn, ngemm;
@@ -911,7 +912,13 @@ int run_lockstep(const SpdPlan& plan, const std::vector<int>& grp, char* gemm_ws
     }
     if (trace) cudaEventRecord(rr.e1, st);
     if (!g.empty()) {
-      int rc = dpk::gemm_launch(g.data(), static_cast<int>(g.size()), gemm_ws, gemm_bytes, DPK_PREC_3XTF32, st);
+      if (!counters_zeroed) {  // once per chain: the GEMM kernels leave the counters zero
+        int rc = cuda_status(cudaMemsetAsync(gemm_ws, 0, GEMM_SCHED_BYTES, st), "cudaMemsetAsync(counters)");
+        if (rc) return rc;
+        counters_zeroed = true;
+      }
+      int rc = dpk::gemm_launch(g.data(), static_cast<int>(g.size()), gemm_ws, gemm_bytes, DPK_PREC_3XTF32, st,
+                                false);
       if (rc) return rc;
     }
     if (trace) {

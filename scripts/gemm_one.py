@@ -4,6 +4,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch
 from paper_2206_15143_b200 import _lib as L, ops
+if os.environ.get("DPK_LIB"):
+    L.load(os.environ["DPK_LIB"])
 
 m, n, k = (int(v) for v in sys.argv[1:4])
 prec = sys.argv[4] if len(sys.argv) > 4 else "tf32"
