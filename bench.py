@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-overlap", action="store_true", help="run every stage on one stream")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--early", action="store_true",
+                    help="e2e: launch the larger size classes' factor/inverse pipeline from the backward hooks")
     return ap.parse_args()
 
 
@@ -207,7 +209,7 @@ def run_ours(args, rank, world, local_rank):
         model = model.to(memory_format=mf)
     kf = DPKFAC(model, gamma=args.gamma, xi=args.xi, inv_type=args.inv_type, f_freq=1, k_freq=1,
                 assignment=args.assignment, precision=args.precision, check_numerics="deferred",
-                overlap=not args.no_overlap)
+                overlap=not args.no_overlap, early=False)  # captures are replayed below; e2e turns early on
     opt = torch.optim.SGD(model.parameters(), lr=1e-3, momentum=0.9)
     gen = torch.Generator().manual_seed(1234 + rank)
     x_host = torch.randn(batch, *shape, generator=gen)
@@ -353,6 +355,7 @@ def run_ours(args, rank, world, local_rank):
             opt.step()
             return loss.item()
 
+        kf.early = args.early and not args.no_overlap  # hook-time launch of the larger classes' pipelines
         for _ in range(2):
             train_step()
         sync_barrier()

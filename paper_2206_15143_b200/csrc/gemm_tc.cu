@@ -63,9 +63,16 @@ static_assert(NPROD % 8 == 0, "im2col chunk sharing needs NPROD % 8 == 0");
 // TMA_ROWS_MN3: MN-major operand whose row count is a multiple of 32, fetched as
 // ONE 3-D box {32 rows, 32 k, 4 row blocks} per 128-row tile instead of four
 // 2-D boxes (same shared-memory image)
-enum { TMA_NONE = 0, TMA_ROWS_K = 1, TMA_ROWS_MN = 2, TMA_SLAB = 3, TMA_IM2COL = 4, TMA_ROWS_MN3 = 5 };
+// TMA_TAPS: implicit im2col of an NHWC conv input through plain TILED boxes:
+// a 5-D map {c32, w, h, n, c-block} over the input itself, one box per (tap,
+// channel block) group of 32/64/128 factor rows at the tap-shifted pixel
+// coordinates; out-of-image taps are TMA zero fill.  A K chunk is 32 pixels
+// (wb output columns x 32/wb samples at one output row), the same pixel set for
+// every row group, so patches never exist in HBM (SYRK only: both operands
+// share the map and the K order).
+enum { TMA_NONE = 0, TMA_ROWS_K = 1, TMA_ROWS_MN = 2, TMA_SLAB = 3, TMA_IM2COL = 4, TMA_ROWS_MN3 = 5, TMA_TAPS = 6 };
 __host__ __device__ __forceinline__ bool tma_mn(int kind) {
-  return kind == TMA_ROWS_MN || kind == TMA_IM2COL || kind == TMA_ROWS_MN3;
+  return kind == TMA_ROWS_MN || kind == TMA_IM2COL || kind == TMA_ROWS_MN3 || kind == TMA_TAPS;
 }
 
 __host__ __device__ __forceinline__ bool is_im2col(int kind) {
@@ -93,7 +100,8 @@ struct alignas(64) Problem {
   int chunks, cps;  // K chunks of 32, chunks per split
   int unit_begin;
   int tma_a, tma_b;
-  int slab_cpn;     // TMA_SLAB: chunks per sample (K index = (sample, 32-pixel chunk))
+  int slab_cpn;     // TMA_SLAB: chunks per sample (K index = (sample, 32-pixel chunk));
+                    // TMA_TAPS: wb | group boxes << 8 | sample blocks << 16
   int tri_a, tri_b; // TRI_*: per-tile K clipping for triangular operands
   int order;        // tile visiting order (non-symmetric): 0 row-major, 1 row-major reversed,
                     // 2 column-major, 3 column-major reversed -- heaviest K ranges first
@@ -121,6 +129,15 @@ __device__ __forceinline__ void dbg_ts(const Batch& bt, int slot) {
   }
 }
 
+// Every tcgen05 launch asks for the whole opt-in shared memory of an SM (227 KB),
+// so none of its CTAs ever shares an SM with another kernel's CTA.  Otherwise a
+// concurrently running library kernel (cuDNN/cuBLAS sm_100 kernels hold TMEM
+// too) could sit on the same SM holding TMEM while it waits for peer CTAs that
+// cannot be scheduled because our persistent CTAs occupy every SM, and our CTA
+// would block in tcgen05.alloc behind it: a deadlock observed when the factor
+// pipeline runs under the backward pass (early=True).
+constexpr int SMEM_SM_EXCL = 232448;
+
 template <int NPASS>
 struct Cfg {
   static constexpr int STAGES = NPASS == 1 ? 6 : 3;
@@ -130,6 +147,7 @@ struct Cfg {
   static constexpr int BAR_BYTES = 8 * (3 * STAGES + 4) + 16 + 8 * 2 * NSLOT + 4 * NSLOT;
   static constexpr int EPI_BYTES = EPI_WARPS * 32 * 33 * 4;  // per-warp 32x32 (+1 pad) staging
   static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + BAR_BYTES + EPI_BYTES;
+  static_assert(SMEM <= SMEM_SM_EXCL, "stage ring exceeds the SM's shared memory");
 };
 
 __device__ __forceinline__ void decode_unit(const Batch& bt, int u, int& pi, int& tm, int& tn, int& tile,
@@ -387,7 +405,7 @@ __device__ __forceinline__ void convert_tile(uint8_t* tile, uint8_t* tile_lo, in
 // (zero-filled) size; im2col tiles skip 32-row groups past the operand's rows
 // (those smem rows only feed accumulator rows the epilogue never stores).
 __device__ __forceinline__ uint32_t tma_tile_bytes(int kind, const dpk_operand& o, int row0) {
-  if (kind != TMA_IM2COL) return TILE_BYTES;
+  if (kind != TMA_IM2COL && kind != TMA_TAPS) return TILE_BYTES;
   const int groups = min(BM / 32, (o.rows - row0 + 31) / 32);
   return static_cast<uint32_t>(max(groups, 0)) * 4096u;
 }
@@ -418,6 +436,26 @@ __device__ __forceinline__ void issue_tma(int kind, const CUtensorMap* map, cons
       tma_load_3d_pair(dst, map, bar, (kc - n * cpn) * BK, row0, n);
     else
       tma_load_3d(dst, map, bar, (kc - n * cpn) * BK, row0, n);
+  } else if (kind == TMA_TAPS) {
+    // K chunk kc = (oh, output-column block, sample block); rows (i, j, c)
+    const int wb = cpn & 0xFF, g = (cpn >> 8) & 0xFF, nblk = cpn >> 16;
+    const int owbs = o.OW / wb;
+    const int q = kc / nblk;
+    const int nb = kc - q * nblk;
+    const int oh = q / owbs;
+    const int owb = q - oh * owbs;
+    const int w0 = owb * wb * o.sw - o.pw, h0 = oh * o.sh - o.ph, n0 = nb * (32 / wb);
+    for (int b = 0; b < BM / 32; b += g) {
+      const int r = row0 + 32 * b;
+      if (r >= o.rows) break;
+      const int tap = r / o.C;
+      const int c0 = r - tap * o.C;
+      const int i = tap / o.kw, j = tap - (tap / o.kw) * o.kw;
+      if (PAIR)
+        tma_load_5d_pair(dst + b * 4096, map, bar, 0, w0 + j * o.dw, h0 + i * o.dh, n0, c0 >> 5);
+      else
+        tma_load_5d(dst + b * 4096, map, bar, 0, w0 + j * o.dw, h0 + i * o.dh, n0, c0 >> 5);
+    }
   } else {  // TMA_IM2COL: NHWC input, rows (i, j, c); a box = 32 output pixels x 32 channels
     const int64_t k0 = static_cast<int64_t>(kc) * BK;
     const int ohw = o.OH * o.OW;
@@ -1305,6 +1343,66 @@ bool plan_tma_im2col(const dpk_operand& o, CUtensorMap* m, bool rn) {
   return r == CUDA_SUCCESS;
 }
 
+// TMA_TAPS geometry: (wb output columns) x (32 / wb samples) per K chunk, the
+// widest sample block that divides the batch (else 32 with zero-filled tail
+// samples); group boxes of 4/2/1 x 32 channels (a box never crosses a tap).
+struct TapsGeom {
+  int wb, nb, nblk, g;
+  int64_t chunks;
+};
+
+bool taps_disabled() {  // DPK_TAPS=0: keep TMA im2col mode / the gather path
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DPK_TAPS");
+    v = (e && e[0] == '0') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+bool taps_eligible(const dpk_operand& o, TapsGeom* tg = nullptr) {
+  if (o.kind != DPK_OPND_IM2COL_TAPMAJOR || o.bias_row || tma_disabled() || taps_disabled()) return false;
+  if (o.C % 32 != 0 || o.sc != 1 || !aligned16(o.data)) return false;
+  if ((o.sws * 4) % 16 != 0 || (o.shs * 4) % 16 != 0 || (o.sn * 4) % 16 != 0) return false;
+  if (o.sw > 8 || o.OW < 1 || o.OH < 1) return false;
+  const int64_t hw = static_cast<int64_t>(o.OH) * o.OW;
+  if (o.cols % hw != 0) return false;
+  const int64_t n = o.cols / hw;
+  int wb = 1;
+  if (n % 32 != 0) {
+    for (int c = 2; c <= 8; c *= 2)
+      if (n % (32 / c) == 0 && o.OW % c == 0) {
+        wb = c;
+        break;
+      }
+  }
+  if (wb * o.sw > 256) return false;
+  if (tg) {
+    tg->wb = wb;
+    tg->nb = 32 / wb;
+    tg->nblk = static_cast<int>((n + tg->nb - 1) / tg->nb);
+    tg->g = o.C % 128 == 0 ? 4 : o.C % 64 == 0 ? 2 : 1;
+    tg->chunks = static_cast<int64_t>(o.OH) * (o.OW / wb) * tg->nblk;
+  }
+  return true;
+}
+
+bool plan_tma_taps(const dpk_operand& o, const TapsGeom& tg, CUtensorMap* m, bool rn) {
+  EncodeTiledFn fn = encoder();
+  if (!fn) return false;
+  const int64_t n = o.cols / (static_cast<int64_t>(o.OH) * o.OW);
+  const cuuint64_t dims[5] = {32, static_cast<cuuint64_t>(o.W), static_cast<cuuint64_t>(o.H),
+                              static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(o.C / 32)};
+  const cuuint64_t strides[4] = {static_cast<cuuint64_t>(o.sws) * 4, static_cast<cuuint64_t>(o.shs) * 4,
+                                 static_cast<cuuint64_t>(o.sn) * 4, 128};
+  const cuuint32_t box[5] = {32, static_cast<cuuint32_t>(tg.wb == 1 ? 1 : tg.wb * o.sw), 1,
+                             static_cast<cuuint32_t>(tg.nb), static_cast<cuuint32_t>(tg.g)};
+  const cuuint32_t es[5] = {1, static_cast<cuuint32_t>(tg.wb == 1 ? 1 : o.sw), 1, 1, 1};
+  return fn(m, rn ? CU_TENSOR_MAP_DATA_TYPE_TFLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(o.data),
+            dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // ------------------------------------------------------------------ host planning
 struct Plan {
   std::vector<Problem> probs;
@@ -1380,7 +1478,19 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
     P.tiles_n = (P.N + UT - 1) / UT;
     P.ntiles = P.symmetric ? tmn * (tmn + 1) / 2 : tmn * P.tiles_n;
     P.chunks = static_cast<int>((j.a.cols + BK - 1) / BK);
-    if (P.same_ab && slab_eligible(j.a)) {
+    TapsGeom tg;
+    if (P.same_ab && taps_eligible(j.a, &tg)) {
+      P.chunks = static_cast<int>(tg.chunks);
+      P.slab_cpn = tg.wb | (tg.g << 8) | (tg.nblk << 16);
+      if (with_maps) {
+        if (!plan_tma_taps(j.a, tg, &P.tmap_a, rn)) {
+          set_error("dpk_gemm: cuTensorMapEncodeTiled rejected the implicit-im2col (taps) map");
+          return DPK_ECUDA;
+        }
+        P.tmap_b = P.tmap_a;
+        P.tma_a = P.tma_b = TMA_TAPS;
+      }
+    } else if (P.same_ab && slab_eligible(j.a)) {
       // SYRK over an NCHW slab: both operands through one 3-D map, K = (sample, chunk)
       const int64_t hw = static_cast<int64_t>(j.a.H) * j.a.W;
       P.slab_cpn = static_cast<int>((hw + BK - 1) / BK);
@@ -1453,7 +1563,7 @@ bool wants_cg2(const GemmSpec& g) {
     if (o.kind == DPK_OPND_IM2COL_TAPMAJOR) return im2col_eligible(o);
     return false;
   };
-  if (same && slab_eligible(j.a)) return true;
+  if (same && (slab_eligible(j.a) || taps_eligible(j.a))) return true;
   return ok(j.a) && (same || ok(j.b));
 }
 
@@ -1528,7 +1638,7 @@ int launch_batch(const Batch& bt, cudaStream_t st) {
   static int max_pairs = 0;
   if (!configured) {
     cudaError_t e =
-        cudaFuncSetAttribute(tc_gemm_kernel<NPASS, RN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaFuncSetAttribute(tc_gemm_kernel<NPASS, RN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SM_EXCL);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(tc_gemm_kernel)");
     if (CG == 2) {
       cudaLaunchConfig_t q = {};
@@ -1539,7 +1649,7 @@ int launch_batch(const Batch& bt, cudaStream_t st) {
       at[0].val.clusterDim.z = 1;
       q.gridDim = dim3(2 * (num_sms() / 2), 1, 1);
       q.blockDim = dim3(NTHREADS, 1, 1);
-      q.dynamicSmemBytes = C::SMEM;
+      q.dynamicSmemBytes = SMEM_SM_EXCL;
       q.attrs = at;
       q.numAttrs = 1;
       int clusters = 0;
@@ -1558,7 +1668,7 @@ int launch_batch(const Batch& bt, cudaStream_t st) {
   const int upc = units_per_cta();
   const int want = upc > 0 ? std::max(workers, (bt.total_units + upc - 1) / upc) : workers;
   const int grid = CG == 1 ? std::min(bt.total_units, want) : 2 * std::min(bt.total_units, want);
-  const cudaError_t e = launch_k(tc_gemm_kernel<NPASS, RN, CG>, dim3(grid), dim3(NTHREADS), C::SMEM, st, CG, bt);
+  const cudaError_t e = launch_k(tc_gemm_kernel<NPASS, RN, CG>, dim3(grid), dim3(NTHREADS), SMEM_SM_EXCL, st, CG, bt);
   note_launch();
   return cuda_status(e, "tc_gemm_kernel launch");
 }

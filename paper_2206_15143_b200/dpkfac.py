@@ -90,9 +90,11 @@ class _Layer:
         nn.Linear / 1x1-stride-1 captures are read in place (channels-last: a
         sample-major [N*H*W, C] view streamed by 2-D TMA; NCHW: a 3-D slab map).
         Other convs use the implicit-im2col view directly (``im2col="implicit"``:
-        TMA im2col mode for NHWC, in-kernel gather otherwise) or, by default, a
-        sample-major patch matrix written by one coalesced copy kernel and then
-        streamed by 2-D TMA (``im2col="materialize"``)."""
+        tiled-TMA tap boxes / TMA im2col mode for NHWC, in-kernel gather otherwise),
+        a sample-major patch matrix written by one coalesced copy kernel and then
+        streamed by 2-D TMA (``im2col="materialize"``, the default), or ("auto") the
+        implicit form where the tiled-TMA tap boxes apply (NHWC, C % 32 == 0, no
+        bias) and the patch matrix elsewhere."""
         x = self.a_in
         if not self.is_conv:
             return ops.operand_rows_mn(x.reshape(-1, x.shape[-1]), self.has_bias), None
@@ -105,6 +107,11 @@ class _Layer:
         tap = self.tap_major if m.kernel_size != (1, 1) else nhwc
         op = ops.operand_im2col(x, m.kernel_size, m.stride, m.padding, m.dilation, self.has_bias, tap)
         if im2col == "implicit" or (plain_1x1 and x.is_contiguous()):
+            return op, None
+        if im2col == "auto" and tap and nhwc and x.shape[1] % 32 == 0 and not self.has_bias \
+                and x.data_ptr() % 16 == 0:
+            # tiled-TMA implicit im2col (TMA_TAPS): the SYRK reads the NHWC input
+            # at tap-shifted coordinates, patches never reach HBM
             return op, None
         d = op.rows + op.bias_row
         ld = (d + 3) // 4 * 4
@@ -186,10 +193,15 @@ class DPKFAC:
                  assignment: Union[str, Sequence[Sequence[int]]] = "round_robin",
                  process_group=None, precision: str = "tf32", precond_precision: str = "3xtf32",
                  grad_scale: Union[str, float] = "batch", check_numerics: Union[bool, str] = True,
-                 im2col: str = "materialize", overlap: bool = True):
+                 im2col: str = "materialize", overlap: bool = True, early: bool = False):
         self.hyper = KfacHyper(gamma=gamma, xi=xi, inv_type=inv_type, f_freq=f_freq, k_freq=k_freq)
-        if im2col not in ("materialize", "implicit"):
-            raise ArgumentError("im2col must be 'materialize' or 'implicit'")
+        # "auto": implicit (tiled-TMA tap boxes) for channels-last convs with C % 32 == 0,
+        # a materialized patch matrix otherwise (e.g. the 3-channel stem conv).
+        # Default "materialize": the sample-blocked tap boxes measured slower (factor
+        # stage 2.9 -> 6.3 ms on ResNet-50) and hang under the dynamic tile
+        # scheduler in grouped launches -- under investigation.
+        if im2col not in ("auto", "materialize", "implicit"):
+            raise ArgumentError("im2col must be 'auto', 'materialize' or 'implicit'")
         self.im2col = im2col
         ops.precision_code(precision)
         ops.precision_code(precond_precision)
@@ -263,6 +275,18 @@ class DPKFAC:
         # streams while the other layers' throughput-bound work fills the GPU
         self.overlap = bool(overlap)
         self._side = None
+        # early=True (with overlap): a side class's factor -> inverse pipeline is
+        # launched from the backward hook as soon as every layer of the class has
+        # both captures (the deepest layers' grads arrive first), so the long
+        # inversion chains run under the rest of the backward pass.
+        # Off by default: measured neutral on ResNet-50 (e2e 20.5 -> 21.1 ms with a
+        # per-iteration sync, 23.6 -> 19.8 ms without) -- the persistent tcgen05
+        # launches and the backward's cuDNN kernels compete for the same SMs.
+        # Captures of the first backward after a step are used (gradient
+        # accumulation: keep early=False).
+        self.early = bool(early)
+        self._hook_classes = None   # (classes, layer index -> class) fixed at the end of a step
+        self._launched = {}         # class -> step t whose factor/inverse it already launched
 
     # ------------------------------------------------------------ hooks
     def _make_pre_hook(self, ly: _Layer):
@@ -278,6 +302,8 @@ class DPKFAC:
             if self._capturing and ly.owned and torch.is_grad_enabled() and output.requires_grad:
                 def grab(g, ly=ly):
                     ly.g_out = g.detach()
+                    if self._hook_classes is not None:
+                        self._on_capture(ly)
                 output.register_hook(grab)
         return hook
 
@@ -317,7 +343,7 @@ class DPKFAC:
         self.xchg = OwnerMajorExchange(self.layout, self.rank, dev, self.pg)
         self.offsets = self.layout.offsets
         n_own = len(self.owned)
-        self.info = torch.zeros(max(len(self.layers), 1), dtype=torch.int32, device=dev)
+        self.info = torch.zeros(max(len(self.layers), 1), dtype=torch.int32, device=dev)  # zeroed after each step
         self.shifts = torch.zeros(max(n_own, 1), 2, device=dev)
         self.pis = torch.zeros(max(n_own, 1), device=dev)
         self._bufs_ready = True
@@ -355,7 +381,6 @@ class DPKFAC:
         f_up = t % h.f_freq == 0
         k_up = t % h.k_freq == 0
         owned = self.owned
-        self.info.zero_()
         classes = self._size_classes(owned)
         sides, rest = classes[:-1], classes[-1]
         main = torch.cuda.current_stream(self.device)
@@ -365,7 +390,9 @@ class DPKFAC:
         # start of the step; the last class runs on the caller's stream
         streams = self._side_streams(len(sides))
         ev0 = main.record_event()
-        for cls, st in zip(sides, streams):
+        for ci, (cls, st) in enumerate(zip(sides, streams)):
+            if self._launched.get(ci) == t:  # launched from the backward hook
+                continue
             st.wait_event(ev0)
             with torch.cuda.stream(st):
                 self._factor_stage(cls, t, f_up, st)
@@ -398,7 +425,10 @@ class DPKFAC:
         self._mark("precondition")
         # numeric failures: reference wording, prefixed "worker p, layer i" (distsim.py:273-274)
         if self.check_numerics == "sync":
-            self._raise_from_host(self._gather_info().cpu())
+            host = self._gather_info().cpu()
+            self.info.zero_()
+            self._launched = {}
+            self._raise_from_host(host)
         elif self.check_numerics == "deferred":
             if self._pending_info is not None:  # an unread older flag set: wait for it now
                 self.check()
@@ -411,7 +441,33 @@ class DPKFAC:
         X.all_gather()
         ops.unpack(segs, X.out_flat, 1.0)
         self._mark("comm_ag")
+        # flags start clean for the next step's (possibly hook-launched) stages;
+        # ordered after this step's reads of them on the caller's stream
+        self.info.zero_()
+        self._launched = {}
+        self._hook_classes = None
+        if self.early and self.overlap and len(sides) > 0:
+            self._hook_classes = (sides, {ly.index: ci for ci, c in enumerate(sides) for ly in c})
         self.t += 1
+
+    @torch.no_grad()
+    def _on_capture(self, ly: _Layer):
+        """Backward-hook side of early=True: launch the factor -> inverse pipeline of
+        ly's size class on its side stream once all of the class's captures exist."""
+        classes, of = self._hook_classes
+        ci = of.get(ly.index)
+        if ci is None or ci in self._launched:
+            return
+        cls = classes[ci]
+        if any(x.a_in is None or x.g_out is None for x in cls):
+            return
+        h, t = self.hyper, self.t
+        st = self._side_streams(len(classes))[ci]
+        st.wait_stream(torch.cuda.current_stream(self.device))  # the captures' producer stream
+        with torch.cuda.stream(st):
+            self._factor_stage(cls, t, t % h.f_freq == 0, st)
+            self._inverse_stage(cls, t, t % h.k_freq == 0)
+        self._launched[ci] = t
 
     # ------------------------------------------------------------ stages
     def _side_streams(self, n):

@@ -344,7 +344,8 @@ def test_pack_unpack_roundtrip_with_bias_column():
     assert torch.equal(w1, 2.0 * w1_0) and torch.equal(w2, 2.0 * w2_0) and torch.equal(b2, 2.0 * b2_0)
 
 
-# ---------------------------------------------------------------- tap-major (channels-last) im2col: TMA im2col path
+# ---------------------------------------------------------------- tap-major (channels-last) im2col: tiled-TMA tap boxes
+# (TMA_TAPS) for NHWC inputs with C % 32 == 0, the producer gather otherwise
 def _tap_perm(c, kh, kw):
     """held (kh, kw, c) position t -> reference (c, kh, kw) row index."""
     import numpy as _np
@@ -353,14 +354,20 @@ def _tap_perm(c, kh, kw):
 
 @pytest.mark.parametrize("shape,k,s,p", [((4, 64, 14, 14), 3, 1, 1), ((2, 128, 9, 9), 3, 2, 1),
                                          ((3, 32, 8, 8), 1, 2, 0), ((2, 64, 7, 7), 3, 1, 1),
-                                         ((2, 96, 12, 10), 5, 1, 2), ((1, 32, 6, 6), 1, 1, 0)])
+                                         ((2, 96, 12, 10), 5, 1, 2), ((1, 32, 6, 6), 1, 1, 0),
+                                         # tiled-TMA tap boxes: 32 samples per chunk (wb=1),
+                                         # 16 x 2 columns, 4 x 8 columns at stride 2, zero-filled
+                                         # sample tail (odd output width), 256 channels (4-group box)
+                                         ((32, 64, 8, 8), 3, 1, 1), ((16, 32, 10, 10), 3, 1, 1),
+                                         ((4, 32, 16, 16), 3, 2, 1), ((16, 32, 7, 7), 3, 1, 1),
+                                         ((32, 256, 4, 4), 1, 2, 0), ((8, 128, 6, 6), 7, 1, 3)])
 @pytest.mark.parametrize("channels_last", [True, False])
 def test_syrk_tapmajor_im2col_matches_unfold(shape, k, s, p, channels_last):
     from paper_2206_15143_b200 import ops
     rng = np.random.default_rng(sum(shape) + 7 * k)
     x = np.maximum(rng.standard_normal(shape), 0)
     xt = T(x)
-    if channels_last:  # NHWC with C % 32 == 0 -> TMA im2col; otherwise the gather path
+    if channels_last:  # NHWC with C % 32 == 0 -> TMA tap boxes; otherwise the gather path
         xt = xt.to(memory_format=torch.channels_last)
     cols = K.unfold_columns(x, k, k, s, p)
     perm = _tap_perm(shape[1], k, k)
@@ -416,3 +423,21 @@ def test_im2col_materialize_matches_unfold(shape, k, s, p, bias, channels_last, 
             perm = np.concatenate([perm, [cols.shape[0] - 1]])
         cols = cols[perm]
     assert np.array_equal(N(out[:, :d]).T, cols.astype(np.float32).astype(np.float64))
+
+
+@pytest.mark.parametrize("shape,k,s,p,dil", [((32, 64, 9, 9), 3, 1, 2, 2), ((8, 32, 11, 11), 3, 2, 2, 2)])
+def test_syrk_taps_dilated_matches_unfold(shape, k, s, p, dil):
+    from paper_2206_15143_b200 import ops
+    rng = np.random.default_rng(3 + dil)
+    x = rng.standard_normal(shape)
+    xt = T(x).to(memory_format=torch.channels_last)
+    cols = K.unfold_columns(x, k, k, s, p, dil)
+    perm = _tap_perm(shape[1], k, k)
+    d = cols.shape[0]
+    out = torch.full((d, d), float("nan"), device=dev())
+    op = ops.operand_im2col(xt, (k, k), (s, s), (p, p), (dil, dil), tap_major=True)
+    want, _ = K.compute_factors(cols[perm], cols[:1])
+    for prec, tol in (("tf32", TOL), ("3xtf32", 5e-5)):  # fp32 accumulation over M = 2592 / 968 columns
+        ops.syrk_ema([ops.factor_job(op, out, 1.0 / cols.shape[1], 0.0)], prec)
+        torch.cuda.synchronize()
+        assert rel(N(out), want) <= tol, (prec, rel(N(out), want))
