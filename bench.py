@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--nchw", action="store_true",
                     help="keep the conv model NCHW (default: channels_last, the B200-native layout)")
     ap.add_argument("--assignment", default="round_robin")
+    ap.add_argument("--algorithm", default="dp_kfac", choices=["dp_kfac", "mpd_kfac_co", "mpd_kfac_mo"],
+                    help="dp_kfac (the product) or the paper's MPD-KFAC comparators on the same kernels")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-overlap", action="store_true", help="run every stage on one stream")
@@ -209,7 +211,7 @@ def run_ours(args, rank, world, local_rank):
         model = model.to(memory_format=mf)
     kf = DPKFAC(model, gamma=args.gamma, xi=args.xi, inv_type=args.inv_type, f_freq=1, k_freq=1,
                 assignment=args.assignment, precision=args.precision, check_numerics="deferred",
-                overlap=not args.no_overlap, early=False)  # captures are replayed below; e2e turns early on
+                overlap=not args.no_overlap, early=False, algorithm=args.algorithm)  # captures are replayed below; e2e turns early on
     opt = torch.optim.SGD(model.parameters(), lr=1e-3, momentum=0.9)
     gen = torch.Generator().manual_seed(1234 + rank)
     x_host = torch.randn(batch, *shape, generator=gen)
@@ -232,12 +234,13 @@ def run_ours(args, rank, world, local_rank):
     kf.step()  # first step builds buffers/balance; captures are consumed
     model.zero_grad(set_to_none=False)
     F.cross_entropy(model(x), y).backward()
-    saved_caps = {ly.index: (ly.a_in, ly.g_out, ly.batch) for ly in kf.owned}
+    capt = kf.layers if args.algorithm != "dp_kfac" else kf.owned
+    saved_caps = {ly.index: (ly.a_in, ly.g_out, ly.batch) for ly in capt}
     layer_params = [p for ly in kf.layers for p in ([ly.module.weight] + ([ly.module.bias] if ly.has_bias else []))]
     saved_grads = [p.grad.clone() for p in layer_params]
 
     def restore():
-        for ly in kf.owned:
+        for ly in capt:
             ly.a_in, ly.g_out, ly.batch = saved_caps[ly.index]
         torch._foreach_copy_([p.grad for p in layer_params], saved_grads)
 
@@ -303,8 +306,9 @@ def run_ours(args, rank, world, local_rank):
     peak_src = ("MEASURED_PEAKS.json bf16_tflops / 2 (tcgen05 kind::tf32 issues at half the bf16 rate)"
                 if bf16 else "B200_PROFILING.md fallback 1.59 PF bf16 / 2")
     own = [geom[ly.index] for ly in kf.owned]
+    built = geom if args.algorithm != "dp_kfac" else own  # MPD: every rank builds every layer's factors
     flops = {
-        "factors": sum(d_in * (d_in + 1) * m + d_out * (d_out + 1) * m for _, d_in, d_out, m, _ in own),
+        "factors": sum(d_in * (d_in + 1) * m + d_out * (d_out + 1) * m for _, d_in, d_out, m, _ in built),
         # inverse mode: Cholesky n^3/3 + triangular inverse n^3/3 (the optimizer keeps
         # A^-1 = X^T X factored, so potri's X^T X product is not part of the step)
         "inversion": sum((2.0 / 3.0) * (float(d_in) ** 3 + float(d_out) ** 3) for _, d_in, d_out, m, _ in own)
@@ -341,7 +345,7 @@ def run_ours(args, rank, world, local_rank):
     e2e = None
     if not args.no_e2e:
         k_e2e = args.e2e_steps or args.steps
-        for ly in kf.owned:
+        for ly in capt:
             ly.a_in = ly.g_out = None
         del saved_caps, saved_grads
 
@@ -397,7 +401,7 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": f"{args.model} DP-KFAC 2nd-order update, batch {batch}/GPU, "
                                    f"inv_type={args.inv_type}, gamma={args.gamma}, xi={args.xi}, F=K=1",
                        "model": args.model, "global_batch": batch * world, "parallelism": f"dp{world}",
-                       "assignment": args.assignment,
+                       "assignment": args.assignment, "algorithm": args.algorithm,
                        "memory_format": "channels_last" if mf is torch.channels_last else "contiguous",
                        "l2": "inputs (layer captures, >1.4 GB) larger than L2; no flush"},
             "overlap": overlap, "ms_per_step_serialized": ms_serial,

@@ -170,3 +170,60 @@ def dp_kfac_step(cl: Cluster, shards, h: Hyper, lr: float, mu: float, t: int):
         cl.momenta[i] += pre[i]
         cl.weights[i] -= lr * cl.momenta[i]
     return float(np.mean(losses)), pre
+
+
+def build_mpd_cluster(spec: MlpSpec, workers: int, seed: int, assignment=None) -> Cluster:
+    """MPD variants keep averaged factors for EVERY layer on every worker (distsim.py:155-156)."""
+    cl = build_cluster(spec, workers, seed, assignment)
+    cl.states = [{i: LayerState() for i in range(spec.depth)} for _ in range(workers)]
+    return cl
+
+
+def mpd_kfac_step(cl: Cluster, shards, h: Hyper, lr: float, mu: float, t: int, variant: str = "co"):
+    """Model-parallel D-KFAC (distsim.py:341-420): raw local factors of every layer,
+    averaged over workers (tree mean), running average on every worker; the owner
+    refreshes; "co" broadcasts the decomposition and every worker preconditions
+    every layer, "mo" preconditions at the owner and broadcasts the result.  Both
+    leave identical replicas, so one weight copy is updated here."""
+    from .kfac_ref import apply_preconditioner, compute_factors, factor_due, inverse_due, refresh_inverses, \
+        update_running_average
+    import copy
+    if variant not in ("co", "mo"):
+        raise OracleArgumentError(f"unknown mpd variant {variant!r}")
+    P, L = cl.workers, cl.spec.depth
+    losses, caps, locgrads = [], [], []
+    for x, y in shards:
+        loss, ins, pgs, gs = forward_backward(cl.spec, cl.weights, x, y)
+        losses.append(loss)
+        caps.append((ins, pgs))
+        locgrads.append(gs)
+    agg = [tree_mean([locgrads[p][i] for p in range(P)]) for i in range(L)]
+    if factor_due(t, h):
+        raw = [[compute_factors(caps[p][0][i], caps[p][1][i]) for i in range(L)] for p in range(P)]
+        for i in range(L):
+            a_avg = tree_mean([raw[p][i][0] for p in range(P)])
+            g_avg = tree_mean([raw[p][i][1] for p in range(P)])
+            for p in range(P):
+                update_running_average(cl.states[p][i], a_avg, g_avg, h.xi, t)
+    owner = {i: p for p, part in enumerate(cl.assignment) for i in part}
+    if inverse_due(t, h):
+        for i in range(L):
+            st = cl.states[owner[i]][i]
+            refresh_inverses(st, h, t)
+            if variant == "co":
+                for p in range(P):
+                    if p != owner[i]:
+                        d = cl.states[p][i]
+                        d.a_eig, d.g_eig = copy.deepcopy(st.a_eig), copy.deepcopy(st.g_eig)
+                        d.a_damped_inv = None if st.a_damped_inv is None else st.a_damped_inv.copy()
+                        d.g_damped_inv = None if st.g_damped_inv is None else st.g_damped_inv.copy()
+                        d.last_inverse_update = t
+    if variant == "co":
+        pre = {i: apply_preconditioner(cl.states[0][i], agg[i], h) for i in range(L)}
+    else:
+        pre = {i: apply_preconditioner(cl.states[owner[i]][i], agg[i], h) for i in range(L)}
+    for i in range(L):
+        cl.momenta[i] *= mu
+        cl.momenta[i] += pre[i]
+        cl.weights[i] -= lr * cl.momenta[i]
+    return float(np.mean(losses)), pre

@@ -5,11 +5,12 @@ Public surface:
   * ``kfac``                        -- functional mirror of kfaclab kfac.py / numerics.py on CUDA tensors
   * ``partition``                   -- reference round-robin partition + the LPT balancer
   * ``errors``                      -- reference exception classes
+  * ``checkpoint``                  -- per-rank factor-state checkpoints in the reference KFACLAB\0 v1 layout
 The arithmetic lives in ``libdpkfac.so`` (csrc/, sm_100a); see include/dpkfac.h.
 """
 
 from . import errors, partition
-from .errors import ArgumentError, KfacLabError, NumericError, OrderingError, ShapeError
+from .errors import ArgumentError, DataFormatError, KfacLabError, NumericError, OrderingError, ShapeError
 from .kfac import EigenPair, FactorState, KfacHyper
 from .partition import balanced_partition, round_robin_partition, validate_partition
 
@@ -21,7 +22,7 @@ def __getattr__(name):
     if name == "DPKFAC":
         from .dpkfac import DPKFAC
         return DPKFAC
-    if name in ("kfac", "ops", "dpkfac"):
+    if name in ("kfac", "ops", "dpkfac", "checkpoint"):
         import importlib
         return importlib.import_module(f".{name}", __name__)
     raise AttributeError(name)

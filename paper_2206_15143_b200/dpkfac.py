@@ -193,8 +193,19 @@ class DPKFAC:
                  assignment: Union[str, Sequence[Sequence[int]]] = "round_robin",
                  process_group=None, precision: str = "tf32", precond_precision: str = "3xtf32",
                  grad_scale: Union[str, float] = "batch", check_numerics: Union[bool, str] = True,
-                 im2col: str = "materialize", overlap: bool = True, early: bool = False):
+                 im2col: str = "materialize", overlap: bool = True, early: bool = False,
+                 algorithm: str = "dp_kfac"):
         self.hyper = KfacHyper(gamma=gamma, xi=xi, inv_type=inv_type, f_freq=f_freq, k_freq=k_freq)
+        # dp_kfac: the product.  mpd_kfac_co / mpd_kfac_mo: the paper's model-parallel
+        # comparators (KAISA COMM-OPT / MEM-OPT, distsim.mpd_kfac_step distsim.py:341-420)
+        # on the same kernels: every rank builds every layer's factors from its local
+        # batch, the factors are all-reduced (the traffic DP-KFAC removes), owners
+        # invert; co broadcasts the decompositions and everyone preconditions every
+        # layer, mo preconditions at the owner and all-gathers (DP-KFAC's exchange).
+        if algorithm not in ("dp_kfac", "mpd_kfac_co", "mpd_kfac_mo"):
+            raise ArgumentError(f"unknown algorithm {algorithm!r}")
+        self.algorithm = algorithm
+        self.mpd = algorithm != "dp_kfac"
         # "auto": implicit (tiled-TMA tap boxes) for channels-last convs with C % 32 == 0,
         # a materialized patch matrix otherwise (e.g. the 3-channel stem conv).
         # Default "materialize": the sample-blocked tap boxes measured slower (factor
@@ -291,7 +302,7 @@ class DPKFAC:
     # ------------------------------------------------------------ hooks
     def _make_pre_hook(self, ly: _Layer):
         def hook(module, inputs):
-            if self._capturing and ly.owned and torch.is_grad_enabled():
+            if self._capturing and (ly.owned or self.mpd) and torch.is_grad_enabled():
                 x = inputs[0]
                 ly.a_in = x.detach()
                 ly.batch = x.shape[0]
@@ -299,7 +310,7 @@ class DPKFAC:
 
     def _make_fwd_hook(self, ly: _Layer):
         def hook(module, inputs, output):
-            if self._capturing and ly.owned and torch.is_grad_enabled() and output.requires_grad:
+            if self._capturing and (ly.owned or self.mpd) and torch.is_grad_enabled() and output.requires_grad:
                 def grab(g, ly=ly):
                     ly.g_out = g.detach()
                     if self._hook_classes is not None:
@@ -317,7 +328,7 @@ class DPKFAC:
         mine = set(self.assignment[self.rank])
         for ly in self.layers:
             ly.owned = ly.index in mine
-            if not ly.owned:
+            if not ly.owned and not self.mpd:
                 ly.a_in = ly.g_out = None
         self.owned = [self.layers[i] for i in sorted(mine)]
         for k, ly in enumerate(self.owned):
@@ -342,13 +353,17 @@ class DPKFAC:
         self.layout = OwnerMajorLayout(self.assignment, [ly.n_grad for ly in self.layers])
         self.xchg = OwnerMajorExchange(self.layout, self.rank, dev, self.pg)
         self.offsets = self.layout.offsets
+        if self.algorithm == "mpd_kfac_co":  # every layer's mean gradient on every rank
+            self._co_layout = OwnerMajorLayout([tuple(range(len(self.layers)))], [ly.n_grad for ly in self.layers])
+            self._co_xchg = OwnerMajorExchange(self._co_layout, 0, dev, None)
         n_own = len(self.owned)
         self.info = torch.zeros(max(len(self.layers), 1), dtype=torch.int32, device=dev)  # zeroed after each step
         self.shifts = torch.zeros(max(n_own, 1), 2, device=dev)
         self.pis = torch.zeros(max(n_own, 1), device=dev)
         self._bufs_ready = True
 
-    def _segments(self, which: str):
+    def _segments(self, which: str, offsets=None):
+        offsets = self.offsets if offsets is None else offsets
         segs = []
         for ly in self.layers:
             w = ly.module.weight
@@ -359,7 +374,7 @@ class DPKFAC:
                 wt, bt = w.grad, (b.grad if b is not None else None)
                 if b is not None and bt is None:
                     raise OrderingError(f"layer {ly.index} ({ly.name}) bias has no gradient")
-            off = self.offsets[ly.index]
+            off = offsets[ly.index]
             segs.append(ops.segment(wt, bt, off, tap_major=ly.tap_major))
         return segs
 
@@ -373,6 +388,8 @@ class DPKFAC:
             self._finalize_balance()
         if not self._bufs_ready:
             self._build_buffers()
+        if self.mpd:
+            return self._step_mpd()
         for ly in self.layers:  # dense grads (NCHW or channels_last) so packing is a plain/permuted copy
             gr = ly.module.weight.grad
             if gr is not None and not gr.is_contiguous() and not (
@@ -561,12 +578,12 @@ class DPKFAC:
             ly.holds = h.inv_type
             ly.last_inverse_update = t
 
-    def _precondition_stage(self, layers):
+    def _precondition_stage(self, layers, xchg=None):
         """A10/A11 for ``layers`` on the reduce-scattered mean gradients."""
         h = self.hyper
         if not layers:
             return
-        X = self.xchg
+        X = self.xchg if xchg is None else xchg
         pj = []
         for ly in layers:
             if ly.holds != h.inv_type:
@@ -583,6 +600,154 @@ class DPKFAC:
             ops.precondition(pj, True, h.gamma, self.precond_precision)
         else:
             ops.precondition_factored(pj, self.precond_precision)
+
+    # ------------------------------------------------------------ MPD-KFAC comparators
+    def _step_mpd(self):
+        """distsim.mpd_kfac_step (distsim.py:341-420) on the B200 kernels, one stream."""
+        h, t, P = self.hyper, self.t, self.world
+        for ly in self.layers:
+            gr = ly.module.weight.grad
+            if gr is not None and not gr.is_contiguous() and not (
+                    gr.dim() == 4 and gr.is_contiguous(memory_format=torch.channels_last)):
+                ly.module.weight.grad = gr.contiguous()
+        self._mark("start")
+        if t % h.f_freq == 0:
+            self._mpd_factors(t)
+        self._mark("factors")
+        if t % h.k_freq == 0:
+            self._inverse_stage(self.owned, t, True)
+            if self.algorithm == "mpd_kfac_co":
+                self._mpd_broadcast_decompositions(t)
+        self._mark("inversion")
+        if self.algorithm == "mpd_kfac_co":
+            # every worker preconditions every layer from its own (identical) state
+            X = self._co_xchg
+            segs = self._segments("grad", self._co_layout.offsets)
+            ops.pack(segs, X.flat, 1.0 / P)
+            if P > 1:
+                dist.all_reduce(X.flat, op=dist.ReduceOp.SUM, group=self.pg)
+                if self.other_params:
+                    self._allreduce_others()
+            self._mark("comm_rs")
+            self._precondition_stage(self.layers, X)
+            self._mark("precondition")
+            self._check_info()
+            ops.unpack(segs, X.out_flat, 1.0)
+        else:  # mo: owner preconditions, preconditioned gradients are gathered (predcomm)
+            X = self.xchg
+            segs = self._segments("grad")
+            ops.pack(segs, X.flat, 1.0 / P)
+            X.reduce_scatter()
+            if P > 1 and self.other_params:
+                self._allreduce_others()
+            self._mark("comm_rs")
+            self._precondition_stage(self.owned)
+            self._mark("precondition")
+            self._check_info()
+            X.all_gather()
+            ops.unpack(segs, X.out_flat, 1.0)
+        self._mark("comm_ag")
+        self.info.zero_()
+        self.t += 1
+
+    def _check_info(self):
+        if self.check_numerics == "sync":
+            host = self._gather_info().cpu()
+            self.info.zero_()
+            self._raise_from_host(host)
+        elif self.check_numerics == "deferred":
+            if self._pending_info is not None:
+                self.check()
+            host = torch.empty(self.info.shape, dtype=torch.int32, pin_memory=True)
+            host.copy_(self._gather_info(), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record()
+            self._pending_info = (host, ev)
+
+    def _mpd_factors(self, t):
+        """Raw local factors of EVERY layer (one grouped SYRK, alpha folds the 1/P of
+        the average), a SUM all-reduce of all of them (factorcomm), then the running
+        average F <- xi F_avg + (1 - xi) F (kfac.update_running_average)."""
+        h, P = self.hyper, self.world
+        dev = self.device
+        if getattr(self, "_mpd_F", None) is None:
+            sizes = [ly.d_in * ly.d_in + ly.d_out * ly.d_out for ly in self.layers]
+            total = sum(sizes)
+            self._mpd_F = torch.zeros(total, device=dev)
+            self._mpd_T = torch.zeros(total, device=dev)
+            self._mpd_views = []
+            off = 0
+            for ly in self.layers:
+                na, ng = ly.d_in * ly.d_in, ly.d_out * ly.d_out
+                ly.a_cov = self._mpd_F[off:off + na].view(ly.d_in, ly.d_in)
+                ly.g_cov = self._mpd_F[off + na:off + na + ng].view(ly.d_out, ly.d_out)
+                self._mpd_views.append((self._mpd_T[off:off + na].view(ly.d_in, ly.d_in),
+                                        self._mpd_T[off + na:off + na + ng].view(ly.d_out, ly.d_out)))
+                off += na + ng
+        jobs, patches = [], []
+        for ly, (ta, tg) in zip(self.layers, self._mpd_views):
+            if ly.a_in is None or ly.g_out is None:
+                raise ArgumentError(f"worker {self.rank}, layer {ly.index}: captured inputs must be a "
+                                    "nonempty d x B matrix (run forward and backward before step())")
+            oa, pending = ly.operand_a(self.im2col)
+            og = ly.operand_g()
+            if pending is not None:
+                patches.append(pending)
+            m = oa.cols
+            if og.cols != m:
+                raise ArgumentError(f"worker {self.rank}, layer {ly.index}: capture batch counts differ: "
+                                    f"{m} inputs vs {og.cols} gradients")
+            s = float(ly.batch) if self.grad_scale == "batch" else float(self.grad_scale)
+            jobs.append(ops.factor_job(oa, ta, 1.0 / (m * P), 0.0))
+            jobs.append(ops.factor_job(og, tg, s * s / (m * P), 0.0))
+        ops.im2col_materialize(patches)
+        ops.syrk_ema(jobs, self.precision, device=dev)
+        if P > 1:
+            dist.all_reduce(self._mpd_T, op=dist.ReduceOp.SUM, group=self.pg)
+        if not self.layers[0].initialized:
+            self._mpd_F.copy_(self._mpd_T)
+        else:
+            self._mpd_F.lerp_(self._mpd_T, h.xi)
+        for ly in self.layers:
+            ly.initialized = True
+            ly.last_factor_update = t
+            ly.a_in = ly.g_out = None
+
+    def _decomposition_tensors(self, ly):
+        if self.hyper.inv_type == "eigen":
+            return [ly.a_q, ly.a_w, ly.g_q, ly.g_w]
+        return [ly.a_x._base if ly.a_x._base is not None else ly.a_x,
+                ly.g_x._base if ly.g_x._base is not None else ly.g_x]
+
+    def _mpd_broadcast_decompositions(self, t):
+        """COMM-OPT: every owner's eigenbases+eigenvalues (or damped inverses, held
+        as their factors X = L^-1) reach every worker (distsim._broadcast_decomposition,
+        distsim.py:423-458) -- one all-gather of an owner-major buffer."""
+        h, P = self.hyper, self.world
+        for ly in self.layers:
+            ly.alloc_state(h.inv_type, self.device)
+        if P > 1:
+            if getattr(self, "_dec_xchg", None) is None:
+                sizes = [sum(x.numel() for x in self._decomposition_tensors(ly)) for ly in self.layers]
+                self._dec_layout = OwnerMajorLayout(self.assignment, sizes)
+                self._dec_xchg = OwnerMajorExchange(self._dec_layout, self.rank, self.device, self.pg)
+            L_, X = self._dec_layout, self._dec_xchg
+            for ly in self.owned:
+                off = L_.local_offset(ly.index, self.rank)
+                for x in self._decomposition_tensors(ly):
+                    X.chunk_out[off:off + x.numel()].copy_(x.reshape(-1))
+                    off += x.numel()
+            X.all_gather()
+            for ly in self.layers:
+                if ly.owned:
+                    continue
+                off = L_.offsets[ly.index]
+                for x in self._decomposition_tensors(ly):
+                    x.view(-1).copy_(X.out_flat[off:off + x.numel()])
+                    off += x.numel()
+        for ly in self.layers:
+            ly.holds = h.inv_type
+            ly.last_inverse_update = t
 
     # ------------------------------------------------------------ stage timing (CUDA events)
     def enable_stage_timing(self, on: bool = True):

@@ -261,3 +261,108 @@ def test_channels_last_model_tap_major_factors_match_reference(inv_type):
         assert rel(sd["layers"][i]["a_cov"].double().cpu().numpy(), states[name].a_cov) <= TOL
     for hk in hooks:
         hk.remove()
+
+
+@pytest.mark.parametrize("inv_type", ["inverse", "eigen"])
+def test_kfaclab_checkpoint_matches_reference_cluster_and_resumes(inv_type, tmp_path):
+    """checkpoint.save writes the reference's v1 layout (trainer.py:218-271) with the
+    values the reference cluster holds after the same steps; checkpoint.load resumes."""
+    from paper_2206_15143_b200 import DPKFAC
+    from paper_2206_15143_b200 import checkpoint as C
+    dev = torch.device("cuda", 0)
+    spec = MLP.MlpSpec((24, 20, 12, 6), "relu", "softmax_cross_entropy", True)
+    h = K.Hyper(gamma=0.05, xi=0.9, inv_type=inv_type, f_freq=1, k_freq=1)
+    cl = MLP.build_cluster(spec, 1, seed=3)
+    model, lins = torch_mlp([w.copy() for w in cl.weights], dev)
+    kf = DPKFAC(model, gamma=0.05, xi=0.9, inv_type=inv_type, precision="3xtf32")
+    opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9)
+    rng = np.random.default_rng(8)
+    data = [(rng.standard_normal((24, 32)), rng.integers(0, 6, size=32)) for _ in range(4)]
+
+    def one(kf, model, opt, t):
+        x, y = data[t]
+        opt.zero_grad()
+        F.cross_entropy(model(torch.from_numpy(x.T.copy()).float().to(dev)), torch.from_numpy(y).to(dev)).backward()
+        kf.step()
+        opt.step()
+
+    for t in range(2):
+        MLP.dp_kfac_step(cl, MLP.shard(*data[t], 1), h, 0.1, 0.9, t)
+        one(kf, model, opt, t)
+    path = tmp_path / "rank0.bin"
+    meta = C.save(path, kf, optimizer=opt, epoch=0, exact_factors=False)
+    assert meta == {"iteration": 2, "epoch": 0, "algorithm": "dp_kfac", "workers": 1,
+                    "factor_states": {f"worker0/layer{i}": {"initialized": True, "last_factor_update": 1,
+                                                            "last_inverse_update": 1} for i in range(3)}}
+    m2, arrays = C.read(path)
+    for i in range(3):
+        assert rel(arrays[f"layer{i}/weight"], cl.weights[i]) <= 1e-4
+        assert rel(arrays[f"layer{i}/momentum"], cl.momenta[i]) <= TOL
+        st = cl.states[0][i]
+        assert rel(arrays[f"worker0/layer{i}/a_cov"], st.a_cov) <= TOL
+        assert rel(arrays[f"worker0/layer{i}/g_cov"], st.g_cov) <= TOL
+        if inv_type == "inverse":
+            assert rel(arrays[f"worker0/layer{i}/a_damped_inv"], st.a_damped_inv) <= TOL
+            assert rel(arrays[f"worker0/layer{i}/g_damped_inv"], st.g_damped_inv) <= TOL
+        else:
+            assert rel(arrays[f"worker0/layer{i}/a_eig_v"], st.a_eig.values) <= TOL
+            assert rel(arrays[f"worker0/layer{i}/g_eig_v"], st.g_eig.values) <= TOL
+    # exact resume from a checkpoint that carries the held factors
+    C.save(path, kf, optimizer=opt, epoch=0)
+    model2, _ = torch_mlp([w.copy() for w in cl.weights], dev)  # weights come from the file
+    kf2 = DPKFAC(model2, gamma=0.05, xi=0.9, inv_type=inv_type, precision="3xtf32")
+    opt2 = torch.optim.SGD(model2.parameters(), lr=0.1, momentum=0.9)
+    C.load(path, kf2, optimizer=opt2)
+    assert kf2.t == 2
+    for t in range(2, 4):
+        one(kf, model, opt, t)
+        one(kf2, model2, opt2, t)
+        for a, b in zip(model.parameters(), model2.parameters()):
+            assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("algorithm,inv_type", [("mpd_kfac_co", "inverse"), ("mpd_kfac_mo", "inverse"),
+                                                ("mpd_kfac_co", "eigen")])
+def test_mpd_comparators_match_reference_single_worker(algorithm, inv_type):
+    """MPD-KFAC comparators (distsim.mpd_kfac_step) through the same kernels; at P=1
+    they must also equal DP-KFAC (reference test_distsim.py:178-186)."""
+    from paper_2206_15143_b200 import DPKFAC
+    dev = torch.device("cuda", 0)
+    spec = MLP.MlpSpec((20, 16, 12, 5), "relu", "softmax_cross_entropy", True)
+    h = K.Hyper(gamma=0.05, xi=0.9, inv_type=inv_type, f_freq=1, k_freq=2)
+    cl = MLP.build_mpd_cluster(spec, 1, seed=5)
+    model, lins = torch_mlp([w.copy() for w in cl.weights], dev)
+    kf = DPKFAC(model, gamma=0.05, xi=0.9, inv_type=inv_type, k_freq=2, precision="3xtf32", algorithm=algorithm)
+    opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9)
+    rng = np.random.default_rng(91)
+    for t in range(4):
+        x, y = rng.standard_normal((20, 16)), rng.integers(0, 5, size=16)
+        _, pre = MLP.mpd_kfac_step(cl, MLP.shard(x, y, 1), h, 0.1, 0.9, t, algorithm[-2:])
+        opt.zero_grad()
+        F.cross_entropy(model(torch.from_numpy(x.T.copy()).float().to(dev)), torch.from_numpy(y).to(dev)).backward()
+        kf.step()
+        for i, lin in enumerate(lins):
+            got = torch.cat([lin.weight.grad, lin.bias.grad[:, None]], 1).double().cpu().numpy()
+            assert rel(got, pre[i]) <= TOL, (t, i, rel(got, pre[i]))
+        opt.step()
+    for i, lin in enumerate(lins):
+        got = torch.cat([lin.weight, lin.bias[:, None]], 1).detach().double().cpu().numpy()
+        assert rel(got, cl.weights[i]) <= 1e-4
+
+
+def test_multi_gpu_dp_and_mpd_match_reference():
+    """P=2 (and P=4 when present): torchrun over NCCL, every algorithm vs the
+    oracle's multi-worker step (scripts/multi_gpu_parity.py)."""
+    import os
+    import subprocess
+    import sys
+    n = torch.cuda.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for p in sorted({2, min(n, 4)}):
+        r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={p}",
+                            "--master-addr", "127.0.0.1", "--master-port", str(29600 + p),
+                            os.path.join(root, "scripts", "multi_gpu_parity.py")],
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0 and "PARITY OK" in r.stdout, (p, r.stdout[-2000:], r.stderr[-2000:])

@@ -133,3 +133,21 @@ def test_unfold_matches_torch():
         t = F.unfold(torch.from_numpy(x), kh, padding=p, stride=s)  # N, C*k*k, L
         want = t.permute(1, 0, 2).reshape(t.shape[1], -1).numpy()
         assert np.array_equal(cols, want)
+
+
+@pytest.mark.parametrize("workers,variant,inv", [(2, "co", "inverse"), (2, "mo", "inverse"), (4, "co", "eigen"),
+                                                 (2, "mo", "eigen"), (1, "co", "inverse")])
+def test_mlp_mpd_kfac_matches_reference(workers, variant, inv):
+    z = _load("mlp_mpd.npz")
+    spec = MLP.MlpSpec((20, 16, 12, 5), "relu", "softmax_cross_entropy", True)
+    h = K.Hyper(gamma=0.05, xi=0.9, inv_type=inv, f_freq=1, k_freq=2)
+    cl = MLP.build_mpd_cluster(spec, workers, seed=5)
+    losses = []
+    for t in range(4):
+        x, y = z[f"batch/{t}/x"], z[f"batch/{t}/y"]
+        loss, _ = MLP.mpd_kfac_step(cl, MLP.shard(x, y, workers), h, 0.1, 0.9, t, variant)
+        losses.append(loss)
+    key = f"run/{workers}/{variant}/{inv}"
+    _close(np.array(losses), z[key + "/losses"], 1e-12)
+    for i in range(3):
+        _close(cl.weights[i], z[key + f"/w{i}"], 1e-10)
