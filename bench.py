@@ -51,7 +51,10 @@ def parse():
     ap.add_argument("--precision", default="tf32", choices=["tf32", "3xtf32"])
     ap.add_argument("--nchw", action="store_true",
                     help="keep the conv model NCHW (default: channels_last, the B200-native layout)")
-    ap.add_argument("--assignment", default="round_robin")
+    # north_star: "layers are assigned to GPUs by a load balancer" -> the LPT balancer
+    # (SURVEY 8(f)1); "round_robin" is the reference's bit-exact default partition
+    ap.add_argument("--assignment", default="balanced")
+    ap.add_argument("--im2col", default="materialize", choices=["materialize", "auto", "implicit"])
     ap.add_argument("--algorithm", default="dp_kfac", choices=["dp_kfac", "mpd_kfac_co", "mpd_kfac_mo"],
                     help="dp_kfac (the product) or the paper's MPD-KFAC comparators on the same kernels")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -211,7 +214,7 @@ def run_ours(args, rank, world, local_rank):
         model = model.to(memory_format=mf)
     kf = DPKFAC(model, gamma=args.gamma, xi=args.xi, inv_type=args.inv_type, f_freq=1, k_freq=1,
                 assignment=args.assignment, precision=args.precision, check_numerics="deferred",
-                overlap=not args.no_overlap, early=False, algorithm=args.algorithm)  # captures are replayed below; e2e turns early on
+                overlap=not args.no_overlap, early=False, algorithm=args.algorithm, im2col=args.im2col)  # captures are replayed below; e2e turns early on
     opt = torch.optim.SGD(model.parameters(), lr=1e-3, momentum=0.9)
     gen = torch.Generator().manual_seed(1234 + rank)
     x_host = torch.randn(batch, *shape, generator=gen)
@@ -401,7 +404,7 @@ def run_ours(args, rank, world, local_rank):
             "config": {"workload": f"{args.model} DP-KFAC 2nd-order update, batch {batch}/GPU, "
                                    f"inv_type={args.inv_type}, gamma={args.gamma}, xi={args.xi}, F=K=1",
                        "model": args.model, "global_batch": batch * world, "parallelism": f"dp{world}",
-                       "assignment": args.assignment, "algorithm": args.algorithm,
+                       "assignment": args.assignment, "algorithm": args.algorithm, "im2col": args.im2col,
                        "memory_format": "channels_last" if mf is torch.channels_last else "contiguous",
                        "l2": "inputs (layer captures, >1.4 GB) larger than L2; no flush"},
             "overlap": overlap, "ms_per_step_serialized": ms_serial,

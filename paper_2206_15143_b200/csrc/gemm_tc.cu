@@ -101,7 +101,7 @@ struct alignas(64) Problem {
   int unit_begin;
   int tma_a, tma_b;
   int slab_cpn;     // TMA_SLAB: chunks per sample (K index = (sample, 32-pixel chunk));
-                    // TMA_TAPS: wb | group boxes << 8 | sample blocks << 16
+                    // TMA_TAPS: wb | hb << 6 | group boxes << 12 | sample blocks << 16
   int tri_a, tri_b; // TRI_*: per-tile K clipping for triangular operands
   int order;        // tile visiting order (non-symmetric): 0 row-major, 1 row-major reversed,
                     // 2 column-major, 3 column-major reversed -- heaviest K ranges first
@@ -437,20 +437,27 @@ __device__ __forceinline__ void issue_tma(int kind, const CUtensorMap* map, cons
     else
       tma_load_3d(dst, map, bar, (kc - n * cpn) * BK, row0, n);
   } else if (kind == TMA_TAPS) {
-    // K chunk kc = (oh, output-column block, sample block); rows (i, j, c)
-    const int wb = cpn & 0xFF, g = (cpn >> 8) & 0xFF, nblk = cpn >> 16;
-    const int owbs = o.OW / wb;
-    const int q = kc / nblk;
-    const int nb = kc - q * nblk;
-    const int oh = q / owbs;
-    const int owb = q - oh * owbs;
-    const int w0 = owb * wb * o.sw - o.pw, h0 = oh * o.sh - o.ph, n0 = nb * (32 / wb);
-    for (int b = 0; b < BM / 32; b += g) {
+    // K chunk kc = (sample block, output-row block, output-column block); rows (i, j, c)
+    const int wb = cpn & 0x3F, hb = (cpn >> 6) & 0x3F, g = (cpn >> 12) & 0xF, nbs = 32 / (wb * hb);
+    const int owbs = o.OW / wb, ohbs = o.OH / hb;
+    const int q = kc / owbs;
+    const int owb = kc - q * owbs;
+    const int nbk = q / ohbs;
+    const int ohb = q - nbk * ohbs;
+    const int w0 = owb * wb * o.sw - o.pw, h0 = ohb * hb * o.sh - o.ph, n0 = nbk * nbs;
+    for (int b = 0; b < BM / 32; b += (g == 0 ? 1 : g)) {
       const int r = row0 + 32 * b;
       if (r >= o.rows) break;
       const int tap = r / o.C;
       const int c0 = r - tap * o.C;
       const int i = tap / o.kw, j = tap - (tap / o.kw) * o.kw;
+      if (g == 0) {  // 4-D map {C, W, H, N}: one 32-channel box per row group
+        if (PAIR)
+          tma_load_4d_pair(dst + b * 4096, map, bar, c0, w0 + j * o.dw, h0 + i * o.dh, n0);
+        else
+          tma_load_4d(dst + b * 4096, map, bar, c0, w0 + j * o.dw, h0 + i * o.dh, n0);
+        continue;
+      }
       if (PAIR)
         tma_load_5d_pair(dst + b * 4096, map, bar, 0, w0 + j * o.dw, h0 + i * o.dh, n0, c0 >> 5);
       else
@@ -1343,11 +1350,14 @@ bool plan_tma_im2col(const dpk_operand& o, CUtensorMap* m, bool rn) {
   return r == CUDA_SUCCESS;
 }
 
-// TMA_TAPS geometry: (wb output columns) x (32 / wb samples) per K chunk, the
-// widest sample block that divides the batch (else 32 with zero-filled tail
-// samples); group boxes of 4/2/1 x 32 channels (a box never crosses a tap).
+// TMA_TAPS geometry: a K chunk is 32 output pixels = wb columns x hb rows of one
+// output image block x nb samples (wb | OW, hb | OH exactly -- an invented pixel
+// past the image edge could still read real input at a shifted tap; the sample
+// tail is safe: samples >= N are TMA zero fill for every tap).  The widest
+// spatial block wins (consecutive pixels are contiguous NHWC rows, so a box is a
+// few dense DRAM runs); group boxes of 4/2/1 x 32 channels never cross a tap.
 struct TapsGeom {
-  int wb, nb, nblk, g;
+  int wb, hb, nb, nblk, g;
   int64_t chunks;
 };
 
@@ -1360,44 +1370,71 @@ bool taps_disabled() {  // DPK_TAPS=0: keep TMA im2col mode / the gather path
   return v == 1;
 }
 
+bool taps_4d();
 bool taps_eligible(const dpk_operand& o, TapsGeom* tg = nullptr) {
   if (o.kind != DPK_OPND_IM2COL_TAPMAJOR || o.bias_row || tma_disabled() || taps_disabled()) return false;
   if (o.C % 32 != 0 || o.sc != 1 || !aligned16(o.data)) return false;
   if ((o.sws * 4) % 16 != 0 || (o.shs * 4) % 16 != 0 || (o.sn * 4) % 16 != 0) return false;
-  if (o.sw > 8 || o.OW < 1 || o.OH < 1) return false;
+  if (o.sw > 8 || o.sh > 8 || o.OW < 1 || o.OH < 1) return false;
   const int64_t hw = static_cast<int64_t>(o.OH) * o.OW;
   if (o.cols % hw != 0) return false;
   const int64_t n = o.cols / hw;
-  int wb = 1;
-  if (n % 32 != 0) {
-    for (int c = 2; c <= 8; c *= 2)
-      if (n % (32 / c) == 0 && o.OW % c == 0) {
-        wb = c;
-        break;
+  int bw = 1, bh = 1;
+  for (int wb = 32; wb >= 1; wb /= 2) {
+    if (o.OW % wb != 0 || wb * o.sw > 256) continue;
+    for (int hb = 32 / wb; hb >= 1; hb /= 2) {
+      if (o.OH % hb != 0 || hb * o.sh > 256) continue;
+      if (wb * hb > bw * bh) {
+        bw = wb;
+        bh = hb;
       }
+      break;
+    }
   }
-  if (wb * o.sw > 256) return false;
   if (tg) {
-    tg->wb = wb;
-    tg->nb = 32 / wb;
+    tg->wb = bw;
+    tg->hb = bh;
+    tg->nb = 32 / (bw * bh);
     tg->nblk = static_cast<int>((n + tg->nb - 1) / tg->nb);
-    tg->g = o.C % 128 == 0 ? 4 : o.C % 64 == 0 ? 2 : 1;
-    tg->chunks = static_cast<int64_t>(o.OH) * (o.OW / wb) * tg->nblk;
+    tg->g = taps_4d() ? 0 : o.C % 128 == 0 ? 4 : o.C % 64 == 0 ? 2 : 1;
+    tg->chunks = static_cast<int64_t>(o.OH / bh) * (o.OW / bw) * tg->nblk;
   }
-  return true;
+  return tg == nullptr || tg->nblk < 65536;
+}
+
+bool taps_4d() {  // DPK_TAPS4D=1: 4-D maps {C, W, H, N}, one box per 32-row group
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DPK_TAPS4D");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
 }
 
 bool plan_tma_taps(const dpk_operand& o, const TapsGeom& tg, CUtensorMap* m, bool rn) {
   EncodeTiledFn fn = encoder();
   if (!fn) return false;
   const int64_t n = o.cols / (static_cast<int64_t>(o.OH) * o.OW);
+  if (tg.g == 0) {
+    const cuuint64_t dims[4] = {static_cast<cuuint64_t>(o.C), static_cast<cuuint64_t>(o.W),
+                                static_cast<cuuint64_t>(o.H), static_cast<cuuint64_t>(n)};
+    const cuuint64_t strides[3] = {static_cast<cuuint64_t>(o.sws) * 4, static_cast<cuuint64_t>(o.shs) * 4,
+                                   static_cast<cuuint64_t>(o.sn) * 4};
+    const cuuint32_t box[4] = {32, static_cast<cuuint32_t>(tg.wb * o.sw), static_cast<cuuint32_t>(tg.hb * o.sh),
+                               static_cast<cuuint32_t>(tg.nb)};
+    const cuuint32_t es[4] = {1, static_cast<cuuint32_t>(o.sw), static_cast<cuuint32_t>(o.sh), 1};
+    return fn(m, rn ? CU_TENSOR_MAP_DATA_TYPE_TFLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+              const_cast<float*>(o.data), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
   const cuuint64_t dims[5] = {32, static_cast<cuuint64_t>(o.W), static_cast<cuuint64_t>(o.H),
                               static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(o.C / 32)};
   const cuuint64_t strides[4] = {static_cast<cuuint64_t>(o.sws) * 4, static_cast<cuuint64_t>(o.shs) * 4,
                                  static_cast<cuuint64_t>(o.sn) * 4, 128};
-  const cuuint32_t box[5] = {32, static_cast<cuuint32_t>(tg.wb == 1 ? 1 : tg.wb * o.sw), 1,
+  const cuuint32_t box[5] = {32, static_cast<cuuint32_t>(tg.wb * o.sw), static_cast<cuuint32_t>(tg.hb * o.sh),
                              static_cast<cuuint32_t>(tg.nb), static_cast<cuuint32_t>(tg.g)};
-  const cuuint32_t es[5] = {1, static_cast<cuuint32_t>(tg.wb == 1 ? 1 : o.sw), 1, 1, 1};
+  const cuuint32_t es[5] = {1, static_cast<cuuint32_t>(o.sw), static_cast<cuuint32_t>(o.sh), 1, 1};
   return fn(m, rn ? CU_TENSOR_MAP_DATA_TYPE_TFLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(o.data),
             dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
@@ -1481,7 +1518,7 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
     TapsGeom tg;
     if (P.same_ab && taps_eligible(j.a, &tg)) {
       P.chunks = static_cast<int>(tg.chunks);
-      P.slab_cpn = tg.wb | (tg.g << 8) | (tg.nblk << 16);
+      P.slab_cpn = tg.wb | (tg.hb << 6) | (tg.g << 12) | (tg.nblk << 16);
       if (with_maps) {
         if (!plan_tma_taps(j.a, tg, &P.tmap_a, rn)) {
           set_error("dpk_gemm: cuTensorMapEncodeTiled rejected the implicit-im2col (taps) map");

@@ -296,6 +296,7 @@ class DPKFAC:
         # Captures of the first backward after a step are used (gradient
         # accumulation: keep early=False).
         self.early = bool(early)
+        self.early_priority = "high"  # "low": hook-launched work on lowest-priority streams
         self._hook_classes = None   # (classes, layer index -> class) fixed at the end of a step
         self._launched = {}         # class -> step t whose factor/inverse it already launched
 
@@ -425,8 +426,10 @@ class DPKFAC:
             self._allreduce_others()
         self._mark("comm_rs")
         ev_rs = main.record_event()
-        for cls, st in zip(sides, streams):
+        for ci, (cls, st) in enumerate(zip(sides, streams)):
             st.wait_event(ev_rs)
+            if self._launched.get(ci) == t:
+                st.wait_event(self._early_done[ci])
             with torch.cuda.stream(st):
                 self._precondition_stage(cls)
         # (1) Kronecker factors + running average: one grouped tcgen05 launch
@@ -480,10 +483,16 @@ class DPKFAC:
             return
         h, t = self.hyper, self.t
         st = self._side_streams(len(classes))[ci]
+        if self.early_priority == "low":  # fill the backward's idle SMs instead of preempting it
+            if not hasattr(self, "_early_st"):
+                self._early_st = {}
+            st = self._early_st.setdefault(ci, torch.cuda.Stream(self.device, priority=0))
         st.wait_stream(torch.cuda.current_stream(self.device))  # the captures' producer stream
         with torch.cuda.stream(st):
             self._factor_stage(cls, t, t % h.f_freq == 0, st)
             self._inverse_stage(cls, t, t % h.k_freq == 0)
+        self._early_done = getattr(self, "_early_done", {})
+        self._early_done[ci] = st.record_event()
         self._launched[ci] = t
 
     # ------------------------------------------------------------ stages

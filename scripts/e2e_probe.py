@@ -37,8 +37,10 @@ def run(kf, n=20, sync_each=True):
     return s.elapsed_time(e) / n, (time.perf_counter() - t0) * 1000 / n
 
 print("no kfac      : %.2f ms (wall %.2f)" % run(None), flush=True)
-for early in (False, True):
-    kf = DPKFAC(model, gamma=0.002, xi=0.95, inv_type="inverse", check_numerics="deferred", early=early)
+for early in (False, True, "low"):
+    kf = DPKFAC(model, gamma=0.002, xi=0.95, inv_type="inverse", check_numerics="deferred", early=bool(early))
+    if early == "low":
+        kf.early_priority = "low"
     print(f"kfac early={early}: %.2f ms (wall %.2f)" % run(kf), flush=True)
     print(f"  no per-step sync : %.2f ms" % run(kf, sync_each=False)[0], flush=True)
     kf.remove_hooks()
