@@ -69,8 +69,10 @@ enum {
   DPK_OPND_IM2COL = 2,  /* X[(c,i,j),(n,oh,ow)] = x[n, c, oh*sh-ph+i*dh, ow*sw-pw+j*dw] or 0:
                            the implicit-im2col linear form of a Conv2d input (F.unfold order) */
   DPK_OPND_IM2COL_TAPMAJOR = 3 /* same values, rows ordered (i, j, c) -- the channels-last
-                           weight order.  With an NHWC input (c contiguous, C % 32 == 0) the
-                           engine fetches it with TMA im2col loads; the factor is then a
+                           weight order.  With an NHWC input (c contiguous, C % 32 == 0) a
+                           SYRK fetches it with tiled TMA tap boxes (5-D map over the input,
+                           tap-shifted coordinates, zero fill outside the image; a GEMM
+                           operand uses TMA im2col loads); the factor is then a
                            symmetric permutation of the (c,i,j) one and the gradient must
                            be packed with dpk_segment.perm_khw. */
 };
@@ -111,7 +113,9 @@ size_t dpk_factor_workspace_bytes(const dpk_factor_job* jobs, int n_jobs);
 int dpk_syrk_ema(const dpk_factor_job* jobs, int n_jobs, void* workspace, size_t ws_bytes, int precision,
                  dpk_stream_t stream);
 /* K2 entry point: identical contract; every job's operand must be DPK_OPND_IM2COL or
- * DPK_OPND_IM2COL_TAPMAJOR (the TMA-im2col form for channels-last inputs). */
+ * DPK_OPND_IM2COL_TAPMAJOR (implicit im2col: patches are never written; see the
+ * operand kinds above).  Measured on B200 the TMA-only implicit forms are TMA-issue
+ * bound, so DPKFAC materializes patches by default (dpk_im2col_materialize). */
 int dpk_conv_im2col_syrk_ema(const dpk_factor_job* jobs, int n_jobs, void* workspace, size_t ws_bytes,
                              int precision, dpk_stream_t stream);
 

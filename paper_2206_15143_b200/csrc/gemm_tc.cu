@@ -66,10 +66,10 @@ static_assert(NPROD % 8 == 0, "im2col chunk sharing needs NPROD % 8 == 0");
 // TMA_TAPS: implicit im2col of an NHWC conv input through plain TILED boxes:
 // a 5-D map {c32, w, h, n, c-block} over the input itself, one box per (tap,
 // channel block) group of 32/64/128 factor rows at the tap-shifted pixel
-// coordinates; out-of-image taps are TMA zero fill.  A K chunk is 32 pixels
-// (wb output columns x 32/wb samples at one output row), the same pixel set for
-// every row group, so patches never exist in HBM (SYRK only: both operands
-// share the map and the K order).
+// coordinates; out-of-image taps are TMA zero fill.  A K chunk is 32 output
+// pixels (wb x hb of one image block x nb samples), the same pixel set for every
+// row group, so patches never exist in HBM (SYRK only: both operands share the
+// map and the K order).  Measured TMA-issue bound.
 enum { TMA_NONE = 0, TMA_ROWS_K = 1, TMA_ROWS_MN = 2, TMA_SLAB = 3, TMA_IM2COL = 4, TMA_ROWS_MN3 = 5, TMA_TAPS = 6 };
 __host__ __device__ __forceinline__ bool tma_mn(int kind) {
   return kind == TMA_ROWS_MN || kind == TMA_IM2COL || kind == TMA_ROWS_MN3 || kind == TMA_TAPS;
