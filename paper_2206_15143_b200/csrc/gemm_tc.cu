@@ -1786,6 +1786,45 @@ std::string specs_key(const GemmSpec* specs, int n, int precision) {
 
 size_t gemm_workspace_bytes_uncached(const GemmSpec* specs, int n);
 
+// DPK_GEMM_FORK=0: run the CTA-pair and the single-CTA plans of one call back to back
+bool concurrent_plans() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DPK_GEMM_FORK");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// One forked stream per caller stream (same priority), with its fork/join events:
+// the single-CTA plan of a call runs there beside the pair plan, so the small
+// problems of a group (precondition phases, SPD rounds with mixed sizes) fill the
+// SMs the pair launch's tail leaves idle instead of queueing behind it.
+struct ForkLane {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+int fork_lane(cudaStream_t st, ForkLane*& out) {
+  static std::mutex mu;
+  static std::vector<std::pair<cudaStream_t, ForkLane*>> lanes;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : lanes)
+    if (e.first == st) {
+      out = e.second;
+      return DPK_OK;
+    }
+  ForkLane* L = new ForkLane();
+  int prio = 0;
+  cudaStreamGetPriority(st, &prio);
+  int rc = cuda_status(cudaStreamCreateWithPriority(&L->side, cudaStreamNonBlocking, prio), "cudaStreamCreate(fork)");
+  if (!rc) rc = cuda_status(cudaEventCreateWithFlags(&L->fork, cudaEventDisableTiming), "cudaEventCreate(fork)");
+  if (!rc) rc = cuda_status(cudaEventCreateWithFlags(&L->join, cudaEventDisableTiming), "cudaEventCreate(join)");
+  if (rc) return rc;
+  lanes.emplace_back(st, L);
+  out = L;
+  return DPK_OK;
+}
+
 size_t gemm_workspace_bytes(const GemmSpec* specs, int n) {
   if (n <= 0) return 0;
   static LruCache<size_t> cache;
@@ -1803,13 +1842,16 @@ size_t gemm_workspace_bytes(const GemmSpec* specs, int n) {
 size_t gemm_workspace_bytes_uncached(const GemmSpec* specs, int n) {
   std::vector<GemmSpec> g1, g2;
   partition_cg(specs, n, g1, g2);
-  size_t ws = 0;
+  size_t w1 = 0, w2 = 0;
   Plan plan;
   if (!g1.empty() && make_plan(g1.data(), static_cast<int>(g1.size()), plan, false, DPK_PREC_TF32, 1) == DPK_OK)
-    ws = std::max(ws, plan.ws_bytes);
+    w1 = plan.ws_bytes;
   if (!g2.empty() && make_plan(g2.data(), static_cast<int>(g2.size()), plan, false, DPK_PREC_TF32, 2) == DPK_OK)
-    ws = std::max(ws, plan.ws_bytes);
-  return ws;
+    w2 = plan.ws_bytes;
+  // both unit shapes present: the single-CTA plan runs concurrently with the pair
+  // plan in its own workspace region behind the pair plan's
+  if (w1 && w2 && concurrent_plans()) return align_up(w2, 1024) + w1;
+  return std::max(w1, w2);
 }
 
 int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int precision, cudaStream_t st,
@@ -1862,6 +1904,26 @@ int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int pre
     }
     std::lock_guard<std::mutex> lock(cache.mu);
     cache.put(key, plans);
+  }
+  if (plans.size() == 2 && concurrent_plans() && ws != nullptr) {
+    // plans[0]: CTA pairs on the caller's stream; plans[1]: single CTAs on the fork lane
+    const size_t off = align_up(plans[0].ws_bytes, 1024);
+    if (ws_bytes >= off + plans[1].ws_bytes) {
+      ForkLane* L = nullptr;
+      int rc = fork_lane(st, L);
+      if (rc) return rc;
+      char* ws2 = static_cast<char*>(ws) + off;
+      rc = cuda_status(cudaEventRecord(L->fork, st), "cudaEventRecord(fork)");
+      if (!rc) rc = cuda_status(cudaStreamWaitEvent(L->side, L->fork, 0), "cudaStreamWaitEvent(fork)");
+      // the region's scheduler counters: offsets move with the job list, so they are
+      // cleared on every fork (callers that skip the clear own only the first region)
+      if (!rc) rc = cuda_status(cudaMemsetAsync(ws2, 0, SCHED_BYTES, L->side), "cudaMemsetAsync(fork counters)");
+      if (!rc) rc = run_plan(plans[1], ws2, ws_bytes - off, precision, L->side);
+      if (!rc) rc = run_plan(plans[0], ws, off, precision, st);
+      if (!rc) rc = cuda_status(cudaEventRecord(L->join, L->side), "cudaEventRecord(join)");
+      if (!rc) rc = cuda_status(cudaStreamWaitEvent(st, L->join, 0), "cudaStreamWaitEvent(join)");
+      return rc;
+    }
   }
   for (Plan& plan : plans) {
     const int rc = run_plan(plan, ws, ws_bytes, precision, st);

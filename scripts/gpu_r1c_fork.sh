@@ -1,0 +1,9 @@
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+for f in 0 1; do
+echo "DPK_GEMM_FORK=$f"
+DPK_GEMM_FORK=$f timeout 120 python scripts/precond_one.py 10 2>&1 | tail -1
+DPK_GEMM_FORK=$f SPD_ONLY=4608 timeout 120 python scripts/inv_factor_one.py 20 2>&1 | tail -1
+DPK_GEMM_FORK=$f timeout 120 python scripts/inv_factor_one.py 20 2>&1 | tail -1
+DPK_GEMM_FORK=$f timeout 300 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/bfork_$f.json 2>/dev/null
+python -c "import json; d=json.load(open('gpurun_out/bfork_$f.json')); print('bench', round(d['ms_per_step'],3), round(d['ms_per_step_serialized'],3), {k: round(v,3) for k,v in d['stages_ms'].items()})"
+done

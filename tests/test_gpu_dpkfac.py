@@ -52,6 +52,7 @@ def test_mlp_config1_dp_kfac_matches_reference(inv_type, precision):
     cl = MLP.build_cluster(spec, 1, seed=0)
     model, lins = torch_mlp([w.copy() for w in cl.weights], dev)
     kf = DPKFAC(model, gamma=0.03, xi=0.95, inv_type=inv_type, precision=precision)
+    kf.OVERLAP_MIN_DIM = 0  # exercise the size-class side streams (785 | 513, 257)
     opt = torch.optim.SGD(model.parameters(), lr=0.05, momentum=0.9)
     rng = np.random.default_rng(1234)
     for t in range(3):
