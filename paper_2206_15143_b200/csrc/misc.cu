@@ -111,27 +111,54 @@ struct SegBatch {
 };
 
 // grid.y = segment; grid.x strides over the segment's rows*(cols_w+has_bias) elements.
+// A plain segment (no bias column, no tap permutation, dense rows, 16-byte aligned
+// ends) is one contiguous run on both sides: float4 copies.  Everything else maps
+// flat element e -> (row, column) with 32-bit arithmetic (segments < 2^31 elements).
 template <bool PACK>
 __global__ void segment_kernel(const __grid_constant__ SegBatch b, float* flat) {
   const dpk_segment& S = b.s[blockIdx.y];
   const int cols = S.cols_w + (S.bias ? 1 : 0);
-  const int64_t total = static_cast<int64_t>(S.rows) * cols;
+  const int total = S.rows * cols;
   float* dst = flat + S.offset;
-  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t r = e / cols;
-    const int c = static_cast<int>(e - r * cols);
+  const float sc = b.scale;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+  const bool plain = S.perm_khw == 0 && S.bias == nullptr && S.ldw == S.cols_w &&
+                     ((reinterpret_cast<uintptr_t>(S.weight) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  if (plain) {
+    float4* w4 = reinterpret_cast<float4*>(S.weight);
+    float4* d4 = reinterpret_cast<float4*>(dst);
+    const int n4 = total >> 2;
+    for (int e = tid; e < n4; e += nth) {
+      if (PACK) {
+        const float4 v = __ldcs(w4 + e);
+        __stcs(d4 + e, make_float4(sc * v.x, sc * v.y, sc * v.z, sc * v.w));
+      } else {
+        const float4 v = __ldcs(d4 + e);
+        __stcs(w4 + e, make_float4(sc * v.x, sc * v.y, sc * v.z, sc * v.w));
+      }
+    }
+    for (int e = (n4 << 2) + tid; e < total; e += nth) {
+      if (PACK)
+        dst[e] = sc * S.weight[e];
+      else
+        S.weight[e] = sc * dst[e];
+    }
+    return;
+  }
+  const int cin = S.perm_khw > 0 ? S.cols_w / S.perm_khw : 1;
+  for (int e = tid; e < total; e += nth) {
+    const int r = e / cols;
+    const int c = e - r * cols;
     int cw = c;
     if (S.perm_khw > 0 && c < S.cols_w) {  // flat (kh, kw, ci) <- weight (ci, kh, kw)
-      const int cin = S.cols_w / S.perm_khw;
       const int tap = c / cin;
       cw = (c - tap * cin) * S.perm_khw + tap;
     }
-    float* src = (c < S.cols_w) ? S.weight + r * S.ldw + cw : S.bias + r;
+    float* src = (c < S.cols_w) ? S.weight + static_cast<int64_t>(r) * S.ldw + cw : S.bias + r;
     if (PACK)
-      dst[e] = b.scale * *src;
+      dst[e] = sc * *src;
     else
-      *src = b.scale * dst[e];
+      *src = sc * dst[e];
   }
 }
 
@@ -149,14 +176,15 @@ int run_segments(const dpk_segment* segs, int n, float* flat, float scale, cudaS
     int64_t maxe = 0;
     for (int i = 0; i < cnt; ++i) {
       b.s[i] = segs[first + i];
-      if (b.s[i].rows < 0 || b.s[i].cols_w < 0 || b.s[i].weight == nullptr) {
+      if (b.s[i].rows < 0 || b.s[i].cols_w < 0 || b.s[i].weight == nullptr ||
+          static_cast<int64_t>(b.s[i].rows) * (b.s[i].cols_w + 1) >= (int64_t{1} << 31)) {
         set_error("dpk_pack/unpack: invalid segment");
         return DPK_EARG;
       }
       maxe = std::max<int64_t>(maxe, static_cast<int64_t>(b.s[i].rows) * (b.s[i].cols_w + (b.s[i].bias ? 1 : 0)));
     }
     const int threads = 256;
-    const int gx = static_cast<int>(std::min<int64_t>((maxe + threads - 1) / threads, 1024));
+    const int gx = static_cast<int>(std::min<int64_t>((maxe + 4 * threads - 1) / (4 * threads), 592));
     if (gx == 0) continue;
     segment_kernel<PACK><<<dim3(gx, cnt), threads, 0, st>>>(b, flat);
     note_launch();
