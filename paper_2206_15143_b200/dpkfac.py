@@ -792,17 +792,29 @@ class DPKFAC:
         return out
 
     def _allreduce_others(self):
+        """Mean of the non-preconditioned gradients (batch-norm etc.): one pack kernel
+        into a flat buffer, one NCCL all-reduce, one unpack kernel (each parameter a
+        plain single-row segment of the owner-major pack/unpack kernel)."""
         grads = [p.grad for p in self.other_params if p.grad is not None]
         if not grads:
             return
-        flat = torch.cat([g.reshape(-1) for g in grads])
-        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.pg)
-        flat.mul_(1.0 / self.world)
-        off = 0
-        for g in grads:
-            n = g.numel()
-            g.copy_(flat[off:off + n].view_as(g))
-            off += n
+        key = tuple((g.data_ptr(), g.numel()) for g in grads)
+        if getattr(self, "_others_key", None) != key:
+            segs, off = [], 0
+            for g in grads:
+                if not g.is_contiguous():
+                    raise ArgumentError("non-preconditioned gradients must be contiguous")
+                sg = L.Segment()
+                sg.weight, sg.bias, sg.offset = g.data_ptr(), None, off
+                sg.rows, sg.cols_w, sg.ldw, sg.perm_khw = 1, g.numel(), g.numel(), 0
+                segs.append(sg)
+                off += (g.numel() + 3) // 4 * 4  # keep every segment 16-byte aligned
+            self._others_flat = torch.zeros(max(off, 1), device=self.device)
+            self._others_segs = segs
+            self._others_key = key
+        ops.pack(self._others_segs, self._others_flat, 1.0 / self.world)
+        dist.all_reduce(self._others_flat, op=dist.ReduceOp.SUM, group=self.pg)
+        ops.unpack(self._others_segs, self._others_flat, 1.0)
 
     def _gather_info(self):
         if self.world > 1:
