@@ -265,6 +265,9 @@ int dpk_precond_eigen(const dpk_precond_job* jobs, int n_jobs, float gamma, void
 /* ------------------------------------------------------------------------
  * K4: batched symmetric eigendecomposition (numerics.sym_eig numerics.py:75-97):
  * symmetrize, decompose, eigenvalues DESCENDING, eigenvectors as columns of q.
+ * On-chip cyclic Jacobi, one CTA per matrix, n <= 128 (DPK_EARG above that).  The
+ * Python layer routes larger factors to cuSOLVER syevd (torch.linalg.eigh) --
+ * a library call, the open K4 gap.
  * ------------------------------------------------------------------------ */
 typedef struct dpk_eig_job {
   const float* src; /* n x n */
