@@ -363,10 +363,30 @@ class DPKFAC:
         self.info = torch.zeros(max(len(self.layers), 1), dtype=torch.int32, device=dev)  # zeroed after each step
         self.shifts = torch.zeros(max(n_own, 1), 2, device=dev)
         self.pis = torch.zeros(max(n_own, 1), device=dev)
+        self._jc = {}  # prepared (ctypes) job arrays, valid for these buffers
         self._bufs_ready = True
 
     def _segments(self, which: str, offsets=None):
+        """The layers' [W | b] gradient segments at their flat offsets, as a Prepared
+        array cached by the gradient tensors' addresses (stable across steps unless
+        the optimizer drops .grad)."""
         offsets = self.offsets if offsets is None else offsets
+        grads = []
+        for ly in self.layers:
+            w, b = ly.module.weight, ly.module.bias
+            if w.grad is None:
+                raise OrderingError(f"layer {ly.index} ({ly.name}) has no gradient: call backward() before step()")
+            if b is not None and b.grad is None:
+                raise OrderingError(f"layer {ly.index} ({ly.name}) bias has no gradient")
+            grads.append((w.grad.data_ptr(), w.grad.stride(), b.grad.data_ptr() if b is not None else 0))
+        key = ("seg", id(offsets))
+        grads = tuple(grads)
+        hit = self._jc.get(key)
+        if hit is None or hit[0] != grads:
+            hit = self._jc[key] = (grads, ops.Prepared(L.Segment, self._segments_uncached(which, offsets)))
+        return hit[1]
+
+    def _segments_uncached(self, which: str, offsets):
         segs = []
         for ly in self.layers:
             w = ly.module.weight
@@ -580,16 +600,22 @@ class DPKFAC:
                 jt.append((ly.g_cov, ly.g_q, ly.g_w, self.info[ly.index]))
             ops.syevd(jt)
         else:
-            ops.trace_pi([(ly.a_cov, ly.g_cov) for ly in layers], h.gamma,
-                         [self.shifts[ly.slot] for ly in layers], [self.pis[ly.slot] for ly in layers],
-                         [self.info[ly.index] for ly in layers])
-            sj = []
-            for ly in layers:
-                sj.append(ops.spd_factor_job(ly.a_cov, ly.a_x, self.shifts[ly.slot, 0], self.info[ly.index],
-                                             L.INFO_NOT_SPD_A))
-                sj.append(ops.spd_factor_job(ly.g_cov, ly.g_x, self.shifts[ly.slot, 1], self.info[ly.index],
-                                             L.INFO_NOT_SPD_G))
-            ops.chol_factor_inv(sj)
+            # the job lists only reference persistent state buffers: built once per class
+            key = ("inv", tuple(ly.index for ly in layers))
+            prep = self._jc.get(key)
+            if prep is None:
+                pi_prep = ops.trace_pi([(ly.a_cov, ly.g_cov) for ly in layers], h.gamma,
+                                       [self.shifts[ly.slot] for ly in layers], [self.pis[ly.slot] for ly in layers],
+                                       [self.info[ly.index] for ly in layers], prepare=True)
+                sj = []
+                for ly in layers:
+                    sj.append(ops.spd_factor_job(ly.a_cov, ly.a_x, self.shifts[ly.slot, 0], self.info[ly.index],
+                                                 L.INFO_NOT_SPD_A))
+                    sj.append(ops.spd_factor_job(ly.g_cov, ly.g_x, self.shifts[ly.slot, 1], self.info[ly.index],
+                                                 L.INFO_NOT_SPD_G))
+                prep = self._jc[key] = (pi_prep, ops.prepare_chol_factor_inv(sj))
+            ops.trace_pi_prepared(prep[0], h.gamma)
+            ops.chol_factor_inv_prepared(prep[1])
         for ly in layers:
             ly.holds = h.inv_type
             ly.last_inverse_update = t
@@ -600,12 +626,25 @@ class DPKFAC:
         if not layers:
             return
         X = self.xchg if xchg is None else xchg
-        pj = []
         for ly in layers:
             if ly.holds != h.inv_type:
                 what = "eigendecomposition" if h.inv_type == "eigen" else "damped inverse"
                 raise OrderingError(f"worker {self.rank}, layer {ly.index}: preconditioning requested "
                                     f"before any {what} exists")
+        if h.inv_type != "eigen":
+            key = ("pre", id(X), tuple(ly.index for ly in layers))
+            prep = self._jc.get(key)
+            if prep is None:
+                pj = []
+                for ly in layers:
+                    shape = (ly.d_out, ly.d_in)
+                    g, o, tmp = X.view_in(ly.index, shape), X.view_out(ly.index, shape), X.view_tmp(ly.index, shape)
+                    pj.append(ops.precond_factor_job(g, ly.a_x, ly.g_x, o, tmp))
+                prep = self._jc[key] = ops.prepare_precondition_factored(pj)
+            ops.precondition_factored_prepared(prep, self.precond_precision)
+            return
+        pj = []
+        for ly in layers:
             shape = (ly.d_out, ly.d_in)
             g, o, tmp = X.view_in(ly.index, shape), X.view_out(ly.index, shape), X.view_tmp(ly.index, shape)
             if h.inv_type == "eigen":

@@ -166,9 +166,10 @@ def gemm(jobs: Sequence[L.GemmJob], precision: str = "tf32"):
 
 
 # ------------------------------------------------------------------ A6 + K3
-def trace_pi(pairs, gamma: float, shifts: torch.Tensor, pis: Optional[torch.Tensor], infos):
+def trace_pi(pairs, gamma: float, shifts: torch.Tensor, pis: Optional[torch.Tensor], infos, prepare=False):
     """pairs: list of (A, G) device matrices; writes shifts[i] = (pi sqrt(g), sqrt(g)/pi);
-    infos[i] (a one-element int32 view) receives DPK_INFO_TRACE on a non-positive trace."""
+    infos[i] (a one-element int32 view) receives DPK_INFO_TRACE on a non-positive trace.
+    prepare=True returns a Prepared job array for trace_pi_prepared instead of launching."""
     jobs = []
     for i, (a, g) in enumerate(pairs):
         j = L.PiJob()
@@ -178,10 +179,17 @@ def trace_pi(pairs, gamma: float, shifts: torch.Tensor, pis: Optional[torch.Tens
         j.pi = pis[i].data_ptr() if pis is not None else None
         j.info = infos[i].data_ptr()
         jobs.append(j)
+    if prepare:
+        return Prepared(L.PiJob, jobs)
     if not jobs:
         return
     lb = lib()
     L.check(lb.dpk_trace_pi(L.array(L.PiJob, jobs), len(jobs), float(gamma), stream_handle()), "dpk_trace_pi")
+
+
+def trace_pi_prepared(prep: Prepared, gamma: float):
+    if prep.n:
+        L.check(lib().dpk_trace_pi(prep.arr, prep.n, float(gamma), stream_handle()), "dpk_trace_pi")
 
 
 def spd_job(src: torch.Tensor, dst: torch.Tensor, shift: Optional[torch.Tensor], info: Optional[torch.Tensor],
@@ -229,11 +237,19 @@ def chol_factor_inv(jobs: Sequence[L.SpdFactorJob]):
     """dst = X = L^-1 with L L^T = src + shift I (the damped inverse is X^T X)."""
     if not jobs:
         return
-    lb = lib()
-    arr = L.array(L.SpdFactorJob, jobs)
-    need = lb.dpk_chol_factor_inv_workspace_bytes(arr, len(jobs))
-    ws = Workspace.get(need, torch.device("cuda", torch.cuda.current_device()), key="spd")
-    L.check(lb.dpk_chol_factor_inv_batched(arr, len(jobs), ws, need, stream_handle()), "dpk_chol_factor_inv_batched")
+    chol_factor_inv_prepared(prepare_chol_factor_inv(jobs))
+
+
+def prepare_chol_factor_inv(jobs: Sequence[L.SpdFactorJob]) -> Prepared:
+    return Prepared(L.SpdFactorJob, jobs, lib().dpk_chol_factor_inv_workspace_bytes)
+
+
+def chol_factor_inv_prepared(prep: Prepared):
+    if not prep.n:
+        return
+    ws = Workspace.get(prep.need, torch.device("cuda", torch.cuda.current_device()), key="spd")
+    L.check(lib().dpk_chol_factor_inv_batched(prep.arr, prep.n, ws, prep.need, stream_handle()),
+            "dpk_chol_factor_inv_batched")
 
 
 def precond_factor_job(grad, xa, xg, out, tmp) -> L.PrecondFactorJob:
@@ -249,12 +265,19 @@ def precondition_factored(jobs: Sequence[L.PrecondFactorJob], precision: str = "
     """out = X_G^T X_G grad X_A^T X_A  (= G_inv grad A_inv) for every job."""
     if not jobs:
         return
-    lb = lib()
-    arr = L.array(L.PrecondFactorJob, jobs)
-    need = lb.dpk_precond_factor_workspace_bytes(arr, len(jobs))
-    ws = Workspace.get(need, torch.device("cuda", torch.cuda.current_device()), key="pre")
-    L.check(lb.dpk_precond_factored(arr, len(jobs), ws, need, precision_code(precision), stream_handle()),
-            "dpk_precond_factored")
+    precondition_factored_prepared(prepare_precondition_factored(jobs), precision)
+
+
+def prepare_precondition_factored(jobs: Sequence[L.PrecondFactorJob]) -> Prepared:
+    return Prepared(L.PrecondFactorJob, jobs, lib().dpk_precond_factor_workspace_bytes)
+
+
+def precondition_factored_prepared(prep: Prepared, precision: str = "3xtf32"):
+    if not prep.n:
+        return
+    ws = Workspace.get(prep.need, torch.device("cuda", torch.cuda.current_device()), key="pre")
+    L.check(lib().dpk_precond_factored(prep.arr, prep.n, ws, prep.need, precision_code(precision),
+                                       stream_handle()), "dpk_precond_factored")
 
 
 # ------------------------------------------------------------------ K4
@@ -389,13 +412,36 @@ def segment(weight: torch.Tensor, bias: Optional[torch.Tensor], offset: int, tap
     return s
 
 
-def pack(segs: Sequence[L.Segment], flat: torch.Tensor, scale: float = 1.0):
-    if segs:
-        L.check(lib().dpk_pack_owner_major(L.array(L.Segment, segs), len(segs), flat.data_ptr(), float(scale),
-                                           stream_handle()), "dpk_pack_owner_major")
+class Prepared:
+    """A job list already turned into its ctypes array (and workspace size): the
+    steady-state step re-launches identical job lists, so the host work of
+    building them is done once (DPKFAC caches these per layer class)."""
+
+    __slots__ = ("arr", "n", "need", "keep")
+
+    def __init__(self, struct, jobs, need_fn=None, keep=None):
+        self.arr = L.array(struct, jobs)
+        self.n = len(jobs)
+        self.need = need_fn(self.arr, self.n) if (need_fn is not None and self.n) else 0
+        self.keep = keep  # tensors whose pointers the jobs hold
 
 
-def unpack(segs: Sequence[L.Segment], flat: torch.Tensor, scale: float = 1.0):
-    if segs:
-        L.check(lib().dpk_unpack_owner_major(L.array(L.Segment, segs), len(segs), flat.data_ptr(), float(scale),
-                                             stream_handle()), "dpk_unpack_owner_major")
+def _seg_array(segs):
+    if isinstance(segs, Prepared):
+        return segs.arr, segs.n
+    return L.array(L.Segment, segs), len(segs)
+
+
+def pack(segs, flat: torch.Tensor, scale: float = 1.0):
+    """segs: a list of L.Segment or a Prepared segment array."""
+    arr, n = _seg_array(segs)
+    if n:
+        L.check(lib().dpk_pack_owner_major(arr, n, flat.data_ptr(), float(scale), stream_handle()),
+                "dpk_pack_owner_major")
+
+
+def unpack(segs, flat: torch.Tensor, scale: float = 1.0):
+    arr, n = _seg_array(segs)
+    if n:
+        L.check(lib().dpk_unpack_owner_major(arr, n, flat.data_ptr(), float(scale), stream_handle()),
+                "dpk_unpack_owner_major")
