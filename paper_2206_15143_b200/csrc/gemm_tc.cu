@@ -56,7 +56,7 @@ constexpr int NPROD = PROD_WARPS * 32;                    // 192 gather / conver
 constexpr int TILE_TASKS = BM * (BK / 4);                 // (row, 16B chunk) tasks per operand tile
 constexpr int NTASK = (TILE_TASKS + NPROD - 1) / NPROD;   // 5 tasks per producer thread
 constexpr int NTHREADS = (PROD_WARP0 + PROD_WARPS) * 32;  // 384
-constexpr int MAXP = 32;                                  // problems per launch (kernel params)
+constexpr int MAXP = 40;                                  // problems per launch (kernel params)
 constexpr size_t SCHED_BYTES = GEMM_SCHED_BYTES;          // scheduler counters at the workspace start
 static_assert(NPROD % 8 == 0, "im2col chunk sharing needs NPROD % 8 == 0");
 
