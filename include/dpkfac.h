@@ -68,13 +68,19 @@ enum {
   DPK_OPND_ROWS_MN = 1, /* X[r,k] = data[k*ld + r]            (e.g. nn.Linear input B x d) */
   DPK_OPND_IM2COL = 2,  /* X[(c,i,j),(n,oh,ow)] = x[n, c, oh*sh-ph+i*dh, ow*sw-pw+j*dw] or 0:
                            the implicit-im2col linear form of a Conv2d input (F.unfold order) */
-  DPK_OPND_IM2COL_TAPMAJOR = 3 /* same values, rows ordered (i, j, c) -- the channels-last
+  DPK_OPND_IM2COL_TAPMAJOR = 3, /* same values, rows ordered (i, j, c) -- the channels-last
                            weight order.  With an NHWC input (c contiguous, C % 32 == 0) a
                            SYRK fetches it with tiled TMA tap boxes (5-D map over the input,
                            tap-shifted coordinates, zero fill outside the image; a GEMM
                            operand uses TMA im2col loads); the factor is then a
                            symmetric permutation of the (c,i,j) one and the gradient must
                            be packed with dpk_segment.perm_khw. */
+  DPK_OPND_ROWS_K_F16 = 4 /* X[r,k] = ((const __half*)data)[r*ld + k]: a feature-major fp16
+                           patch matrix (dpk_im2col_materialize_f16), ld % 8 == 0.  SYRKs on
+                           it run tcgen05 kind::f16 (fp32 accumulate): the same 11-bit
+                           significand as the TF32 path at half the operand bytes and twice
+                           the MMA rate; values beyond the fp16 range become inf and surface
+                           as a non-SPD factor (NumericError). */
 };
 
 typedef struct dpk_operand {
@@ -133,6 +139,9 @@ typedef struct dpk_im2col_job {
 } dpk_im2col_job;
 
 int dpk_im2col_materialize(const dpk_im2col_job* jobs, int n_jobs, dpk_stream_t stream);
+/* The same patch values as fp16, FEATURE-major: out[r*ld + k] = half(X[r, k])
+ * (round to nearest), ld >= cols and ld % 8 == 0; read back as DPK_OPND_ROWS_K_F16. */
+int dpk_im2col_materialize_f16(const dpk_im2col_job* jobs, int n_jobs, dpk_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * Grouped tensor-core GEMM used by preconditioning (and exposed for tests):

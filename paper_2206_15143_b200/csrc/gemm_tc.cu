@@ -70,7 +70,10 @@ static_assert(NPROD % 8 == 0, "im2col chunk sharing needs NPROD % 8 == 0");
 // pixels (wb x hb of one image block x nb samples), the same pixel set for every
 // row group, so patches never exist in HBM (SYRK only: both operands share the
 // map and the K order).  Measured TMA-issue bound.
-enum { TMA_NONE = 0, TMA_ROWS_K = 1, TMA_ROWS_MN = 2, TMA_SLAB = 3, TMA_IM2COL = 4, TMA_ROWS_MN3 = 5, TMA_TAPS = 6 };
+// TMA_ROWS_K16: K-major fp16 operand (DPK_OPND_ROWS_K_F16), 64 elements per 128-B
+// stage row, consumed by kind::f16 MMAs; a K chunk of such a problem covers 64 columns.
+enum { TMA_NONE = 0, TMA_ROWS_K = 1, TMA_ROWS_MN = 2, TMA_SLAB = 3, TMA_IM2COL = 4, TMA_ROWS_MN3 = 5, TMA_TAPS = 6,
+       TMA_ROWS_K16 = 7 };
 __host__ __device__ __forceinline__ bool tma_mn(int kind) {
   return kind == TMA_ROWS_MN || kind == TMA_IM2COL || kind == TMA_ROWS_MN3 || kind == TMA_TAPS;
 }
@@ -422,6 +425,8 @@ __device__ __forceinline__ void issue_tma(int kind, const CUtensorMap* map, cons
   };
   if (kind == TMA_ROWS_K) {
     ld2(dst, kc * BK, row0);
+  } else if (kind == TMA_ROWS_K16) {
+    ld2(dst, kc * 2 * BK, row0);
   } else if (kind == TMA_ROWS_MN) {
 #pragma unroll
     for (int b = 0; b < BM / 32; ++b) ld2(dst + b * 4096, row0 + 32 * b, kc * BK);
@@ -936,7 +941,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         const bool skip_b = P.same_ab && tm == tn;
         const int a_mn = tma_mn(P.tma_a);
         const int b_mn = skip_b ? a_mn : tma_mn(P.tma_b);
-        const uint32_t idesc = idesc_tf32(UT, UT, a_mn, b_mn);
+        const bool f16 = P.tma_a == TMA_ROWS_K16;  // SYRK on an fp16 patch matrix (both operands)
+        const uint32_t idesc = f16 ? idesc_f16(UT, UT) : idesc_tf32(UT, UT, a_mn, b_mn);
         const int acc = it & 1;
         if (CG == 2)
           mbar_wait_cluster(tempty_bar(acc), ((it >> 1) & 1) ^ 1);
@@ -966,10 +972,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
             const uint64_t da = a_mn ? sdesc_mnmajor_sw128(sa + oa, 4096) : sdesc_kmajor_sw128(sa + oa);
             const uint64_t db = b_mn ? sdesc_mnmajor_sw128(sb + ob, 4096) : sdesc_kmajor_sw128(sb + ob);
             const uint32_t accum = (kc > kc0 || s > 0) ? 1u : 0u;
-            if (CG == 2)
+            if (NPASS == 1 && f16) {  // UMMA_K = 16 fp16 = the same 32 B step
+              if (CG == 2)
+                mma_f16_pair(d, da, db, idesc, accum);
+              else
+                mma_f16(d, da, db, idesc, accum);
+            } else if (CG == 2) {
               mma_tf32_pair(d, da, db, idesc, accum);
-            else
+            } else {
               mma_tf32(d, da, db, idesc, accum);
+            }
             if (NPASS == 3) {
               const uint64_t dbl = b_mn ? sdesc_mnmajor_sw128(sbl + ob, 4096) : sdesc_kmajor_sw128(sbl + ob);
               const uint64_t dal = a_mn ? sdesc_mnmajor_sw128(sal + oa, 4096) : sdesc_kmajor_sw128(sal + oa);
@@ -1262,6 +1274,20 @@ bool encode(CUtensorMap* m, int rank, const void* data, const cuuint64_t* dims, 
 
 // 2-D maps for row-major (K-major) / column-major (MN-major) operands.
 int plan_tma_2d(const dpk_operand& o, CUtensorMap* m, bool rn) {
+  if (o.kind == DPK_OPND_ROWS_K_F16) {
+    if (tma_disabled() || o.bias_row || o.rows < 1 || !aligned16(o.data) || (o.ld * 2) % 16 != 0) return TMA_NONE;
+    EncodeTiledFn fn = encoder();
+    if (!fn) return TMA_NONE;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(o.cols), static_cast<cuuint64_t>(o.rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(o.ld) * 2};
+    const cuuint32_t box[2] = {2 * BK, BM};
+    const cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<float*>(o.data), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS
+               ? TMA_ROWS_K16
+               : TMA_NONE;
+  }
   if (tma_disabled() || o.bias_row || o.rows < 1 || !aligned16(o.data) || (o.ld * 4) % 16 != 0) return TMA_NONE;
   if (o.kind == DPK_OPND_ROWS_K) {
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(o.cols), static_cast<cuuint64_t>(o.rows)};
@@ -1455,7 +1481,7 @@ bool valid_operand(const dpk_operand& o) {
   if (is_im2col(o.kind)) {
     if (o.kh < 1 || o.kw < 1 || o.sh < 1 || o.sw < 1 || o.dh < 1 || o.dw < 1 || o.OH < 1 || o.OW < 1) return false;
     if (o.rows != o.C * o.kh * o.kw) return false;
-  } else if (o.kind != DPK_OPND_ROWS_K && o.kind != DPK_OPND_ROWS_MN) {
+  } else if (o.kind != DPK_OPND_ROWS_K && o.kind != DPK_OPND_ROWS_MN && o.kind != DPK_OPND_ROWS_K_F16) {
     return false;
   }
   return true;
@@ -1515,6 +1541,14 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
     P.tiles_n = (P.N + UT - 1) / UT;
     P.ntiles = P.symmetric ? tmn * (tmn + 1) / 2 : tmn * P.tiles_n;
     P.chunks = static_cast<int>((j.a.cols + BK - 1) / BK);
+    const bool f16a = j.a.kind == DPK_OPND_ROWS_K_F16, f16b = j.b.kind == DPK_OPND_ROWS_K_F16;
+    if (f16a || f16b) {
+      if (!(f16a && f16b) || precision != DPK_PREC_TF32 || P.tri_a || P.tri_b) {
+        set_error("dpk_gemm: fp16 operands need fp16 on both sides, 1-pass precision, no triangular clipping");
+        return DPK_EARG;
+      }
+      P.chunks = static_cast<int>((j.a.cols + 2 * BK - 1) / (2 * BK));
+    }
     TapsGeom tg;
     if (P.same_ab && taps_eligible(j.a, &tg)) {
       P.chunks = static_cast<int>(tg.chunks);
@@ -1577,6 +1611,8 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
 // be TMA-addressable (CG=2 has no manual gather path) and both output edges
 // must exceed one 128 tile (smaller problems waste the 256-wide unit).
 bool tma_possible_2d(const dpk_operand& o) {
+  if (o.kind == DPK_OPND_ROWS_K_F16)
+    return !tma_disabled() && !o.bias_row && o.rows >= 1 && aligned16(o.data) && (o.ld * 2) % 16 == 0;
   return !tma_disabled() && !o.bias_row && o.rows >= 1 && aligned16(o.data) && (o.ld * 4) % 16 == 0 &&
          (o.kind == DPK_OPND_ROWS_K || o.kind == DPK_OPND_ROWS_MN);
 }

@@ -7,6 +7,7 @@
 // input and tap-major rows, each (pixel, tap) is one contiguous run of C floats
 // moved as float4s (coalesced reads and writes).  The SYRK then streams the
 // result through 2-D TMA as an MN-major operand.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -211,8 +212,193 @@ bool vec_ok(const dpk_im2col_job& j) {
          o.sn % 4 == 0 && o.shs % 4 == 0 && o.sws % 4 == 0 && j.ld % 4 == 0;
 }
 
+// ---------------------------------------------------------------- fp16, feature-major
+// out[r*ld + k] = half(X[r, k]).  Tiled: NHWC tap-major, C % 32 == 0 -- a block
+// gathers 64 output pixels x 32 channels of one tap (coalesced 128-B rows of the
+// input, zero outside the image), transposes through shared memory and writes
+// 32 rows x 64 halves (128 B each).  Generic: one element per thread, k fastest.
+constexpr int K16_PIX = 64;
+// A flat 1-D grid: job q owns blocks [first[q], first[q+1]) = its (pixel block,
+// 32-row group) pairs, pixel blocks fastest -- no empty blocks for small jobs.
+struct K16Batch {
+  int n;
+  int first[I2C_MAX + 1];
+  dpk_im2col_job j[I2C_MAX];
+};
+constexpr int K16_GROUPS = 4;  // 32-row groups per block (the pixel decode is shared)
+__global__ void __launch_bounds__(256) im2col_k16_tiled_kernel(const __grid_constant__ K16Batch b) {
+  __shared__ float T[2][32][K16_PIX + 1];
+  int q = 0;
+  while (q + 1 < b.n && b.first[q + 1] <= static_cast<int>(blockIdx.x)) ++q;
+  const dpk_im2col_job& J = b.j[q];
+  const dpk_operand& o = J.x;
+  const int local = static_cast<int>(blockIdx.x) - b.first[q];
+  const int kblocks = static_cast<int>((o.cols + K16_PIX - 1) / K16_PIX);
+  const int gb = local / kblocks;  // block of K16_GROUPS row groups
+  const int64_t k0 = static_cast<int64_t>(local - gb * kblocks) * K16_PIX;
+  const int ohw = o.OH * o.OW;
+  // this thread's two (pixel, 4-channel) slots, decoded once
+  int pn[2], poh[2], pow_[2];
+  bool pin[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int p = (threadIdx.x + 256 * h) >> 3;
+    const int64_t k = k0 + p;
+    pin[h] = k < o.cols;
+    const int64_t kk = pin[h] ? k : 0;
+    pn[h] = static_cast<int>(kk / ohw);
+    const int rem = static_cast<int>(kk - static_cast<int64_t>(pn[h]) * ohw);
+    poh[h] = rem / o.OW;
+    pow_[h] = rem - poh[h] * o.OW;
+  }
+  const int nrg = (o.rows + 31) / 32;
+  for (int g = 0; g < K16_GROUPS; ++g) {
+    const int rg = gb * K16_GROUPS + g;
+    if (rg >= nrg) break;
+    const int r0 = rg * 32;
+    const int tap = r0 / o.C, c0 = r0 - tap * o.C;
+    const int i = tap / o.kw, j = tap - (tap / o.kw) * o.kw;
+    float (*Tb)[K16_PIX + 1] = T[g & 1];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int idx = threadIdx.x + 256 * h;
+      const int p = idx >> 3, qq = idx & 7;
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      const int ih = poh[h] * o.sh - o.ph + i * o.dh, iw = pow_[h] * o.sw - o.pw + j * o.dw;
+      if (pin[h] && static_cast<unsigned>(ih) < static_cast<unsigned>(o.H) &&
+          static_cast<unsigned>(iw) < static_cast<unsigned>(o.W))
+        v = __ldg(reinterpret_cast<const float4*>(o.data + static_cast<int64_t>(pn[h]) * o.sn +
+                                                  static_cast<int64_t>(ih) * o.shs + static_cast<int64_t>(iw) * o.sws +
+                                                  c0) + qq);
+      Tb[4 * qq][p] = v.x;
+      Tb[4 * qq + 1][p] = v.y;
+      Tb[4 * qq + 2][p] = v.z;
+      Tb[4 * qq + 3][p] = v.w;
+    }
+    __syncthreads();  // (double-buffered T: one barrier per group)
+    const int row = threadIdx.x >> 3, seg = threadIdx.x & 7;
+    __half* out = reinterpret_cast<__half*>(J.out) + static_cast<int64_t>(r0 + row) * J.ld + k0 + seg * 8;
+    const int64_t kk = k0 + seg * 8;
+    if (kk + 8 <= o.cols) {
+      __half2 hv[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) hv[e] = __floats2half2_rn(Tb[row][seg * 8 + 2 * e], Tb[row][seg * 8 + 2 * e + 1]);
+      __stcs(reinterpret_cast<uint4*>(out), *reinterpret_cast<const uint4*>(hv));
+    } else {
+      for (int e = 0; e < 8 && kk + e < o.cols; ++e) out[e] = __float2half_rn(Tb[row][seg * 8 + e]);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) im2col_k16_generic_kernel(const __grid_constant__ I2cBatch b) {
+  const dpk_im2col_job& J = b.j[blockIdx.y];
+  const dpk_operand& o = J.x;
+  const int d = o.rows + (o.bias_row ? 1 : 0);
+  const int kk = o.kh * o.kw;
+  const int ohw = o.OH * o.OW;
+  const int64_t total = static_cast<int64_t>(d) * o.cols;
+  __half* out = reinterpret_cast<__half*>(J.out);
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(e / o.cols);
+    const int64_t k = e - static_cast<int64_t>(r) * o.cols;
+    float v = 1.0f;  // the bias row
+    if (r < o.rows) {
+      int c, i, j;
+      if (o.kind == DPK_OPND_IM2COL) {
+        c = r / kk;
+        const int t = r - c * kk;
+        i = t / o.kw;
+        j = t - i * o.kw;
+      } else {
+        const int t = r / o.C;
+        c = r - t * o.C;
+        i = t / o.kw;
+        j = t - i * o.kw;
+      }
+      const int n = static_cast<int>(k / ohw);
+      const int rem = static_cast<int>(k - static_cast<int64_t>(n) * ohw);
+      const int oh = rem / o.OW, ow = rem - (rem / o.OW) * o.OW;
+      const int ih = oh * o.sh - o.ph + i * o.dh, iw = ow * o.sw - o.pw + j * o.dw;
+      v = 0.0f;
+      if (static_cast<unsigned>(ih) < static_cast<unsigned>(o.H) && static_cast<unsigned>(iw) < static_cast<unsigned>(o.W))
+        v = __ldg(o.data + static_cast<int64_t>(n) * o.sn + static_cast<int64_t>(c) * o.sc +
+                  static_cast<int64_t>(ih) * o.shs + static_cast<int64_t>(iw) * o.sws);
+    }
+    out[static_cast<int64_t>(r) * J.ld + k] = __float2half_rn(v);
+  }
+}
+
+bool k16_tiled_ok(const dpk_im2col_job& j) {
+  const dpk_operand& o = j.x;
+  return o.kind == DPK_OPND_IM2COL_TAPMAJOR && o.sc == 1 && o.C % 32 == 0 && !o.bias_row &&
+         (reinterpret_cast<uintptr_t>(o.data) & 15) == 0 && o.sn % 4 == 0 && o.shs % 4 == 0 && o.sws % 4 == 0;
+}
+
 }  // namespace
 }  // namespace dpk
+
+extern "C" int dpk_im2col_materialize_f16(const dpk_im2col_job* jobs, int n_jobs, dpk_stream_t stream) {
+  if (n_jobs == 0) return DPK_OK;
+  if (n_jobs < 0 || jobs == nullptr) {
+    dpk::set_error("dpk_im2col_materialize_f16: bad job list");
+    return DPK_EARG;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  thread_local dpk::K16Batch tb;
+  thread_local dpk::I2cBatch gb;
+  tb.n = gb.n = 0;
+  tb.first[0] = 0;
+  int64_t gmax = 0;
+  auto flush_t = [&]() -> int {
+    if (tb.n == 0) return DPK_OK;
+    dpk::im2col_k16_tiled_kernel<<<tb.first[tb.n], 256, 0, st>>>(tb);
+    dpk::note_launch();
+    tb.n = 0;
+    return dpk::cuda_status(cudaGetLastError(), "im2col_k16_tiled_kernel launch");
+  };
+  auto flush_g = [&]() -> int {
+    if (gb.n == 0) return DPK_OK;
+    const int gx = static_cast<int>(std::min<int64_t>((gmax + 255) / 256, 4 * 148 * 8));
+    dpk::im2col_k16_generic_kernel<<<dim3(gx, gb.n), 256, 0, st>>>(gb);
+    dpk::note_launch();
+    gb.n = 0;
+    gmax = 0;
+    return dpk::cuda_status(cudaGetLastError(), "im2col_k16_generic_kernel launch");
+  };
+  for (int i = 0; i < n_jobs; ++i) {
+    const dpk_im2col_job& j = jobs[i];
+    const dpk_operand& o = j.x;
+    if ((o.kind != DPK_OPND_IM2COL && o.kind != DPK_OPND_IM2COL_TAPMAJOR) || j.out == nullptr || o.data == nullptr ||
+        o.cols < 1 || o.rows != o.C * o.kh * o.kw || j.ld < o.cols || j.ld % 8 != 0 ||
+        (reinterpret_cast<uintptr_t>(j.out) & 15) != 0 || o.OH * static_cast<int64_t>(o.OW) < 1) {
+      dpk::set_error("dpk_im2col_materialize_f16: invalid job " + std::to_string(i));
+      return DPK_EARG;
+    }
+    const int64_t nblk = ((o.cols + dpk::K16_PIX - 1) / dpk::K16_PIX) *
+                         ((((o.rows + 31) / 32) + dpk::K16_GROUPS - 1) / dpk::K16_GROUPS);
+    if (dpk::k16_tiled_ok(j) && nblk < (int64_t{1} << 30)) {
+      if (tb.n == dpk::I2C_MAX || tb.first[tb.n] + nblk >= (int64_t{1} << 31)) {
+        int rc = flush_t();
+        if (rc) return rc;
+        tb.first[0] = 0;
+      }
+      tb.j[tb.n] = j;
+      tb.first[tb.n + 1] = tb.first[tb.n] + static_cast<int>(nblk);
+      ++tb.n;
+    } else {
+      if (gb.n == dpk::I2C_MAX) {
+        int rc = flush_g();
+        if (rc) return rc;
+      }
+      gb.j[gb.n++] = j;
+      gmax = std::max<int64_t>(gmax, static_cast<int64_t>(o.rows + (o.bias_row ? 1 : 0)) * o.cols);
+    }
+  }
+  int rc = flush_t();
+  if (rc) return rc;
+  return flush_g();
+}
 
 extern "C" int dpk_im2col_materialize(const dpk_im2col_job* jobs, int n_jobs, dpk_stream_t stream) {
   if (n_jobs == 0) return DPK_OK;

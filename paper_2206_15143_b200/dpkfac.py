@@ -82,9 +82,10 @@ class _Layer:
                               and w.is_contiguous(memory_format=torch.channels_last) and not w.is_contiguous())
 
         self.patch: Optional[torch.Tensor] = None  # materialized patch matrix (M x ld), reused
+        self.patch16: Optional[torch.Tensor] = None  # fp16 feature-major patch matrix (d x ld), reused
 
     # ---- operand views of the captures (reference layout: d x M, columns = samples)
-    def operand_a(self, im2col: str = "implicit"):
+    def operand_a(self, im2col: str = "implicit", f16: bool = False):
         """-> (SYRK operand, (im2col operand, patch buffer) to materialize first, or None).
 
         nn.Linear / 1x1-stride-1 captures are read in place (channels-last: a
@@ -114,6 +115,14 @@ class _Layer:
             # at tap-shifted coordinates, patches never reach HBM
             return op, None
         d = op.rows + op.bias_row
+        # fp16 patches where the tiled transpose kernel applies (NHWC, C % 32 == 0);
+        # small-C stems keep the fp32 row-staged path (its fp16 gather is slower)
+        if f16 and tap and nhwc and x.shape[1] % 32 == 0 and not self.has_bias and x.data_ptr() % 16 == 0:
+            # feature-major fp16 patches: half the HBM bytes, tcgen05 kind::f16 SYRK
+            ld = (op.cols + 7) // 8 * 8
+            if self.patch16 is None or self.patch16.shape != (d, ld):
+                self.patch16 = torch.empty(d, ld, dtype=torch.float16, device=x.device)
+            return ops.operand_rows_k_f16(self.patch16, op.cols), (op, self.patch16)
         ld = (d + 3) // 4 * 4
         if self.patch is None or self.patch.shape[0] < op.cols or self.patch.shape[1] != ld:
             self.patch = torch.empty(op.cols, ld, device=x.device)
@@ -196,7 +205,7 @@ class DPKFAC:
                  process_group=None, precision: str = "tf32", precond_precision: str = "3xtf32",
                  grad_scale: Union[str, float] = "batch", check_numerics: Union[bool, str] = True,
                  im2col: str = "materialize", overlap: bool = True, early: bool = False,
-                 algorithm: str = "dp_kfac"):
+                 algorithm: str = "dp_kfac", patch_dtype: str = "f16"):
         self.hyper = KfacHyper(gamma=gamma, xi=xi, inv_type=inv_type, f_freq=f_freq, k_freq=k_freq)
         # dp_kfac: the product.  mpd_kfac_co / mpd_kfac_mo: the paper's model-parallel
         # comparators (KAISA COMM-OPT / MEM-OPT, distsim.mpd_kfac_step distsim.py:341-420)
@@ -219,6 +228,11 @@ class DPKFAC:
         ops.precision_code(precision)
         ops.precision_code(precond_precision)
         self.precision = precision  # factor SYRK (tcgen05 kind::tf32, RN-rounded operands)
+        # materialized conv patches as fp16 (same 11-bit significand as RN TF32, half the
+        # bytes, kind::f16 MMAs at twice the tf32 rate); only with the 1-pass precision
+        if patch_dtype not in ("f16", "f32"):
+            raise ArgumentError("patch_dtype must be 'f16' or 'f32'")
+        self.patch_f16 = patch_dtype == "f16" and precision == "tf32"
         self.precond_precision = precond_precision  # preconditioning GEMMs
         if not (grad_scale == "batch" or isinstance(grad_scale, (int, float))):
             raise ArgumentError("grad_scale must be 'batch' or a number")
@@ -562,7 +576,7 @@ class DPKFAC:
             first = not ly.initialized
             w = 1.0 if first else h.xi
             beta = 0.0 if first else 1.0 - h.xi
-            oa, pending = ly.operand_a(self.im2col)
+            oa, pending = ly.operand_a(self.im2col, self.patch_f16)
             og = ly.operand_g()
             if pending is not None:
                 patches.append(pending)
@@ -576,7 +590,9 @@ class DPKFAC:
             if stream is not None:
                 ly.a_in.record_stream(stream)
                 ly.g_out.record_stream(stream)
-        ops.im2col_materialize(patches)  # one launch for every materialized conv
+        # one launch for every materialized conv (fp16 patches: their own kernel)
+        ops.im2col_materialize([p for p in patches if p[1].dtype != torch.float16])
+        ops.im2col_materialize_f16([p for p in patches if p[1].dtype == torch.float16])
         ops.syrk_ema(jobs, self.precision, device=self.device)
         for ly in layers:
             ly.initialized = True

@@ -117,6 +117,35 @@ def operand_im2col(x: torch.Tensor, kernel, stride, padding, dilation, bias_row:
     return o
 
 
+def operand_rows_k_f16(x: torch.Tensor, cols: int) -> L.Operand:
+    """Feature-major fp16 patch matrix x (rows x ld, ld % 8 == 0): X[r, k] = x[r, k], k < cols."""
+    if x.dtype != torch.float16 or x.dim() != 2 or x.stride(1) != 1 or x.stride(0) % 8 != 0:
+        raise ShapeError("fp16 patch operand must be a row-major rows x ld half matrix with ld % 8 == 0")
+    o = L.Operand()
+    o.data = x.data_ptr()
+    o.kind = L.OPND_ROWS_K_F16
+    o.rows = x.shape[0]
+    o.bias_row = 0
+    o.cols = cols
+    o.ld = x.stride(0)
+    return o
+
+
+def im2col_materialize_f16(pairs):
+    """pairs: [(im2col operand, out half tensor d x ld)] -> out[r, k] = half(X[r, k]) (feature-major)."""
+    if not pairs:
+        return
+    jobs = []
+    for op, out in pairs:
+        j = L.Im2colJob()
+        j.x = op
+        j.out = out.data_ptr()
+        j.ld = out.stride(0)
+        jobs.append(j)
+    L.check(lib().dpk_im2col_materialize_f16(L.array(L.Im2colJob, jobs), len(jobs), stream_handle()),
+            "dpk_im2col_materialize_f16")
+
+
 def im2col_materialize(pairs):
     """pairs: [(im2col operand, out tensor M x ld)] -> out[k, r] = X[r, k] (one launch)."""
     if not pairs:

@@ -441,3 +441,38 @@ def test_syrk_taps_dilated_matches_unfold(shape, k, s, p, dil):
         ops.syrk_ema([ops.factor_job(op, out, 1.0 / cols.shape[1], 0.0)], prec)
         torch.cuda.synchronize()
         assert rel(N(out), want) <= tol, (prec, rel(N(out), want))
+
+
+# ---------------------------------------------------------------- fp16 feature-major patches + kind::f16 SYRK
+@pytest.mark.parametrize("shape,k,s,p,bias,channels_last", [((4, 64, 14, 14), 3, 1, 1, False, True),
+                                                           ((3, 32, 9, 9), 3, 2, 1, False, True),
+                                                           ((2, 3, 20, 20), 7, 2, 3, False, True),
+                                                           ((2, 16, 8, 8), 3, 1, 1, True, False),
+                                                           ((32, 256, 7, 7), 1, 2, 0, False, True),
+                                                           ((2, 96, 12, 10), 5, 1, 2, False, True)])
+def test_f16_patches_and_syrk_match_unfold(shape, k, s, p, bias, channels_last):
+    from paper_2206_15143_b200 import ops
+    rng = np.random.default_rng(sum(shape) + k)
+    x = np.maximum(rng.standard_normal(shape), 0)
+    xt = T(x)
+    if channels_last:
+        xt = xt.to(memory_format=torch.channels_last)
+    tap = channels_last and k > 1
+    op = ops.operand_im2col(xt, (k, k), (s, s), (p, p), (1, 1), bias_row=bias, tap_major=tap)
+    cols = K.unfold_columns(x, k, k, s, p, 1, bias)
+    perm = _tap_perm(shape[1], k, k) if tap else np.arange(shape[1] * k * k)
+    if bias:
+        perm = np.concatenate([perm, [cols.shape[0] - 1]])
+    want_cols = cols[perm]
+    d, M = want_cols.shape
+    ld = (M + 7) // 8 * 8
+    patch = torch.full((d, ld), float("nan"), dtype=torch.float16, device=dev())
+    ops.im2col_materialize_f16([(op, patch)])
+    torch.cuda.synchronize()
+    got = patch[:, :M].float().cpu().numpy()
+    assert np.array_equal(got, torch.from_numpy(want_cols).float().half().float().numpy())  # RN half, bit-exact
+    out = torch.full((d, d), float("nan"), device=dev())
+    ops.syrk_ema([ops.factor_job(ops.operand_rows_k_f16(patch, M), out, 1.0 / M, 0.0)], "tf32")
+    torch.cuda.synchronize()
+    want, _ = K.compute_factors(want_cols, want_cols[:1])
+    assert rel(N(out), want) <= TOL, rel(N(out), want)
