@@ -195,6 +195,19 @@ class DPKFAC:
     Hyper-parameters and their validation are the reference's KfacHyper
     (kfac.py:55-74): gamma (damping, >= 0), xi (running-average weight of the
     NEW factor, in (0, 1]), inv_type ("eigen" | "inverse"), f_freq, k_freq.
+
+    B200 knobs (defaults are the measured-fastest parity-green settings):
+      assignment         "round_robin" (reference, bit-exact) | "balanced" (LPT) | explicit partition
+      precision          factor SYRK: "tf32" (1 pass, RN operands) | "3xtf32"
+      precond_precision  preconditioning GEMMs: "3xtf32" (fp32-grade)
+      patch_dtype        "f16": conv patches materialized as fp16 + kind::f16 SYRKs
+                         (with precision="tf32"); "f32": fp32 patches + kind::tf32
+      im2col             "materialize" | "auto" / "implicit" (TMA-only implicit forms)
+      check_numerics     True/"sync" | "deferred" (non-blocking flag read) | False
+      overlap            size-class pipeline on prioritized side streams
+      early              launch the larger classes' factor/inverse from the backward hooks
+      algorithm          "dp_kfac" | "mpd_kfac_co" | "mpd_kfac_mo" (paper comparators)
+      grad_scale         "batch" (B_local * grad_output, model.py:9-12) or a number
     """
 
     OVERLAP_MIN_DIM = 1024
