@@ -61,7 +61,7 @@ def _worker(rank, world, port, assign_kind, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,kind", [(2, "rr"), (3, "rr"), (2, "balanced")])
+@pytest.mark.parametrize("world,kind", [(2, "rr"), (3, "rr"), (2, "balanced"), (8, "balanced"), (8, "rr")])
 def test_owner_major_exchange_gloo(world, kind):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
