@@ -367,3 +367,34 @@ def test_multi_gpu_dp_and_mpd_match_reference():
                             os.path.join(root, "scripts", "multi_gpu_parity.py")],
                            capture_output=True, text=True, timeout=600)
         assert r.returncode == 0 and "PARITY OK" in r.stdout, (p, r.stdout[-2000:], r.stderr[-2000:])
+
+
+def test_early_launch_matches_reference():
+    """early=True: the larger size class's factor -> inverse pipeline is launched from
+    the backward hook; results equal the reference step for step."""
+    from paper_2206_15143_b200 import DPKFAC
+    dev = torch.device("cuda", 0)
+    spec = MLP.MlpSpec((784, 512, 256, 10), "relu", "softmax_cross_entropy", True)
+    h = K.Hyper(gamma=0.03, xi=0.95, inv_type="inverse", f_freq=1, k_freq=1)
+    cl = MLP.build_cluster(spec, 1, seed=0)
+    model, lins = torch_mlp([w.copy() for w in cl.weights], dev)
+    kf = DPKFAC(model, gamma=0.03, xi=0.95, inv_type="inverse", precision="3xtf32", early=True,
+                check_numerics="deferred")
+    kf.OVERLAP_MIN_DIM = 0  # two size classes: (785, 513) on a side stream, (257) on the caller's
+    opt = torch.optim.SGD(model.parameters(), lr=0.05, momentum=0.9)
+    rng = np.random.default_rng(99)
+    launched = []
+    for t in range(4):
+        x = rng.standard_normal((784, 64))
+        y = rng.integers(0, 10, size=64)
+        _, pre = MLP.dp_kfac_step(cl, MLP.shard(x, y, 1), h, 0.05, 0.9, t)
+        opt.zero_grad()
+        F.cross_entropy(model(torch.from_numpy(x.T.copy()).float().to(dev)), torch.from_numpy(y).to(dev)).backward()
+        launched.append(dict(kf._launched))
+        kf.step()
+        for i, lin in enumerate(lins):
+            got = torch.cat([lin.weight.grad, lin.bias.grad[:, None]], 1).double().cpu().numpy()
+            assert rel(got, pre[i]) <= TOL, (t, i, rel(got, pre[i]))
+        opt.step()
+    kf.check()
+    assert launched[0] == {} and all(l == {0: t} for t, l in enumerate(launched) if t > 0), launched
