@@ -211,6 +211,8 @@ class DPKFAC:
     """
 
     OVERLAP_MIN_DIM = 1024
+    MAX_CLASSES = 3      # size classes of the overlapped step (the last on the caller's stream)
+    CLASS_RATIO = 0.6    # a new class starts below this fraction of the current class's largest
 
     def __init__(self, model: nn.Module, *, gamma: float = 0.03, xi: float = 0.95, inv_type: str = "eigen",
                  f_freq: int = 1, k_freq: int = 1,
@@ -568,7 +570,7 @@ class DPKFAC:
         classes, top = [], None
         for ly in order:
             d = max(ly.d_in, ly.d_out)
-            if top is None or (10 * d < 6 * top and len(classes) < 3):
+            if top is None or (d < self.CLASS_RATIO * top and len(classes) < self.MAX_CLASSES):
                 classes.append([])
                 top = d
             classes[-1].append(ly)
@@ -763,8 +765,12 @@ class DPKFAC:
             off = 0
             for ly in self.layers:
                 na, ng = ly.d_in * ly.d_in, ly.d_out * ly.d_out
+                a_old, g_old = ly.a_cov, ly.g_cov  # e.g. restored by load_state_dict
                 ly.a_cov = self._mpd_F[off:off + na].view(ly.d_in, ly.d_in)
                 ly.g_cov = self._mpd_F[off + na:off + na + ng].view(ly.d_out, ly.d_out)
+                if a_old is not None:
+                    ly.a_cov.copy_(a_old)
+                    ly.g_cov.copy_(g_old)
                 self._mpd_views.append((self._mpd_T[off:off + na].view(ly.d_in, ly.d_in),
                                         self._mpd_T[off + na:off + na + ng].view(ly.d_out, ly.d_out)))
                 off += na + ng
