@@ -213,6 +213,7 @@ class DPKFAC:
     OVERLAP_MIN_DIM = 1024
     MAX_CLASSES = 3      # size classes of the overlapped step (the last on the caller's stream)
     CLASS_RATIO = 0.6    # a new class starts below this fraction of the current class's largest
+    FACTOR_ORDER = 0     # see step(): gating of the classes' factor SYRKs
 
     def __init__(self, model: nn.Module, *, gamma: float = 0.03, xi: float = 0.95, inv_type: str = "eigen",
                  f_freq: int = 1, k_freq: int = 1,
@@ -459,12 +460,21 @@ class DPKFAC:
         # start of the step; the last class runs on the caller's stream
         streams = self._side_streams(len(sides))
         ev0 = main.record_event()
+        # FACTOR_ORDER: 1 = the other classes' factor SYRKs wait for the largest class's
+        # (its SYRK then runs on the whole GPU and the critical inversion chain starts
+        # earlier); 2 = each class's SYRK waits for the previous class's; 0 = all at once
+        gate = None
         for ci, (cls, st) in enumerate(zip(sides, streams)):
             if self._launched.get(ci) == t:  # launched from the backward hook
                 continue
             st.wait_event(ev0)
+            if gate is not None:
+                st.wait_event(gate)
             with torch.cuda.stream(st):
                 self._factor_stage(cls, t, f_up, st)
+                done = st.record_event()
+                if self.FACTOR_ORDER == 2 or (self.FACTOR_ORDER == 1 and ci == 0):
+                    gate = done
                 self._inverse_stage(cls, t, k_up)
         # (3) pack every layer's [W | b] gradient, owner-major (scaled by 1/P)
         segs = self._segments("grad")
@@ -484,6 +494,8 @@ class DPKFAC:
             with torch.cuda.stream(st):
                 self._precondition_stage(cls)
         # (1) Kronecker factors + running average: one grouped tcgen05 launch
+        if gate is not None:
+            main.wait_event(gate)
         self._factor_stage(rest, t, f_up, None)
         self._mark("factors")
         # (2) inverses / eigendecompositions
