@@ -73,6 +73,25 @@ def main():
             if not rel(got, cl.weights[i]) <= 1e-4:
                 bad.append((algorithm, inv, "weights", i, rel(got, cl.weights[i])))
         kf.remove_hooks()
+    # non-preconditioned parameters (batch norm) are averaged over ranks, unpreconditioned
+    torch.manual_seed(0)
+    net = torch.nn.Sequential(torch.nn.Linear(20, 16), torch.nn.BatchNorm1d(16), torch.nn.ReLU(),
+                              torch.nn.Linear(16, 5)).to(dev)
+    kf = DPKFAC(net, gamma=0.05, xi=0.9, inv_type="inverse", precision="3xtf32")
+    gen = torch.Generator().manual_seed(100 + rank)
+    xb = torch.randn(8, 20, generator=gen).to(dev)
+    yb = torch.randint(0, 5, (8,), generator=gen).to(dev)
+    F.cross_entropy(net(xb), yb).backward()
+    bn = net[1]
+    local = torch.cat([bn.weight.grad, bn.bias.grad]).clone()
+    allg = [torch.empty_like(local) for _ in range(P)]
+    dist.all_gather(allg, local)
+    kf.step()
+    mean = sum(allg) / P
+    got = torch.cat([bn.weight.grad, bn.bias.grad])
+    if not torch.allclose(got, mean, rtol=1e-6, atol=1e-7):
+        bad.append(("batchnorm mean", float((got - mean).abs().max())))
+    kf.remove_hooks()
     flag = torch.tensor([len(bad)], device=dev)
     dist.all_reduce(flag)
     if rank == 0:
