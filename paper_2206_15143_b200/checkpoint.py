@@ -155,6 +155,10 @@ def load(path, kf, optimizer=None, restore_weights: bool = True, algorithm: str 
     weights and SGD momentum, from a v1 checkpoint (trainer.restore_cluster,
     trainer.py:299-324).  Accepts a per-rank file or a merged cluster file."""
     import torch
+    from .errors import OrderingError
+    if kf.assignment is None:
+        raise OrderingError("the balanced assignment is fixed at the first step(); load after it "
+                            "or pass the checkpoint's assignment explicitly")
     meta, arrays = read(path)
     if meta["algorithm"] != algorithm or meta["workers"] != kf.world:
         raise ArgumentError("checkpoint was produced with a different algorithm/worker configuration")
