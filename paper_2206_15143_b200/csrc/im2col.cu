@@ -329,6 +329,85 @@ __global__ void __launch_bounds__(256) im2col_k16_generic_kernel(const __grid_co
   }
 }
 
+// fp16 feature-major from the row-staged layout (small-C stems, any input strides):
+// one CTA per output row (n, oh) stages the kh input rows in smem exactly like
+// im2col_rows_kernel, then writes, for every patch row r, the OW contiguous halves
+// of this output row as uint4s (OW % 8 == 0).
+__global__ void __launch_bounds__(ROWS_THREADS) im2col_k16_rows_kernel(const __grid_constant__ I2cBatch b) {
+  extern __shared__ float sm[];
+  const dpk_im2col_job& J = b.j[blockIdx.y];
+  const dpk_operand& o = J.x;
+  const RowsGeom g = rows_geom(o);
+  const int d = o.rows + (o.bias_row ? 1 : 0);
+  float* stage = sm;
+  int* off = reinterpret_cast<int*>(sm + o.kh * g.rowlen);
+  for (int r = threadIdx.x; r < d; r += ROWS_THREADS) {
+    int v = -2;  // the bias row
+    if (r < o.rows) {
+      int c, i, j;
+      if (o.kind == DPK_OPND_IM2COL) {
+        const int kk = o.kh * o.kw;
+        c = r / kk;
+        const int t = r - c * kk;
+        i = t / o.kw;
+        j = t - i * o.kw;
+      } else {
+        const int t = r / o.C;
+        c = r - t * o.C;
+        i = t / o.kw;
+        j = t - i * o.kw;
+      }
+      v = i * g.rowlen + j * o.dw * o.C + c;
+    }
+    off[r] = v;
+  }
+  const int64_t nrows = o.cols / o.OW;
+  const int segs = o.OW / 8;
+  const int shift = o.sw * o.C;
+  for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
+    const int n = static_cast<int>(row / o.OH);
+    const int oh = static_cast<int>(row - static_cast<int64_t>(n) * o.OH);
+    const float* base = o.data + static_cast<int64_t>(n) * o.sn;
+    __syncthreads();
+    for (int e = threadIdx.x; e < o.kh * g.rowlen; e += ROWS_THREADS) {
+      const int i = e / g.rowlen;
+      const int q = e - i * g.rowlen;
+      const int wq = q / o.C;
+      const int c = q - wq * o.C;
+      const int ih = oh * o.sh - o.ph + i * o.dh, iw = wq - g.padl;
+      float v = 0.0f;
+      if (static_cast<unsigned>(ih) < static_cast<unsigned>(o.H) && static_cast<unsigned>(iw) < static_cast<unsigned>(o.W))
+        v = __ldg(base + static_cast<int64_t>(c) * o.sc + static_cast<int64_t>(ih) * o.shs +
+                  static_cast<int64_t>(iw) * o.sws);
+      stage[e] = v;
+    }
+    __syncthreads();
+    __half* out = reinterpret_cast<__half*>(J.out) + row * o.OW;
+    for (int u = threadIdx.x; u < d * segs; u += ROWS_THREADS) {
+      const int r = u / segs;
+      const int sgi = u - r * segs;
+      const int t = off[r];
+      __half2 hv[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int ow0 = sgi * 8 + 2 * e;
+        const float a = t >= 0 ? stage[t + ow0 * shift] : (t == -2 ? 1.0f : 0.0f);
+        const float c2 = t >= 0 ? stage[t + (ow0 + 1) * shift] : (t == -2 ? 1.0f : 0.0f);
+        hv[e] = __floats2half2_rn(a, c2);
+      }
+      __stcs(reinterpret_cast<uint4*>(out + static_cast<int64_t>(r) * J.ld + sgi * 8),
+             *reinterpret_cast<const uint4*>(hv));
+    }
+  }
+}
+
+bool k16_rows_ok(const dpk_im2col_job& j) {
+  const dpk_operand& o = j.x;
+  const RowsGeom g = rows_geom(o);
+  const size_t smem = (static_cast<size_t>(o.kh) * g.rowlen + o.rows + 1) * 4;
+  return o.OW % 8 == 0 && o.cols % o.OW == 0 && smem <= static_cast<size_t>(ROWS_SMEM_MAX);
+}
+
 bool k16_tiled_ok(const dpk_im2col_job& j) {
   const dpk_operand& o = j.x;
   return o.kind == DPK_OPND_IM2COL_TAPMAJOR && o.sc == 1 && o.C % 32 == 0 && !o.bias_row &&
@@ -346,8 +425,26 @@ extern "C" int dpk_im2col_materialize_f16(const dpk_im2col_job* jobs, int n_jobs
   }
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   thread_local dpk::K16Batch tb;
-  thread_local dpk::I2cBatch gb;
-  tb.n = gb.n = 0;
+  thread_local dpk::I2cBatch gb, rbf;
+  tb.n = gb.n = rbf.n = 0;
+  size_t rsm = 0;
+  auto flush_r = [&]() -> int {
+    if (rbf.n == 0) return DPK_OK;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(dpk::im2col_k16_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           dpk::ROWS_SMEM_MAX);
+      attr = true;
+    }
+    int64_t rows = 0;
+    for (int i = 0; i < rbf.n; ++i) rows = std::max<int64_t>(rows, rbf.j[i].x.cols / rbf.j[i].x.OW);
+    const int gx = static_cast<int>(std::min<int64_t>(rows, 4 * 148));
+    dpk::im2col_k16_rows_kernel<<<dim3(gx, rbf.n), dpk::ROWS_THREADS, rsm, st>>>(rbf);
+    dpk::note_launch();
+    rbf.n = 0;
+    rsm = 0;
+    return dpk::cuda_status(cudaGetLastError(), "im2col_k16_rows_kernel launch");
+  };
   tb.first[0] = 0;
   int64_t gmax = 0;
   auto flush_t = [&]() -> int {
@@ -386,6 +483,14 @@ extern "C" int dpk_im2col_materialize_f16(const dpk_im2col_job* jobs, int n_jobs
       tb.j[tb.n] = j;
       tb.first[tb.n + 1] = tb.first[tb.n] + static_cast<int>(nblk);
       ++tb.n;
+    } else if (dpk::k16_rows_ok(j)) {
+      if (rbf.n == dpk::I2C_MAX) {
+        int rc = flush_r();
+        if (rc) return rc;
+      }
+      rbf.j[rbf.n++] = j;
+      const dpk::RowsGeom g = dpk::rows_geom(o);
+      rsm = std::max(rsm, (static_cast<size_t>(o.kh) * g.rowlen + o.rows + 1) * 4);
     } else {
       if (gb.n == dpk::I2C_MAX) {
         int rc = flush_g();
@@ -396,6 +501,8 @@ extern "C" int dpk_im2col_materialize_f16(const dpk_im2col_job* jobs, int n_jobs
     }
   }
   int rc = flush_t();
+  if (rc) return rc;
+  rc = flush_r();
   if (rc) return rc;
   return flush_g();
 }

@@ -115,9 +115,10 @@ class _Layer:
             # at tap-shifted coordinates, patches never reach HBM
             return op, None
         d = op.rows + op.bias_row
-        # fp16 patches where the tiled transpose kernel applies (NHWC, C % 32 == 0);
-        # small-C stems keep the fp32 row-staged path (its fp16 gather is slower)
-        if f16 and tap and nhwc and x.shape[1] % 32 == 0 and not self.has_bias and x.data_ptr() % 16 == 0:
+        # fp16 patches: the tiled transpose kernel (NHWC, C % 32 == 0) or the row-staged
+        # one (small-C stems, output width a multiple of 8); else the fp32 paths
+        tiled = tap and nhwc and x.shape[1] % 32 == 0 and not self.has_bias and x.data_ptr() % 16 == 0
+        if f16 and (tiled or op.OW % 8 == 0):
             # feature-major fp16 patches: half the HBM bytes, tcgen05 kind::f16 SYRK
             ld = (op.cols + 7) // 8 * 8
             if self.patch16 is None or self.patch16.shape != (d, ld):

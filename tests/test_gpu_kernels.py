@@ -449,7 +449,11 @@ def test_syrk_taps_dilated_matches_unfold(shape, k, s, p, dil):
                                                            ((2, 3, 20, 20), 7, 2, 3, False, True),
                                                            ((2, 16, 8, 8), 3, 1, 1, True, False),
                                                            ((32, 256, 7, 7), 1, 2, 0, False, True),
-                                                           ((2, 96, 12, 10), 5, 1, 2, False, True)])
+                                                           ((2, 96, 12, 10), 5, 1, 2, False, True),
+                                                           # row-staged fp16 kernel: stem-like 7x7/2
+                                                           # (OW % 8 == 0), NHWC and NCHW, bias row
+                                                           ((2, 3, 32, 32), 7, 2, 3, False, True),
+                                                           ((2, 3, 32, 32), 7, 2, 3, True, False)])
 def test_f16_patches_and_syrk_match_unfold(shape, k, s, p, bias, channels_last):
     from paper_2206_15143_b200 import ops
     rng = np.random.default_rng(sum(shape) + k)
