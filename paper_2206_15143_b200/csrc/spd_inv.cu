@@ -373,15 +373,40 @@ __global__ void __launch_bounds__(PREP_WARPS * 32) prep_kernel(const __grid_cons
   const int64_t ldw = J.ldw;
   const float sh = J.shift ? *J.shift : 0.0f;
   const int lane = threadIdx.x & 31;
+  // float4 path: every row of src / Aw / X starts 16-byte aligned
+  const bool vec = (n % 4) == 0 && (ldw % 4) == 0 &&
+                   ((reinterpret_cast<uintptr_t>(J.src) | reinterpret_cast<uintptr_t>(J.dst) |
+                     reinterpret_cast<uintptr_t>(J.x)) & 15) == 0;
   for (int i = blockIdx.x * PREP_WARPS + (threadIdx.x >> 5); i < n; i += gridDim.x * PREP_WARPS) {
     const float* srow = J.src + static_cast<int64_t>(i) * n;
     float* arow = J.dst + static_cast<int64_t>(i) * ldw;
     float* xrow = J.x + static_cast<int64_t>(i) * ldw;
-    for (int c = lane; c <= i; c += 32) {
-      const float v = __ldg(srow + c);
-      arow[c] = c == i ? v + sh : v;
+    if (vec) {
+      // lower part [0, i] in whole float4s (the entries past i in the last vector are
+      // upper-triangle values of Aw the recursion never reads), the damping on the diagonal
+      const int q_end = i / 4;  // last vector touching column i
+      for (int q = lane; q <= q_end; q += 32) {
+        float4 v = __ldg(reinterpret_cast<const float4*>(srow) + q);
+        if (q == q_end) {
+          const int e = i - 4 * q;
+          if (e == 0) v.x += sh;
+          else if (e == 1) v.y += sh;
+          else if (e == 2) v.z += sh;
+          else v.w += sh;
+        }
+        reinterpret_cast<float4*>(arow)[q] = v;
+      }
+      // X[i][i+1..n) = 0: the partial vector scalar, then float4s
+      const int z0 = i + 1, zq = (z0 + 3) / 4;
+      if (lane < 4 * zq - z0 && z0 + lane < n) xrow[z0 + lane] = 0.0f;
+      for (int q = zq + lane; q < n / 4; q += 32) reinterpret_cast<float4*>(xrow)[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+      for (int c = lane; c <= i; c += 32) {
+        const float v = __ldg(srow + c);
+        arow[c] = c == i ? v + sh : v;
+      }
+      for (int c = i + 1 + lane; c < n; c += 32) xrow[c] = 0.0f;
     }
-    for (int c = i + 1 + lane; c < n; c += 32) xrow[c] = 0.0f;
   }
 }
 
