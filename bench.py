@@ -16,9 +16,9 @@ iterations (pinned-host batch H2D, forward, backward, DPKFAC.step(),
 optimizer.step(), loss D2H).
 
 ``--impl reference`` times the reference algorithm on the host CPU (the
-float64 oracle port of kfaclab's kfac.py, all host threads) on a bounded,
-rotating sample of the same layers, extrapolated to a whole update by the
-per-layer cost model.
+float64 oracle port of kfaclab's kfac.py, all host threads): each step is a
+bounded, rotating 1/9 of the layers; the full-update time is the sum of every
+layer's median MEASURED time (no cost-model extrapolation).
 """
 
 from __future__ import annotations
@@ -48,7 +48,7 @@ def parse():
     ap.add_argument("--inv-type", default="inverse", choices=["inverse", "eigen"])
     ap.add_argument("--gamma", type=float, default=0.002)
     ap.add_argument("--xi", type=float, default=0.95)      # reference default (kfac.py:61)
-    ap.add_argument("--precision", default="tf32", choices=["tf32", "3xtf32"])
+    ap.add_argument("--precision", default="auto", choices=["auto", "tf32", "3xtf32"])
     ap.add_argument("--nchw", action="store_true",
                     help="keep the conv model NCHW (default: channels_last, the B200-native layout)")
     # north_star: "layers are assigned to GPUs by a load balancer" -> the LPT balancer
@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--early", action="store_true",
                     help="e2e: launch the larger size classes' factor/inverse pipeline from the backward hooks")
+    ap.add_argument("--ncu-step", action="store_true",
+                    help="profiling helper: after warm-up run ONE serialized step between cudaProfilerStart/Stop "
+                         "with NVTX stage ranges (DPK_NVTX) and exit without a result line")
     return ap.parse_args()
 
 
@@ -150,23 +153,21 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------- CPU reference (oracle port)
-def cpu_reference_sample(geom, group: int, groups: int, inv_type: str, gamma: float, xi: float, seed: int = 0):
-    """Run the reference algorithm (float64 oracle port of kfaclab kfac.py) on the
-    layers i with i % groups == group: factor SYRK (second update, so the EMA
-    blend runs), damped inverses or eigendecompositions, preconditioning.
-    Synthetic captures of the exact unfolded shapes.  Returns (seconds, sample_cost)."""
+def cpu_reference_layers(geom, layers, inv_type: str, gamma: float, xi: float, seed: int = 0):
+    """Time the reference algorithm (float64 oracle port of kfaclab kfac.py:
+    kfac_layer_step = factor SYRK + running-average blend, damped inverses or
+    eigendecompositions, preconditioning) on each listed layer, synthetic captures
+    of the exact unfolded shapes.  Returns {layer index: seconds} -- every number
+    measured, nothing extrapolated."""
     import numpy as np
 
     from oracle import kfac_ref as K  # bench.py's cpu_baseline / reference leg only
-    from paper_2206_15143_b200.partition import layer_cost
 
-    rng = np.random.default_rng(seed + group)
     h = K.Hyper(gamma=gamma, xi=xi, inv_type=inv_type)
-    total = 0.0
-    cost = 0.0
-    for i, (name, d_in, d_out, m, conv) in enumerate(geom):
-        if i % groups != group:
-            continue
+    out = {}
+    for i in layers:
+        _, d_in, d_out, m, _ = geom[i]
+        rng = np.random.default_rng(seed + i)
         x = np.maximum(rng.standard_normal((d_in, m)), 0.0)
         x[-1] = 1.0
         g = rng.standard_normal((d_out, m)) * 1e-2
@@ -176,10 +177,9 @@ def cpu_reference_sample(geom, group: int, groups: int, inv_type: str, gamma: fl
         K.update_running_average(st, a0, g0, xi, 0)  # initialised state: the timed update blends
         t0 = time.perf_counter()
         K.kfac_layer_step(st, x, g, grad, h, 1)
-        total += time.perf_counter() - t0
-        cost += layer_cost(d_in, d_out, m, inv_type)
+        out[i] = time.perf_counter() - t0
         del x, g
-    return total, cost
+    return out
 
 
 def host_threads():
@@ -190,36 +190,53 @@ def host_threads():
 
 
 def run_reference(args, rank, world):
-    """--impl reference: rank 0 times the CPU reference on rotating bounded samples."""
+    """--impl reference: rank 0 times the CPU reference.  Step s runs the layers
+    i % G == s % G (G = 9 groups for the 54-layer ResNet-50, so one step is ~1/9
+    of an update and the whole run fits a few minutes); the full-update time is
+    the SUM over all layers of each layer's median measured time (layers the
+    timed steps did not reach are measured after them), never a model estimate."""
     if rank != 0:
         return
     import bench_models as BM
-    from paper_2206_15143_b200.partition import layer_cost
 
     ctor, batch, shape, classes = BM.WORKLOADS[args.model]
     geom = BM.layer_geometry(ctor(), shape, batch)
-    full_cost = sum(layer_cost(d_in, d_out, m, args.inv_type) for _, d_in, d_out, m, _ in geom)
-    groups = 9 if len(geom) > 20 else 1
-    est = []
+    n = len(geom)
+    groups = 9 if n > 20 else 1
+    per_layer: dict = {}
+    step_ms = []
     for s in range(args.warmup + args.steps):
-        secs, c = cpu_reference_sample(geom, s % groups, groups, args.inv_type, args.gamma, args.xi)
-        if s >= args.warmup and c > 0:
-            est.append(secs * full_cost / c)
-    ms = 1000.0 * statistics.median(est)
+        layers = [i for i in range(n) if i % groups == s % groups]
+        t0 = time.perf_counter()
+        got = cpu_reference_layers(geom, layers, args.inv_type, args.gamma, args.xi)
+        wall = time.perf_counter() - t0
+        if s >= args.warmup:
+            step_ms.append(1000.0 * wall)
+            for i, sec in got.items():
+                per_layer.setdefault(i, []).append(sec)
+    missing = [i for i in range(n) if i not in per_layer]
+    extra = cpu_reference_layers(geom, missing, args.inv_type, args.gamma, args.xi)
+    for i, sec in extra.items():
+        per_layer.setdefault(i, []).append(sec)
+    ms_iter = 1000.0 * sum(statistics.median(v) for v in per_layer.values())
     # P ranks of the simulated cluster run their owned layers sequentially (distsim.py:310-329),
     # so the reference's whole-job iteration time does not shrink with P: samples/s = B*P / t.
-    value = batch * world / (ms / 1000.0)
+    value = batch * world / (ms_iter / 1000.0)
+    sample = (f"step s = layers i % {groups} == s % {groups} of {n} (synthetic captures of the exact unfolded "
+              "shapes), kfac_layer_step in float64 numpy/scipy (OpenBLAS, all host threads); value = one "
+              "full update = sum over all layers of each layer's median measured seconds "
+              f"({min(len(v) for v in per_layer.values())}-{max(len(v) for v in per_layer.values())} "
+              f"samples per layer{'; ' + str(len(missing)) + ' layers measured after the timed steps' if missing else ''})")
     line = {
         "metric": METRIC, "impl": "reference", "value": value, "unit": "samples/s", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "iter_per_s": 1000.0 / ms,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.median(step_ms),
+        "ms_per_iter": ms_iter, "iter_per_s": 1000.0 / ms_iter,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.model} DP-KFAC 2nd-order update, batch {batch}/GPU, {args.inv_type}",
-                   "model": args.model, "global_batch": batch * world, "parallelism": f"dp{world}"},
+                   "model": args.model, "global_batch": batch * world, "parallelism": f"dp{world}",
+                   "step": f"one bounded sample = 1/{groups} of the layers; ms_per_iter = the full update"},
         "cpu_baseline": {"value": value, "unit": "samples/s", "cores": host_threads(), "kind": "port",
-                         "sample": f"per step: layers i % {groups} == step % {groups} of {len(geom)} "
-                                   "(synthetic captures of the exact unfolded shapes), kfac_layer_step in "
-                                   "float64 numpy/scipy (OpenBLAS, all host threads), extrapolated to all "
-                                   "layers by the per-layer flop model; median over timed steps"},
+                         "ms_per_iter": ms_iter, "sample": sample},
         "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     emit(line)
@@ -234,7 +251,6 @@ def run_ours(args, rank, world, local_rank):
 
     import bench_models as BM
     from paper_2206_15143_b200 import DPKFAC, _lib
-    from paper_2206_15143_b200.partition import layer_cost
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
@@ -288,6 +304,20 @@ def run_ours(args, rank, world, local_rank):
         kf.step()
     kf.check()
     sync_barrier()
+    if args.ncu_step:  # ncu --profile-from-start off --nvtx --nvtx-include "<stage>/" ...
+        kf.overlap = False
+        restore()
+        kf.step()
+        sync_barrier()
+        kf.nvtx = True
+        restore()
+        torch.cuda.cudart().cudaProfilerStart()
+        kf.step()
+        sync_barrier()
+        torch.cuda.cudart().cudaProfilerStop()
+        kf.check()
+        kf.remove_hooks()
+        return
     launches0 = lib.dpk_launch_count()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     # DPK_PROFILE_TIMED=1: bracket exactly the timed steps for `ncu --profile-from-start off`
@@ -340,14 +370,25 @@ def run_ours(args, rank, world, local_rank):
     if os.path.exists(pk):
         with open(pk) as f:
             peaks = json.load(f)
-    bf16 = peaks.get("bf16_tflops")
-    tf32_peak = (bf16 / 2.0) if bf16 else 1590.0 / 2.0
-    peak_src = ("MEASURED_PEAKS.json bf16_tflops / 2 (tcgen05 kind::tf32 issues at half the bf16 rate)"
-                if bf16 else "B200_PROFILING.md fallback 1.59 PF bf16 / 2")
+    bf16 = peaks.get("bf16_tflops") or 1590.0  # f16 and bf16 issue at the same kind::f16 rate
+    bf16_src = "MEASURED_PEAKS.json bf16_tflops" if peaks.get("bf16_tflops") else "B200_PROFILING.md fallback"
+    tf32_peak, tf32_src = bf16 / 2.0, bf16_src + " / 2 (kind::tf32 issues at half the f16 rate)"
+    tp = os.path.join(ROOT, "profiles", "tf32_peak.json")  # scripts/tf32_peak.py, measured on a B200
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tpj = json.load(f)
+        tf32_peak = tpj["tf32_peak_tflops"]
+        tf32_src = ("profiles/tf32_peak.json: measured 8192^3 TF32 matmul, best of 10 (max of cuBLAS "
+                    f"{tpj['cublas_tf32_tflops']:.0f} and this engine {tpj['dpk_tf32_tflops']:.0f} TF/s)")
     own = [geom[ly.index] for ly in kf.owned]
+    f16_a = {ly.index for ly in kf.layers if ly.patch16 is not None}  # conv A factors on kind::f16
     built = geom if args.algorithm != "dp_kfac" else own  # MPD: every rank builds every layer's factors
+    built_idx = range(len(geom)) if args.algorithm != "dp_kfac" else [ly.index for ly in kf.owned]
+    syrk_f16 = sum(geom[i][1] * (geom[i][1] + 1) * geom[i][3] for i in built_idx if i in f16_a)
+    syrk_all = sum(d_in * (d_in + 1) * m + d_out * (d_out + 1) * m for _, d_in, d_out, m, _ in built)
+    fac_passes = 3.0 if kf.precision == "3xtf32" else 1.0
     flops = {
-        "factors": sum(d_in * (d_in + 1) * m + d_out * (d_out + 1) * m for _, d_in, d_out, m, _ in built),
+        "factors": syrk_all,
         # inverse mode: Cholesky n^3/3 + triangular inverse n^3/3 (the optimizer keeps
         # A^-1 = X^T X factored, so potri's X^T X product is not part of the step)
         "inversion": sum((2.0 / 3.0) * (float(d_in) ** 3 + float(d_out) ** 3) for _, d_in, d_out, m, _ in own)
@@ -355,30 +396,47 @@ def run_ours(args, rank, world, local_rank):
         "precondition": sum(2.0 * (d_out * d_out * d_in + d_out * d_in * d_in) * (1 if args.inv_type == "inverse" else 2)
                             for _, d_in, d_out, m, _ in own),
     }
+    # ideal (roofline) time of each stage at the peak of the precision its MMAs run in:
+    # factors = kind::f16 conv patches at the f16 peak + the rest at tf32 (x3 passes if
+    # 3xtf32); inversion / precondition = 3xTF32 products (tf32 peak / 3)
+    ideal_ms = {"factors": 1e3 * (syrk_f16 / (bf16 * 1e12) + fac_passes * (syrk_all - syrk_f16) / (tf32_peak * 1e12)),
+                "inversion": 1e3 * 3.0 * flops["inversion"] / (tf32_peak * 1e12),
+                "precondition": 1e3 * 3.0 * flops["precondition"] / (tf32_peak * 1e12)}
     compute_stages = {k: stages.get(k, 0.0) for k in flops}
     dom = max(compute_stages, key=compute_stages.get)
     achieved = flops[dom] / (compute_stages[dom] / 1000.0) / 1e12 if compute_stages[dom] > 0 else 0.0
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    traffic, traffic_src = None, None
+    prof = os.path.join(ROOT, "profiles", "stage_traffic.json")  # scripts/stage_traffic.sh (ncu, HEAD)
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                t = json.load(f).get(dom)
-                traffic = t.get("bytes") if isinstance(t, dict) else t
-        except (OSError, ValueError):
+                tj = json.load(f)
+            st_ = tj.get("stages", {}).get(dom)
+            if st_ and tj.get("model") == args.model and tj.get("inv_type") == args.inv_type and world == 1:
+                traffic = st_["dram_bytes"]
+                traffic_src = (f"profiles/stage_traffic.json: sum of dram__bytes_read+write over the "
+                               f"{st_['launches']} kernels of the {dom} stage of one serialized step (ncu, "
+                               f"commit {tj.get('commit', '?')})")
+        except (OSError, ValueError, KeyError):
             traffic = None
     three_pass = dom in ("inversion", "precondition")
     roofline = {"bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
-                "frac": achieved / tf32_peak, "traffic": traffic, "kernel": dom,
-                "peak_source": peak_src,
+                "frac": achieved / tf32_peak, "traffic": traffic, "traffic_source": traffic_src, "kernel": dom,
+                "peak_source": tf32_src,
                 "frac_of_3xtf32_ceiling": (3.0 * achieved / tf32_peak) if three_pass else None,
+                "frac_of_stage_roofline": ideal_ms[dom] / compute_stages[dom] if compute_stages[dom] > 0 else None,
                 "note": ("fp32-grade stage: every product is 3 tf32 MMA passes (3xTF32), so its tensor-core "
-                         "ceiling is peak/3" if three_pass else "1-pass tf32 (RN) stage"),
+                         "ceiling is peak/3" if three_pass else "mixed kind::f16 / tf32 stage"),
                 "algorithmic_work": f"{dom}: {flops[dom] / 1e12:.4f} TFLOP per step (SURVEY 8(d) conventions)"}
     stage_roofline = {k: {"ms": compute_stages[k], "tflops": (flops[k] / (compute_stages[k] / 1000.0) / 1e12)
                           if compute_stages[k] > 0 else None,
                           "frac_of_tf32": ((flops[k] / (compute_stages[k] / 1000.0) / 1e12) / tf32_peak)
-                          if compute_stages[k] > 0 else None} for k in flops}
+                          if compute_stages[k] > 0 else None,
+                          "ideal_ms": ideal_ms[k],
+                          "frac_of_stage_roofline": ideal_ms[k] / compute_stages[k] if compute_stages[k] > 0 else None}
+                      for k in flops}
+    stage_roofline["factors"]["f16_flops_share"] = syrk_f16 / syrk_all if syrk_all else 0.0
+    stage_roofline["peaks_tflops"] = {"f16": bf16, "tf32": tf32_peak, "3xtf32": tf32_peak / 3.0}
 
     # ---- e2e through the public API: pinned H2D + fwd + bwd + DPKFAC.step() + SGD + loss D2H
     e2e = None
@@ -421,21 +479,27 @@ def run_ours(args, rank, world, local_rank):
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        full_cost = sum(layer_cost(d_in, d_out, m, args.inv_type) for _, d_in, d_out, m, _ in geom)
-        groups = 9 if len(geom) > 20 else 1
-        secs, c = cpu_reference_sample(geom, 0, groups, args.inv_type, args.gamma, args.xi)
-        cpu_ms = 1000.0 * secs * full_cost / c
+        # every layer once (the same per-layer measurement as --impl reference): ~15 s
+        # of host work for ResNet-50 in inverse mode
+        per = cpu_reference_layers(geom, range(len(geom)), args.inv_type, args.gamma, args.xi)
+        cpu_ms = 1000.0 * sum(per.values())
         cpu_baseline = {"value": batch / (cpu_ms / 1000.0), "unit": "samples/s", "cores": host_threads(),
                         "kind": "port", "ms_per_iter": cpu_ms,
-                        "sample": f"layers i % {groups} == 0 of {len(geom)} (synthetic captures of the exact "
-                                  "unfolded shapes), float64 kfac_layer_step (oracle port of kfaclab kfac.py, "
-                                  "numpy/scipy OpenBLAS, all host threads), extrapolated by the per-layer flop model"}
+                        "sample": f"all {len(geom)} layers once (synthetic captures of the exact unfolded shapes), "
+                                  "float64 kfac_layer_step (oracle port of kfaclab kfac.py, numpy/scipy "
+                                  "OpenBLAS, all host threads), summed -- measured, not extrapolated"}
 
+    if kf.precision == "tf32":
+        dtype_label = ("f32 (conv A-factor patches as fp16 with an exact power-of-two prescale from a fused amax "
+                       "-> tcgen05 kind::f16 SYRK, fp32 accumulate; other factors 1-pass RN tf32; inverse and "
+                       "precondition 3xtf32)" if f16_a else "f32 (1-pass RN tf32 factors; 3xtf32 inverse/precondition)")
+    else:
+        dtype_label = "f32 (3xtf32 factors, inverse/eigen and precondition)"
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "iter_per_s": 1000.0 / ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32 (tf32 tensor-core factors, 3xtf32 inverse/precondition)" if args.precision == "tf32" else "f32 (3xtf32)",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype_label,
             "data": "synthetic (randn images, random labels, torch.manual_seed(0) random-init weights)",
             "config": {"workload": f"{args.model} DP-KFAC 2nd-order update, batch {batch}/GPU, "
                                    f"inv_type={args.inv_type}, gamma={args.gamma}, xi={args.xi}, F=K=1",

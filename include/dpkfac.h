@@ -113,6 +113,11 @@ typedef struct dpk_factor_job {
   float* factor;
   float alpha;
   float beta;
+  /* Optional (may be NULL): device int32 holding the float bits of amax|X| when the
+   * operand stores the power-of-two prescaled values X * 2^-e (the fp16 patches of
+   * dpk_im2col_materialize_f16 with dpk_im2col_job.amax set); the epilogue then
+   * applies alpha * 2^(2e), exactly.  e = dpk_prescale_exponent(amax). */
+  const int32_t* x_amax;
 } dpk_factor_job;
 
 size_t dpk_factor_workspace_bytes(const dpk_factor_job* jobs, int n_jobs);
@@ -136,12 +141,24 @@ typedef struct dpk_im2col_job {
   dpk_operand x; /* DPK_OPND_IM2COL or DPK_OPND_IM2COL_TAPMAJOR */
   float* out;
   int64_t ld;
+  /* fp16 patches only, optional (NULL = no scaling): device int32 written by
+   * dpk_im2col_amax (the float bits of amax|X|, the bias ones row included).  The
+   * fp16 kernel then stores half(X * 2^-e) with e = floor(log2 amax) - 14, so the
+   * largest patch value lands in [2^14, 2^15): nothing can overflow the fp16 range
+   * (65504) and small values sit as far above the subnormals as possible; pass the
+   * same pointer as dpk_factor_job.x_amax so the SYRK undoes the scale exactly. */
+  int32_t* amax;
 } dpk_im2col_job;
 
 int dpk_im2col_materialize(const dpk_im2col_job* jobs, int n_jobs, dpk_stream_t stream);
 /* The same patch values as fp16, FEATURE-major: out[r*ld + k] = half(X[r, k])
  * (round to nearest), ld >= cols and ld % 8 == 0; read back as DPK_OPND_ROWS_K_F16. */
 int dpk_im2col_materialize_f16(const dpk_im2col_job* jobs, int n_jobs, dpk_stream_t stream);
+/* amax|X| of every job's implicit-im2col view (= amax over the conv input, or 1 with
+ * a bias row, whichever is larger) into *jobs[i].amax as float bits (non-finite
+ * inputs propagate: the factor then fails as non-SPD, never silently).  One launch;
+ * jobs without an amax pointer are skipped. */
+int dpk_im2col_amax(const dpk_im2col_job* jobs, int n_jobs, dpk_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * Grouped tensor-core GEMM used by preconditioning (and exposed for tests):

@@ -33,11 +33,12 @@ class Operand(C.Structure):
 
 
 class FactorJob(C.Structure):
-    _fields_ = [("x", Operand), ("factor", C.c_void_p), ("alpha", C.c_float), ("beta", C.c_float)]
+    _fields_ = [("x", Operand), ("factor", C.c_void_p), ("alpha", C.c_float), ("beta", C.c_float),
+                ("x_amax", C.c_void_p)]
 
 
 class Im2colJob(C.Structure):
-    _fields_ = [("x", Operand), ("out", C.c_void_p), ("ld", C.c_int64)]
+    _fields_ = [("x", Operand), ("out", C.c_void_p), ("ld", C.c_int64), ("amax", C.c_void_p)]
 
 
 class GemmJob(C.Structure):
@@ -96,6 +97,7 @@ _SIGNATURES = [
     ("dpk_conv_im2col_syrk_ema", C.c_int, [C.POINTER(FactorJob), C.c_int, _P, C.c_size_t, C.c_int, _P]),
     ("dpk_im2col_materialize", C.c_int, [C.POINTER(Im2colJob), C.c_int, _P]),
     ("dpk_im2col_materialize_f16", C.c_int, [C.POINTER(Im2colJob), C.c_int, _P]),
+    ("dpk_im2col_amax", C.c_int, [C.POINTER(Im2colJob), C.c_int, _P]),
     ("dpk_gemm_workspace_bytes", C.c_size_t, [C.POINTER(GemmJob), C.c_int]),
     ("dpk_gemm", C.c_int, [C.POINTER(GemmJob), C.c_int, _P, C.c_size_t, C.c_int, _P]),
     ("dpk_trace_pi", C.c_int, [C.POINTER(PiJob), C.c_int, C.c_float, _P]),

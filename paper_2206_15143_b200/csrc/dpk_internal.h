@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 #include <string>
@@ -20,6 +21,16 @@ unsigned long long launch_counter();
 void set_launch_counter(unsigned long long v);  // captures launch nothing: undo their counts
 int cuda_status(cudaError_t e, const char* what);
 int num_sms();
+
+// Function attributes (cudaFuncSetAttribute) apply to the CURRENT device only:
+// true the first time it is called for a given flag word on the current device.
+// Usage: static std::atomic<uint64_t> done{0}; if (first_on_device(done)) {...}
+inline bool first_on_device(std::atomic<uint64_t>& done) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return true;
+  const uint64_t bit = 1ull << dev;
+  return (done.fetch_or(bit, std::memory_order_relaxed) & bit) == 0;
+}
 
 // -------------------------------------------------------------- GEMM engine
 enum { EPI_LINEAR = 0, EPI_EIGDIV = 1 };
@@ -40,7 +51,19 @@ struct GemmSpec {
   // upper triangle of the output is left as it was, or -- on diagonal tiles --
   // receives the full product)
   int lower_only = 0;
+  // optional: device float bits of amax|operand| -- the operands hold X * 2^-e
+  // (fp16 prescaled patches), the epilogue multiplies alpha by 2^(2e)
+  const int32_t* alpha_amax = nullptr;
 };
+
+// Power-of-two prescale of fp16 patch operands (dpk_im2col_job.amax): the largest
+// magnitude lands in [2^14, 2^15).  Shared by the patch writers and the SYRK epilogue.
+__host__ __device__ inline int prescale_exponent(int32_t amax_bits) {
+  const uint32_t u = static_cast<uint32_t>(amax_bits) & 0x7fffffffu;
+  const int be = static_cast<int>(u >> 23);
+  if (be == 0 || be == 255) return 0;  // zero/subnormal amax, or inf/nan: no scaling
+  return (be - 127) - 14;
+}
 constexpr int TRI_NONE = 0;
 constexpr int TRI_LOWER = 1;  // op[r][k] == 0 for k > r
 constexpr int TRI_UPPER = 2;  // op[r][k] == 0 for k < r
@@ -127,6 +150,7 @@ inline void key_spec(std::string& k, const GemmSpec& g) {
   key_put(k, g.tri_a);
   key_put(k, g.tri_b);
   key_put(k, g.lower_only);
+  key_put(k, g.alpha_amax);
 }
 
 // Kernel launch with optional programmatic dependent launch (DPK_PDL=1) and an

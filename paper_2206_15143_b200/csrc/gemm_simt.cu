@@ -186,7 +186,7 @@ bool simt_eligible(const GemmSpec* specs, int n, int precision) {
     const GemmSpec& g = specs[i];
     const dpk_operand& a = g.job.a;
     const dpk_operand& b = g.job.b;
-    if (g.epi != EPI_LINEAR || g.out_t) return false;
+    if (g.epi != EPI_LINEAR || g.out_t || g.alpha_amax) return false;
     for (const dpk_operand* o : {&a, &b})
       if ((o->kind != DPK_OPND_ROWS_K && o->kind != DPK_OPND_ROWS_MN) || o->bias_row) return false;
     if (a.rows > 640 || b.rows > 640 || a.cols > 640) return false;

@@ -96,6 +96,7 @@ struct alignas(64) Problem {
   int64_t ldt;
   int64_t ldo;
   int64_t ldc;
+  const int32_t* alpha_amax;  // optional: prescaled fp16 operands, alpha *= 2^(2e)
   float alpha, beta, gamma;
   int M, N;
   int symmetric, same_ab, epi;  // symmetric: 1 lower tiles + mirror, 2 lower tiles only
@@ -563,6 +564,7 @@ __device__ __forceinline__ Epi load_epi(const Problem& P, int tile, int split) {
   e.ldc = pin(P.ldc);
   e.ldt = pin(P.ldt);
   e.alpha = pin(P.alpha);
+  if (P.alpha_amax) e.alpha = ldexpf(e.alpha, 2 * prescale_exponent(__ldg(P.alpha_amax)));
   e.beta = pin(P.beta);
   e.gamma = pin(P.gamma);
   e.M = pin(P.M);
@@ -1097,6 +1099,7 @@ struct RedJob {
   const float* partials;
   float* out_t;
   int64_t ldo, ldc, ldt;
+  const int32_t* alpha_amax;
   float alpha, beta, gamma;
   int M, N, symmetric, epi, tiles_n, splits;
   int ut;          // unit tile edge (128 or 256)
@@ -1164,11 +1167,12 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
   for (int q = 0; q < 4; ++q) acc[q] = (acc4[0][q] + acc4[1][q]) + (acc4[2][q] + acc4[3][q]);
   const int gn = gn0 + tx;
   const float vc = (J.epi == EPI_EIGDIV && gn < J.N) ? fmaxf(J.vcol[gn], 0.0f) : 0.0f;
+  const float alpha = J.alpha_amax ? ldexpf(J.alpha, 2 * prescale_exponent(__ldg(J.alpha_amax))) : J.alpha;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int r = ty + 8 * q;
     const int gm = gm0 + r;
-    float val = J.alpha * acc[q];
+    float val = alpha * acc[q];
     const bool in = gm < J.M && gn < J.N;
     if (J.epi == EPI_EIGDIV) {
       val = in ? val / (fmaxf(J.vrow[gm], 0.0f) * vc + J.gamma) : 0.0f;
@@ -1513,6 +1517,7 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
     P.ldo = j.ldo;
     P.ldc = j.ldc;
     P.alpha = j.alpha;
+    P.alpha_amax = specs[i].alpha_amax;
     P.beta = j.beta;
     P.M = operand_rows(j.a);
     P.N = operand_rows(j.b);
@@ -1689,6 +1694,7 @@ int launch_reduce(const std::vector<Problem>& probs, int ut, cudaStream_t st) {
     J.ldc = P.ldc;
     J.ldt = P.ldt;
     J.alpha = P.alpha;
+    J.alpha_amax = P.alpha_amax;
     J.beta = P.beta;
     J.gamma = P.gamma;
     J.M = P.M;
@@ -1707,9 +1713,9 @@ int launch_reduce(const std::vector<Problem>& probs, int ut, cudaStream_t st) {
 template <int NPASS, bool RN, int CG>
 int launch_batch(const Batch& bt, cudaStream_t st) {
   using C = Cfg<NPASS>;
-  static bool configured = false;
+  static std::atomic<uint64_t> configured_on{0};
   static int max_pairs = 0;
-  if (!configured) {
+  if (first_on_device(configured_on)) {
     cudaError_t e =
         cudaFuncSetAttribute(tc_gemm_kernel<NPASS, RN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SM_EXCL);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(tc_gemm_kernel)");
@@ -1730,7 +1736,6 @@ int launch_batch(const Batch& bt, cudaStream_t st) {
       if (e != cudaSuccess) return cuda_status(e, "cudaOccupancyMaxActiveClusters(tc_gemm_kernel)");
       max_pairs = std::max(clusters, 1);
     }
-    configured = true;
   }
   // persistent CTAs (CTA pairs) walk the units round-robin; DPK_UNITS_PER_CTA
   // caps how many units one CTA takes, so long launches hand SMs back to the
@@ -2006,6 +2011,7 @@ static std::vector<dpk::GemmSpec> factor_specs(const dpk_factor_job* jobs, int n
     g.beta = jobs[i].beta;
     g.symmetric = 1;
     specs[i] = dpk::GemmSpec{g, dpk::EPI_LINEAR, nullptr, nullptr, 0.f, nullptr, 0, 0, 0};
+    specs[i].alpha_amax = jobs[i].x_amax;
   }
   return specs;
 }

@@ -252,6 +252,7 @@ __global__ void __launch_bounds__(256) im2col_k16_tiled_kernel(const __grid_cons
     pow_[h] = rem - poh[h] * o.OW;
   }
   const int nrg = (o.rows + 31) / 32;
+  const float sc = J.amax ? ldexpf(1.0f, -prescale_exponent(__ldg(J.amax))) : 1.0f;  // exact 2^-e
   for (int g = 0; g < K16_GROUPS; ++g) {
     const int rg = gb * K16_GROUPS + g;
     if (rg >= nrg) break;
@@ -270,10 +271,10 @@ __global__ void __launch_bounds__(256) im2col_k16_tiled_kernel(const __grid_cons
         v = __ldg(reinterpret_cast<const float4*>(o.data + static_cast<int64_t>(pn[h]) * o.sn +
                                                   static_cast<int64_t>(ih) * o.shs + static_cast<int64_t>(iw) * o.sws +
                                                   c0) + qq);
-      Tb[4 * qq][p] = v.x;
-      Tb[4 * qq + 1][p] = v.y;
-      Tb[4 * qq + 2][p] = v.z;
-      Tb[4 * qq + 3][p] = v.w;
+      Tb[4 * qq][p] = v.x * sc;
+      Tb[4 * qq + 1][p] = v.y * sc;
+      Tb[4 * qq + 2][p] = v.z * sc;
+      Tb[4 * qq + 3][p] = v.w * sc;
     }
     __syncthreads();  // (double-buffered T: one barrier per group)
     const int row = threadIdx.x >> 3, seg = threadIdx.x & 7;
@@ -298,6 +299,7 @@ __global__ void __launch_bounds__(256) im2col_k16_generic_kernel(const __grid_co
   const int ohw = o.OH * o.OW;
   const int64_t total = static_cast<int64_t>(d) * o.cols;
   __half* out = reinterpret_cast<__half*>(J.out);
+  const float sc = J.amax ? ldexpf(1.0f, -prescale_exponent(__ldg(J.amax))) : 1.0f;  // exact 2^-e
   for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int r = static_cast<int>(e / o.cols);
@@ -325,7 +327,7 @@ __global__ void __launch_bounds__(256) im2col_k16_generic_kernel(const __grid_co
         v = __ldg(o.data + static_cast<int64_t>(n) * o.sn + static_cast<int64_t>(c) * o.sc +
                   static_cast<int64_t>(ih) * o.shs + static_cast<int64_t>(iw) * o.sws);
     }
-    out[static_cast<int64_t>(r) * J.ld + k] = __float2half_rn(v);
+    out[static_cast<int64_t>(r) * J.ld + k] = __float2half_rn(v * sc);
   }
 }
 
@@ -364,6 +366,7 @@ __global__ void __launch_bounds__(ROWS_THREADS) im2col_k16_rows_kernel(const __g
   const int64_t nrows = o.cols / o.OW;
   const int segs = o.OW / 8;
   const int shift = o.sw * o.C;
+  const float sc = J.amax ? ldexpf(1.0f, -prescale_exponent(__ldg(J.amax))) : 1.0f;  // exact 2^-e
   for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
     const int n = static_cast<int>(row / o.OH);
     const int oh = static_cast<int>(row - static_cast<int64_t>(n) * o.OH);
@@ -393,12 +396,61 @@ __global__ void __launch_bounds__(ROWS_THREADS) im2col_k16_rows_kernel(const __g
         const int ow0 = sgi * 8 + 2 * e;
         const float a = t >= 0 ? stage[t + ow0 * shift] : (t == -2 ? 1.0f : 0.0f);
         const float c2 = t >= 0 ? stage[t + (ow0 + 1) * shift] : (t == -2 ? 1.0f : 0.0f);
-        hv[e] = __floats2half2_rn(a, c2);
+        hv[e] = __floats2half2_rn(a * sc, c2 * sc);
       }
       __stcs(reinterpret_cast<uint4*>(out + static_cast<int64_t>(r) * J.ld + sgi * 8),
              *reinterpret_cast<const uint4*>(hv));
     }
   }
+}
+
+// ---------------------------------------------------------------- amax for the fp16 prescale
+// grid (x: blocks striding over the input, y: job).  Dense inputs (the four strides
+// a permutation of a packed layout, any memory format) are read as one flat range
+// (float4 when aligned); others element by element through the strides.  |x| as
+// int bits is order-preserving for non-negative floats (NaN bits sort above inf).
+__global__ void amax_zero_kernel(const __grid_constant__ I2cBatch b) {
+  for (int i = threadIdx.x; i < b.n; i += blockDim.x)
+    if (b.j[i].amax) *b.j[i].amax = b.j[i].x.bias_row ? __float_as_int(1.0f) : 0;
+}
+
+__device__ __forceinline__ int abs_bits(float v) { return __float_as_int(v) & 0x7fffffff; }
+
+__global__ void __launch_bounds__(256) amax_kernel(const __grid_constant__ I2cBatch b) {
+  const dpk_im2col_job& J = b.j[blockIdx.y];
+  if (!J.amax) return;
+  const dpk_operand& o = J.x;
+  const int64_t numel = static_cast<int64_t>(o.cols / (static_cast<int64_t>(o.OH) * o.OW)) * o.C * o.H * o.W;
+  const int64_t nb = o.cols / (static_cast<int64_t>(o.OH) * o.OW);
+  int m = 0;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t first = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  // dense: max offset + 1 == numel (strides a permutation of a packed layout)
+  const int64_t span = (nb - 1) * o.sn + (o.C - 1) * o.sc + (o.H - 1) * o.shs + (o.W - 1) * o.sws + 1;
+  if (span == numel) {
+    if ((reinterpret_cast<uintptr_t>(o.data) & 15) == 0) {
+      const float4* p4 = reinterpret_cast<const float4*>(o.data);
+      for (int64_t e = first; e < numel / 4; e += stride) {
+        const float4 v = __ldg(p4 + e);
+        m = max(m, max(max(abs_bits(v.x), abs_bits(v.y)), max(abs_bits(v.z), abs_bits(v.w))));
+      }
+      for (int64_t e = (numel / 4) * 4 + first; e < numel; e += stride) m = max(m, abs_bits(__ldg(o.data + e)));
+    } else {
+      for (int64_t e = first; e < numel; e += stride) m = max(m, abs_bits(__ldg(o.data + e)));
+    }
+  } else {
+    const int64_t hw = static_cast<int64_t>(o.H) * o.W, chw = o.C * hw;
+    for (int64_t e = first; e < numel; e += stride) {
+      const int64_t n = e / chw;
+      int64_t r = e - n * chw;
+      const int64_t c = r / hw;
+      r -= c * hw;
+      const int64_t h = r / o.W, w = r - (r / o.W) * o.W;
+      m = max(m, abs_bits(__ldg(o.data + n * o.sn + c * o.sc + h * o.shs + w * o.sws)));
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(J.amax, m);
 }
 
 bool k16_rows_ok(const dpk_im2col_job& j) {
@@ -430,11 +482,10 @@ extern "C" int dpk_im2col_materialize_f16(const dpk_im2col_job* jobs, int n_jobs
   size_t rsm = 0;
   auto flush_r = [&]() -> int {
     if (rbf.n == 0) return DPK_OK;
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr_on{0};
+    if (dpk::first_on_device(attr_on)) {
       cudaFuncSetAttribute(dpk::im2col_k16_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            dpk::ROWS_SMEM_MAX);
-      attr = true;
     }
     int64_t rows = 0;
     for (int i = 0; i < rbf.n; ++i) rows = std::max<int64_t>(rows, rbf.j[i].x.cols / rbf.j[i].x.OW);
@@ -507,6 +558,43 @@ extern "C" int dpk_im2col_materialize_f16(const dpk_im2col_job* jobs, int n_jobs
   return flush_g();
 }
 
+extern "C" int dpk_im2col_amax(const dpk_im2col_job* jobs, int n_jobs, dpk_stream_t stream) {
+  if (n_jobs == 0) return DPK_OK;
+  if (n_jobs < 0 || jobs == nullptr) {
+    dpk::set_error("dpk_im2col_amax: bad job list");
+    return DPK_EARG;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  thread_local dpk::I2cBatch ab;
+  for (int first = 0; first < n_jobs; first += dpk::I2C_MAX) {
+    const int cnt = std::min(dpk::I2C_MAX, n_jobs - first);
+    ab.n = cnt;
+    int64_t most = 0;
+    for (int i = 0; i < cnt; ++i) {
+      const dpk_im2col_job& j = jobs[first + i];
+      const dpk_operand& o = j.x;
+      if ((o.kind != DPK_OPND_IM2COL && o.kind != DPK_OPND_IM2COL_TAPMAJOR) || o.data == nullptr || o.cols < 1 ||
+          o.OH < 1 || o.OW < 1 ||
+          o.cols % (static_cast<int64_t>(o.OH) * o.OW) != 0) {
+        dpk::set_error("dpk_im2col_amax: invalid job " + std::to_string(first + i));
+        return DPK_EARG;
+      }
+      ab.j[i] = j;
+      most = std::max<int64_t>(most, (o.cols / (static_cast<int64_t>(o.OH) * o.OW)) * o.C * o.H * o.W);
+    }
+    dpk::amax_zero_kernel<<<1, 128, 0, st>>>(ab);
+    dpk::note_launch();
+    int rc = dpk::cuda_status(cudaGetLastError(), "amax_zero_kernel launch");
+    if (rc) return rc;
+    const int gx = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((most / 4 + 255) / 256, 2 * 148)));
+    dpk::amax_kernel<<<dim3(gx, cnt), 256, 0, st>>>(ab);
+    dpk::note_launch();
+    rc = dpk::cuda_status(cudaGetLastError(), "amax_kernel launch");
+    if (rc) return rc;
+  }
+  return DPK_OK;
+}
+
 extern "C" int dpk_im2col_materialize(const dpk_im2col_job* jobs, int n_jobs, dpk_stream_t stream) {
   if (n_jobs == 0) return DPK_OK;
   if (n_jobs < 0 || jobs == nullptr) {
@@ -520,10 +608,9 @@ extern "C" int dpk_im2col_materialize(const dpk_im2col_job* jobs, int n_jobs, dp
   size_t rsmem = 0;
   auto flush_rows = [&]() -> int {
     if (rb.n == 0) return DPK_OK;
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr_on{0};
+    if (dpk::first_on_device(attr_on)) {
       cudaFuncSetAttribute(dpk::im2col_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dpk::ROWS_SMEM_MAX);
-      attr = true;
     }
     int64_t rows = 0;
     for (int i = 0; i < rb.n; ++i) rows = std::max<int64_t>(rows, rb.j[i].x.cols / rb.j[i].x.OW);

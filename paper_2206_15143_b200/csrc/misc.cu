@@ -60,45 +60,44 @@ namespace {
 constexpr int PI_MAX = 256;
 struct PiBatch {
   int n;
-  float root_gamma;
+  double root_gamma;
   dpk_pi_job j[PI_MAX];
 };
 
-__device__ float block_sum(float v) {
-  __shared__ float red[32];
+__device__ double block_sum(double v) {
+  __shared__ double red[32];
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   if (l == 0) red[w] = v;
   __syncthreads();
-  v = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0f;
+  v = (threadIdx.x < (blockDim.x >> 5)) ? red[threadIdx.x] : 0.0;
   if (w == 0)
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   __syncthreads();
   return v;
 }
 
-// One block per layer: tr A, tr G in double (the diagonal is short), then
-// pi = sqrt((trA/dA)/(trG/dG)) on the RAW averaged factors (kfac.py:128-137, 145).
+// One block per layer: tr A, tr G accumulated in double (the diagonal is short:
+// d fp64 adds), then pi = sqrt((trA/dA)/(trG/dG)) in double on the RAW averaged
+// factors (kfac.py:128-137, 145); the shifts are rounded to fp32 once at the end.
 __global__ void trace_pi_kernel(const __grid_constant__ PiBatch b) {
   const dpk_pi_job& J = b.j[blockIdx.x];
-  float sa = 0.f, sg = 0.f;
+  double sa = 0.0, sg = 0.0;
   for (int i = threadIdx.x; i < J.da; i += blockDim.x) sa += J.a[static_cast<int64_t>(i) * (J.da + 1)];
   for (int i = threadIdx.x; i < J.dg; i += blockDim.x) sg += J.g[static_cast<int64_t>(i) * (J.dg + 1)];
   sa = block_sum(sa);
   sg = block_sum(sg);
   if (threadIdx.x == 0) {
-    float sh_a = 0.f, sh_g = 0.f, pi = 0.f;
-    if (!(sa > 0.f) || !(sg > 0.f)) {
+    double pi = 1.0;
+    if (!(sa > 0.0) || !(sg > 0.0)) {
       if (J.info) *J.info = DPK_INFO_TRACE;
-      pi = 1.0f;
     } else {
-      pi = static_cast<float>(sqrt((static_cast<double>(sa) / J.da) / (static_cast<double>(sg) / J.dg)));
+      pi = sqrt((sa / J.da) / (sg / J.dg));
     }
-    sh_a = pi * b.root_gamma;
-    sh_g = b.root_gamma / pi;
-    J.shifts[0] = sh_a;
-    J.shifts[1] = sh_g;
-    if (J.pi) *J.pi = pi;
+    const double rg = static_cast<double>(b.root_gamma);
+    J.shifts[0] = static_cast<float>(pi * rg);
+    J.shifts[1] = static_cast<float>(rg / pi);
+    if (J.pi) *J.pi = static_cast<float>(pi);
   }
 }
 
@@ -214,7 +213,7 @@ int dpk_trace_pi(const dpk_pi_job* jobs, int n_jobs, float gamma, dpk_stream_t s
   for (int first = 0; first < n_jobs; first += dpk::PI_MAX) {
     const int cnt = std::min(dpk::PI_MAX, n_jobs - first);
     b.n = cnt;
-    b.root_gamma = std::sqrt(gamma);
+    b.root_gamma = std::sqrt(static_cast<double>(gamma));
     for (int i = 0; i < cnt; ++i) {
       b.j[i] = jobs[first + i];
       if (b.j[i].a == nullptr || b.j[i].g == nullptr || b.j[i].shifts == nullptr || b.j[i].da < 1 ||

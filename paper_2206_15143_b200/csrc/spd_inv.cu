@@ -616,12 +616,11 @@ void make_spd_plan(const SpdReq* jobs, int n, char* base, SpdPlan& plan) {
 
 template <int NB, int W>
 int launch_leaf_nb(const LeafBatch& b, int cnt, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<uint64_t> configured_on{0};
+  if (first_on_device(configured_on)) {
     cudaError_t e = cudaFuncSetAttribute(spd_leaf_kernel<NB, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          leaf_smem_bytes<NB, W>());
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(spd_leaf_kernel)");
-    configured = true;
   }
   const cudaError_t e = launch_k(spd_leaf_kernel<NB, W>, dim3(cnt), dim3(LEAF_THREADS), leaf_smem_bytes<NB, W>(),
                                  st, 1, b);

@@ -147,6 +147,22 @@ __global__ void __launch_bounds__(JAC_THREADS) jacobi_kernel(const __grid_consta
     if (rot_count == 0) break;
     __syncthreads();
   }
+  // re-normalize V's columns: thousands of rotations with c^2 + s^2 = 1 only to
+  // 1/2 ulp drift the column norms by ~1e-5; orthogonality between columns is
+  // already at the 1e-7 level, so a rescale restores an orthonormal basis.
+  // (8 warps; warp w owns columns w, w+8, ...; lanes stride the rows.)
+  {
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int c = wid; c < n; c += JAC_THREADS / 32) {
+      float ss = 0.f;
+      for (int r = lane; r < n; r += 32) ss = fmaf(V[r * ld + c], V[r * ld + c], ss);
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      const float inv = ss > 0.f ? rsqrtf(ss) : 1.f;
+      const float fix = inv * (1.5f - 0.5f * ss * inv * inv);  // one Newton step: rsqrt to ~1 ulp
+      for (int r = lane; r < n; r += 32) V[r * ld + c] *= fix;
+    }
+  }
+  __syncthreads();
   // rank eigenvalues descending (ties by index) and scatter
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const float wi = A[i * ld + i];
@@ -198,12 +214,11 @@ int dpk_syevd_batched(const dpk_eig_job* jobs, int n_jobs, void* workspace, size
     maxm = std::max(maxm, jobs[i].n + (jobs[i].n & 1));
   }
   const int smem = 2 * maxm * (maxm + 1) * 4;
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<uint64_t> configured_on{0};
+  if (dpk::first_on_device(configured_on)) {
     cudaError_t e = cudaFuncSetAttribute(dpk::jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          2 * dpk::JAC_N * (dpk::JAC_N + 1) * 4);
     if (e != cudaSuccess) return dpk::cuda_status(e, "cudaFuncSetAttribute(jacobi_kernel)");
-    configured = true;
   }
   thread_local dpk::EigBatch b;
   cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -287,10 +287,13 @@ def apply_preconditioner(state: FactorState, grad, hyper: KfacHyper, precision: 
 
 
 def kfac_layer_step(state: FactorState, captured_inputs, captured_preact_grads, grad, hyper: KfacHyper, t: int,
-                    precision: str = "tf32", precond_precision: str = "3xtf32"):
+                    precision: str = "auto", precond_precision: str = "3xtf32"):
     """Factor update if due (fused SYRK+EMA), refresh if due, always precondition
     (kfac.py:257-276).  Returns (preconditioned grad, state).  ``precision``
-    applies to the factor SYRK, ``precond_precision`` to the preconditioning GEMMs."""
+    applies to the factor SYRK ("auto": 3xtf32 for eigen, tf32 for inverse -- the
+    same rule as DPKFAC), ``precond_precision`` to the preconditioning GEMMs."""
+    if precision == "auto":
+        precision = "3xtf32" if hyper.inv_type == "eigen" else "tf32"
     if is_factor_update(t, hyper):
         update_factors_fused(state, captured_inputs, captured_preact_grads, hyper.xi, t, precision)
     if is_inverse_update(t, hyper):

@@ -132,18 +132,27 @@ def operand_rows_k_f16(x: torch.Tensor, cols: int) -> L.Operand:
 
 
 def im2col_materialize_f16(pairs):
-    """pairs: [(im2col operand, out half tensor d x ld)] -> out[r, k] = half(X[r, k]) (feature-major)."""
+    """pairs: [(im2col operand, out half tensor d x ld[, amax int32 slot])] ->
+    out[r, k] = half(X[r, k] * 2^-e) (feature-major).  With an amax slot, one
+    dpk_im2col_amax launch first measures amax|X| and e puts the largest value in
+    [2^14, 2^15) (no fp16 overflow); the SYRK job must carry the same slot
+    (factor_job(..., x_amax=slot)) to undo the scale.  Without it, e = 0."""
     if not pairs:
         return
     jobs = []
-    for op, out in pairs:
+    for pr in pairs:
+        op, out = pr[0], pr[1]
+        amax = pr[2] if len(pr) > 2 else None
         j = L.Im2colJob()
         j.x = op
         j.out = out.data_ptr()
         j.ld = out.stride(0)
+        j.amax = amax.data_ptr() if amax is not None else None
         jobs.append(j)
-    L.check(lib().dpk_im2col_materialize_f16(L.array(L.Im2colJob, jobs), len(jobs), stream_handle()),
-            "dpk_im2col_materialize_f16")
+    arr = L.array(L.Im2colJob, jobs)
+    if any(j.amax for j in jobs):
+        L.check(lib().dpk_im2col_amax(arr, len(jobs), stream_handle()), "dpk_im2col_amax")
+    L.check(lib().dpk_im2col_materialize_f16(arr, len(jobs), stream_handle()), "dpk_im2col_materialize_f16")
 
 
 def im2col_materialize(pairs):
@@ -175,12 +184,15 @@ def syrk_ema(jobs: Sequence[L.FactorJob], precision: str = "tf32", keepalive=Non
             "dpk_syrk_ema")
 
 
-def factor_job(x: L.Operand, factor: torch.Tensor, alpha: float, beta: float) -> L.FactorJob:
+def factor_job(x: L.Operand, factor: torch.Tensor, alpha: float, beta: float,
+               x_amax: Optional[torch.Tensor] = None) -> L.FactorJob:
+    """x_amax: the amax slot of prescaled fp16 patches (see im2col_materialize_f16)."""
     j = L.FactorJob()
     j.x = x
     j.factor = factor.data_ptr()
     j.alpha = alpha
     j.beta = beta
+    j.x_amax = x_amax.data_ptr() if x_amax is not None else None
     return j
 
 

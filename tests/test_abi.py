@@ -37,7 +37,7 @@ def test_struct_layouts_match_header(tmp_path):
     names = {"dpk_operand": L.Operand, "dpk_factor_job": L.FactorJob, "dpk_gemm_job": L.GemmJob,
              "dpk_pi_job": L.PiJob, "dpk_spd_job": L.SpdJob, "dpk_precond_job": L.PrecondJob,
              "dpk_eig_job": L.EigJob, "dpk_segment": L.Segment, "dpk_spd_factor_job": L.SpdFactorJob,
-             "dpk_precond_factor_job": L.PrecondFactorJob}
+             "dpk_precond_factor_job": L.PrecondFactorJob, "dpk_im2col_job": L.Im2colJob}
     prog = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', "int main(void){"]
     for cname in names:
         prog.append(f'printf("{cname} %zu\\n", sizeof({cname}));')

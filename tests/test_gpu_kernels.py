@@ -480,3 +480,49 @@ def test_f16_patches_and_syrk_match_unfold(shape, k, s, p, bias, channels_last):
     torch.cuda.synchronize()
     want, _ = K.compute_factors(want_cols, want_cols[:1])
     assert rel(N(out), want) <= TOL, rel(N(out), want)
+
+
+@pytest.mark.parametrize("scale", [1e6, 1e-9, 1.0])
+@pytest.mark.parametrize("shape,k,s,p,bias,channels_last", [((4, 64, 14, 14), 3, 1, 1, False, True),
+                                                           ((2, 3, 32, 32), 7, 2, 3, False, True),
+                                                           ((2, 16, 8, 8), 3, 1, 1, True, False)])
+def test_f16_patch_prescale_survives_fp16_range(scale, shape, k, s, p, bias, channels_last):
+    """Exact power-of-two prescale from a fused amax (dpk_im2col_amax): activations
+    far beyond 65504 (scale 1e6) or far below the fp16 normals (1e-9) give the same
+    factor as the float64 reference; the patches hold exactly half(x * 2^-e)."""
+    from paper_2206_15143_b200 import ops
+    rng = np.random.default_rng(sum(shape) + k + 7)
+    x = np.maximum(rng.standard_normal(shape), 0) * scale
+    xt = T(x)
+    if channels_last:
+        xt = xt.to(memory_format=torch.channels_last)
+    tap = channels_last and k > 1
+    op = ops.operand_im2col(xt, (k, k), (s, s), (p, p), (1, 1), bias_row=bias, tap_major=tap)
+    cols = K.unfold_columns(x, k, k, s, p, 1, bias)
+    perm = _tap_perm(shape[1], k, k) if tap else np.arange(shape[1] * k * k)
+    if bias:
+        perm = np.concatenate([perm, [cols.shape[0] - 1]])
+    want_cols = cols[perm]
+    d, M = want_cols.shape
+    ld = (M + 7) // 8 * 8
+    patch = torch.full((d, ld), float("nan"), dtype=torch.float16, device=dev())
+    amax = torch.full((1,), -1, dtype=torch.int32, device=dev())
+    ops.im2col_materialize_f16([(op, patch, amax)])
+    torch.cuda.synchronize()
+    am = float(np.abs(want_cols.astype(np.float32)).max())
+    assert amax.view(torch.float32).item() == am
+    e = int(np.floor(np.log2(am))) - 14
+    got = patch[:, :M].float().cpu().numpy()
+    assert np.isfinite(got).all() and np.abs(got).max() < 2.0 ** 15
+    ref = torch.from_numpy(want_cols).float() * (2.0 ** -e)
+    assert np.array_equal(got, ref.half().float().numpy())
+    out = torch.full((d, d), float("nan"), device=dev())
+    for prev in (None, out):  # plain and EMA (beta) epilogues both undo the scale
+        a0 = None if prev is None else N(out).copy()
+        ops.syrk_ema([ops.factor_job(ops.operand_rows_k_f16(patch, M), out, 1.0 / M, 0.0 if prev is None else 0.5,
+                                     x_amax=amax)], "tf32")
+        torch.cuda.synchronize()
+        want, _ = K.compute_factors(want_cols, want_cols[:1])
+        if a0 is not None:
+            want = want + 0.5 * a0
+        assert rel(N(out), want) <= TOL, rel(N(out), want)
