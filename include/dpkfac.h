@@ -332,6 +332,26 @@ int dpk_pack_owner_major(const dpk_segment* segs, int n_segs, float* flat, float
 int dpk_unpack_owner_major(const dpk_segment* segs, int n_segs, const float* flat, float scale,
                            dpk_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * KL-clip of the preconditioned update (north_star; opt-in -- the reference has
+ * none, so DPKFAC defaults it off).  With vg = lr^2 * sum over every
+ * preconditioned layer of <preconditioned grad, grad>, all preconditioned grads are
+ * scaled by nu = min(1, sqrt(kl_clip / |vg|)) (Ba et al. 2017; KAISA).
+ *   dpk_kl_dot: out = <pre, grad> over n floats (fp64 accumulation, deterministic),
+ *     one launch; workspace of dpk_kl_dot_workspace_bytes(), zeroed once (the
+ *     kernel leaves its counter at zero).  Each owner writes its partial into a
+ *     slot of its owner-major chunk, so the all-gather that already carries the
+ *     preconditioned gradients also carries every rank's partial.
+ *   dpk_unpack_owner_major_klclip: the unpack with nu applied in the same pass
+ *     (nu computed on the device from the n_slots partials slot_stride apart).
+ * ------------------------------------------------------------------------ */
+size_t dpk_kl_dot_workspace_bytes(void);
+int dpk_kl_dot(const float* pre, const float* grad, int64_t n, float* out, void* workspace, size_t ws_bytes,
+               dpk_stream_t stream);
+int dpk_unpack_owner_major_klclip(const dpk_segment* segs, int n_segs, const float* flat, float scale,
+                                  const float* kl_slots, int n_slots, int64_t slot_stride, float kl_clip, float lr,
+                                  dpk_stream_t stream);
+
 /* Library / device introspection. */
 const char* dpk_version(void);
 const char* dpk_last_error(void);

@@ -273,24 +273,31 @@ def validate_partition(parts, n_layers: int) -> None:
 # conv linear form (defined by this build at the boundary)
 
 
-def unfold_columns(x_nchw: np.ndarray, kh: int, kw: int, stride: int, pad: int,
-                   dilation: int = 1, bias: bool = False) -> np.ndarray:
+def _pair(v):
+    return (int(v[0]), int(v[1])) if isinstance(v, (tuple, list)) else (int(v), int(v))
+
+
+def unfold_columns(x_nchw: np.ndarray, kh: int, kw: int, stride, pad,
+                   dilation=1, bias: bool = False) -> np.ndarray:
     """im2col of an NCHW batch into the reference's column-per-sample form.
 
     Row order (C_in, kh, kw) == ``weight.view(C_out, -1)`` == ``F.unfold``;
     columns enumerate (n, oh, ow); a ones row is appended LAST when the layer
-    has a bias (reference model.py:140-143).
+    has a bias (reference model.py:140-143).  ``stride``, ``pad`` and
+    ``dilation`` are ints or (h, w) pairs (Inception's 1x7 / 7x1 convs pad
+    (0, 3) / (3, 0)).
     """
+    (sh, sw), (ph, pw), (dh, dw) = _pair(stride), _pair(pad), _pair(dilation)
     n, c, h, w = x_nchw.shape
-    oh = (h + 2 * pad - dilation * (kh - 1) - 1) // stride + 1
-    ow = (w + 2 * pad - dilation * (kw - 1) - 1) // stride + 1
-    xp = np.zeros((n, c, h + 2 * pad, w + 2 * pad), dtype=np.float64)
-    xp[:, :, pad:pad + h, pad:pad + w] = x_nchw
+    oh = (h + 2 * ph - dh * (kh - 1) - 1) // sh + 1
+    ow = (w + 2 * pw - dw * (kw - 1) - 1) // sw + 1
+    xp = np.zeros((n, c, h + 2 * ph, w + 2 * pw), dtype=np.float64)
+    xp[:, :, ph:ph + h, pw:pw + w] = x_nchw
     cols = np.empty((c, kh, kw, n, oh, ow), dtype=np.float64)
     for i in range(kh):
         for j in range(kw):
-            hs, ws = i * dilation, j * dilation
-            cols[:, i, j] = xp[:, :, hs:hs + stride * oh:stride, ws:ws + stride * ow:stride].transpose(1, 0, 2, 3)
+            hs, ws = i * dh, j * dw
+            cols[:, i, j] = xp[:, :, hs:hs + sh * oh:sh, ws:ws + sw * ow:sw].transpose(1, 0, 2, 3)
     out = cols.reshape(c * kh * kw, n * oh * ow)
     if bias:
         out = np.vstack([out, np.ones((1, out.shape[1]))])

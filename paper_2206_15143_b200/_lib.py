@@ -114,6 +114,10 @@ _SIGNATURES = [
     ("dpk_syevd_batched", C.c_int, [C.POINTER(EigJob), C.c_int, _P, C.c_size_t, _P]),
     ("dpk_pack_owner_major", C.c_int, [C.POINTER(Segment), C.c_int, _P, C.c_float, _P]),
     ("dpk_unpack_owner_major", C.c_int, [C.POINTER(Segment), C.c_int, _P, C.c_float, _P]),
+    ("dpk_kl_dot_workspace_bytes", C.c_size_t, []),
+    ("dpk_kl_dot", C.c_int, [_P, _P, C.c_int64, _P, _P, C.c_size_t, _P]),
+    ("dpk_unpack_owner_major_klclip", C.c_int, [C.POINTER(Segment), C.c_int, _P, C.c_float, _P, C.c_int,
+                                                C.c_int64, C.c_float, C.c_float, _P]),
     ("dpk_version", C.c_char_p, []),
     ("dpk_last_error", C.c_char_p, []),
     ("dpk_launch_count", C.c_ulonglong, []),

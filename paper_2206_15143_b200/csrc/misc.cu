@@ -106,8 +106,23 @@ constexpr int SEG_MAX = 128;
 struct SegBatch {
   int n;
   float scale;
+  // unpack only, optional: KL-clip scale nu = min(1, sqrt(kl_clip / (lr^2 |sum_r slot_r|)))
+  // from the per-rank partial <preconditioned, gradient> dots (kl_n slots, kl_stride apart)
+  const float* kl_slots;
+  int64_t kl_stride;
+  int kl_n;
+  float kl_clip, lr2;
   dpk_segment s[SEG_MAX];
 };
+
+__device__ __forceinline__ float kl_scale(const SegBatch& b) {
+  if (!b.kl_slots) return 1.0f;
+  double vg = 0.0;
+  for (int r = 0; r < b.kl_n; ++r) vg += static_cast<double>(__ldg(b.kl_slots + r * b.kl_stride));
+  vg = fabs(vg) * static_cast<double>(b.lr2);
+  if (!(vg > 0.0)) return 1.0f;
+  return static_cast<float>(fmin(1.0, sqrt(static_cast<double>(b.kl_clip) / vg)));
+}
 
 // grid.y = segment; grid.x strides over the segment's rows*(cols_w+has_bias) elements.
 // A plain segment (no bias column, no tap permutation, dense rows, 16-byte aligned
@@ -119,7 +134,7 @@ __global__ void segment_kernel(const __grid_constant__ SegBatch b, float* flat) 
   const int cols = S.cols_w + (S.bias ? 1 : 0);
   const int total = S.rows * cols;
   float* dst = flat + S.offset;
-  const float sc = b.scale;
+  const float sc = PACK ? b.scale : b.scale * kl_scale(b);
   const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
   const bool plain = S.perm_khw == 0 && S.bias == nullptr && S.ldw == S.cols_w &&
                      ((reinterpret_cast<uintptr_t>(S.weight) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
@@ -162,7 +177,9 @@ __global__ void segment_kernel(const __grid_constant__ SegBatch b, float* flat) 
 }
 
 template <bool PACK>
-int run_segments(const dpk_segment* segs, int n, float* flat, float scale, cudaStream_t st) {
+int run_segments(const dpk_segment* segs, int n, float* flat, float scale, cudaStream_t st,
+                 const float* kl_slots = nullptr, int kl_n = 0, int64_t kl_stride = 0, float kl_clip = 0.f,
+                 float lr2 = 0.f) {
   if (n < 0 || (n > 0 && (segs == nullptr || flat == nullptr))) {
     set_error("dpk_pack/unpack: bad arguments");
     return DPK_EARG;
@@ -172,6 +189,11 @@ int run_segments(const dpk_segment* segs, int n, float* flat, float scale, cudaS
     const int cnt = std::min(SEG_MAX, n - first);
     b.n = cnt;
     b.scale = scale;
+    b.kl_slots = kl_slots;
+    b.kl_n = kl_n;
+    b.kl_stride = kl_stride;
+    b.kl_clip = kl_clip;
+    b.lr2 = lr2;
     int64_t maxe = 0;
     for (int i = 0; i < cnt; ++i) {
       b.s[i] = segs[first + i];
@@ -193,10 +215,71 @@ int run_segments(const dpk_segment* segs, int n, float* flat, float scale, cudaS
   return DPK_OK;
 }
 
+// <a, b> over n floats, deterministic: every block writes its fp64 partial, the
+// last block to finish (ticket) sums them in block order and stores the result.
+constexpr int DOT_BLOCKS = 148;
+__global__ void __launch_bounds__(256) kl_dot_kernel(const float* a, const float* b, int64_t n, float* out,
+                                                     double* partials, unsigned int* ticket) {
+  double acc = 0.0;
+  const int64_t nth = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool vec = ((reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(b)) & 15) == 0;
+  const int64_t n4 = vec ? n / 4 : 0;
+  for (int64_t e = tid; e < n4; e += nth) {
+    const float4 x = __ldg(reinterpret_cast<const float4*>(a) + e), y = __ldg(reinterpret_cast<const float4*>(b) + e);
+    acc += static_cast<double>(x.x) * y.x + static_cast<double>(x.y) * y.y + static_cast<double>(x.z) * y.z +
+           static_cast<double>(x.w) * y.w;
+  }
+  for (int64_t e = 4 * n4 + tid; e < n; e += nth) acc += static_cast<double>(__ldg(a + e)) * __ldg(b + e);
+  acc = block_sum(acc);
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = acc;
+    __threadfence();
+    last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    double s = 0.0;
+    for (unsigned i = 0; i < gridDim.x; ++i) s += static_cast<volatile double*>(partials)[i];
+    *out = static_cast<float>(s);
+    *ticket = 0u;  // ready for the next call
+  }
+}
+
 }  // namespace
 }  // namespace dpk
 
 extern "C" {
+
+size_t dpk_kl_dot_workspace_bytes(void) { return dpk::DOT_BLOCKS * sizeof(double) + 256; }
+
+int dpk_kl_dot(const float* pre, const float* grad, int64_t n, float* out, void* workspace, size_t ws_bytes,
+               dpk_stream_t stream) {
+  if (n < 0 || out == nullptr || (n > 0 && (pre == nullptr || grad == nullptr)) || workspace == nullptr ||
+      ws_bytes < dpk_kl_dot_workspace_bytes() || (reinterpret_cast<uintptr_t>(workspace) & 7) != 0) {
+    dpk::set_error("dpk_kl_dot: bad arguments (workspace: dpk_kl_dot_workspace_bytes(), zeroed once, 8-aligned)");
+    return DPK_EARG;
+  }
+  double* partials = static_cast<double*>(workspace);
+  unsigned int* ticket = reinterpret_cast<unsigned int*>(static_cast<char*>(workspace) + dpk::DOT_BLOCKS * sizeof(double));
+  const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(dpk::DOT_BLOCKS, (n + 1023) / 1024)));
+  dpk::kl_dot_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(pre, grad, n, out, partials, ticket);
+  dpk::note_launch();
+  return dpk::cuda_status(cudaGetLastError(), "kl_dot_kernel launch");
+}
+
+int dpk_unpack_owner_major_klclip(const dpk_segment* segs, int n_segs, const float* flat, float scale,
+                                  const float* kl_slots, int n_slots, int64_t slot_stride, float kl_clip, float lr,
+                                  dpk_stream_t stream) {
+  if (kl_slots == nullptr || n_slots < 1 || !(kl_clip > 0.0f)) {
+    dpk::set_error("dpk_unpack_owner_major_klclip: need kl_slots, n_slots >= 1 and kl_clip > 0");
+    return DPK_EARG;
+  }
+  return dpk::run_segments<false>(segs, n_segs, const_cast<float*>(flat), scale, static_cast<cudaStream_t>(stream),
+                                  kl_slots, n_slots, slot_stride, kl_clip, lr * lr);
+}
 
 const char* dpk_version(void) { return "dpkfac-b200 0.1.0 (sm_100a, tcgen05 tf32/3xtf32)"; }
 

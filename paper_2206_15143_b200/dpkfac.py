@@ -218,6 +218,8 @@ class DPKFAC:
       overlap            size-class pipeline on prioritized side streams
       early              launch the larger classes' factor/inverse from the backward hooks
       algorithm          "dp_kfac" | "mpd_kfac_co" | "mpd_kfac_mo" (paper comparators)
+      kl_clip, lr        opt-in KL-clip of the preconditioned update (None = the reference's
+                         exact Eq. 6 update)
       grad_scale         "batch" (B_local * grad_output, model.py:9-12) or a number
     """
 
@@ -232,8 +234,20 @@ class DPKFAC:
                  process_group=None, precision: str = "auto", precond_precision: str = "3xtf32",
                  grad_scale: Union[str, float] = "batch", check_numerics: Union[bool, str] = True,
                  im2col: str = "materialize", overlap: bool = True, early: bool = False,
-                 algorithm: str = "dp_kfac", patch_dtype: str = "auto"):
+                 algorithm: str = "dp_kfac", patch_dtype: str = "auto", kl_clip: Optional[float] = None,
+                 lr=None):
         self.hyper = KfacHyper(gamma=gamma, xi=xi, inv_type=inv_type, f_freq=f_freq, k_freq=k_freq)
+        # KL-clip (north_star; off by default: the reference has none):
+        # every preconditioned gradient is scaled by nu = min(1, sqrt(kl_clip / |lr^2 sum
+        # <pre, grad>|)) -- the partial dots ride the all-gather, nu is applied inside the
+        # unpack kernel.  lr: a number or a callable returning the current learning rate.
+        if kl_clip is not None:
+            if not kl_clip > 0 or lr is None:
+                raise ArgumentError("kl_clip needs kl_clip > 0 and the learning rate (lr=number or callable)")
+            if algorithm != "dp_kfac":
+                raise ArgumentError("kl_clip is implemented for algorithm='dp_kfac'")
+        self.kl_clip = kl_clip
+        self.lr = lr
         # dp_kfac: the product.  mpd_kfac_co / mpd_kfac_mo: the paper's model-parallel
         # comparators (KAISA COMM-OPT / MEM-OPT, distsim.mpd_kfac_step distsim.py:341-420)
         # on the same kernels: every rank builds every layer's factors from its local
@@ -402,7 +416,10 @@ class DPKFAC:
 
     def _build_buffers(self):
         dev = self.device
-        self.layout = OwnerMajorLayout(self.assignment, [ly.n_grad for ly in self.layers])
+        self.layout = OwnerMajorLayout(self.assignment, [ly.n_grad for ly in self.layers],
+                                       scalar_slot=self.kl_clip is not None)
+        if self.kl_clip is not None:
+            self._kl_ws = ops.kl_dot_workspace(dev)
         self.xchg = OwnerMajorExchange(self.layout, self.rank, dev, self.pg)
         self.offsets = self.layout.offsets
         if self.algorithm == "mpd_kfac_co":  # every layer's mean gradient on every rank
@@ -546,8 +563,16 @@ class DPKFAC:
         elif self.check_numerics == "deferred":
             self._defer_info()
         # (6) all-gather preconditioned grads, unpack into .grad
-        X.all_gather()
-        ops.unpack(segs, X.out_flat, 1.0)
+        if self.kl_clip is None:
+            X.all_gather()
+            ops.unpack(segs, X.out_flat, 1.0)
+        else:  # KL-clip: my partial <pre, grad> into my chunk's slot, nu applied by the unpack
+            so = X.layout.slot_offset
+            ops.kl_dot(X.chunk_out, X.chunk_in, so, X.chunk_out[so:so + 1], self._kl_ws)
+            X.all_gather()
+            lr = float(self.lr() if callable(self.lr) else self.lr)
+            ops.unpack_klclip(segs, X.out_flat, X.out_flat.data_ptr() + 4 * so, self.world, X.layout.chunk,
+                              self.kl_clip, lr)
         self._mark("comm_ag")
         # flags start clean for the next step's (possibly hook-launched) stages;
         # ordered after this step's reads of them on the caller's stream

@@ -23,13 +23,19 @@ import torch.distributed as dist
 
 
 class OwnerMajorLayout:
-    def __init__(self, assignment: Sequence[Sequence[int]], n_grad: Sequence[int], align: int = 32):
+    """``scalar_slot``: reserve the last float of every rank's chunk for one per-rank
+    scalar that rides the all-gather (the KL-clip partial dot): ``slot_offset``
+    inside a chunk, ``chunk`` apart in the gathered buffer."""
+
+    def __init__(self, assignment: Sequence[Sequence[int]], n_grad: Sequence[int], align: int = 32,
+                 scalar_slot: bool = False):
         self.assignment = tuple(tuple(p) for p in assignment)
         self.world = len(self.assignment)
         self.n_grad = list(n_grad)
         sizes = [sum(self.n_grad[i] for i in part) for part in self.assignment]
-        chunk = max(max(sizes) if sizes else 0, 1)
+        chunk = max(max(sizes) if sizes else 0, 1) + (1 if scalar_slot else 0)
         self.chunk = (chunk + align - 1) // align * align
+        self.slot_offset = self.chunk - 1 if scalar_slot else None
         self.offsets = {}
         for p, part in enumerate(self.assignment):
             off = p * self.chunk

@@ -486,3 +486,24 @@ def unpack(segs, flat: torch.Tensor, scale: float = 1.0):
     if n:
         L.check(lib().dpk_unpack_owner_major(arr, n, flat.data_ptr(), float(scale), stream_handle()),
                 "dpk_unpack_owner_major")
+
+
+# ------------------------------------------------------------------ KL-clip (opt-in)
+def kl_dot(pre: torch.Tensor, grad: torch.Tensor, n: int, out: torch.Tensor, ws: torch.Tensor):
+    """out[0] = <pre[:n], grad[:n]> (fp64 accumulate, deterministic); ws: a zeroed
+    uint8 buffer of dpk_kl_dot_workspace_bytes() reused across calls."""
+    L.check(lib().dpk_kl_dot(pre.data_ptr(), grad.data_ptr(), int(n), out.data_ptr(), ws.data_ptr(), ws.numel(),
+                             stream_handle()), "dpk_kl_dot")
+
+
+def kl_dot_workspace(device) -> torch.Tensor:
+    return torch.zeros(int(lib().dpk_kl_dot_workspace_bytes()), dtype=torch.uint8, device=device)
+
+
+def unpack_klclip(segs, flat: torch.Tensor, slots_ptr: int, n_slots: int, slot_stride: int, kl_clip: float,
+                  lr: float, scale: float = 1.0):
+    arr, n = _seg_array(segs)
+    if n:
+        L.check(lib().dpk_unpack_owner_major_klclip(arr, n, flat.data_ptr(), float(scale), slots_ptr, int(n_slots),
+                                                     int(slot_stride), float(kl_clip), float(lr), stream_handle()),
+                "dpk_unpack_owner_major_klclip")

@@ -16,7 +16,7 @@ try:
                                    text=True).stdout.strip()
 except OSError:
     pass
-UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6, "msecond": 1e-3,
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "msecond": 1e-3,
         "second": 1.0}
 for st in ("factors", "inversion", "precondition", "comm_rs", "comm_ag"):
     p = os.path.join(src, f"stage_traffic_{st}.csv")

@@ -179,7 +179,7 @@ def _oracle_layer(m, cap, batch):
     x, g = cap["x"], cap["g"]
     bias = m.bias is not None
     if isinstance(m, nn.Conv2d):
-        X = K.unfold_columns(x, m.kernel_size[0], m.kernel_size[1], m.stride[0], m.padding[0], m.dilation[0], bias)
+        X = K.unfold_columns(x, m.kernel_size[0], m.kernel_size[1], m.stride, m.padding, m.dilation, bias)
         Gm = g.transpose(1, 0, 2, 3).reshape(g.shape[1], -1) * batch
     else:
         X = x.T
@@ -467,3 +467,95 @@ def test_early_launch_matches_reference():
         opt.step()
     kf.check()
     assert launched[0] == {} and all(l == {0: t} for t, l in enumerate(launched) if t > 0), launched
+
+
+class InceptionBits(nn.Module):
+    """Inception-v4 building blocks (config C5): 1x7 / 7x1 and 1x3 / 3x1 convs with
+    asymmetric padding, a strided 3x3 reduction, an fc."""
+
+    def __init__(self):
+        super().__init__()
+        self.stem = nn.Conv2d(3, 32, 3, 2, bias=False)
+        self.a = nn.Conv2d(32, 32, (1, 7), padding=(0, 3), bias=False)
+        self.b = nn.Conv2d(32, 64, (7, 1), padding=(3, 0), bias=False)
+        self.c = nn.Conv2d(64, 32, (1, 3), padding=(0, 1), bias=True)
+        self.d = nn.Conv2d(32, 32, (3, 1), padding=(1, 0), bias=False)
+        self.e = nn.Conv2d(32, 64, 3, 2, bias=False)
+        self.fc = nn.Linear(64, 10)
+
+    def forward(self, x):
+        for m in (self.stem, self.a, self.b, self.c, self.d, self.e):
+            x = F.relu(m(x))
+        return self.fc(x.mean((2, 3)))
+
+
+@pytest.mark.parametrize("inv_type", ["inverse", "eigen"])
+@pytest.mark.parametrize("channels_last", [True, False])
+def test_inception_asymmetric_convs_match_reference_layer_step(inv_type, channels_last):
+    from paper_2206_15143_b200 import DPKFAC
+    torch.manual_seed(11)
+    dev = torch.device("cuda", 0)
+    model = InceptionBits().to(dev)
+    if channels_last:
+        model = model.to(memory_format=torch.channels_last)
+    kf = DPKFAC(model, gamma=0.01, xi=0.8, inv_type=inv_type, f_freq=1, k_freq=1)
+    h = K.Hyper(gamma=0.01, xi=0.8, inv_type=inv_type, f_freq=1, k_freq=1)
+    rec, hooks = _record(model)
+    states = {}
+    gen = torch.Generator().manual_seed(12)
+    for t in range(2):
+        x = torch.randn(4, 3, 33, 29, generator=gen).to(dev)
+        if channels_last:
+            x = x.to(memory_format=torch.channels_last)
+        y = torch.randint(0, 10, (4,), generator=gen).to(dev)
+        model.zero_grad()
+        F.cross_entropy(model(x), y).backward()
+        want = {}
+        for name, m in model.named_modules():
+            if isinstance(m, (nn.Conv2d, nn.Linear)):
+                X, Gm, W = _oracle_layer(m, rec[name], 4)
+                st = states.setdefault(name, K.LayerState())
+                want[name], _ = K.kfac_layer_step(st, X, Gm, W, h, t)
+        kf.step()
+        for name, m in model.named_modules():
+            if isinstance(m, (nn.Conv2d, nn.Linear)):
+                got = m.weight.grad.double().cpu().numpy().reshape(m.weight.shape[0], -1)
+                if m.bias is not None:
+                    got = np.hstack([got, m.bias.grad.double().cpu().numpy()[:, None]])
+                assert rel(got, want[name]) <= TOL, (t, name, rel(got, want[name]))
+    sd = kf.state_dict()
+    for i, (name, m) in enumerate((n, m) for n, m in model.named_modules() if isinstance(m, (nn.Conv2d, nn.Linear))):
+        assert rel(sd["layers"][i]["a_cov"].double().cpu().numpy(), states[name].a_cov) <= TOL
+    for hk in hooks:
+        hk.remove()
+
+
+@pytest.mark.parametrize("inv_type", ["inverse", "eigen"])
+def test_kl_clip_scale_matches_formula(inv_type):
+    """Opt-in KL-clip (north_star; the reference has none): the oracle's
+    preconditioned gradients scaled by nu = min(1, sqrt(kl / |lr^2 sum <pre, grad>|))."""
+    from paper_2206_15143_b200 import DPKFAC
+    dev = torch.device("cuda", 0)
+    spec = MLP.MlpSpec((784, 512, 256, 10), "relu", "softmax_cross_entropy", True)
+    h = K.Hyper(gamma=0.03, xi=0.95, inv_type=inv_type, f_freq=1, k_freq=1)
+    cl = MLP.build_cluster(spec, 1, seed=0)
+    model, lins = torch_mlp([w.copy() for w in cl.weights], dev)
+    lr, kl = 0.05, 1e-4
+    kf = DPKFAC(model, gamma=0.03, xi=0.95, inv_type=inv_type, kl_clip=kl, lr=lambda: lr)
+    rng = np.random.default_rng(5)
+    nus = []
+    for t in range(2):
+        x = rng.standard_normal((784, 64))
+        y = rng.integers(0, 10, size=64)
+        _, ins, pgs, grads = MLP.forward_backward(spec, cl.weights, x, y)
+        pre = [K.kfac_layer_step(cl.states[0][i], ins[i], pgs[i], grads[i], h, t)[0] for i in range(3)]
+        vg = sum(float((p * g).sum()) for p, g in zip(pre, grads)) * lr * lr
+        nu = min(1.0, (kl / abs(vg)) ** 0.5)
+        nus.append(nu)
+        model.zero_grad()
+        F.cross_entropy(model(torch.from_numpy(x.T.copy()).float().to(dev)), torch.from_numpy(y).to(dev)).backward()
+        kf.step()
+        for i, lin in enumerate(lins):
+            got = torch.cat([lin.weight.grad, lin.bias.grad[:, None]], 1).double().cpu().numpy()
+            assert rel(got, nu * pre[i]) <= TOL, (t, i, rel(got, nu * pre[i]), nu)
+    assert min(nus) < 1.0  # the clip is active in this setting

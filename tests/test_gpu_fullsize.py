@@ -166,3 +166,10 @@ def test_resnet50_config3_fullsize_eigen_mode():
     preconditioned gradient equals the exact (A (x) G + gamma I)^-1 solve."""
     w = _run("resnet50", steps=2, inv_type="eigen", every=2)
     assert len(w) == 27
+
+
+def test_inception_v4_config5_fullsize_properties():
+    """Config C5 at its real shapes (B=16, 299x299): 1x7/7x1 and 1x3/3x1 convs with
+    asymmetric padding, 1537-dim fc factor."""
+    w = _run("inception_v4", every=4)
+    assert len(w) >= 37

@@ -526,3 +526,49 @@ def test_f16_patch_prescale_survives_fp16_range(scale, shape, k, s, p, bias, cha
         if a0 is not None:
             want = want + 0.5 * a0
         assert rel(N(out), want) <= TOL, rel(N(out), want)
+
+
+# ---------------------------------------------------------------- non-square kernels / asymmetric padding
+# Inception-v4 (config C5): 1x7 / 7x1 convs padded (0,3) / (3,0), 1x3 / 3x1 padded (0,1) / (1,0),
+# plus an asymmetric stride -- every im2col form against F.unfold-order columns.
+ASYM = [((2, 64, 17, 17), (1, 7), (1, 1), (0, 3)), ((2, 64, 17, 17), (7, 1), (1, 1), (3, 0)),
+        ((2, 32, 8, 8), (1, 3), (1, 1), (0, 1)), ((2, 32, 8, 8), (3, 1), (1, 1), (1, 0)),
+        ((2, 32, 12, 9), (3, 5), (2, 1), (1, 2)), ((1, 3, 16, 24), (7, 1), (1, 2), (3, 0))]
+
+
+@pytest.mark.parametrize("shape,kk,ss,pp", ASYM)
+@pytest.mark.parametrize("channels_last", [True, False])
+def test_asymmetric_kernels_all_im2col_forms_match_unfold(shape, kk, ss, pp, channels_last):
+    from paper_2206_15143_b200 import ops
+    rng = np.random.default_rng(sum(shape) + 3 * kk[0] + kk[1])
+    x = np.maximum(rng.standard_normal(shape), 0)
+    xt = T(x)
+    if channels_last:
+        xt = xt.to(memory_format=torch.channels_last)
+    cols = K.unfold_columns(x, kk[0], kk[1], ss, pp)
+    d, M = cols.shape
+    for tap in (False, True):
+        perm = _tap_perm(shape[1], kk[0], kk[1]) if tap else np.arange(d)
+        want_cols = cols[perm]
+        want, _ = K.compute_factors(want_cols, want_cols[:1])
+        op = ops.operand_im2col(xt, kk, ss, pp, (1, 1), tap_major=tap)
+        assert op.cols == M
+        # implicit im2col SYRK (gather / TMA tap boxes)
+        out = torch.full((d, d), float("nan"), device=dev())
+        ops.syrk_ema([ops.factor_job(op, out, 1.0 / M, 0.0)], "3xtf32")
+        torch.cuda.synchronize()
+        assert rel(N(out), want) <= 1e-5, ("implicit", tap, rel(N(out), want))
+        # fp32 sample-major patches, bit-exact
+        ld = (d + 3) // 4 * 4
+        pm = torch.full((M, ld), float("nan"), device=dev())
+        ops.im2col_materialize([(op, pm)])
+        torch.cuda.synchronize()
+        assert np.array_equal(N(pm[:, :d]).T, want_cols.astype(np.float32).astype(np.float64)), ("f32", tap)
+        # fp16 feature-major patches (prescaled), kind::f16 SYRK
+        p16 = torch.full((d, (M + 7) // 8 * 8), float("nan"), dtype=torch.float16, device=dev())
+        amax = torch.zeros(1, dtype=torch.int32, device=dev())
+        ops.im2col_materialize_f16([(op, p16, amax)])
+        out.fill_(float("nan"))
+        ops.syrk_ema([ops.factor_job(ops.operand_rows_k_f16(p16, M), out, 1.0 / M, 0.0, x_amax=amax)], "tf32")
+        torch.cuda.synchronize()
+        assert rel(N(out), want) <= TOL, ("f16", tap, rel(N(out), want))
