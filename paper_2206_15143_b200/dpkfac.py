@@ -36,8 +36,8 @@ from . import _lib as L
 from . import ops
 from .errors import ArgumentError, NumericError, OrderingError, ShapeError
 from .kfac import KfacHyper
-from .exchange import OwnerMajorExchange, OwnerMajorLayout
-from .partition import balanced_partition, layer_cost, round_robin_partition, validate_partition
+from .exchange import OwnerMajorExchange, OwnerMajorLayout, agree_max
+from .partition import round_robin_partition, step_time_partition, validate_partition
 
 
 def _nhwc(t: torch.Tensor) -> bool:
@@ -395,21 +395,21 @@ class DPKFAC:
             ly.slot = k
 
     def _finalize_balance(self):
-        costs = []
+        """assignment="balanced": partition.step_time_partition over (d_in, d_out, M)
+        of every layer -- estimated B200 step time per rank (throughput work, the
+        latency-bound inversion chain, the owner-major exchange's chunk)."""
+        ms = []
         for ly in self.layers:
             if ly.a_in is None:
                 raise OrderingError("balanced assignment needs one forward/backward pass before step()")
-            m = ly.operand_a("implicit")[0].cols
-            costs.append(layer_cost(ly.d_in, ly.d_out, m, self.hyper.inv_type))
+            ms.append(ly.operand_a("implicit")[0].cols)
         # the ranks must agree on the partition (the owner-major collectives' chunk
         # sizes follow from it): local shapes may differ (e.g. a ragged last batch),
-        # so the per-layer costs are first made identical everywhere by a MAX
-        # all-reduce; the LPT is deterministic on identical costs.
-        if self.world > 1:
-            ct = torch.tensor(costs, dtype=torch.float64, device=self.device)
-            dist.all_reduce(ct, op=dist.ReduceOp.MAX, group=self.pg)
-            costs = ct.tolist()
-        self.assignment = balanced_partition(costs, self.world)
+        # so the per-layer sample counts are first made identical everywhere by a MAX
+        # all-reduce; the balancer is deterministic on identical input.
+        ms = agree_max(ms, self.pg, self.device)
+        self.assignment = step_time_partition([(ly.d_in, ly.d_out, m) for ly, m in zip(self.layers, ms)],
+                                              self.world, self.hyper.inv_type)
         validate_partition(self.assignment, len(self.layers))
         self._pending_balance = False
         self._set_ownership()

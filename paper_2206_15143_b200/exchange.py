@@ -99,3 +99,14 @@ class OwnerMajorExchange:
         off = self.layout.local_offset(layer, self.rank)
         n = shape[0] * shape[1]
         return self.chunk_tmp[off:off + n].view(*shape)
+
+
+def agree_max(values, group=None, device="cpu"):
+    """Element-wise MAX of a per-rank integer list over the group (identity when
+    not distributed): every rank then feeds the same numbers to the deterministic
+    balancer, so all ranks build the same owner-major layout."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return [int(v) for v in values]
+    t = torch.tensor([float(v) for v in values], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return [int(v) for v in t.tolist()]

@@ -83,3 +83,36 @@ def test_owner_major_exchange_gloo(world, kind):
     for _, out, _ in results[1:]:
         for i in range(len(SHAPES)):
             assert (out[i] == base[i]).all()
+
+
+def _agree_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2206_15143_b200.exchange import agree_max
+        from paper_2206_15143_b200.partition import step_time_partition
+        # ragged local batches: rank r sees M = 64 - 8 r samples on every layer
+        dims = [(785, 512), (513, 256), (257, 10), (1153, 128), (2305, 64)]
+        ms = agree_max([64 - 8 * rank] * len(dims))
+        q.put((rank, ms, step_time_partition([(a, b, m) for (a, b), m in zip(dims, ms)], world)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_balanced_partition_agrees_across_ranks_with_ragged_batches_gloo():
+    """every rank must build the same partition even when local batch
+    shapes differ -- the sample counts are MAX-all-reduced before the balancer."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_agree_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert all(r[1] == [64] * 5 for r in res)
+    assert len({r[2] for r in res}) == 1

@@ -65,3 +65,26 @@ def test_balanced_is_deterministic_valid_and_better_than_round_robin():
 def test_balanced_tie_break_by_index_then_rank():
     assert balanced_partition([1.0, 1.0, 1.0, 1.0], 2) == ((0, 2), (1, 3))
     assert balanced_partition([5.0], 3) == ((0,), (), ())
+
+
+def test_step_time_partition_matches_golden_and_removes_padding():
+    """DPKFAC assignment="balanced": bit-exact against the committed golden
+    partitions (validated by the reference's distsim.validate_partition when they
+    were generated, tests/golden/make_partition_golden.py); owner-major padding
+    <= 5% at P = 2/4/8 and an estimated step no slower than round robin."""
+    from paper_2206_15143_b200.partition import partition_report, step_time_partition
+    with open(os.path.join(GOLDEN, "balanced_partitions.json")) as f:
+        gold = json.load(f)
+    for model in ("resnet50", "inception_v4"):  # densenet201: same code path, slower to recompute
+        layers = [tuple(x) for x in gold[model]["layers"]]
+        for P, g in gold[model]["partitions"].items():
+            a = step_time_partition(layers, int(P))
+            assert [list(p) for p in a] == g["assignment"], (model, P)
+            validate_partition(a, len(layers))
+            rep = partition_report(layers, a)
+            assert rep["padding"] <= 0.05
+            assert rep["est_ms"] <= g["round_robin_report"]["est_ms"] + 1e-9
+    for model in gold:
+        for P, g in gold[model]["partitions"].items():
+            validate_partition(tuple(tuple(p) for p in g["assignment"]), len(gold[model]["layers"]))
+            assert g["report"]["padding"] <= 0.05
