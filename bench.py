@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--early", action="store_true",
                     help="e2e: launch the larger size classes' factor/inverse pipeline from the backward hooks")
+    ap.add_argument("--early-priority", default="high", choices=["high", "low"],
+                    help="e2e with --early: stream priority of the hook-launched pipelines")
     ap.add_argument("--ncu-step", action="store_true",
                     help="profiling helper: after warm-up run ONE serialized step between cudaProfilerStart/Stop "
                          "with NVTX stage ranges (DPK_NVTX) and exit without a result line")
@@ -457,6 +459,7 @@ def run_ours(args, rank, world, local_rank):
             return loss.item()
 
         kf.early = args.early and not args.no_overlap  # hook-time launch of the larger classes' pipelines
+        kf.early_priority = args.early_priority
         for _ in range(2):
             train_step()
         sync_barrier()
