@@ -67,8 +67,15 @@ __host__ __device__ inline int prescale_exponent(int32_t amax_bits) {
 constexpr int TRI_NONE = 0;
 constexpr int TRI_LOWER = 1;  // op[r][k] == 0 for k > r
 constexpr int TRI_UPPER = 2;  // op[r][k] == 0 for k < r
+// block diagonal: op[r][k] == 0 unless r and k lie in the same unit-tile-sized
+// block (128 or 256, the engine's tile edge; zeros must be stored inside a
+// 256 block) -- the rotation sets of the block-Jacobi eigensolver (syevj.cu)
+constexpr int TRI_BLOCK = 3;
 
 size_t gemm_workspace_bytes(const GemmSpec* specs, int n);
+// K4 n > 128: block Jacobi (syevj.cu); jobs with n <= 128 are ignored
+size_t syevj_workspace_bytes(const dpk_eig_job* jobs, int n_jobs);
+int syevj_run(const dpk_eig_job* jobs, int n_jobs, void* workspace, size_t ws_bytes, cudaStream_t st);
 // CUDA-core latency path for groups of small problems (gemm_simt.cu)
 bool simt_eligible(const GemmSpec* specs, int n, int precision);
 double simt_fma_limit();

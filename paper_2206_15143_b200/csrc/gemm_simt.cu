@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(256, 1) simt_gemm_kernel(const __grid_constant
   if (P.tri_b == TRI_UPPER) klo = max(klo, n0);
   if (P.tri_a == TRI_LOWER) khi = min(khi, m0 + T);
   if (P.tri_b == TRI_LOWER) khi = min(khi, n0 + T);
+  if (P.tri_a == TRI_BLOCK || P.tri_b == TRI_BLOCK) return;  // never planned here (simt_eligible)
   const int kstart = (klo / SK) * SK;
   float acc[R][R] = {};
   float va[T / 8], vb[T / 8];
@@ -186,7 +187,7 @@ bool simt_eligible(const GemmSpec* specs, int n, int precision) {
     const GemmSpec& g = specs[i];
     const dpk_operand& a = g.job.a;
     const dpk_operand& b = g.job.b;
-    if (g.epi != EPI_LINEAR || g.out_t || g.alpha_amax) return false;
+    if (g.epi != EPI_LINEAR || g.out_t || g.alpha_amax || g.tri_a == TRI_BLOCK || g.tri_b == TRI_BLOCK) return false;
     for (const dpk_operand* o : {&a, &b})
       if ((o->kind != DPK_OPND_ROWS_K && o->kind != DPK_OPND_ROWS_MN) || o->bias_row) return false;
     if (a.rows > 640 || b.rows > 640 || a.cols > 640) return false;

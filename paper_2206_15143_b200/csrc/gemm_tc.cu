@@ -197,6 +197,14 @@ __device__ __forceinline__ void chunk_range(const Problem& P, int tm, int tn, in
   if (P.tri_b == TRI_UPPER) lo = max(lo, tn * TC);
   if (P.tri_a == TRI_LOWER) hi = min(hi, (tm + 1) * TC);
   if (P.tri_b == TRI_LOWER) hi = min(hi, (tn + 1) * TC);
+  if (P.tri_a == TRI_BLOCK) {
+    lo = max(lo, tm * TC);
+    hi = min(hi, (tm + 1) * TC);
+  }
+  if (P.tri_b == TRI_BLOCK) {
+    lo = max(lo, tn * TC);
+    hi = min(hi, (tn + 1) * TC);
+  }
   kc0 = lo + split * P.cps;
   kc1 = min(hi, kc0 + P.cps);
 }
@@ -1594,7 +1602,9 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
         P.tma_b = plan_one(j.b, &P.tmap_b);
       }
     }
-    total_work += static_cast<int64_t>(P.ntiles) * P.chunks;
+    // block-diagonal operands: every tile reads one tile edge of K (no split-K)
+    const bool blockdiag = P.tri_a == TRI_BLOCK || P.tri_b == TRI_BLOCK;
+    total_work += static_cast<int64_t>(P.ntiles) * (blockdiag ? std::min(P.chunks, UT / BK) : P.chunks);
   }
   // Split K so that the group yields ~3 units per SM, but never below 32 chunks
   // (1024 samples) per unit so tile set-up and the partial round trip stay amortised.
@@ -1603,6 +1613,7 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
   size_t partial_tiles = 0;
   for (auto& P : plan.probs) {
     P.splits = static_cast<int>(std::max<int64_t>(1, (P.chunks + target - 1) / target));
+    if (P.tri_a == TRI_BLOCK || P.tri_b == TRI_BLOCK) P.splits = 1;
     P.cps = (P.chunks + P.splits - 1) / P.splits;
     P.splits = (P.chunks + P.cps - 1) / P.cps;
     if (P.splits > 1) partial_tiles += static_cast<size_t>(P.ntiles) * P.splits;

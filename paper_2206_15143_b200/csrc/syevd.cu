@@ -13,6 +13,8 @@
 
 #include "dpk_internal.h"
 
+#include <vector>
+
 namespace dpk {
 namespace {
 
@@ -188,14 +190,11 @@ __global__ void __launch_bounds__(JAC_THREADS) jacobi_kernel(const __grid_consta
 extern "C" {
 
 size_t dpk_syevd_workspace_bytes(const dpk_eig_job* jobs, int n_jobs) {
-  (void)jobs;
-  (void)n_jobs;
-  return 0;
+  if (n_jobs <= 0 || jobs == nullptr) return 0;
+  return dpk::syevj_workspace_bytes(jobs, n_jobs);
 }
 
 int dpk_syevd_batched(const dpk_eig_job* jobs, int n_jobs, void* workspace, size_t ws_bytes, dpk_stream_t stream) {
-  (void)workspace;
-  (void)ws_bytes;
   if (n_jobs == 0) return DPK_OK;
   if (n_jobs < 0 || jobs == nullptr) {
     dpk::set_error("dpk_syevd_batched: bad job list");
@@ -207,12 +206,18 @@ int dpk_syevd_batched(const dpk_eig_job* jobs, int n_jobs, void* workspace, size
       dpk::set_error("dpk_syevd_batched: invalid job");
       return DPK_EARG;
     }
-    if (jobs[i].n > dpk::JAC_N) {
-      dpk::set_error("dpk_syevd_batched: n > 128 is not supported by the on-chip Jacobi kernel yet");
-      return DPK_EARG;
-    }
-    maxm = std::max(maxm, jobs[i].n + (jobs[i].n & 1));
+    if (jobs[i].n <= dpk::JAC_N) maxm = std::max(maxm, jobs[i].n + (jobs[i].n & 1));
   }
+  cudaStream_t st0 = static_cast<cudaStream_t>(stream);
+  // n > 128: block Jacobi on the tensor cores (syevj.cu)
+  int rc0 = dpk::syevj_run(jobs, n_jobs, workspace, ws_bytes, st0);
+  if (rc0) return rc0;
+  std::vector<dpk_eig_job> small;
+  for (int i = 0; i < n_jobs; ++i)
+    if (jobs[i].n <= dpk::JAC_N) small.push_back(jobs[i]);
+  if (small.empty()) return DPK_OK;
+  jobs = small.data();
+  n_jobs = static_cast<int>(small.size());
   const int smem = 2 * maxm * (maxm + 1) * 4;
   static std::atomic<uint64_t> configured_on{0};
   if (dpk::first_on_device(configured_on)) {

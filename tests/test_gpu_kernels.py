@@ -288,6 +288,38 @@ def test_sym_eig_onchip_jacobi(n):
     assert rel(q @ np.diag(N(e.values)) @ q.T, a) <= 5e-5  # fp32 Jacobi, n <= 128
 
 
+@pytest.mark.parametrize("n,m", [(129, 400), (200, 60), (256, 1000), (577, 300), (1000, 1568), (2049, 700)])
+def test_sym_eig_block_jacobi_native(n, m):
+    """n > 128: the tensor-core block Jacobi (csrc/syevj.cu) -- no library
+    eigensolver.  Rank-deficient K-FAC-like factors (m < n: a cluster of zero
+    eigenvalues), odd n (zero padding to a multiple of 128)."""
+    from paper_2206_15143_b200 import kfac as FK
+    rng = np.random.default_rng(n + m)
+    x = np.maximum(rng.standard_normal((n, m)), 0) * np.exp(-np.arange(n) / (n / 3))[:, None]
+    a = x @ x.T / m
+    e = FK.sym_eig(T(a))
+    r = K.symmetric_eig(a)
+    v, q = N(e.values), N(e.q)
+    assert np.all(np.diff(v) <= 0)
+    assert np.abs(v - r.values).max() <= 1e-5 * np.abs(r.values).max()
+    assert np.abs(q.T @ q - np.eye(n)).max() <= 1e-4
+    assert rel(q @ np.diag(v) @ q.T, a) <= 5e-5
+
+
+@pytest.mark.parametrize("din,dout,gamma", [(577, 256, 0.002), (1153, 512, 0.03), (2305, 129, 0.002)])
+def test_precondition_eigen_large_native_matches_oracle(din, dout, gamma):
+    from paper_2206_15143_b200 import kfac as FK
+    rng = np.random.default_rng(din + 3 * dout)
+    x = np.maximum(rng.standard_normal((din, 800)), 0)
+    x[-1] = 1.0
+    g = rng.standard_normal((dout, 800)) * 0.1
+    grad = rng.standard_normal((dout, din)) * 0.01
+    a, gg = K.compute_factors(x, g)
+    got = FK.precondition_eigen(FK.sym_eig(T(a)), FK.sym_eig(T(gg)), T(grad), gamma)
+    want = K.precondition_eigen(K.symmetric_eig(a), K.symmetric_eig(gg), grad, gamma)
+    assert rel(N(got), want) <= TOL
+
+
 # ---------------------------------------------------------------- K5 / K6
 @pytest.mark.parametrize("din,dout,gamma", [(785, 512, 0.03), (65, 9, 0.002), (2049, 1000, 0.002), (3, 2, 0.03)])
 def test_precondition_inverse_matches_oracle(din, dout, gamma):
