@@ -220,6 +220,8 @@ class DPKFAC:
       algorithm          "dp_kfac" | "mpd_kfac_co" | "mpd_kfac_mo" (paper comparators)
       kl_clip, lr        opt-in KL-clip of the preconditioned update (None = the reference's
                          exact Eq. 6 update)
+      eig_solver         n > 128 eigendecompositions: "cusolver" (default, measured
+                         fastest) | "native" (tensor-core block Jacobi, no library)
       grad_scale         "batch" (B_local * grad_output, model.py:9-12) or a number
     """
 
@@ -235,7 +237,7 @@ class DPKFAC:
                  grad_scale: Union[str, float] = "batch", check_numerics: Union[bool, str] = True,
                  im2col: str = "materialize", overlap: bool = True, early: bool = False,
                  algorithm: str = "dp_kfac", patch_dtype: str = "auto", kl_clip: Optional[float] = None,
-                 lr=None):
+                 lr=None, eig_solver: str = "cusolver"):
         self.hyper = KfacHyper(gamma=gamma, xi=xi, inv_type=inv_type, f_freq=f_freq, k_freq=k_freq)
         # KL-clip (north_star; off by default: the reference has none):
         # every preconditioned gradient is scaled by nu = min(1, sqrt(kl_clip / |lr^2 sum
@@ -248,6 +250,9 @@ class DPKFAC:
                 raise ArgumentError("kl_clip is implemented for algorithm='dp_kfac'")
         self.kl_clip = kl_clip
         self.lr = lr
+        if eig_solver not in ops.EIG_SOLVERS:
+            raise ArgumentError(f"eig_solver must be one of {ops.EIG_SOLVERS}")
+        self.eig_solver = eig_solver  # n > 128 eigendecompositions (n <= 128: on-chip Jacobi)
         # dp_kfac: the product.  mpd_kfac_co / mpd_kfac_mo: the paper's model-parallel
         # comparators (KAISA COMM-OPT / MEM-OPT, distsim.mpd_kfac_step distsim.py:341-420)
         # on the same kernels: every rank builds every layer's factors from its local
@@ -696,7 +701,7 @@ class DPKFAC:
             for ly in layers:
                 jt.append((ly.a_cov, ly.a_q, ly.a_w, self.info[ly.index]))
                 jt.append((ly.g_cov, ly.g_q, ly.g_w, self.info[ly.index]))
-            ops.syevd(jt)
+            ops.syevd(jt, self.eig_solver)
         else:
             # the job lists only reference persistent state buffers: built once per class
             key = ("inv", tuple(ly.index for ly in layers))

@@ -105,14 +105,15 @@ def _raise_info(code: int, n: int, side: str = "") -> None:
 
 
 # ------------------------------------------------------------------ numerics.py
-def sym_eig(m: torch.Tensor) -> EigenPair:
-    """Symmetrize, decompose, descending order (numerics.py:75-97)."""
+def sym_eig(m: torch.Tensor, solver: str = "cusolver") -> EigenPair:
+    """Symmetrize, decompose, descending order (numerics.py:75-97).  n > 128:
+    ``solver`` "cusolver" (default) or "native" (tensor-core block Jacobi)."""
     m = _square(_f32(m), "sym_eig")
     n = m.shape[0]
     q = torch.empty_like(m)
     w = torch.empty(n, device=m.device, dtype=torch.float32)
     info = torch.zeros(1, dtype=torch.int32, device=m.device)
-    ops.syevd([(m, q, w, info)])
+    ops.syevd([(m, q, w, info)], solver)
     _raise_info(int(info.item()), n)
     return EigenPair(q, w)
 

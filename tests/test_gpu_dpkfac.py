@@ -122,6 +122,13 @@ def _c1_run(kf_kwargs, h, steps, seed_data=1234, lr=0.05, teacher_forcing=False)
     return kf, worst
 
 
+def test_mlp_config1_eigen_native_solver_matches_reference():
+    """eig_solver="native": every eigendecomposition on libdpkfac (785/513/257 via the
+    tensor-core block Jacobi, no library), C1 end to end over 3 steps."""
+    h = K.Hyper(gamma=0.03, xi=0.95, inv_type="eigen", f_freq=1, k_freq=1)
+    _c1_run(dict(eig_solver="native"), h, 3)
+
+
 def test_mlp_config1_default_constructor_matches_reference():
     """DPKFAC(model) with every default (gamma 0.03, xi 0.95, inv_type "eigen",
     precision "auto" -> 3xTF32 factors) is parity-green (kfac.py:55-64 defaults)."""
