@@ -1252,7 +1252,12 @@ bool dynamic_schedule() {  // DPK_DYN=0: static round-robin units
   return v == 1;
 }
 
+thread_local int g_cap_override = 0;
+}  // namespace
+void set_grid_cap_override(int cap) { g_cap_override = cap; }
+namespace {
 int grid_cap() {
+  if (g_cap_override > 0) return g_cap_override;
   static int v = -2;
   if (v == -2) {
     const char* e = getenv("DPK_GRID_CAP");

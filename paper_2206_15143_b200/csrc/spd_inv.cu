@@ -524,11 +524,25 @@ struct SpdReq {
   int32_t factor;
   int32_t _pad;
 };
+// Right-looking blocked Cholesky with look-ahead (the largest size class): the
+// matrix's working buffers, kept per job so the schedule can be generated.
+struct RlMat {
+  float* Aw;
+  float* Lb;
+  float* Xb;
+  int64_t ld;
+  int n;
+  int fail_code;
+  int32_t* info;
+};
 struct SpdPlan {
   std::vector<std::vector<Op>> lists;
   std::vector<PrepJob> preps;
   std::vector<std::vector<int>> groups;   // job indices; groups[0] = the largest factors
   std::vector<size_t> group_ws;           // split-K workspace offset of each group
+  std::vector<int> group_rl;              // 1: the group runs the right-looking schedule
+  std::vector<size_t> group_ws_side;      // RL groups: workspace offset of the side (T2) stream
+  std::vector<RlMat> mats;                // per job (blocked path only)
   size_t rec_bytes = 0;
   size_t gemm_bytes = 0;                  // sum over groups
 };
@@ -551,6 +565,133 @@ void make_groups(const SpdReq* jobs, int n, SpdPlan& plan) {
     plan.groups.back().push_back(i);
   }
   for (auto& g : plan.groups) std::sort(g.begin(), g.end());  // ascending layer order inside a group
+}
+
+// ---------------------------------------------------------------- right-looking schedule
+// Blocks of 128 (the last may be smaller).  Step k, all matrices of the group in
+// lock-step:
+//   LEAF(k)   X_kk = L_kk^-1 of the (fully updated) diagonal block     [critical]
+//   PANEL(k)  L_ik = A_ik X_kk^T, i > k                                 [critical]
+//   T1(k)     A_{i,k+1} -= L_ik L_{k+1,k}^T, i >= k+1  (next column)     [critical,
+//             after T2(k-1)]
+//   T2(k)     A_ij -= L_ik L_jk^T, i >= j >= k+2 (lower tiles)           [side stream,
+//             after PANEL(k); capped to leave SMs to the critical stream]
+// so the bulk trailing update of step k runs under LEAF(k+1) / PANEL(k+1) instead
+// of on the critical path.  Then X = L^-1 from the leaf inverses, level-batched
+// recursion over block ranges (X21 = -X22 (L21 X11)): 2 rounds per level.
+struct RlStep {
+  int stream;          // 0 critical, 1 side (T2)
+  int wait;            // 0 none, 1 wait ev_panel (side), 2 wait ev_t2 (critical)
+  int record;          // 0 none, 1 record ev_panel (critical), 2 record ev_t2 (side)
+  std::vector<LeafJob> leaves;
+  std::vector<GemmSpec> g;
+};
+
+inline int rl_blocks(int n) { return (n + LEAF_N - 1) / LEAF_N; }
+
+void rl_schedule(const std::vector<const RlMat*>& mats, std::vector<RlStep>& out) {
+  out.clear();
+  int maxb = 0;
+  for (auto* M : mats) maxb = std::max(maxb, rl_blocks(M->n));
+  for (int k = 0; k < maxb; ++k) {
+    RlStep leaf{0, 0, 0, {}, {}}, panel{0, 0, 1, {}, {}}, t1{0, k > 0 ? 2 : 0, 0, {}, {}}, t2{1, 1, 2, {}, {}};
+    for (auto* M : mats) {
+      const int B = rl_blocks(M->n);
+      if (k >= B) continue;
+      const int64_t ld = M->ld;
+      const int r0 = k * LEAF_N, bk = std::min(LEAF_N, M->n - r0);
+      const int r1 = r0 + bk, rest = M->n - r1;
+      leaf.leaves.push_back(LeafJob{M->Aw + r0 * ld + r0, M->Xb + r0 * ld + r0, nullptr, ld, ld, bk, 0,
+                                    M->fail_code, 0, M->info});
+      if (rest <= 0) continue;
+      // PANEL: L[r1:, r0:r1] = A[r1:, r0:r1] X_kk^T   (X_kk lower: column block j needs k <= j)
+      GemmSpec pg = spec(rows_k(M->Aw + r1 * ld + r0, rest, bk, ld), rows_k(M->Xb + r0 * ld + r0, bk, bk, ld),
+                         M->Lb + r1 * ld + r0, ld, 1.0f, 0.0f, 0);
+      pg.tri_b = TRI_LOWER;
+      panel.g.push_back(pg);
+      // T1: A[r1:, r1:r1+b1] -= L[r1:, k] L[r1:r1+b1, k]^T
+      const int b1 = std::min(LEAF_N, rest);
+      t1.g.push_back(spec(rows_k(M->Lb + r1 * ld + r0, rest, bk, ld), rows_k(M->Lb + r1 * ld + r0, b1, bk, ld),
+                          M->Aw + r1 * ld + r1, ld, -1.0f, 1.0f, 0));
+      // T2: A[r2:, r2:] -= L[r2:, k] L[r2:, k]^T (lower tiles)
+      const int r2 = r1 + b1, rest2 = M->n - r2;
+      if (rest2 > 0) {
+        GemmSpec g2 = spec(rows_k(M->Lb + r2 * ld + r0, rest2, bk, ld), rows_k(M->Lb + r2 * ld + r0, rest2, bk, ld),
+                           M->Aw + r2 * ld + r2, ld, -1.0f, 1.0f, 1);
+        g2.lower_only = 1;
+        t2.g.push_back(g2);
+      }
+    }
+    out.push_back(std::move(leaf));
+    if (!panel.g.empty()) out.push_back(std::move(panel));
+    else out.push_back(RlStep{0, 0, 1, {}, {}});  // keep the event sequence uniform
+    if (!t1.g.empty() || k > 0) out.push_back(std::move(t1));
+    out.push_back(std::move(t2));
+  }
+  // join: the critical stream waits for the last trailing update
+  out.push_back(RlStep{0, 2, 0, {}, {}});
+  // X = L^-1, level-batched over block ranges [s, e) of each matrix
+  struct Rng {
+    const RlMat* M;
+    int s, e;  // block indices
+  };
+  std::vector<std::vector<Rng>> levels;  // levels[0] = the whole ranges
+  {
+    std::vector<Rng> cur;
+    for (auto* M : mats) cur.push_back(Rng{M, 0, rl_blocks(M->n)});
+    while (!cur.empty()) {
+      levels.push_back(cur);
+      std::vector<Rng> nxt;
+      for (auto& r : cur)
+        if (r.e - r.s > 1) {
+          const int mid = r.s + (r.e - r.s + 1) / 2;
+          nxt.push_back(Rng{r.M, r.s, mid});
+          nxt.push_back(Rng{r.M, mid, r.e});
+        }
+      cur.swap(nxt);
+    }
+  }
+  for (int lv = static_cast<int>(levels.size()) - 1; lv >= 0; --lv) {  // bottom-up
+    RlStep ra{0, 0, 0, {}, {}}, rb{0, 0, 0, {}, {}};
+    for (auto& r : levels[lv]) {
+      if (r.e - r.s < 2) continue;
+      const RlMat* M = r.M;
+      const int64_t ld = M->ld;
+      const int mid = r.s + (r.e - r.s + 1) / 2;
+      const int c0 = r.s * LEAF_N, c1 = mid * LEAF_N, c2 = std::min(M->n, r.e * LEAF_N);
+      const int n1 = c1 - c0, n2 = c2 - c1;
+      // T = L21 X11 into the (consumed) working block A[c1:c2, c0:c1]
+      GemmSpec ta = spec(rows_k(M->Lb + c1 * ld + c0, n2, n1, ld), rows_mn(M->Xb + c0 * ld + c0, n1, n1, ld),
+                         M->Aw + c1 * ld + c0, ld, 1.0f, 0.0f, 0);
+      ta.tri_b = TRI_UPPER;  // op view of X11 is X11^T: k >= j
+      ra.g.push_back(ta);
+      // X21 = -X22 T
+      GemmSpec tb = spec(rows_k(M->Xb + c1 * ld + c1, n2, n2, ld), rows_mn(M->Aw + c1 * ld + c0, n1, n2, ld),
+                         M->Xb + c1 * ld + c0, ld, -1.0f, 0.0f, 0);
+      tb.tri_a = TRI_LOWER;  // X22 lower: k <= i
+      rb.g.push_back(tb);
+    }
+    if (!ra.g.empty()) {
+      out.push_back(std::move(ra));
+      out.push_back(std::move(rb));
+    }
+  }
+}
+
+// DPK_SPD_RL=<n>: groups whose largest factor is >= n use the right-looking schedule.
+// Off by default: measured slower than the recursion on B200 (three 4608 factors
+// 3.90 vs 3.66 ms, the ResNet-50 set 5.75 vs 4.82 ms): the chain is ~65% bound by
+// the 3xTF32 flops, and the rank-128 trailing updates stream the whole trailing
+// matrix per block column (n^3 / 3b floats of traffic) where the recursion's
+// large-K products reuse operands on chip; the side lane also contends for SMs.
+int rl_min_n() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DPK_SPD_RL");
+    v = e ? atoi(e) : 0;
+    if (v <= 0) v = 1 << 30;
+  }
+  return v;
 }
 
 void make_spd_plan(const SpdReq* jobs, int n, char* base, SpdPlan& plan) {
@@ -577,6 +718,8 @@ void make_spd_plan(const SpdReq* jobs, int n, char* base, SpdPlan& plan) {
     float* Xb = factor ? jobs[i].dst : Lb + blk;
     off += align_up(matrix_ws_floats(m, factor) * sizeof(float), 256);
     plan.preps.push_back(PrepJob{jobs[i].src, Aw, Xb, jobs[i].shift, m, ldw});
+    if (static_cast<int>(plan.mats.size()) < n) plan.mats.resize(n);
+    plan.mats[i] = RlMat{Aw, Lb, Xb, ldw, m, jobs[i].fail_code, jobs[i].info};
     build_ops(Aw, Lb, Xb, ldw, m, jobs[i].fail_code, jobs[i].info, ops);
     if (factor) continue;  // X is the result
     Op op{};
@@ -588,10 +731,41 @@ void make_spd_plan(const SpdReq* jobs, int n, char* base, SpdPlan& plan) {
     ops.push_back(op);
   }
   plan.rec_bytes = off;
+  plan.mats.resize(n);
   make_groups(jobs, n, plan);
   plan.gemm_bytes = 0;
   plan.group_ws.clear();
+  plan.group_rl.clear();
+  plan.group_ws_side.clear();
   for (const auto& grp : plan.groups) {
+    // right-looking schedule: factored-mode groups of large factors (explicit
+    // inverses keep the recursion, whose X^T X round follows the same lists)
+    bool rl = true;
+    int gmax = 0;
+    for (int q : grp) {
+      rl = rl && jobs[q].factor && jobs[q].n > LEAF_N;
+      gmax = std::max(gmax, jobs[q].n);
+    }
+    rl = rl && gmax >= rl_min_n();
+    plan.group_rl.push_back(rl ? 1 : 0);
+    if (rl) {
+      std::vector<const RlMat*> ms;
+      for (int q : grp) ms.push_back(&plan.mats[q]);
+      std::vector<RlStep> steps;
+      rl_schedule(ms, steps);
+      size_t wc = 0, wsd = 0;
+      for (auto& stp : steps)
+        if (!stp.g.empty()) {
+          const size_t w = gemm_workspace_bytes(stp.g.data(), static_cast<int>(stp.g.size()));
+          (stp.stream ? wsd : wc) = std::max(stp.stream ? wsd : wc, w);
+        }
+      plan.group_ws.push_back(plan.gemm_bytes);
+      plan.gemm_bytes += align_up(std::max<size_t>(wc, GEMM_SCHED_BYTES), 1024);
+      plan.group_ws_side.push_back(plan.gemm_bytes);
+      plan.gemm_bytes += align_up(std::max<size_t>(wsd, GEMM_SCHED_BYTES), 1024);
+      continue;
+    }
+    plan.group_ws_side.push_back(0);
     std::vector<size_t> idx(grp.size(), 0);
     size_t worst = 0;
     for (;;) {
@@ -723,6 +897,84 @@ int ensure_side_streams(int n) {
   return DPK_OK;
 }
 int run_cached_graph(const SpdReq* jobs, int n_jobs, void* workspace, size_t ws_bytes, cudaStream_t st);
+
+// per-device streams and events of the right-looking schedule's side (T2) lane
+struct RlLanes {
+  cudaStream_t side[MAX_GROUPS] = {};
+  cudaEvent_t ev_panel[MAX_GROUPS] = {};
+  cudaEvent_t ev_t2[MAX_GROUPS] = {};
+};
+int rl_lane(int g, cudaStream_t& side, cudaEvent_t& ev_panel, cudaEvent_t& ev_t2) {
+  static std::mutex mu;
+  static std::vector<RlLanes> per_dev;
+  std::lock_guard<std::mutex> lock(mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (static_cast<int>(per_dev.size()) <= dev) per_dev.resize(dev + 1);
+  RlLanes& L = per_dev[dev];
+  if (!L.side[g]) {
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    int rc = cuda_status(cudaStreamCreateWithPriority(&L.side[g], cudaStreamNonBlocking, least), "cudaStreamCreate(rl)");
+    if (!rc) rc = cuda_status(cudaEventCreateWithFlags(&L.ev_panel[g], cudaEventDisableTiming), "cudaEventCreate(rl)");
+    if (!rc) rc = cuda_status(cudaEventCreateWithFlags(&L.ev_t2[g], cudaEventDisableTiming), "cudaEventCreate(rl)");
+    if (rc) return rc;
+  }
+  side = L.side[g];
+  ev_panel = L.ev_panel[g];
+  ev_t2 = L.ev_t2[g];
+  return DPK_OK;
+}
+
+int rl_side_cap() {  // SMs the trailing updates may use (DPK_RL_CAP, default num_sms - 32)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DPK_RL_CAP");
+    v = e ? atoi(e) : std::max(16, num_sms() - 32);
+  }
+  return v;
+}
+
+int run_rl(const SpdPlan& plan, int g, char* ws_crit, size_t bytes_crit, char* ws_side, size_t bytes_side,
+           cudaStream_t st) {
+  std::vector<const RlMat*> ms;
+  for (int q : plan.groups[g]) ms.push_back(&plan.mats[q]);
+  std::vector<RlStep> steps;
+  rl_schedule(ms, steps);
+  cudaStream_t side;
+  cudaEvent_t ev_panel, ev_t2;
+  int rc = rl_lane(g, side, ev_panel, ev_t2);
+  if (rc) return rc;
+  // the side lane starts after everything already on the critical stream (prep)
+  rc = cuda_status(cudaEventRecord(ev_panel, st), "cudaEventRecord(rl fork)");
+  if (!rc) rc = cuda_status(cudaStreamWaitEvent(side, ev_panel, 0), "cudaStreamWaitEvent(rl fork)");
+  if (!rc) rc = cuda_status(cudaMemsetAsync(ws_crit, 0, GEMM_SCHED_BYTES, st), "cudaMemsetAsync(rl counters)");
+  if (!rc) rc = cuda_status(cudaMemsetAsync(ws_side, 0, GEMM_SCHED_BYTES, side), "cudaMemsetAsync(rl counters)");
+  if (!rc) rc = cuda_status(cudaEventRecord(ev_t2, side), "cudaEventRecord(rl)");
+  if (rc) return rc;
+  for (const RlStep& stp : steps) {
+    cudaStream_t s = stp.stream ? side : st;
+    if (stp.wait == 1) rc = cuda_status(cudaStreamWaitEvent(s, ev_panel, 0), "cudaStreamWaitEvent(rl panel)");
+    if (stp.wait == 2) rc = cuda_status(cudaStreamWaitEvent(s, ev_t2, 0), "cudaStreamWaitEvent(rl t2)");
+    if (rc) return rc;
+    if (!stp.leaves.empty()) {
+      std::vector<LeafJob> lv = stp.leaves;
+      rc = launch_leaves(lv, s);
+      if (rc) return rc;
+    }
+    if (!stp.g.empty()) {
+      if (stp.stream) set_grid_cap_override(rl_side_cap());
+      rc = gemm_launch(stp.g.data(), static_cast<int>(stp.g.size()), stp.stream ? ws_side : ws_crit,
+                       stp.stream ? bytes_side : bytes_crit, DPK_PREC_3XTF32, s, false);
+      set_grid_cap_override(0);
+      if (rc) return rc;
+    }
+    if (stp.record == 1) rc = cuda_status(cudaEventRecord(ev_panel, s), "cudaEventRecord(rl panel)");
+    if (stp.record == 2) rc = cuda_status(cudaEventRecord(ev_t2, s), "cudaEventRecord(rl t2)");
+    if (rc) return rc;
+  }
+  return DPK_OK;
+}
 
 }  // namespace
 }  // namespace dpk
@@ -872,7 +1124,17 @@ int run_inverse(const SpdReq* jobs, int n_jobs, void* workspace, cudaStream_t st
     return run_lockstep(plan, all, gemm_ws, plan.gemm_bytes, st, true);
   }
   const int ng = static_cast<int>(plan.groups.size());
-  if (ng == 1) return run_lockstep(plan, plan.groups[0], gemm_ws + plan.group_ws[0], plan.gemm_bytes, st, false);
+  auto run_group = [&](int g, cudaStream_t s) -> int {
+    const size_t off = plan.group_ws[g];
+    if (plan.group_rl[g]) {
+      const size_t side = plan.group_ws_side[g];
+      const size_t end = g + 1 < ng ? plan.group_ws[g + 1] : plan.gemm_bytes;
+      return run_rl(plan, g, gemm_ws + off, side - off, gemm_ws + side, end - side, s);
+    }
+    const size_t bytes = (g + 1 < ng ? plan.group_ws[g + 1] : plan.gemm_bytes) - off;
+    return run_lockstep(plan, plan.groups[g], gemm_ws + off, bytes, s, false);
+  };
+  if (ng == 1) return run_group(0, st);
   int rc = ensure_side_streams(ng - 1);
   if (rc) return rc;
   SideStreams& ss = side_streams();
@@ -883,9 +1145,7 @@ int run_inverse(const SpdReq* jobs, int n_jobs, void* workspace, cudaStream_t st
     if (rc) return rc;
   }
   for (int g = 0; g < ng; ++g) {
-    const size_t off = plan.group_ws[g];
-    const size_t bytes = (g + 1 < ng ? plan.group_ws[g + 1] : plan.gemm_bytes) - off;
-    rc = run_lockstep(plan, plan.groups[g], gemm_ws + off, bytes, g == 0 ? st : ss.s[g - 1], false);
+    rc = run_group(g, g == 0 ? st : ss.s[g - 1]);
     if (rc) return rc;
   }
   for (int g = 1; g < ng; ++g) {
