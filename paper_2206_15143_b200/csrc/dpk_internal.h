@@ -76,6 +76,8 @@ size_t gemm_workspace_bytes(const GemmSpec* specs, int n);
 // tcgen05 launches made by this thread use at most `cap` SMs (0 = all): a
 // concurrent stream keeps the rest (spd_inv.cu's right-looking trailing updates)
 void set_grid_cap_override(int cap);
+// K4 Jacobi rotation thresholds (syevd.cu), shared by the on-chip and block kernels
+void jac_tolerances(float& rel, float& abs_);
 // K4 n > 128: block Jacobi (syevj.cu); jobs with n <= 128 are ignored
 size_t syevj_workspace_bytes(const dpk_eig_job* jobs, int n_jobs);
 int syevj_run(const dpk_eig_job* jobs, int n_jobs, void* workspace, size_t ws_bytes, cudaStream_t st);

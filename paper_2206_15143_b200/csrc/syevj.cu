@@ -38,15 +38,13 @@
 #include <vector>
 
 #include "dpk_internal.h"
+#include "jacobi1s.cuh"
 
 namespace dpk {
 namespace {
 
 constexpr int BJ_B = 64;          // block edge; a pair is one 128 x 128 on-chip problem
 constexpr int BJ_P = 2 * BJ_B;
-constexpr int BJ_THREADS = 256;
-constexpr int BJ_LD = BJ_P + 1;
-constexpr int BJ_INNER_SWEEPS = 15;
 constexpr int BJ_MAXJ = 128;      // pair-kernel jobs per launch
 
 struct PairJob {
@@ -59,32 +57,19 @@ struct PairJob {
 };
 struct PairBatch {
   int n;
+  float rel_tol, abs_tol;
   PairJob j[BJ_MAXJ];
 };
 
-__device__ __forceinline__ void pair_of(int round, int slot, int m, int& p, int& q) {
-  int a, b;
-  if (slot == 0) {
-    a = m - 1;
-    b = round;
-  } else {
-    a = (round + slot) % (m - 1);
-    b = (round - slot + (m - 1)) % (m - 1);
-  }
-  p = min(a, b);
-  q = max(a, b);
-}
 
-// One CTA per pair: on-chip cyclic Jacobi of the 128 x 128 diagonal block, then
-// the UBC column order + half swap, written into Vbig.
-__global__ void __launch_bounds__(BJ_THREADS) bj_pair_kernel(const __grid_constant__ PairBatch b) {
+// One CTA per pair: one-sided Jacobi (jacobi1s.cuh) of the 128 x 128 diagonal
+// block, then the UBC column order + half swap, written into Vbig.
+__global__ void __launch_bounds__(J1_THREADS) bj_pair_kernel(const __grid_constant__ PairBatch b) {
   extern __shared__ float sm[];
-  float* A = sm;
-  float* V = sm + BJ_P * BJ_LD;
-  __shared__ float cs[BJ_P / 2], sn[BJ_P / 2], dp_new[BJ_P / 2], dq_new[BJ_P / 2];
-  __shared__ int pp[BJ_P / 2], qq[BJ_P / 2];
-  __shared__ int rot_count;
-  __shared__ float fro2;
+  constexpr int m = BJ_P, ld = BJ_P;
+  float* U = sm;
+  float* V = sm + m * ld;
+  __shared__ float lam[BJ_P];
   __shared__ float wgt[BJ_P];
   __shared__ int dest[BJ_P];
   int q = 0;
@@ -94,7 +79,6 @@ __global__ void __launch_bounds__(BJ_THREADS) bj_pair_kernel(const __grid_consta
   const int64_t N = J.N;
   const int64_t base = static_cast<int64_t>(p) * BJ_P * (N + 1);  // diagonal block (p, p)
   float* vout = J.Vbig + base;
-  constexpr int m = BJ_P, ld = BJ_LD, half = BJ_P / 2;
   if (p == J.ident) {  // the two ends of the line: identity, no swap
     for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
       const int i = e / m, c = e - (e / m) * m;
@@ -104,109 +88,25 @@ __global__ void __launch_bounds__(BJ_THREADS) bj_pair_kernel(const __grid_consta
   }
   const float* src = J.A + base;
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-    const int i = e / m, c = e - (e / m) * m;
-    A[i * ld + c] = 0.5f * (src[i * N + c] + src[c * N + i]);
-    V[i * ld + c] = (i == c) ? 1.0f : 0.0f;
+    const int c = e / m, r = e - (e / m) * m;
+    U[c * ld + r] = 0.5f * (src[r * N + c] + src[c * N + r]);
+    V[c * ld + r] = (r == c) ? 1.0f : 0.0f;
   }
-  if (threadIdx.x == 0) fro2 = 0.0f;
   __syncthreads();
+  onesided_jacobi(U, V, ld, m, m, b.rel_tol, lam);
+  // UBC order: weight of each eigenvector column in the first block (rows 0..63);
+  // the 64 heaviest continue block 1 and move to slot 2 (the swap), the rest go to
+  // slot 1; original column order within each half
   {
-    float acc = 0.0f;
-    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
-      const float a = A[(e / m) * ld + (e % m)];
-      acc += a * a;
-    }
-    atomicAdd(&fro2, acc);
-  }
-  __syncthreads();
-  const float abs_tol = 3e-8f * sqrtf(fro2);
-  for (int sweep = 0; sweep < BJ_INNER_SWEEPS; ++sweep) {
-    if (threadIdx.x == 0) rot_count = 0;
-    __syncthreads();
-    for (int round = 0; round < m - 1; ++round) {
-      for (int s = threadIdx.x; s < half; s += blockDim.x) {
-        int pi, qi;
-        pair_of(round, s, m, pi, qi);
-        pp[s] = pi;
-        qq[s] = qi;
-        const float apq = A[pi * ld + qi];
-        const float app = A[pi * ld + pi], aqq = A[qi * ld + qi];
-        float c = 1.f, si = 0.f;
-        if (fabsf(apq) > 2e-7f * sqrtf(fabsf(app * aqq)) && fabsf(apq) > abs_tol && fabsf(apq) > 1e-36f) {
-          const float tau = (aqq - app) / (2.0f * apq);
-          const float t = copysignf(1.0f, tau) / (fabsf(tau) + __fsqrt_rn(1.0f + tau * tau));
-          c = __fdiv_rn(1.0f, __fsqrt_rn(1.0f + t * t));
-          si = t * c;
-          atomicAdd(&rot_count, 1);
-          dp_new[s] = app - t * apq;
-          dq_new[s] = aqq + t * apq;
-        } else {
-          dp_new[s] = app;
-          dq_new[s] = aqq;
-        }
-        cs[s] = c;
-        sn[s] = si;
-      }
-      __syncthreads();
-      for (int e = threadIdx.x; e < half * m; e += blockDim.x) {
-        const int s = e / m, c = e - s * m;
-        const int pi = pp[s], qi = qq[s];
-        const float co = cs[s], si = sn[s];
-        const float ap = A[pi * ld + c], aq = A[qi * ld + c];
-        A[pi * ld + c] = co * ap - si * aq;
-        A[qi * ld + c] = si * ap + co * aq;
-      }
-      __syncthreads();
-      for (int e = threadIdx.x; e < half * m; e += blockDim.x) {
-        const int s = e / m, r = e - s * m;
-        const int pi = pp[s], qi = qq[s];
-        const float co = cs[s], si = sn[s];
-        const float ap = A[r * ld + pi], aq = A[r * ld + qi];
-        A[r * ld + pi] = co * ap - si * aq;
-        A[r * ld + qi] = si * ap + co * aq;
-        const float vp = V[r * ld + pi], vq = V[r * ld + qi];
-        V[r * ld + pi] = co * vp - si * vq;
-        V[r * ld + qi] = si * vp + co * vq;
-      }
-      __syncthreads();
-      for (int s = threadIdx.x; s < half; s += blockDim.x) {
-        if (sn[s] != 0.0f) {
-          const int pi = pp[s], qi = qq[s];
-          A[pi * ld + pi] = dp_new[s];
-          A[qi * ld + qi] = dq_new[s];
-          A[pi * ld + qi] = 0.0f;
-          A[qi * ld + pi] = 0.0f;
-        }
-      }
-      __syncthreads();
-    }
-    if (rot_count == 0) break;
-    __syncthreads();
-  }
-  // re-normalise V's columns (rotation rounding drifts the norms by ~1e-5) and
-  // weigh each column by its mass in the first block (rows 0..63)
-  {
-    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int c = wid; c < m; c += BJ_THREADS / 32) {
-      float ss = 0.f, s1 = 0.f;
-      for (int r = lane; r < m; r += 32) {
-        const float v = V[r * ld + c];
-        ss = fmaf(v, v, ss);
-        if (r < BJ_B) s1 = fmaf(v, v, s1);
-      }
-      for (int o = 16; o > 0; o >>= 1) {
-        ss += __shfl_xor_sync(0xffffffffu, ss, o);
-        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-      }
-      const float inv = ss > 0.f ? rsqrtf(ss) : 1.f;
-      const float fix = inv * (1.5f - 0.5f * ss * inv * inv);
-      for (int r = lane; r < m; r += 32) V[r * ld + c] *= fix;
-      if (lane == 0) wgt[c] = s1 * fix * fix;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int c = warp; c < m; c += (J1_THREADS >> 5)) {
+      float s1 = 0.f;
+      for (int r = lane; r < BJ_B; r += 32) s1 = fmaf(V[c * ld + r], V[c * ld + r], s1);
+      s1 = j1_warp_sum(s1);
+      if (lane == 0) wgt[c] = s1;
     }
   }
   __syncthreads();
-  // UBC order: the 64 columns heaviest in the first block continue block 1 and move
-  // to slot 2 (the swap); the rest go to slot 1; original column order within each
   if (threadIdx.x < m) {
     const int c = threadIdx.x;
     const float w = wgt[c];
@@ -228,7 +128,7 @@ __global__ void __launch_bounds__(BJ_THREADS) bj_pair_kernel(const __grid_consta
   __syncthreads();
   for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
     const int r = e / m, c = e - (e / m) * m;
-    vout[r * N + __float_as_int(wgt[c])] = V[r * ld + c];
+    vout[r * N + __float_as_int(wgt[c])] = V[c * ld + r];
   }
 }
 
@@ -425,7 +325,7 @@ int bj_run(const dpk_eig_job* jobs, const std::vector<int>& big, void* workspace
   char* gemm_ws = static_cast<char*>(workspace) + used;
   const size_t gemm_bytes = ws_bytes - used;
   static std::atomic<uint64_t> attr_on{0};
-  const int pair_smem = 2 * BJ_P * BJ_LD * 4;
+  const int pair_smem = 2 * BJ_P * BJ_P * 4;
   if (first_on_device(attr_on)) {
     cudaError_t e = cudaFuncSetAttribute(bj_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, pair_smem);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(bj_pair_kernel)");
@@ -451,13 +351,14 @@ int bj_run(const dpk_eig_job* jobs, const std::vector<int>& big, void* workspace
   int max_rounds = 0;
   for (auto& M : mats) max_rounds = std::max(max_rounds, M.rounds);
   thread_local PairBatch pb;
+  jac_tolerances(pb.rel_tol, pb.abs_tol);
   for (int r = 0; r < max_rounds; ++r) {
     // 1. pair eigenproblems of every active matrix
     pb.n = 0;
     int total_pairs = 0;
     auto flush_pairs = [&]() -> int {
       if (pb.n == 0) return DPK_OK;
-      bj_pair_kernel<<<total_pairs, BJ_THREADS, pair_smem, st>>>(pb);
+      bj_pair_kernel<<<total_pairs, J1_THREADS, pair_smem, st>>>(pb);
       note_launch();
       pb.n = 0;
       total_pairs = 0;
