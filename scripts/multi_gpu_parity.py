@@ -73,6 +73,43 @@ def main():
             if not rel(got, cl.weights[i]) <= 1e-4:
                 bad.append((algorithm, inv, "weights", i, rel(got, cl.weights[i])))
         kf.remove_hooks()
+    # KL-clip over NCCL: every rank's partial <pre, grad> rides the all-gather (one slot per
+    # owner chunk); the unpack applies nu = min(1, sqrt(kl / |lr^2 sum <pre, grad>|))
+    for inv in ("inverse", "eigen"):
+        h = K.Hyper(gamma=0.05, xi=0.9, inv_type=inv, f_freq=1, k_freq=1)
+        cl = MLP.build_cluster(spec, P, seed=7)
+        mods = []
+        for i, w in enumerate(cl.weights):
+            lin = torch.nn.Linear(w.shape[1] - 1, w.shape[0])
+            with torch.no_grad():
+                lin.weight.copy_(torch.from_numpy(w[:, :-1]))
+                lin.bias.copy_(torch.from_numpy(w[:, -1]))
+            mods += [lin, torch.nn.ReLU()]
+        model = torch.nn.Sequential(*mods[:-1]).to(dev)
+        lins = [m for m in model if isinstance(m, torch.nn.Linear)]
+        lr, kl = 0.1, 1e-5
+        kf = DPKFAC(model, gamma=0.05, xi=0.9, inv_type=inv, precision="3xtf32", kl_clip=kl, lr=lr,
+                    assignment="balanced")
+        rng = np.random.default_rng(17)
+        x, y = rng.standard_normal((20, B)), rng.integers(0, 5, size=B)
+        shards = MLP.shard(x, y, P)
+        xs, ys = shards[rank]
+        F.cross_entropy(model(torch.from_numpy(xs.T.copy()).float().to(dev)), torch.from_numpy(ys).to(dev)).backward()
+        kf.step()
+        cl = MLP.build_cluster(spec, P, seed=7, assignment=kf.assignment)
+        _, pre = MLP.dp_kfac_step(cl, shards, h, lr, 0.9, 0)
+        loc = [MLP.forward_backward(spec, MLP.init_weights(spec, 7), xx, yy)[3] for xx, yy in shards]
+        agg = [MLP.tree_mean([loc[p][i] for p in range(P)]) for i in range(len(lins))]
+        vg = sum(float((pre[i] * agg[i]).sum()) for i in range(len(lins))) * lr * lr
+        nu = min(1.0, (kl / abs(vg)) ** 0.5)
+        if not nu < 1.0:
+            bad.append(("kl_clip inactive", inv, nu))
+        for i, lin in enumerate(lins):
+            got = torch.cat([lin.weight.grad, lin.bias.grad[:, None]], 1).double().cpu().numpy()
+            e = rel(got, nu * pre[i])
+            if not e <= 1e-3:
+                bad.append(("kl_clip", inv, i, e, nu))
+        kf.remove_hooks()
     # non-preconditioned parameters (batch norm) are averaged over ranks, unpreconditioned
     torch.manual_seed(0)
     net = torch.nn.Sequential(torch.nn.Linear(20, 16), torch.nn.BatchNorm1d(16), torch.nn.ReLU(),
