@@ -225,9 +225,15 @@ struct K16Batch {
   int first[I2C_MAX + 1];
   dpk_im2col_job j[I2C_MAX];
 };
-constexpr int K16_GROUPS = 4;  // 32-row groups per block (the pixel decode is shared)
+constexpr int K16_GROUPS = 16;  // 32-row groups per block (the pixel decode is shared)
 __global__ void __launch_bounds__(256) im2col_k16_tiled_kernel(const __grid_constant__ K16Batch b) {
-  __shared__ float T[2][32][K16_PIX + 1];
+  // Each group: 64 pixels x 32 channels of one tap.  Thread t loads the 4 channels
+  // 4*(t&7).. of the two adjacent pixels 2*(t>>3), 2*(t>>3)+1 (8 threads cover one
+  // pixel's 128-B row: coalesced), packs them as half2 (pixel pair) per channel into a
+  // [32 rows][32 words] fp16 tile whose word column is XOR-swizzled by 4*(row/4) --
+  // conflict-free for these stores and for the 16-B row reads -- then every thread
+  // writes 8 halves (16 B) of one channel row.  ~3 instructions per element.
+  __shared__ __align__(16) uint32_t T[2][32 * 32];
   int q = 0;
   while (q + 1 < b.n && b.first[q + 1] <= static_cast<int>(blockIdx.x)) ++q;
   const dpk_im2col_job& J = b.j[q];
@@ -236,57 +242,79 @@ __global__ void __launch_bounds__(256) im2col_k16_tiled_kernel(const __grid_cons
   const int kblocks = static_cast<int>((o.cols + K16_PIX - 1) / K16_PIX);
   const int gb = local / kblocks;  // block of K16_GROUPS row groups
   const int64_t k0 = static_cast<int64_t>(local - gb * kblocks) * K16_PIX;
-  const int ohw = o.OH * o.OW;
-  // this thread's two (pixel, 4-channel) slots, decoded once
-  int pn[2], poh[2], pow_[2];
+  // job parameters into registers once (a dynamically indexed __grid_constant__
+  // struct is otherwise re-read from the constant bank at every use)
+  const int OW = o.OW, ohw = o.OH * OW, C = o.C, H = o.H, W = o.W, kw = o.kw;
+  const int sh = o.sh, sw = o.sw, dh = o.dh, dw = o.dw;
+  const int shs = static_cast<int>(o.shs), sws = static_cast<int>(o.sws);  // within one image
+  const int64_t cols = o.cols, ld = J.ld;
+  const int tid = threadIdx.x;
+  const int pp = tid >> 3, qq = tid & 7;
+  // the thread's two pixels, decoded once: image base pointer and tap-0 input coordinates
+  const float* base[2];
+  int ih0[2], iw0[2];
   bool pin[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    const int p = (threadIdx.x + 256 * h) >> 3;
-    const int64_t k = k0 + p;
-    pin[h] = k < o.cols;
-    const int64_t kk = pin[h] ? k : 0;
-    pn[h] = static_cast<int>(kk / ohw);
-    const int rem = static_cast<int>(kk - static_cast<int64_t>(pn[h]) * ohw);
-    poh[h] = rem / o.OW;
-    pow_[h] = rem - poh[h] * o.OW;
+    const int64_t k = k0 + 2 * pp + h;
+    pin[h] = k < cols;
+    const uint32_t kk = pin[h] ? static_cast<uint32_t>(k) : 0u;  // cols < 2^31 (k16_tiled_ok)
+    const uint32_t n = kk / static_cast<uint32_t>(ohw);
+    const int rem = static_cast<int>(kk - n * static_cast<uint32_t>(ohw));
+    const int oh = rem / OW, ow = rem - (rem / OW) * OW;
+    base[h] = o.data + static_cast<int64_t>(n) * o.sn + 4 * qq;
+    ih0[h] = oh * sh - o.ph;
+    iw0[h] = ow * sw - o.pw;
   }
-  const int nrg = (o.rows + 31) / 32;
   const float sc = J.amax ? ldexpf(1.0f, -prescale_exponent(__ldg(J.amax))) : 1.0f;  // exact 2^-e
-  for (int g = 0; g < K16_GROUPS; ++g) {
-    const int rg = gb * K16_GROUPS + g;
+  const int nrg = (o.rows + 31) / 32;
+  const int cblk = C >> 5;  // 32-channel groups per tap
+  int rg = gb * K16_GROUPS;
+  int tap = rg / cblk, c0 = (rg - tap * cblk) * 32;
+  int ti = tap / kw, tj = tap - (tap / kw) * kw;
+  // store-phase coordinates: row = tid >> 3 (channel), segment = tid & 7 (8 pixels)
+  const int srow = tid >> 3, sseg = tid & 7;
+  const int64_t kk0 = k0 + sseg * 8;
+  __half* out = reinterpret_cast<__half*>(J.out) + static_cast<int64_t>(32 * rg + srow) * ld + kk0;
+  const int rsw = (4 * sseg) ^ (4 * (srow >> 2));  // swizzled word of the store-phase read
+  const int wcol = pp ^ (4 * qq);                  // rows 4qq..4qq+3 share the swizzle 4*qq
+  for (int g = 0; g < K16_GROUPS; ++g, ++rg) {
     if (rg >= nrg) break;
-    const int r0 = rg * 32;
-    const int tap = r0 / o.C, c0 = r0 - tap * o.C;
-    const int i = tap / o.kw, j = tap - (tap / o.kw) * o.kw;
-    float (*Tb)[K16_PIX + 1] = T[g & 1];
+    uint32_t* Tb = T[g & 1];
+    float4 v[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int idx = threadIdx.x + 256 * h;
-      const int p = idx >> 3, qq = idx & 7;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      const int ih = poh[h] * o.sh - o.ph + i * o.dh, iw = pow_[h] * o.sw - o.pw + j * o.dw;
-      if (pin[h] && static_cast<unsigned>(ih) < static_cast<unsigned>(o.H) &&
-          static_cast<unsigned>(iw) < static_cast<unsigned>(o.W))
-        v = __ldg(reinterpret_cast<const float4*>(o.data + static_cast<int64_t>(pn[h]) * o.sn +
-                                                  static_cast<int64_t>(ih) * o.shs + static_cast<int64_t>(iw) * o.sws +
-                                                  c0) + qq);
-      Tb[4 * qq][p] = v.x * sc;
-      Tb[4 * qq + 1][p] = v.y * sc;
-      Tb[4 * qq + 2][p] = v.z * sc;
-      Tb[4 * qq + 3][p] = v.w * sc;
+      v[h] = make_float4(0.f, 0.f, 0.f, 0.f);
+      const int ih = ih0[h] + ti * dh, iw = iw0[h] + tj * dw;
+      if (pin[h] && static_cast<unsigned>(ih) < static_cast<unsigned>(H) &&
+          static_cast<unsigned>(iw) < static_cast<unsigned>(W))
+        v[h] = __ldg(reinterpret_cast<const float4*>(base[h] + (ih * shs + iw * sws + c0)));
     }
+    const __half2 h0 = __floats2half2_rn(v[0].x * sc, v[1].x * sc);
+    const __half2 h1 = __floats2half2_rn(v[0].y * sc, v[1].y * sc);
+    const __half2 h2 = __floats2half2_rn(v[0].z * sc, v[1].z * sc);
+    const __half2 h3 = __floats2half2_rn(v[0].w * sc, v[1].w * sc);
+    uint32_t* tw = Tb + 4 * qq * 32 + wcol;
+    tw[0] = *reinterpret_cast<const uint32_t*>(&h0);
+    tw[32] = *reinterpret_cast<const uint32_t*>(&h1);
+    tw[64] = *reinterpret_cast<const uint32_t*>(&h2);
+    tw[96] = *reinterpret_cast<const uint32_t*>(&h3);
     __syncthreads();  // (double-buffered T: one barrier per group)
-    const int row = threadIdx.x >> 3, seg = threadIdx.x & 7;
-    __half* out = reinterpret_cast<__half*>(J.out) + static_cast<int64_t>(r0 + row) * J.ld + k0 + seg * 8;
-    const int64_t kk = k0 + seg * 8;
-    if (kk + 8 <= o.cols) {
-      __half2 hv[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) hv[e] = __floats2half2_rn(Tb[row][seg * 8 + 2 * e], Tb[row][seg * 8 + 2 * e + 1]);
-      __stcs(reinterpret_cast<uint4*>(out), *reinterpret_cast<const uint4*>(hv));
+    const uint4 w = *reinterpret_cast<const uint4*>(Tb + srow * 32 + rsw);
+    if (kk0 + 8 <= cols) {
+      __stcs(reinterpret_cast<uint4*>(out), w);
     } else {
-      for (int e = 0; e < 8 && kk + e < o.cols; ++e) out[e] = __float2half_rn(Tb[row][seg * 8 + e]);
+      const __half* hv = reinterpret_cast<const __half*>(&w);
+      for (int e = 0; e < 8 && kk0 + e < cols; ++e) out[e] = hv[e];
+    }
+    out += 32 * ld;
+    c0 += 32;
+    if (c0 == C) {
+      c0 = 0;
+      if (++tj == kw) {
+        tj = 0;
+        ++ti;
+      }
     }
   }
 }
@@ -463,7 +491,9 @@ bool k16_rows_ok(const dpk_im2col_job& j) {
 bool k16_tiled_ok(const dpk_im2col_job& j) {
   const dpk_operand& o = j.x;
   return o.kind == DPK_OPND_IM2COL_TAPMAJOR && o.sc == 1 && o.C % 32 == 0 && !o.bias_row &&
-         (reinterpret_cast<uintptr_t>(o.data) & 15) == 0 && o.sn % 4 == 0 && o.shs % 4 == 0 && o.sws % 4 == 0;
+         (reinterpret_cast<uintptr_t>(o.data) & 15) == 0 && o.sn % 4 == 0 && o.shs % 4 == 0 && o.sws % 4 == 0 &&
+         static_cast<int64_t>(o.H) * o.shs + static_cast<int64_t>(o.W) * o.sws + o.C < (int64_t{1} << 31) &&
+         o.cols < (int64_t{1} << 31);
 }
 
 }  // namespace
