@@ -361,16 +361,25 @@ __global__ void __launch_bounds__(256) im2col_k16_generic_kernel(const __grid_co
 
 // fp16 feature-major from the row-staged layout (small-C stems, any input strides):
 // one CTA per output row (n, oh) stages the kh input rows in smem exactly like
-// im2col_rows_kernel, then writes, for every patch row r, the OW contiguous halves
-// of this output row as uint4s (OW % 8 == 0).
+// im2col_rows_kernel, expands them into a [d][OW] fp16 tile in smem -- lanes walk
+// the feature rows r (consecutive staged words: conflict-free reads; the tile's
+// odd word stride makes the transposed half2 writes conflict-free) -- and writes
+// the tile's rows to global memory as 16-byte stores (OW % 8 == 0).
+constexpr int K16R_TILE_WORDS_MAX = 12 * 1024;  // d * (OW/2 + 1) words of the fp16 tile
 __global__ void __launch_bounds__(ROWS_THREADS) im2col_k16_rows_kernel(const __grid_constant__ I2cBatch b) {
   extern __shared__ float sm[];
   const dpk_im2col_job& J = b.j[blockIdx.y];
   const dpk_operand& o = J.x;
   const RowsGeom g = rows_geom(o);
   const int d = o.rows + (o.bias_row ? 1 : 0);
+  const int C = o.C, OW = o.OW, OH = o.OH, kh = o.kh, rowlen = g.rowlen;
+  const int half_ow = OW >> 1;
+  const int tw = half_ow + 1;  // tile word stride (odd when OW/2 is even)
+  const int64_t ld = J.ld, nrows = o.cols / OW;
   float* stage = sm;
-  int* off = reinterpret_cast<int*>(sm + o.kh * g.rowlen);
+  int* off = reinterpret_cast<int*>(sm + kh * rowlen);
+  uint32_t* tile = reinterpret_cast<uint32_t*>(off + d);
+  const float sc = J.amax ? ldexpf(1.0f, -prescale_exponent(__ldg(J.amax))) : 1.0f;  // exact 2^-e
   for (int r = threadIdx.x; r < d; r += ROWS_THREADS) {
     int v = -2;  // the bias row
     if (r < o.rows) {
@@ -382,52 +391,69 @@ __global__ void __launch_bounds__(ROWS_THREADS) im2col_k16_rows_kernel(const __g
         i = t / o.kw;
         j = t - i * o.kw;
       } else {
-        const int t = r / o.C;
-        c = r - t * o.C;
+        const int t = r / C;
+        c = r - t * C;
         i = t / o.kw;
         j = t - i * o.kw;
       }
-      v = i * g.rowlen + j * o.dw * o.C + c;
+      v = i * rowlen + j * o.dw * C + c;
     }
     off[r] = v;
   }
-  const int64_t nrows = o.cols / o.OW;
-  const int segs = o.OW / 8;
-  const int shift = o.sw * o.C;
-  const float sc = J.amax ? ldexpf(1.0f, -prescale_exponent(__ldg(J.amax))) : 1.0f;  // exact 2^-e
+  const int shift = o.sw * C;
   for (int64_t row = blockIdx.x; row < nrows; row += gridDim.x) {
-    const int n = static_cast<int>(row / o.OH);
-    const int oh = static_cast<int>(row - static_cast<int64_t>(n) * o.OH);
+    const int n = static_cast<int>(row / OH);
+    const int oh = static_cast<int>(row - static_cast<int64_t>(n) * OH);
     const float* base = o.data + static_cast<int64_t>(n) * o.sn;
     __syncthreads();
-    for (int e = threadIdx.x; e < o.kh * g.rowlen; e += ROWS_THREADS) {
-      const int i = e / g.rowlen;
-      const int q = e - i * g.rowlen;
-      const int wq = q / o.C;
-      const int c = q - wq * o.C;
-      const int ih = oh * o.sh - o.ph + i * o.dh, iw = wq - g.padl;
-      float v = 0.0f;
-      if (static_cast<unsigned>(ih) < static_cast<unsigned>(o.H) && static_cast<unsigned>(iw) < static_cast<unsigned>(o.W))
-        v = __ldg(base + static_cast<int64_t>(c) * o.sc + static_cast<int64_t>(ih) * o.shs +
-                  static_cast<int64_t>(iw) * o.sws);
-      stage[e] = v;
+    // stage: input rows oh*sh - ph + i*dh (i < kh), padded columns, channel-interleaved
+    // (thread over padded input columns, channels inner: no division per element)
+    for (int i = 0; i < kh; ++i) {
+      const int ih = oh * o.sh - o.ph + i * o.dh;
+      const bool rin = static_cast<unsigned>(ih) < static_cast<unsigned>(o.H);
+      for (int wq = threadIdx.x; wq < g.wp; wq += ROWS_THREADS) {
+        const int iw = wq - g.padl;
+        const bool in = rin && static_cast<unsigned>(iw) < static_cast<unsigned>(o.W);
+        const float* src = base + static_cast<int64_t>(ih) * o.shs + static_cast<int64_t>(iw) * o.sws;
+        for (int c = 0; c < C; ++c)
+          stage[i * rowlen + wq * C + c] = in ? __ldg(src + static_cast<int64_t>(c) * o.sc) * sc : 0.0f;
+      }
     }
     __syncthreads();
-    __half* out = reinterpret_cast<__half*>(J.out) + row * o.OW;
-    for (int u = threadIdx.x; u < d * segs; u += ROWS_THREADS) {
-      const int r = u / segs;
-      const int sgi = u - r * segs;
-      const int t = off[r];
-      __half2 hv[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int ow0 = sgi * 8 + 2 * e;
-        const float a = t >= 0 ? stage[t + ow0 * shift] : (t == -2 ? 1.0f : 0.0f);
-        const float c2 = t >= 0 ? stage[t + (ow0 + 1) * shift] : (t == -2 ? 1.0f : 0.0f);
-        hv[e] = __floats2half2_rn(a * sc, c2 * sc);
+    // expand into the fp16 tile: warp w takes pixel pairs p = w, w+8, ...; lanes walk the
+    // feature rows r (consecutive staged words: conflict-free; odd tile stride)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int p = warp; p < half_ow; p += ROWS_THREADS / 32) {
+      const int s0 = 2 * p * shift;
+      for (int r = lane; r < d; r += 32) {
+        const int t = off[r];
+        float a, c2;
+        if (t >= 0) {
+          a = stage[t + s0];
+          c2 = stage[t + s0 + shift];
+        } else {
+          a = c2 = (t == -2 ? sc : 0.0f);  // the bias row holds 1 (prescaled)
+        }
+        const __half2 hv = __floats2half2_rn(a, c2);
+        tile[r * tw + p] = *reinterpret_cast<const uint32_t*>(&hv);
       }
-      __stcs(reinterpret_cast<uint4*>(out + static_cast<int64_t>(r) * J.ld + sgi * 8),
-             *reinterpret_cast<const uint4*>(hv));
+    }
+    __syncthreads();
+    // rows out as 16-byte stores: half-warp h of warp w takes rows r = 2(w + 8j) + h,
+    // its lanes the row's 8-half segments
+    __half* out = reinterpret_cast<__half*>(J.out) + row * OW;
+    const int segs = OW >> 3;
+    const int hh = lane >> 4, sq = lane & 15;
+    for (int r = 2 * warp + hh; r < d; r += 2 * (ROWS_THREADS / 32)) {
+      for (int q = sq; q < segs; q += 16) {
+        const uint32_t* tr = tile + r * tw + 4 * q;
+        uint4 w;
+        w.x = tr[0];
+        w.y = tr[1];
+        w.z = tr[2];
+        w.w = tr[3];
+        __stcs(reinterpret_cast<uint4*>(out + r * ld + 8 * q), w);
+      }
     }
   }
 }
@@ -484,8 +510,10 @@ __global__ void __launch_bounds__(256) amax_kernel(const __grid_constant__ I2cBa
 bool k16_rows_ok(const dpk_im2col_job& j) {
   const dpk_operand& o = j.x;
   const RowsGeom g = rows_geom(o);
-  const size_t smem = (static_cast<size_t>(o.kh) * g.rowlen + o.rows + 1) * 4;
-  return o.OW % 8 == 0 && o.cols % o.OW == 0 && smem <= static_cast<size_t>(ROWS_SMEM_MAX);
+  const int d = o.rows + (o.bias_row ? 1 : 0);
+  const size_t smem = (static_cast<size_t>(o.kh) * g.rowlen + d) * 4 + static_cast<size_t>(d) * (o.OW / 2 + 1) * 4;
+  return o.OW % 8 == 0 && o.cols % o.OW == 0 && smem <= static_cast<size_t>(ROWS_SMEM_MAX) &&
+         static_cast<int64_t>(d) * (o.OW / 2 + 1) <= K16R_TILE_WORDS_MAX;
 }
 
 bool k16_tiled_ok(const dpk_im2col_job& j) {
@@ -571,7 +599,8 @@ extern "C" int dpk_im2col_materialize_f16(const dpk_im2col_job* jobs, int n_jobs
       }
       rbf.j[rbf.n++] = j;
       const dpk::RowsGeom g = dpk::rows_geom(o);
-      rsm = std::max(rsm, (static_cast<size_t>(o.kh) * g.rowlen + o.rows + 1) * 4);
+      const int d = o.rows + (o.bias_row ? 1 : 0);
+      rsm = std::max(rsm, (static_cast<size_t>(o.kh) * g.rowlen + d) * 4 + static_cast<size_t>(d) * (o.OW / 2 + 1) * 4);
     } else {
       if (gb.n == dpk::I2C_MAX) {
         int rc = flush_g();
