@@ -1072,8 +1072,15 @@ class DPKFAC:
                 ly.holds = "eigen"
             if "a_damped_inv" in d:
                 ly.alloc_state("inverse", self.device)
-                if "a_inv_factor" in d:  # reference order -> held (lower-triangular) order
-                    ly.a_x.copy_(sym(d["a_inv_factor"]))
+                if "a_inv_factor" in d:  # reference order -> held order
+                    xa = sym(d["a_inv_factor"]).to(self.device)
+                    if bool(torch.triu(xa, 1).any()):
+                        # saved from a model whose held order differs (channels-last <->
+                        # NCHW): P X P^T is a factor of the same inverse but not lower
+                        # triangular in this order -- rebuild the triangular one from it
+                        xd = xa.double()
+                        xa = _factor_of_inverse(xd.T @ xd)
+                    ly.a_x.copy_(xa)
                     ly.g_x.copy_(d["g_inv_factor"])
                 else:
                     ly.a_x.copy_(_factor_of_inverse(sym(d["a_damped_inv"]).to(self.device)))

@@ -154,6 +154,26 @@ def compute_factors(captured_inputs: torch.Tensor, captured_preact_grads: torch.
     return a_new, g_new
 
 
+def compute_conv_input_factor(x: torch.Tensor, kernel_size, stride=1, padding=0, dilation=1, bias: bool = False,
+                              precision: str = "3xtf32") -> torch.Tensor:
+    """A = X X^T / M for a Conv2d input x (N x C x H x W, NCHW or channels-last) without
+    materializing X: X is the conv's implicit-im2col linear form -- rows in the
+    reference (C, kh, kw) = ``weight.view(C_out, -1)`` order, columns (n, oh, ow), a
+    ones row last when the layer has a bias (kfac.py:85-104
+    applied to ``F.unfold`` columns).  One ``dpk_conv_im2col_syrk_ema`` launch."""
+    if not isinstance(x, torch.Tensor) or not x.is_cuda or x.dim() != 4:
+        raise ArgumentError("expected a 4-D CUDA conv input")
+    pair = lambda v: (int(v[0]), int(v[1])) if isinstance(v, (tuple, list)) else (int(v), int(v))
+    x = x.float()
+    op = ops.operand_im2col(x, pair(kernel_size), pair(stride), pair(padding), pair(dilation), bias_row=bias)
+    if op.cols < 1:
+        raise ArgumentError("captured inputs must be a nonempty d x B matrix")
+    d = op.rows + op.bias_row
+    a = torch.empty(d, d, device=x.device)
+    ops.conv_syrk_ema([ops.factor_job(op, a, 1.0 / op.cols, 0.0)], precision)
+    return a
+
+
 def update_running_average(state: FactorState, a_new, g_new, xi: float, t: int) -> FactorState:
     """First update assigns copies; later xi*new + (1-xi)*old (kfac.py:107-125)."""
     if not state.initialized:

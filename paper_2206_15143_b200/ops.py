@@ -8,6 +8,7 @@ per-(device, stream) zero-initialised workspace that only grows.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from typing import Optional, Sequence
 
 import torch
@@ -184,6 +185,20 @@ def syrk_ema(jobs: Sequence[L.FactorJob], precision: str = "tf32", keepalive=Non
             "dpk_syrk_ema")
 
 
+def conv_syrk_ema(jobs: Sequence[L.FactorJob], precision: str = "3xtf32", device=None):
+    """K2: implicit-im2col factor SYRK + EMA (``dpk_conv_im2col_syrk_ema``): every job's
+    operand is a conv input's implicit-im2col view; patches are never written."""
+    if not jobs:
+        return
+    lb = lib()
+    arr = L.array(L.FactorJob, jobs)
+    need = lb.dpk_factor_workspace_bytes(arr, len(jobs))
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    ws = Workspace.get(need, dev)
+    L.check(lb.dpk_conv_im2col_syrk_ema(arr, len(jobs), ws, need, precision_code(precision), stream_handle()),
+            "dpk_conv_im2col_syrk_ema")
+
+
 def factor_job(x: L.Operand, factor: torch.Tensor, alpha: float, beta: float,
                x_amax: Optional[torch.Tensor] = None) -> L.FactorJob:
     """x_amax: the amax slot of prescaled fp16 patches (see im2col_materialize_f16)."""
@@ -335,7 +350,7 @@ EIG_ONCHIP_MAX = 128
 
 _EIG_POOL = None
 _EIG_STREAMS: dict = {}
-EIG_CONCURRENCY = 8
+EIG_CONCURRENCY = int(os.environ.get("DPK_EIG_STREAMS", "8"))  # cuSOLVER lanes (n > 128)
 
 
 def _eig_one(src, q, w, info, stream, ready):

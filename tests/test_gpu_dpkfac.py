@@ -566,3 +566,38 @@ def test_kl_clip_scale_matches_formula(inv_type):
             got = torch.cat([lin.weight.grad, lin.bias.grad[:, None]], 1).double().cpu().numpy()
             assert rel(got, nu * pre[i]) <= TOL, (t, i, rel(got, nu * pre[i]), nu)
     assert min(nus) < 1.0  # the clip is active in this setting
+
+
+def test_state_dict_moves_between_nchw_and_channels_last_models():
+    """state_dict exports every A-side matrix -- a_cov, a_damped_inv and the held factor
+    a_inv_factor -- in the reference (C, kh, kw) order, so inverse-mode state saved from a
+    channels-last model (tap-major held order) resumes exactly in an NCHW model."""
+    from paper_2206_15143_b200 import DPKFAC
+    torch.manual_seed(4)
+    dev = torch.device("cuda", 0)
+    m_cl = ClConv().to(dev).to(memory_format=torch.channels_last)
+    m_nc = ClConv().to(dev)
+    m_nc.load_state_dict(m_cl.state_dict())
+    kw = dict(gamma=0.01, xi=0.8, inv_type="inverse", precision="3xtf32", f_freq=1, k_freq=3)
+    kf_cl = DPKFAC(m_cl, **kw)
+    gen = torch.Generator().manual_seed(6)
+    data = [(torch.randn(8, 3, 16, 16, generator=gen), torch.randint(0, 10, (8,), generator=gen)) for _ in range(3)]
+    for t in range(2):
+        x, y = data[t]
+        m_cl.zero_grad()
+        F.cross_entropy(m_cl(x.to(dev).to(memory_format=torch.channels_last)), y.to(dev)).backward()
+        kf_cl.step()
+    assert kf_cl.layers[1].tap_major
+    kf_nc = DPKFAC(m_nc, **kw)
+    assert not kf_nc.layers[1].tap_major
+    kf_nc.load_state_dict(kf_cl.state_dict())
+    # t = 2: factors update but the inverses are stale (k_freq = 3): the loaded factors are used
+    x, y = data[2]
+    grads = []
+    for m, kf, xx in ((m_cl, kf_cl, x.to(dev).to(memory_format=torch.channels_last)), (m_nc, kf_nc, x.to(dev))):
+        m.zero_grad()
+        F.cross_entropy(m(xx), y.to(dev)).backward()
+        kf.step()
+        grads.append([p.grad.double().contiguous() for p in m.parameters()])
+    for a, b in zip(*grads):
+        assert rel(a.cpu().numpy(), b.cpu().numpy()) <= 1e-5

@@ -605,3 +605,24 @@ def test_asymmetric_kernels_all_im2col_forms_match_unfold(shape, kk, ss, pp, cha
         ops.syrk_ema([ops.factor_job(ops.operand_rows_k_f16(p16, M), out, 1.0 / M, 0.0, x_amax=amax)], "tf32")
         torch.cuda.synchronize()
         assert rel(N(out), want) <= TOL, ("f16", tap, rel(N(out), want))
+
+
+@pytest.mark.parametrize("shape,k,s,p,bias,channels_last", [((2, 8, 12, 12), 3, 1, 1, True, False),
+                                                           ((2, 64, 9, 9), (1, 7), 1, (0, 3), False, True),
+                                                           ((3, 16, 10, 10), 5, 2, 2, False, False)])
+def test_compute_conv_input_factor_matches_unfold(shape, k, s, p, bias, channels_last):
+    """kfac.compute_conv_input_factor: the K2 entry point (dpk_conv_im2col_syrk_ema) on a
+    conv input, reference (C, kh, kw) row order, against compute_factors on F.unfold
+    columns."""
+    from paper_2206_15143_b200 import kfac as FK
+    rng = np.random.default_rng(sum(shape))
+    x = np.maximum(rng.standard_normal(shape), 0)
+    xt = T(x)
+    if channels_last:
+        xt = xt.to(memory_format=torch.channels_last)
+    kk = k if isinstance(k, tuple) else (k, k)
+    a = FK.compute_conv_input_factor(xt, kk, s, p, bias=bias)
+    torch.cuda.synchronize()
+    cols = K.unfold_columns(x, kk[0], kk[1], s, p, 1, bias)
+    want, _ = K.compute_factors(cols, cols[:1])
+    assert rel(N(a), want) <= 1e-5, rel(N(a), want)
