@@ -76,6 +76,15 @@ size_t gemm_workspace_bytes(const GemmSpec* specs, int n);
 // tcgen05 launches made by this thread use at most `cap` SMs (0 = all): a
 // concurrent stream keeps the rest (spd_inv.cu's right-looking trailing updates)
 void set_grid_cap_override(int cap);
+// split-K depth of the tcgen05 plans made by this thread (units per SM; 0 = default 3)
+int units_per_sm();
+int units_per_sm_override();
+void set_units_per_sm_override(int u);
+struct UnitsPerSm {  // scoped override
+  int prev;
+  explicit UnitsPerSm(int u) : prev(units_per_sm_override()) { set_units_per_sm_override(u); }
+  ~UnitsPerSm() { set_units_per_sm_override(prev); }
+};
 // K4 Jacobi rotation thresholds (syevd.cu), shared by the on-chip and block kernels
 void jac_tolerances(float& rel, float& abs_);
 // K4 n > 128: block Jacobi (syevj.cu); jobs with n <= 128 are ignored

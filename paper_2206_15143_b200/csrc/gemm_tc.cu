@@ -1253,8 +1253,23 @@ bool dynamic_schedule() {  // DPK_DYN=0: static round-robin units
 }
 
 thread_local int g_cap_override = 0;
+thread_local int g_units_override = 0;
 }  // namespace
 void set_grid_cap_override(int cap) { g_cap_override = cap; }
+int units_per_sm_override() { return g_units_override; }
+void set_units_per_sm_override(int u) { g_units_override = u; }
+// split-K target: about this many units per worker.  Callers set it per context
+// (UnitsPerSm guards: factor SYRKs 2, the latency-bound SPD rounds 1, everything else
+// 3); DPK_UNITS_PER_SM overrides all of them (tuning).
+int units_per_sm() {
+  static int env = -1;
+  if (env < 0) {
+    const char* e = getenv("DPK_UNITS_PER_SM");
+    env = e ? std::max(1, atoi(e)) : 0;
+  }
+  if (env > 0) return env;
+  return g_units_override > 0 ? g_units_override : 3;
+}
 namespace {
 int grid_cap() {
   if (g_cap_override > 0) return g_cap_override;
@@ -1504,6 +1519,7 @@ bool valid_operand(const dpk_operand& o) {
   return true;
 }
 
+
 int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int precision = DPK_PREC_TF32, int cg = 1) {
   const bool rn = precision == DPK_PREC_TF32;
   const int UT = 128 * cg;
@@ -1614,7 +1630,8 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
   // Split K so that the group yields ~3 units per SM, but never below 32 chunks
   // (1024 samples) per unit so tile set-up and the partial round trip stay amortised.
   const int64_t sms = num_sms() / cg;  // workers: CTAs or CTA pairs
-  const int64_t target = std::max<int64_t>(32, (total_work + 3 * sms - 1) / (3 * sms));
+  const int64_t per = units_per_sm();
+  const int64_t target = std::max<int64_t>(32, (total_work + per * sms - 1) / (per * sms));
   size_t partial_tiles = 0;
   for (auto& P : plan.probs) {
     P.splits = static_cast<int>(std::max<int64_t>(1, (P.chunks + target - 1) / target));
@@ -1837,6 +1854,7 @@ std::string specs_key(const GemmSpec* specs, int n, int precision) {
   cudaGetDevice(&dev);
   key_put(k, dev);
   key_put(k, precision);
+  key_put(k, units_per_sm());  // the split-K plan depends on it
   for (int i = 0; i < n; ++i) key_spec(k, specs[i]);
   return k;
 }
@@ -2033,6 +2051,7 @@ static std::vector<dpk::GemmSpec> factor_specs(const dpk_factor_job* jobs, int n
 }
 
 size_t dpk_factor_workspace_bytes(const dpk_factor_job* jobs, int n_jobs) {
+  dpk::UnitsPerSm units(2);  // factor SYRKs: measured best split-K depth
   auto specs = factor_specs(jobs, n_jobs);
   return dpk::gemm_workspace_bytes(specs.data(), n_jobs);
 }
@@ -2053,6 +2072,7 @@ int dpk_syrk_ema(const dpk_factor_job* jobs, int n_jobs, void* workspace, size_t
       return DPK_EARG;
     }
   }
+  dpk::UnitsPerSm units(2);
   auto specs = factor_specs(jobs, n_jobs);
   return dpk::gemm_launch(specs.data(), n_jobs, workspace, ws_bytes, precision, static_cast<cudaStream_t>(stream));
 }

@@ -986,6 +986,7 @@ namespace {
 size_t spd_workspace_bytes(const std::vector<SpdReq>& r) {
   const int n_jobs = static_cast<int>(r.size());
   if (n_jobs <= 0) return 0;
+  UnitsPerSm units(1);  // latency-bound rounds: no split-K reduce launches on the chain
   // depends only on the sizes and modes (the plan is built against a dummy base)
   static LruCache<size_t> cache;
   std::string key;
@@ -1011,6 +1012,7 @@ size_t spd_workspace_bytes(const std::vector<SpdReq>& r) {
 int spd_run(const std::vector<SpdReq>& r, void* workspace, size_t ws_bytes, cudaStream_t st, const char* who) {
   const int n_jobs = static_cast<int>(r.size());
   if (n_jobs == 0) return DPK_OK;
+  UnitsPerSm units(1);  // same split-K depth as spd_workspace_bytes
   for (const auto& q : r) {
     if (q.n < 1 || q.src == nullptr || q.dst == nullptr || q.src == q.dst) {
       set_error(std::string(who) + ": invalid job (n >= 1, distinct src/dst required)");
