@@ -78,6 +78,7 @@ size_t gemm_workspace_bytes(const GemmSpec* specs, int n);
 void set_grid_cap_override(int cap);
 // split-K depth of the tcgen05 plans made by this thread (units per SM; 0 = default 3)
 int units_per_sm();
+int split_min_chunks();
 int units_per_sm_override();
 void set_units_per_sm_override(int u);
 struct UnitsPerSm {  // scoped override

@@ -1261,6 +1261,14 @@ void set_units_per_sm_override(int u) { g_units_override = u; }
 // split-K target: about this many units per worker.  Callers set it per context
 // (UnitsPerSm guards: factor SYRKs 2, the latency-bound SPD rounds 1, everything else
 // 3); DPK_UNITS_PER_SM overrides all of them (tuning).
+int split_min_chunks() {  // no split-K piece below this many K chunks (DPK_SPLIT_MIN, default 32)
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DPK_SPLIT_MIN");
+    v = e ? std::max(1, atoi(e)) : 32;
+  }
+  return v;
+}
 int units_per_sm() {
   static int env = -1;
   if (env < 0) {
@@ -1631,7 +1639,7 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
   // (1024 samples) per unit so tile set-up and the partial round trip stay amortised.
   const int64_t sms = num_sms() / cg;  // workers: CTAs or CTA pairs
   const int64_t per = units_per_sm();
-  const int64_t target = std::max<int64_t>(32, (total_work + per * sms - 1) / (per * sms));
+  const int64_t target = std::max<int64_t>(split_min_chunks(), (total_work + per * sms - 1) / (per * sms));
   size_t partial_tiles = 0;
   for (auto& P : plan.probs) {
     P.splits = static_cast<int>(std::max<int64_t>(1, (P.chunks + target - 1) / target));
