@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--early", action="store_true",
                     help="e2e: launch the larger size classes' factor/inverse pipeline from the backward hooks")
+    ap.add_argument("--max-classes", type=int, default=None, help="tuning: DPKFAC.MAX_CLASSES")
+    ap.add_argument("--class-ratio", type=float, default=None, help="tuning: DPKFAC.CLASS_RATIO")
+    ap.add_argument("--factor-order", type=int, default=None, help="tuning: DPKFAC.FACTOR_ORDER")
     ap.add_argument("--early-priority", default="high", choices=["high", "low"],
                     help="e2e with --early: stream priority of the hook-launched pipelines")
     ap.add_argument("--ncu-step", action="store_true",
@@ -269,6 +272,10 @@ def run_ours(args, rank, world, local_rank):
     kf = DPKFAC(model, gamma=args.gamma, xi=args.xi, inv_type=args.inv_type, f_freq=1, k_freq=1,
                 assignment=args.assignment, precision=args.precision, check_numerics="deferred",
                 overlap=not args.no_overlap, early=False, algorithm=args.algorithm, im2col=args.im2col)  # captures are replayed below; e2e turns early on
+    for attr, val in (("MAX_CLASSES", args.max_classes), ("CLASS_RATIO", args.class_ratio),
+                      ("FACTOR_ORDER", args.factor_order)):
+        if val is not None:
+            setattr(kf, attr, val)
     opt = torch.optim.SGD(model.parameters(), lr=1e-3, momentum=0.9)
     gen = torch.Generator().manual_seed(1234 + rank)
     x_host = torch.randn(batch, *shape, generator=gen)
