@@ -1261,11 +1261,11 @@ void set_units_per_sm_override(int u) { g_units_override = u; }
 // split-K target: about this many units per worker.  Callers set it per context
 // (UnitsPerSm guards: factor SYRKs 2, the latency-bound SPD rounds 1, everything else
 // 3); DPK_UNITS_PER_SM overrides all of them (tuning).
-int split_min_chunks() {  // no split-K piece below this many K chunks (DPK_SPLIT_MIN, default 32)
+int split_min_chunks() {  // no split-K piece below this many K chunks (DPK_SPLIT_MIN, default 64: measured)
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("DPK_SPLIT_MIN");
-    v = e ? std::max(1, atoi(e)) : 32;
+    v = e ? std::max(1, atoi(e)) : 64;
   }
   return v;
 }
