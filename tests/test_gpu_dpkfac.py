@@ -606,3 +606,31 @@ def test_state_dict_moves_between_nchw_and_channels_last_models():
     torch.backends.cudnn.allow_tf32 = tf32
     for a, b in zip(*grads):
         assert rel(a.cpu().numpy(), b.cpu().numpy()) <= 1e-5
+
+
+def test_deferred_numerics_raise_at_a_fixed_step():
+    """check_numerics="deferred": the flags of step t are read with a blocking
+    wait at the start of step t+2 -- a fixed, rank-consistent point before any collective
+    -- so a non-SPD factor at t=1 raises the reference's NumericError at step 3, never
+    earlier and never depending on timing; check() raises it at once."""
+    from paper_2206_15143_b200 import DPKFAC, NumericError
+    dev = torch.device("cuda", 0)
+    torch.manual_seed(2)
+    for explicit in (False, True):
+        model = nn.Sequential(nn.Linear(6, 5), nn.Tanh(), nn.Linear(5, 3)).to(dev)
+        kf = DPKFAC(model, inv_type="inverse", gamma=0.0, check_numerics="deferred")
+        xs = [torch.randn(8, 6, device=dev) for _ in range(4)]
+        xs[1][:, 2] = float("nan")  # step 1: NaN captures -> the damped factor is not SPD
+        raised_at = None
+        for t in range(4):
+            model.zero_grad()
+            F.cross_entropy(model(xs[t]), torch.zeros(8, dtype=torch.long, device=dev)).backward()
+            try:
+                kf.step()
+                if explicit and t == 1:
+                    kf.check()
+            except NumericError as e:
+                raised_at = t
+                assert "worker 0, layer" in str(e)
+                break
+        assert raised_at == (1 if explicit else 3), raised_at
