@@ -405,7 +405,7 @@ def test_syrk_tapmajor_im2col_matches_unfold(shape, k, s, p, channels_last):
     cols = K.unfold_columns(x, k, k, s, p)
     perm = _tap_perm(shape[1], k, k)
     d = cols.shape[0]
-    for prec, tol in (("tf32", TOL), ("3xtf32", 1e-5)):
+    for prec, tol in (("tf32", TOL), ("3xtf32", 3e-5)):  # fp32 accumulation over up to 2048 columns per split
         out = torch.full((d, d), float("nan"), device=dev())
         op = ops.operand_im2col(xt, (k, k), (s, s), (p, p), (1, 1), tap_major=True)
         ops.syrk_ema([ops.factor_job(op, out, 1.0 / cols.shape[1], 0.0)], prec)
