@@ -66,6 +66,9 @@ def parse():
     ap.add_argument("--max-classes", type=int, default=None, help="tuning: DPKFAC.MAX_CLASSES")
     ap.add_argument("--class-ratio", type=float, default=None, help="tuning: DPKFAC.CLASS_RATIO")
     ap.add_argument("--factor-order", type=int, default=None, help="tuning: DPKFAC.FACTOR_ORDER")
+    ap.add_argument("--comm-overlap", action="store_true",
+                    help="bucketed gradient reduce-scatter launched from the backward hooks (e2e)")
+    ap.add_argument("--bucket-mb", type=float, default=16.0)
     ap.add_argument("--early-priority", default="high", choices=["high", "low"],
                     help="e2e with --early: stream priority of the hook-launched pipelines")
     ap.add_argument("--ncu-step", action="store_true",
@@ -271,7 +274,8 @@ def run_ours(args, rank, world, local_rank):
         model = model.to(memory_format=mf)
     kf = DPKFAC(model, gamma=args.gamma, xi=args.xi, inv_type=args.inv_type, f_freq=1, k_freq=1,
                 assignment=args.assignment, precision=args.precision, check_numerics="deferred",
-                overlap=not args.no_overlap, early=False, algorithm=args.algorithm, im2col=args.im2col)  # captures are replayed below; e2e turns early on
+                overlap=not args.no_overlap, early=False, algorithm=args.algorithm, im2col=args.im2col,
+                comm_overlap=args.comm_overlap, bucket_mb=args.bucket_mb)  # captures are replayed below; e2e turns early on
     for attr, val in (("MAX_CLASSES", args.max_classes), ("CLASS_RATIO", args.class_ratio),
                       ("FACTOR_ORDER", args.factor_order)):
         if val is not None:
@@ -515,6 +519,8 @@ def run_ours(args, rank, world, local_rank):
                                    f"inv_type={args.inv_type}, gamma={args.gamma}, xi={args.xi}, F=K=1",
                        "model": args.model, "global_batch": batch * world, "parallelism": f"dp{world}",
                        "assignment": args.assignment, "algorithm": args.algorithm, "im2col": args.im2col,
+                       "comm_overlap": (f"bucketed reduce-scatter from the backward hooks, {args.bucket_mb} MB buckets"
+                                        if args.comm_overlap else False),
                        "memory_format": "channels_last" if mf is torch.channels_last else "contiguous",
                        "l2": "inputs (layer captures, >1.4 GB) larger than L2; no flush"},
             "overlap": overlap, "ms_per_step_serialized": ms_serial,

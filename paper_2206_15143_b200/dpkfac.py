@@ -222,6 +222,11 @@ class DPKFAC:
                          exact Eq. 6 update)
       eig_solver         n > 128 eigendecompositions: "cusolver" (default, measured
                          fastest) | "native" (tensor-core block Jacobi, no library)
+      comm_overlap       bucketed gradient reduce-scatter launched from the backward pass:
+                         each bucket (~bucket_mb MB of layer gradients, backward order) is
+                         packed and reduce-scattered on a side stream as soon as its last
+                         gradient is accumulated.  The gradients must not be modified
+                         between backward() and step() (e.g. clipped) in this mode.
       grad_scale         "batch" (B_local * grad_output, model.py:9-12) or a number
     """
 
@@ -237,7 +242,7 @@ class DPKFAC:
                  grad_scale: Union[str, float] = "batch", check_numerics: Union[bool, str] = True,
                  im2col: str = "materialize", overlap: bool = True, early: bool = False,
                  algorithm: str = "dp_kfac", patch_dtype: str = "auto", kl_clip: Optional[float] = None,
-                 lr=None, eig_solver: str = "cusolver"):
+                 lr=None, eig_solver: str = "cusolver", comm_overlap: bool = False, bucket_mb: float = 16.0):
         self.hyper = KfacHyper(gamma=gamma, xi=xi, inv_type=inv_type, f_freq=f_freq, k_freq=k_freq)
         # KL-clip (north_star; off by default: the reference has none):
         # every preconditioned gradient is scaled by nu = min(1, sqrt(kl_clip / |lr^2 sum
@@ -363,6 +368,23 @@ class DPKFAC:
         self.early_priority = "high"  # "low": hook-launched work on lowest-priority streams
         self._hook_classes = None   # (classes, layer index -> class) fixed at the end of a step
         self._launched = {}         # class -> step t whose factor/inverse it already launched
+        # comm_overlap=True: the reduce-scatter runs in buckets from post-accumulate-grad
+        # hooks.  Hooks act only once the owner-major buffers
+        # exist (after the first step()); a bucket whose hooks did not all fire (a
+        # parameter without a gradient, a non-dense gradient) is packed and reduce-
+        # scattered by step() itself, so the result never depends on the hooks.
+        if comm_overlap and algorithm != "dp_kfac":
+            raise ArgumentError("comm_overlap is implemented for algorithm='dp_kfac'")
+        if not bucket_mb > 0:
+            raise ArgumentError("bucket_mb must be > 0")
+        self.comm_overlap = bool(comm_overlap)
+        self.bucket_mb = float(bucket_mb)
+        self._bucket_ev = {}        # bucket -> event of its hook-launched pack + reduce-scatter
+        if self.comm_overlap:
+            for ly in self.layers:
+                for prm in ((ly.module.weight, ly.module.bias) if ly.has_bias else (ly.module.weight,)):
+                    self._hooks.append(prm.register_post_accumulate_grad_hook(
+                        lambda _p, i=ly.index: self._on_grad(i)))
 
     # ------------------------------------------------------------ hooks
     def _make_pre_hook(self, ly: _Layer):
@@ -421,12 +443,19 @@ class DPKFAC:
 
     def _build_buffers(self):
         dev = self.device
+        buckets = self._grad_buckets() if self.comm_overlap else None
         self.layout = OwnerMajorLayout(self.assignment, [ly.n_grad for ly in self.layers],
-                                       scalar_slot=self.kl_clip is not None)
+                                       scalar_slot=self.kl_clip is not None, buckets=buckets)
         if self.kl_clip is not None:
             self._kl_ws = ops.kl_dot_workspace(dev)
         self.xchg = OwnerMajorExchange(self.layout, self.rank, dev, self.pg)
         self.offsets = self.layout.offsets
+        # pack offsets (bucket-major); the same dict object when there is one bucket
+        self.in_offsets = self.offsets if len(self.layout.buckets) == 1 else self.layout.in_offsets
+        nb = len(self.layout.buckets)
+        self._bucket_need = [sum(2 if self.layers[i].has_bias else 1 for i in b) for b in self.layout.buckets]
+        self._bucket_got = [0] * nb
+        self._bucket_ev = {}
         if self.algorithm == "mpd_kfac_co":  # every layer's mean gradient on every rank
             self._co_layout = OwnerMajorLayout([tuple(range(len(self.layers)))], [ly.n_grad for ly in self.layers])
             self._co_xchg = OwnerMajorExchange(self._co_layout, 0, dev, None)
@@ -436,6 +465,85 @@ class DPKFAC:
         self.pis = torch.zeros(max(n_own, 1), device=dev)
         self._jc = {}  # prepared (ctypes) job arrays, valid for these buffers
         self._bufs_ready = True
+
+    def _grad_buckets(self):
+        """Layers in backward order (reverse registration order), cut into buckets of
+        about bucket_mb MB of [W | b] gradient."""
+        cap = max(int(self.bucket_mb * 2 ** 20 / 4), 1)
+        buckets, cur, size = [], [], 0
+        for ly in reversed(self.layers):
+            cur.append(ly.index)
+            size += ly.n_grad
+            if size >= cap:
+                buckets.append(cur)
+                cur, size = [], 0
+        if cur:
+            buckets.append(cur)
+        return buckets
+
+    def _on_grad(self, layer: int):
+        """post-accumulate-grad hook (comm_overlap): count the bucket's gradients and
+        launch its pack + reduce-scatter on the comm stream when the last one lands
+        (every complete backward of the bucket relaunches it, so accumulated
+        gradients are exchanged as accumulated)."""
+        if not self._bufs_ready or self._pending_balance:
+            return
+        b = self.layout.bucket_of[layer]
+        self._bucket_got[b] += 1
+        if self._bucket_got[b] % self._bucket_need[b]:
+            return
+        with torch.no_grad(), torch.cuda.device(self.device):
+            segs = self._bucket_segments(b)
+            if segs is None:  # a non-dense gradient: step() exchanges this bucket
+                self._bucket_ev.pop(b, None)
+                return
+            if not hasattr(self, "_comm_st"):
+                self._comm_st = torch.cuda.Stream(self.device)
+            st = self._comm_st
+            st.wait_stream(torch.cuda.current_stream(self.device))
+            with torch.cuda.stream(st):
+                ops.pack(segs, self.xchg.flat, 1.0 / self.world)
+                self.xchg.reduce_scatter_bucket(b)
+                self._bucket_ev[b] = st.record_event()
+
+    def _bucket_segments(self, b: int):
+        layers = [self.layers[i] for i in self.layout.buckets[b]]
+        grads = []
+        for ly in layers:
+            w, bb = ly.module.weight.grad, (ly.module.bias.grad if ly.has_bias else None)
+            if w is None or (ly.has_bias and bb is None):
+                return None
+            if not (w.is_contiguous() or (w.dim() == 4 and w.is_contiguous(memory_format=torch.channels_last))):
+                return None
+            grads.append((w.data_ptr(), w.stride(), bb.data_ptr() if bb is not None else 0))
+        key = ("bseg", b)
+        grads = tuple(grads)
+        hit = self._jc.get(key)
+        if hit is None or hit[0] != grads:
+            segs = [ops.segment(ly.module.weight.grad, ly.module.bias.grad if ly.has_bias else None,
+                                self.in_offsets[ly.index], tap_major=ly.tap_major) for ly in layers]
+            hit = self._jc[key] = (grads, ops.Prepared(L.Segment, segs))
+        return hit[1]
+
+    def _exchange_grads(self, main):
+        """Pack + reduce-scatter of the gradient buckets the backward hooks did not
+        already launch; the caller's stream then waits for the hook-launched ones."""
+        X = self.xchg
+        P = self.world
+        if len(self.layout.buckets) == 1 and not self._bucket_ev:
+            ops.pack(self._segments("grad", self.in_offsets), X.flat, 1.0 / P)
+            X.reduce_scatter()
+            return
+        for b in range(len(self.layout.buckets)):
+            ev = self._bucket_ev.get(b)
+            if ev is not None:
+                main.wait_event(ev)
+            else:
+                segs = self._bucket_segments(b)
+                if segs is None:
+                    raise OrderingError("a layer has no dense gradient: call backward() before step()")
+                ops.pack(segs, X.flat, 1.0 / P)
+                X.reduce_scatter_bucket(b)
 
     def _segments(self, which: str, offsets=None):
         """The layers' [W | b] gradient segments at their flat offsets, as a Prepared
@@ -529,13 +637,13 @@ class DPKFAC:
                 if self.FACTOR_ORDER == 2 or (self.FACTOR_ORDER == 1 and ci == 0):
                     gate = done
                 self._inverse_stage(cls, t, k_up)
-        # (3) pack every layer's [W | b] gradient, owner-major (scaled by 1/P)
+        # (3) pack every layer's [W | b] gradient, owner-major (scaled by 1/P), and
+        # (4) reduce-scatter: SUM of grad/P over ranks == mean, my layers only
+        # (comm_overlap: the buckets the backward hooks already exchanged are awaited)
         segs = self._segments("grad")
         P = self.world
         X = self.xchg
-        ops.pack(segs, X.flat, 1.0 / P)
-        # (4) reduce-scatter: SUM of grad/P over ranks == mean, my layers only
-        X.reduce_scatter()
+        self._exchange_grads(main)
         if P > 1 and self.other_params:
             self._allreduce_others()
         self._mark("comm_rs")
@@ -584,6 +692,9 @@ class DPKFAC:
         self.info.zero_()
         self._launched = {}
         self._hook_classes = None
+        if self._bufs_ready:
+            self._bucket_got = [0] * len(self.layout.buckets)
+            self._bucket_ev = {}
         if self.early and self.overlap and len(sides) > 0:
             self._hook_classes = (sides, {ly.index: ci for ci, c in enumerate(sides) for ly in c})
         self.t += 1

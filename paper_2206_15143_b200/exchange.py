@@ -16,7 +16,7 @@ exercised by the CPU gloo tests as well.
 
 from __future__ import annotations
 
-from typing import Sequence
+from typing import Optional, Sequence
 
 import torch
 import torch.distributed as dist
@@ -25,23 +25,65 @@ import torch.distributed as dist
 class OwnerMajorLayout:
     """``scalar_slot``: reserve the last float of every rank's chunk for one per-rank
     scalar that rides the all-gather (the KL-clip partial dot): ``slot_offset``
-    inside a chunk, ``chunk`` apart in the gathered buffer."""
+    inside a chunk, ``chunk`` apart in the gathered buffer.
+
+    ``buckets`` (layer index lists covering every layer once; default one bucket):
+    the reduce-scatter is split into one collective per bucket so it can run as
+    soon as the backward pass has produced that bucket's gradients.
+    A rank's chunk is then the concatenation of its per-bucket parts, each padded
+    to the bucket's largest part (``bucket_chunk[b]`` floats at ``bucket_base[b]``):
+
+      pack buffer  flat     = [bucket 0: r0 | r1 | ... ][bucket 1: r0 | r1 | ... ] ...
+      RS of bucket b        : flat[P*base_b : P*(base_b + chunk_b)] -> chunk_in[base_b : base_b + chunk_b]
+      gathered     out_flat = [rank 0: b0 | b1 | ... ][rank 1: b0 | b1 | ... ] ...
+
+    so layers are packed at ``in_offsets`` and unpacked from ``offsets``; with one
+    bucket the two coincide and the layout is the plain owner-major one."""
 
     def __init__(self, assignment: Sequence[Sequence[int]], n_grad: Sequence[int], align: int = 32,
-                 scalar_slot: bool = False):
+                 scalar_slot: bool = False, buckets: Optional[Sequence[Sequence[int]]] = None):
         self.assignment = tuple(tuple(p) for p in assignment)
         self.world = len(self.assignment)
         self.n_grad = list(n_grad)
-        sizes = [sum(self.n_grad[i] for i in part) for part in self.assignment]
-        chunk = max(max(sizes) if sizes else 0, 1) + (1 if scalar_slot else 0)
-        self.chunk = (chunk + align - 1) // align * align
-        self.slot_offset = self.chunk - 1 if scalar_slot else None
-        self.offsets = {}
+        if buckets is None:
+            buckets = [sorted(i for part in self.assignment for i in part)]
+        self.buckets = tuple(tuple(int(i) for i in b) for b in buckets)
+        seen = sorted(i for b in self.buckets for i in b)
+        if seen != sorted(i for part in self.assignment for i in part):
+            raise ValueError("buckets must cover every assigned layer exactly once")
+        bucket_of = {i: k for k, b in enumerate(self.buckets) for i in b}
+        self.bucket_of = bucket_of
+        nb = len(self.buckets)
+        # per (bucket, rank) part sizes; the KL slot rides at the end of the last bucket
+        sizes = [[0] * self.world for _ in range(nb)]
         for p, part in enumerate(self.assignment):
-            off = p * self.chunk
             for i in part:
-                self.offsets[i] = off
-                off += self.n_grad[i]
+                sizes[bucket_of[i]][p] += self.n_grad[i]
+        self.bucket_chunk, self.bucket_base = [], []
+        base = 0
+        for k in range(nb):
+            c = max(max(sizes[k]) if sizes[k] else 0, 1 if nb == 1 else 0) + (1 if scalar_slot and k == nb - 1 else 0)
+            c = (c + align - 1) // align * align
+            self.bucket_base.append(base)
+            self.bucket_chunk.append(c)
+            base += c
+        self.chunk = max(base, align)
+        if self.chunk > base:  # (only an empty single bucket) keep the padding in the last bucket
+            self.bucket_chunk[-1] += self.chunk - base
+        self.slot_offset = self.chunk - 1 if scalar_slot else None
+        self.offsets = {}      # gathered (rank-major) layout: unpack / preconditioned output
+        self.in_offsets = {}   # pack (bucket-major) layout: the reduce-scatter input
+        self._local = {}
+        for p, part in enumerate(self.assignment):
+            fill = list(self.bucket_base)
+            for i in part:
+                k = bucket_of[i]
+                loc = fill[k]
+                fill[k] += self.n_grad[i]
+                self._local[i] = loc
+                self.offsets[i] = p * self.chunk + loc
+                self.in_offsets[i] = (self.world * self.bucket_base[k] + p * self.bucket_chunk[k] +
+                                      loc - self.bucket_base[k])
         self.total = self.world * self.chunk
         # elements that travel but carry no gradient (equal-chunk padding for NCCL RS/AG)
         self.padding = self.total - sum(self.n_grad)
@@ -54,7 +96,7 @@ class OwnerMajorLayout:
 
     def local_offset(self, layer: int, rank: int) -> int:
         """Offset of an owned layer inside that rank's chunk."""
-        return self.offsets[layer] - rank * self.chunk
+        return self._local[layer]
 
 
 class OwnerMajorExchange:
@@ -78,8 +120,16 @@ class OwnerMajorExchange:
 
     def reduce_scatter(self):
         """flat must already hold grad / P (pack scale); SUM then equals the mean."""
+        for b in range(len(self.layout.buckets)):
+            self.reduce_scatter_bucket(b)
+
+    def reduce_scatter_bucket(self, b: int):
+        """The reduce-scatter of one gradient bucket (its region of flat must be packed)."""
         if self.layout.world > 1:
-            dist.reduce_scatter_tensor(self.chunk_in, self.flat, op=dist.ReduceOp.SUM, group=self.group)
+            L_ = self.layout
+            base, c, P = L_.bucket_base[b], L_.bucket_chunk[b], L_.world
+            dist.reduce_scatter_tensor(self.chunk_in[base:base + c], self.flat[P * base:P * (base + c)],
+                                       op=dist.ReduceOp.SUM, group=self.group)
 
     def all_gather(self):
         if self.layout.world > 1:

@@ -29,8 +29,11 @@ def main():
     B = 8 * P
     bad = []
     for algorithm, inv in [("dp_kfac", "inverse"), ("dp_kfac", "eigen"), ("mpd_kfac_co", "inverse"),
-                           ("mpd_kfac_mo", "inverse"), ("mpd_kfac_co", "eigen"), ("dp_kfac:balanced", "inverse")]:
+                           ("mpd_kfac_mo", "inverse"), ("mpd_kfac_co", "eigen"), ("dp_kfac:balanced", "inverse"),
+                           ("dp_kfac:round_robin+overlap", "inverse"), ("dp_kfac:balanced+overlap", "eigen")]:
         alg, _, asg = algorithm.partition(":")
+        # +overlap: bucketed reduce-scatter from the backward hooks, one layer per bucket
+        asg, _, ov = asg.partition("+")
         h = K.Hyper(gamma=0.05, xi=0.9, inv_type=inv, f_freq=1, k_freq=2)
         cl = (MLP.build_cluster if alg == "dp_kfac" else MLP.build_mpd_cluster)(spec, P, seed=5)
         mods = []
@@ -43,7 +46,7 @@ def main():
         model = torch.nn.Sequential(*mods[:-1]).to(dev)
         lins = [m for m in model if isinstance(m, torch.nn.Linear)]
         kf = DPKFAC(model, gamma=0.05, xi=0.9, inv_type=inv, k_freq=2, precision="3xtf32", algorithm=alg,
-                    assignment=asg or "round_robin")
+                    assignment=asg or "round_robin", comm_overlap=ov == "overlap", bucket_mb=1e-4)
         opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9)
         rng = np.random.default_rng(91)
         for t in range(4):
@@ -55,6 +58,8 @@ def main():
             opt.zero_grad()
             F.cross_entropy(model(torch.from_numpy(xs.T.copy()).float().to(dev)),
                             torch.from_numpy(ys).to(dev)).backward()
+            if ov and t > 0 and len(kf._bucket_ev) != len(kf.layout.buckets):
+                bad.append((algorithm, inv, t, "hooks did not launch every bucket"))
             kf.step()
             if asg == "balanced" and t == 0:
                 cl = MLP.build_cluster(spec, P, seed=5, assignment=kf.assignment)

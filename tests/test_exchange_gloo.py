@@ -31,7 +31,10 @@ def _local_grad(rank, i):
     return torch.randn(*SHAPES[i], generator=g)
 
 
-def _worker(rank, world, port, assign_kind, q):
+BUCKETS = [[4, 3], [2], [1, 0]]  # backward order, as DPKFAC._grad_buckets cuts them
+
+
+def _worker(rank, world, port, assign_kind, q, bucketed=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -41,12 +44,17 @@ def _worker(rank, world, port, assign_kind, q):
             assignment = round_robin_partition(n, world)
         else:
             assignment = balanced_partition([r * c for r, c in SHAPES], world)
-        layout = OwnerMajorLayout(assignment, [r * c for r, c in SHAPES], align=4)
+        layout = OwnerMajorLayout(assignment, [r * c for r, c in SHAPES], align=4,
+                                  buckets=BUCKETS if bucketed else None)
         x = OwnerMajorExchange(layout, rank, "cpu")
         for i in range(n):  # pack (the CUDA pack kernel's job on the GPU): flat = grad / P
-            off = layout.offsets[i]
+            off = layout.in_offsets[i]
             x.flat[off:off + SHAPES[i][0] * SHAPES[i][1]] = (_local_grad(rank, i) / world).reshape(-1)
-        x.reduce_scatter()
+        if bucketed:  # one collective per bucket, in backward order (as the hooks issue them)
+            for b in range(len(layout.buckets)):
+                x.reduce_scatter_bucket(b)
+        else:
+            x.reduce_scatter()
         for i in assignment[rank]:  # "precondition": owner tags its result with (i+1)
             x.view_out(i, SHAPES[i]).copy_(x.view_in(i, SHAPES[i]) * (i + 1))
         x.all_gather()
@@ -61,12 +69,14 @@ def _worker(rank, world, port, assign_kind, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,kind", [(2, "rr"), (3, "rr"), (2, "balanced"), (8, "balanced"), (8, "rr")])
-def test_owner_major_exchange_gloo(world, kind):
+@pytest.mark.parametrize("world,kind,bucketed", [(2, "rr", False), (3, "rr", False), (2, "balanced", False),
+                                                (8, "balanced", False), (8, "rr", False), (2, "rr", True),
+                                                (3, "balanced", True)])
+def test_owner_major_exchange_gloo(world, kind, bucketed):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, kind, q, bucketed)) for r in range(world)]
     for p in procs:
         p.start()
     results = [q.get(timeout=120) for _ in range(world)]
@@ -83,6 +93,26 @@ def test_owner_major_exchange_gloo(world, kind):
     for _, out, _ in results[1:]:
         for i in range(len(SHAPES)):
             assert (out[i] == base[i]).all()
+
+
+def test_bucketed_layout_offsets():
+    """comm_overlap layout: every bucket's reduce-scatter input region holds rank r's
+    layers of that bucket at r * bucket_chunk; the gathered layout is rank-major and
+    equals the plain owner-major one when there is a single bucket."""
+    n_grad = [r * c for r, c in SHAPES]
+    assignment = round_robin_partition(len(SHAPES), 2)
+    one = OwnerMajorLayout(assignment, n_grad, align=4)
+    assert one.in_offsets == one.offsets and one.buckets == ((0, 1, 2, 3, 4),)
+    lay = OwnerMajorLayout(assignment, n_grad, align=4, buckets=BUCKETS, scalar_slot=True)
+    assert sum(lay.bucket_chunk) == lay.chunk and lay.total == 2 * lay.chunk
+    for i, g in enumerate(n_grad):
+        p, b = lay.owner_of(i), lay.bucket_of[i]
+        base, c = lay.bucket_base[b], lay.bucket_chunk[b]
+        assert 2 * base + p * c <= lay.in_offsets[i] and lay.in_offsets[i] + g <= 2 * base + (p + 1) * c
+        assert p * lay.chunk + base <= lay.offsets[i] and lay.offsets[i] + g <= p * lay.chunk + base + c
+        assert lay.offsets[i] - p * lay.chunk < lay.slot_offset  # the KL slot is never a layer's float
+    with pytest.raises(ValueError):
+        OwnerMajorLayout(assignment, n_grad, buckets=[[0, 1], [2, 3]])
 
 
 def _agree_worker(rank, world, port, q):

@@ -476,6 +476,62 @@ def test_early_launch_matches_reference():
     assert launched[0] == {} and all(l == {0: t} for t, l in enumerate(launched) if t > 0), launched
 
 
+@pytest.mark.parametrize("bucket_mb", [1e-4, 0.5])
+def test_comm_overlap_buckets_match_reference(bucket_mb):
+    """comm_overlap=True: the gradient buckets are packed and reduce-scattered from the
+    post-accumulate-grad hooks during backward; results equal the
+    reference step for step."""
+    from paper_2206_15143_b200 import DPKFAC
+    dev = torch.device("cuda", 0)
+    spec = MLP.MlpSpec((784, 512, 256, 10), "relu", "softmax_cross_entropy", True)
+    h = K.Hyper(gamma=0.03, xi=0.95, inv_type="inverse", f_freq=1, k_freq=1)
+    cl = MLP.build_cluster(spec, 1, seed=0)
+    model, lins = torch_mlp([w.copy() for w in cl.weights], dev)
+    kf = DPKFAC(model, gamma=0.03, xi=0.95, inv_type="inverse", precision="3xtf32", comm_overlap=True,
+                bucket_mb=bucket_mb, check_numerics="deferred")
+    assert len(kf._grad_buckets()) == (3 if bucket_mb < 0.01 else 2)  # fc3+fc2 | fc1 at 0.5 MB
+    opt = torch.optim.SGD(model.parameters(), lr=0.05, momentum=0.9)
+    rng = np.random.default_rng(99)
+    for t in range(4):
+        x = rng.standard_normal((784, 64))
+        y = rng.integers(0, 10, size=64)
+        _, pre = MLP.dp_kfac_step(cl, MLP.shard(x, y, 1), h, 0.05, 0.9, t)
+        opt.zero_grad()
+        F.cross_entropy(model(torch.from_numpy(x.T.copy()).float().to(dev)), torch.from_numpy(y).to(dev)).backward()
+        if t > 0:  # buffers exist after the first step: every bucket went out from the hooks
+            assert sorted(kf._bucket_ev) == list(range(len(kf.layout.buckets))), (t, kf._bucket_ev)
+        kf.step()
+        for i, lin in enumerate(lins):
+            got = torch.cat([lin.weight.grad, lin.bias.grad[:, None]], 1).double().cpu().numpy()
+            assert rel(got, pre[i]) <= TOL, (t, i, rel(got, pre[i]))
+        opt.step()
+    kf.check()
+
+
+def test_comm_overlap_exchanges_accumulated_gradients():
+    """Two backwards before step(): every complete backward of a bucket relaunches its
+    pack + reduce-scatter, so the exchanged buffer holds the ACCUMULATED gradients."""
+    from paper_2206_15143_b200 import DPKFAC
+    dev = torch.device("cuda", 0)
+    torch.manual_seed(3)
+    model = nn.Sequential(nn.Linear(40, 32), nn.ReLU(), nn.Linear(32, 24), nn.ReLU(), nn.Linear(24, 5)).to(dev)
+    kf = DPKFAC(model, inv_type="inverse", comm_overlap=True, bucket_mb=1e-4)
+    x, y = torch.randn(16, 40, device=dev), torch.randint(0, 5, (16,), device=dev)
+    F.cross_entropy(model(x), y).backward()
+    kf.step()
+    model.zero_grad()
+    for sl in (slice(0, 8), slice(8, 16)):
+        F.cross_entropy(model(x[sl]), y[sl]).backward()
+    torch.cuda.synchronize()
+    X = kf.xchg
+    for ly in kf.layers:
+        want = torch.cat([ly.module.weight.grad, ly.module.bias.grad[:, None]], 1).flatten()
+        off = kf.layout.in_offsets[ly.index]
+        assert torch.equal(X.flat[off:off + want.numel()], want), ly.index
+    kf.step()
+    kf.remove_hooks()
+
+
 class InceptionBits(nn.Module):
     """Inception-v4 building blocks (config C5): 1x7 / 7x1 and 1x3 / 3x1 convs with
     asymmetric padding, a strided 3x3 reduction, an fc."""
