@@ -54,7 +54,7 @@ def parse():
     # north_star: "layers are assigned to GPUs by a load balancer" -> the LPT balancer
     # (SURVEY 8(f)1); "round_robin" is the reference's bit-exact default partition
     ap.add_argument("--assignment", default="balanced")
-    ap.add_argument("--im2col", default="materialize", choices=["materialize", "auto", "implicit"])
+    ap.add_argument("--im2col", default="materialize", choices=["materialize", "auto", "implicit", "implicit16"])
     ap.add_argument("--algorithm", default="dp_kfac", choices=["dp_kfac", "mpd_kfac_co", "mpd_kfac_mo"],
                     help="dp_kfac (the product) or the paper's MPD-KFAC comparators on the same kernels")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -394,7 +394,7 @@ def run_ours(args, rank, world, local_rank):
         tf32_src = ("profiles/tf32_peak.json: measured 8192^3 TF32 matmul, best of 10 (max of cuBLAS "
                     f"{tpj['cublas_tf32_tflops']:.0f} and this engine {tpj['dpk_tf32_tflops']:.0f} TF/s)")
     own = [geom[ly.index] for ly in kf.owned]
-    f16_a = {ly.index for ly in kf.layers if ly.patch16 is not None}  # conv A factors on kind::f16
+    f16_a = {ly.index for ly in kf.layers if ly.patch16 is not None or ly.nhwc16 is not None}  # conv A factors on kind::f16
     built = geom if args.algorithm != "dp_kfac" else own  # MPD: every rank builds every layer's factors
     built_idx = range(len(geom)) if args.algorithm != "dp_kfac" else [ly.index for ly in kf.owned]
     syrk_f16 = sum(geom[i][1] * (geom[i][1] + 1) * geom[i][3] for i in built_idx if i in f16_a)

@@ -80,7 +80,13 @@ enum {
                            it run tcgen05 kind::f16 (fp32 accumulate): the same 11-bit
                            significand as the TF32 path at half the operand bytes and twice
                            the MMA rate; values beyond the fp16 range become inf and surface
-                           as a non-SPD factor (NumericError). */
+                           as a non-SPD factor (NumericError). */,
+  DPK_OPND_IM2COL_TAPMAJOR_F16 = 5 /* the DPK_OPND_IM2COL_TAPMAJOR view over an fp16 NHWC copy of
+                           the input (dpk_im2col_convert_f16; strides in halves): SYRK only,
+                           TMA-only -- rows (i, j, c) fetched by TMA im2col loads of 64 output
+                           pixels x 64 channels straight into the kind::f16 MN-major operand
+                           layout, so the patch matrix never exists in memory.  Requires
+                           C % 64 == 0, c contiguous, 16-byte aligned strides, no bias row. */
 };
 
 typedef struct dpk_operand {
@@ -154,6 +160,12 @@ int dpk_im2col_materialize(const dpk_im2col_job* jobs, int n_jobs, dpk_stream_t 
 /* The same patch values as fp16, FEATURE-major: out[r*ld + k] = half(X[r, k])
  * (round to nearest), ld >= cols and ld % 8 == 0; read back as DPK_OPND_ROWS_K_F16. */
 int dpk_im2col_materialize_f16(const dpk_im2col_job* jobs, int n_jobs, dpk_stream_t stream);
+/* The implicit-SYRK input: out = half(x * 2^-e), the dense channels-last conv input copied
+ * element for element (N*H*W*C halves, 16-byte aligned; e from jobs[i].amax as above, or
+ * 0 without it).  The job's x must be the dense NHWC DPK_OPND_IM2COL_TAPMAJOR view with
+ * C % 8 == 0; read back through DPK_OPND_IM2COL_TAPMAJOR_F16 (same geometry, data = out).
+ * One launch. */
+int dpk_im2col_convert_f16(const dpk_im2col_job* jobs, int n_jobs, dpk_stream_t stream);
 /* amax|X| of every job's implicit-im2col view (= amax over the conv input, or 1 with
  * a bias row, whichever is larger) into *jobs[i].amax as float bits (non-finite
  * inputs propagate: the factor then fails as non-SPD, never silently).  One launch;

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(_HERE, "libdpkfac.so")
 DPK_OK, DPK_EARG, DPK_ESHAPE, DPK_ECUDA, DPK_ENOSPACE = 0, 1, 2, 3, 4
 DPK_PREC_TF32, DPK_PREC_TF32_TRUNC, DPK_PREC_3XTF32 = 1, 2, 3
 INFO_OK, INFO_TRACE, INFO_NOT_SPD_A, INFO_NOT_SPD_G, INFO_EIG_DENOM, INFO_NONFINITE = range(6)
-OPND_ROWS_K, OPND_ROWS_MN, OPND_IM2COL, OPND_IM2COL_TAPMAJOR, OPND_ROWS_K_F16 = 0, 1, 2, 3, 4
+OPND_ROWS_K, OPND_ROWS_MN, OPND_IM2COL, OPND_IM2COL_TAPMAJOR, OPND_ROWS_K_F16, OPND_IM2COL_TAPMAJOR_F16 = 0, 1, 2, 3, 4, 5
 
 
 class Operand(C.Structure):
@@ -98,6 +98,7 @@ _SIGNATURES = [
     ("dpk_im2col_materialize", C.c_int, [C.POINTER(Im2colJob), C.c_int, _P]),
     ("dpk_im2col_materialize_f16", C.c_int, [C.POINTER(Im2colJob), C.c_int, _P]),
     ("dpk_im2col_amax", C.c_int, [C.POINTER(Im2colJob), C.c_int, _P]),
+    ("dpk_im2col_convert_f16", C.c_int, [C.POINTER(Im2colJob), C.c_int, _P]),
     ("dpk_gemm_workspace_bytes", C.c_size_t, [C.POINTER(GemmJob), C.c_int]),
     ("dpk_gemm", C.c_int, [C.POINTER(GemmJob), C.c_int, _P, C.c_size_t, C.c_int, _P]),
     ("dpk_trace_pi", C.c_int, [C.POINTER(PiJob), C.c_int, C.c_float, _P]),

@@ -145,9 +145,25 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn = 0, in
          | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
 }
 
-// Instruction descriptor: kind::f16 with fp16 A/B (format 0), fp32 accumulate, K-major.
-__host__ __device__ constexpr uint32_t idesc_f16(int M, int N) {
-  return (1u << 4) | (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+// Instruction descriptor: kind::f16 with fp16 A/B (format 0), fp32 accumulate;
+// a_mn / b_mn select MN-major operands (default K-major).
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int a_mn = 0, int b_mn = 0) {
+  return (1u << 4) | (static_cast<uint32_t>(a_mn) << 15) | (static_cast<uint32_t>(b_mn) << 16) |
+         (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+// Shared-memory matrix descriptor: MN-major 16-bit operand, SWIZZLE_128B: atoms of
+// 8 k-rows x 128 B (64 halves along M/N), k-row groups 1024 B apart (SBO), 64-wide
+// M/N blocks mn_block_bytes apart (LBO) -- the image TMA writes for boxes of
+// {64 halves of M/N, k rows} with CU_TENSOR_MAP_SWIZZLE_128B.
+__device__ __forceinline__ uint64_t sdesc_mnmajor_sw128_16b(uint32_t saddr, uint32_t mn_block_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((mn_block_bytes >> 4) & 0x3FFF) << 16;  // LBO
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;                        // SBO
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;                                // SWIZZLE_128B
+  return d;
 }
 
 // ---------------------------------------------------------------- CTA pairs (cta_group::2)

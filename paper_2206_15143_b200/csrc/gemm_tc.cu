@@ -72,11 +72,17 @@ static_assert(NPROD % 8 == 0, "im2col chunk sharing needs NPROD % 8 == 0");
 // map and the K order).  Measured TMA-issue bound.
 // TMA_ROWS_K16: K-major fp16 operand (DPK_OPND_ROWS_K_F16), 64 elements per 128-B
 // stage row, consumed by kind::f16 MMAs; a K chunk of such a problem covers 64 columns.
+// TMA_IM2COL16: implicit im2col of an fp16 NHWC input (DPK_OPND_IM2COL_TAPMAJOR_F16):
+// a K chunk is 64 output pixels; per 64-row group (one tap, 64 channels) one TMA
+// im2col box of 64 pixels x 128 B lands as the MN-major SWIZZLE_128B kind::f16
+// operand (8 KB, two per 128-row tile).
 enum { TMA_NONE = 0, TMA_ROWS_K = 1, TMA_ROWS_MN = 2, TMA_SLAB = 3, TMA_IM2COL = 4, TMA_ROWS_MN3 = 5, TMA_TAPS = 6,
-       TMA_ROWS_K16 = 7 };
+       TMA_ROWS_K16 = 7, TMA_IM2COL16 = 8 };
 __host__ __device__ __forceinline__ bool tma_mn(int kind) {
-  return kind == TMA_ROWS_MN || kind == TMA_IM2COL || kind == TMA_ROWS_MN3 || kind == TMA_TAPS;
+  return kind == TMA_ROWS_MN || kind == TMA_IM2COL || kind == TMA_ROWS_MN3 || kind == TMA_TAPS ||
+         kind == TMA_IM2COL16;
 }
+__host__ __device__ __forceinline__ bool tma_f16(int kind) { return kind == TMA_ROWS_K16 || kind == TMA_IM2COL16; }
 
 __host__ __device__ __forceinline__ bool is_im2col(int kind) {
   return kind == DPK_OPND_IM2COL || kind == DPK_OPND_IM2COL_TAPMAJOR;
@@ -417,6 +423,10 @@ __device__ __forceinline__ void convert_tile(uint8_t* tile, uint8_t* tile_lo, in
 // (zero-filled) size; im2col tiles skip 32-row groups past the operand's rows
 // (those smem rows only feed accumulator rows the epilogue never stores).
 __device__ __forceinline__ uint32_t tma_tile_bytes(int kind, const dpk_operand& o, int row0) {
+  if (kind == TMA_IM2COL16) {
+    const int groups = min(BM / 64, (o.rows - row0 + 63) / 64);
+    return static_cast<uint32_t>(max(groups, 0)) * 8192u;
+  }
   if (kind != TMA_IM2COL && kind != TMA_TAPS) return TILE_BYTES;
   const int groups = min(BM / 32, (o.rows - row0 + 31) / 32);
   return static_cast<uint32_t>(max(groups, 0)) * 4096u;
@@ -476,6 +486,27 @@ __device__ __forceinline__ void issue_tma(int kind, const CUtensorMap* map, cons
         tma_load_5d_pair(dst + b * 4096, map, bar, 0, w0 + j * o.dw, h0 + i * o.dh, n0, c0 >> 5);
       else
         tma_load_5d(dst + b * 4096, map, bar, 0, w0 + j * o.dw, h0 + i * o.dh, n0, c0 >> 5);
+    }
+  } else if (kind == TMA_IM2COL16) {  // fp16 NHWC input; a box = 64 output pixels x 64 channels
+    const int64_t k0 = static_cast<int64_t>(kc) * 2 * BK;
+    const int ohw = o.OH * o.OW;
+    const int n = static_cast<int>(k0 / ohw);
+    const int rem = static_cast<int>(k0 - static_cast<int64_t>(n) * ohw);
+    const int oh = rem / o.OW;
+    const int ow = rem - oh * o.OW;
+    const int w0 = ow * o.sw - o.pw, h0 = oh * o.sh - o.ph;
+    for (int b = 0; b < BM / 64; ++b) {
+      const int r = row0 + 64 * b;
+      if (r >= o.rows) break;
+      const int tap = r / o.C;
+      const int c0 = r - tap * o.C;
+      const int i = tap / o.kw, j = tap - (tap / o.kw) * o.kw;
+      if (PAIR)
+        tma_load_im2col_4d_pair(dst + b * 8192, map, bar, c0, w0, h0, n, static_cast<uint16_t>(j * o.dw),
+                                static_cast<uint16_t>(i * o.dh));
+      else
+        tma_load_im2col_4d(dst + b * 8192, map, bar, c0, w0, h0, n, static_cast<uint16_t>(j * o.dw),
+                           static_cast<uint16_t>(i * o.dh));
     }
   } else {  // TMA_IM2COL: NHWC input, rows (i, j, c); a box = 32 output pixels x 32 channels
     const int64_t k0 = static_cast<int64_t>(kc) * BK;
@@ -951,8 +982,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         const bool skip_b = P.same_ab && tm == tn;
         const int a_mn = tma_mn(P.tma_a);
         const int b_mn = skip_b ? a_mn : tma_mn(P.tma_b);
-        const bool f16 = P.tma_a == TMA_ROWS_K16;  // SYRK on an fp16 patch matrix (both operands)
-        const uint32_t idesc = f16 ? idesc_f16(UT, UT) : idesc_tf32(UT, UT, a_mn, b_mn);
+        const bool f16 = tma_f16(P.tma_a);  // SYRK on fp16 operands (both sides)
+        const uint32_t idesc = f16 ? idesc_f16(UT, UT, a_mn, b_mn) : idesc_tf32(UT, UT, a_mn, b_mn);
         const int acc = it & 1;
         if (CG == 2)
           mbar_wait_cluster(tempty_bar(acc), ((it >> 1) & 1) ^ 1);
@@ -975,12 +1006,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
           const uint32_t sal = sa + 2 * TILE_BYTES;
           const uint32_t sbl = skip_b ? sal : sa + 3 * TILE_BYTES;
 #pragma unroll
-          for (int s = 0; s < BK / 8; ++s) {  // UMMA_K = 8 for tf32
-            // K-major: +32 B along the 128 B row; MN-major: next 8-row k group (+1024 B)
-            const uint32_t oa = a_mn ? s * 1024 : s * 32;
-            const uint32_t ob = b_mn ? s * 1024 : s * 32;
-            const uint64_t da = a_mn ? sdesc_mnmajor_sw128(sa + oa, 4096) : sdesc_kmajor_sw128(sa + oa);
-            const uint64_t db = b_mn ? sdesc_mnmajor_sw128(sb + ob, 4096) : sdesc_kmajor_sw128(sb + ob);
+          for (int s = 0; s < BK / 8; ++s) {  // UMMA_K = 8 for tf32 (16 for f16: the same 32 B)
+            // K-major: +32 B along the 128 B row; MN-major: next 8-row k group (+1024 B),
+            // two groups for a 16-deep f16 step (+2048 B, 64-wide M/N blocks 8 KB apart)
+            const uint32_t mstep = f16 ? 2048u : 1024u;
+            const uint32_t oa = a_mn ? s * mstep : s * 32;
+            const uint32_t ob = b_mn ? s * mstep : s * 32;
+            const uint64_t da = a_mn ? (f16 ? sdesc_mnmajor_sw128_16b(sa + oa, 8192) : sdesc_mnmajor_sw128(sa + oa, 4096))
+                                     : sdesc_kmajor_sw128(sa + oa);
+            const uint64_t db = b_mn ? (f16 ? sdesc_mnmajor_sw128_16b(sb + ob, 8192) : sdesc_mnmajor_sw128(sb + ob, 4096))
+                                     : sdesc_kmajor_sw128(sb + ob);
             const uint32_t accum = (kc > kc0 || s > 0) ? 1u : 0u;
             if (NPASS == 1 && f16) {  // UMMA_K = 16 fp16 = the same 32 B step
               if (CG == 2)
@@ -1416,6 +1451,33 @@ bool plan_tma_im2col(const dpk_operand& o, CUtensorMap* m, bool rn) {
   return r == CUDA_SUCCESS;
 }
 
+// DPK_OPND_IM2COL_TAPMAJOR_F16: the same im2col-mode map over the fp16 NHWC copy;
+// a box is 64 output pixels x 64 channels (128 B per pixel), SWIZZLE_128B -- the
+// MN-major kind::f16 operand image.  A 64-row group never crosses a tap (C % 64).
+bool im2col16_eligible(const dpk_operand& o) {
+  return o.kind == DPK_OPND_IM2COL_TAPMAJOR_F16 && !o.bias_row && !tma_disabled() && o.C % 64 == 0 &&
+         o.sc == 1 && aligned16(o.data) && (o.sws * 2) % 16 == 0 && (o.shs * 2) % 16 == 0 &&
+         (o.sn * 2) % 16 == 0 && o.pw <= 127 && o.ph <= 127 && o.pw - o.dw * (o.kw - 1) >= -128 &&
+         o.ph - o.dh * (o.kh - 1) >= -128 && o.sw <= 8 && o.sh <= 8 && o.dw * (o.kw - 1) < 65536 &&
+         o.dh * (o.kh - 1) < 65536 && o.cols % (static_cast<int64_t>(o.OH) * o.OW) == 0;
+}
+
+bool plan_tma_im2col16(const dpk_operand& o, CUtensorMap* m) {
+  EncodeIm2colFn fn = im2col_encoder();
+  if (!fn) return false;
+  const int64_t n = o.cols / (static_cast<int64_t>(o.OH) * o.OW);
+  const cuuint64_t dims[4] = {static_cast<cuuint64_t>(o.C), static_cast<cuuint64_t>(o.W),
+                              static_cast<cuuint64_t>(o.H), static_cast<cuuint64_t>(n)};
+  const cuuint64_t strides[3] = {static_cast<cuuint64_t>(o.sws) * 2, static_cast<cuuint64_t>(o.shs) * 2,
+                                 static_cast<cuuint64_t>(o.sn) * 2};
+  const int lower[2] = {-o.pw, -o.ph};
+  const int upper[2] = {o.pw - o.dw * (o.kw - 1), o.ph - o.dh * (o.kh - 1)};
+  const cuuint32_t es[4] = {1, static_cast<cuuint32_t>(o.sw), static_cast<cuuint32_t>(o.sh), 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<float*>(o.data), dims, strides, lower, upper, 64, 64,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // TMA_TAPS geometry: a K chunk is 32 output pixels = wb columns x hb rows of one
 // output image block x nb samples (wb | OW, hb | OH exactly -- an invented pixel
 // past the image edge could still read real input at a shifted tap; the sample
@@ -1518,7 +1580,7 @@ int operand_rows(const dpk_operand& o) { return o.rows + (o.bias_row ? 1 : 0); }
 bool valid_operand(const dpk_operand& o) {
   if (o.data == nullptr && o.rows > 0) return false;
   if (o.rows < 0 || o.cols < 1) return false;
-  if (is_im2col(o.kind)) {
+  if (is_im2col(o.kind) || o.kind == DPK_OPND_IM2COL_TAPMAJOR_F16) {
     if (o.kh < 1 || o.kw < 1 || o.sh < 1 || o.sw < 1 || o.dh < 1 || o.dw < 1 || o.OH < 1 || o.OW < 1) return false;
     if (o.rows != o.C * o.kh * o.kw) return false;
   } else if (o.kind != DPK_OPND_ROWS_K && o.kind != DPK_OPND_ROWS_MN && o.kind != DPK_OPND_ROWS_K_F16) {
@@ -1583,10 +1645,16 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
     P.tiles_n = (P.N + UT - 1) / UT;
     P.ntiles = P.symmetric ? tmn * (tmn + 1) / 2 : tmn * P.tiles_n;
     P.chunks = static_cast<int>((j.a.cols + BK - 1) / BK);
-    const bool f16a = j.a.kind == DPK_OPND_ROWS_K_F16, f16b = j.b.kind == DPK_OPND_ROWS_K_F16;
+    const bool f16a = j.a.kind == DPK_OPND_ROWS_K_F16 || j.a.kind == DPK_OPND_IM2COL_TAPMAJOR_F16;
+    const bool f16b = j.b.kind == DPK_OPND_ROWS_K_F16 || j.b.kind == DPK_OPND_IM2COL_TAPMAJOR_F16;
     if (f16a || f16b) {
       if (!(f16a && f16b) || precision != DPK_PREC_TF32 || P.tri_a || P.tri_b) {
         set_error("dpk_gemm: fp16 operands need fp16 on both sides, 1-pass precision, no triangular clipping");
+        return DPK_EARG;
+      }
+      if (j.a.kind == DPK_OPND_IM2COL_TAPMAJOR_F16 && (!P.same_ab || !im2col16_eligible(j.a))) {
+        set_error("dpk_gemm: DPK_OPND_IM2COL_TAPMAJOR_F16 is a SYRK-only, TMA-only view (C % 64 == 0, c "
+                  "contiguous, 16-byte aligned strides, no bias row, padding within the TMA im2col limits)");
         return DPK_EARG;
       }
       P.chunks = static_cast<int>((j.a.cols + 2 * BK - 1) / (2 * BK));
@@ -1619,11 +1687,16 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
       }
     } else if (with_maps) {
       auto plan_one = [&](const dpk_operand& o, CUtensorMap* m) -> int {
+        if (o.kind == DPK_OPND_IM2COL_TAPMAJOR_F16) return plan_tma_im2col16(o, m) ? TMA_IM2COL16 : TMA_NONE;
         if (o.kind == DPK_OPND_IM2COL_TAPMAJOR)
           return (im2col_eligible(o) && plan_tma_im2col(o, m, rn)) ? TMA_IM2COL : TMA_NONE;
         return plan_tma_2d(o, m, rn);
       };
       P.tma_a = plan_one(j.a, &P.tmap_a);
+      if (j.a.kind == DPK_OPND_IM2COL_TAPMAJOR_F16 && P.tma_a == TMA_NONE) {
+        set_error("dpk_gemm: cuTensorMapEncodeIm2col rejected the fp16 implicit-im2col map");
+        return DPK_ECUDA;
+      }
       if (P.same_ab) {
         P.tma_b = P.tma_a;
         P.tmap_b = P.tmap_a;
@@ -1679,6 +1752,7 @@ bool wants_cg2(const GemmSpec& g) {
   const bool same = std::memcmp(&j.a, &j.b, sizeof(dpk_operand)) == 0;
   auto ok = [&](const dpk_operand& o) {
     if (tma_possible_2d(o)) return true;
+    if (o.kind == DPK_OPND_IM2COL_TAPMAJOR_F16) return im2col16_eligible(o);
     if (o.kind == DPK_OPND_IM2COL_TAPMAJOR) return im2col_eligible(o);
     return false;
   };
@@ -2088,8 +2162,9 @@ int dpk_syrk_ema(const dpk_factor_job* jobs, int n_jobs, void* workspace, size_t
 int dpk_conv_im2col_syrk_ema(const dpk_factor_job* jobs, int n_jobs, void* workspace, size_t ws_bytes,
                              int precision, dpk_stream_t stream) {
   for (int i = 0; i < n_jobs; ++i) {
-    if (!dpk::is_im2col(jobs[i].x.kind)) {
-      dpk::set_error("dpk_conv_im2col_syrk_ema: operand must be DPK_OPND_IM2COL or DPK_OPND_IM2COL_TAPMAJOR");
+    if (!dpk::is_im2col(jobs[i].x.kind) && jobs[i].x.kind != DPK_OPND_IM2COL_TAPMAJOR_F16) {
+      dpk::set_error("dpk_conv_im2col_syrk_ema: operand must be DPK_OPND_IM2COL, DPK_OPND_IM2COL_TAPMAJOR or "
+                     "DPK_OPND_IM2COL_TAPMAJOR_F16");
       return DPK_EARG;
     }
   }

@@ -507,6 +507,41 @@ __global__ void __launch_bounds__(256) amax_kernel(const __grid_constant__ I2cBa
   if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(J.amax, m);
 }
 
+// ---------------------------------------------------------------- fp16 NHWC copy for the implicit SYRK
+// out = half(x * 2^-e), the dense channels-last input itself (N*H*W*C halves, the
+// same element order): the operand DPK_OPND_IM2COL_TAPMAJOR_F16 then gathers the
+// patches by TMA im2col loads inside the SYRK, so no patch matrix is ever written.
+// 8 elements per thread: two float4 loads, one 16-byte store.
+bool convert_ok(const dpk_im2col_job& j) {
+  const dpk_operand& o = j.x;
+  const int64_t hw = static_cast<int64_t>(o.H) * o.W;
+  return o.kind == DPK_OPND_IM2COL_TAPMAJOR && o.data != nullptr && j.out != nullptr && o.C % 8 == 0 &&
+         o.sc == 1 && o.sws == o.C && o.shs == static_cast<int64_t>(o.W) * o.C && o.sn == hw * o.C && o.OH > 0 &&
+         o.OW > 0 && o.cols % (static_cast<int64_t>(o.OH) * o.OW) == 0 &&
+         (reinterpret_cast<uintptr_t>(o.data) & 15) == 0 && (reinterpret_cast<uintptr_t>(j.out) & 15) == 0;
+}
+
+__global__ void __launch_bounds__(256) convert_f16_kernel(const __grid_constant__ I2cBatch b) {
+  const dpk_im2col_job& J = b.j[blockIdx.y];
+  const dpk_operand& o = J.x;
+  const int64_t n8 = (o.cols / (static_cast<int64_t>(o.OH) * o.OW)) * o.sn / 8;
+  const float sc = J.amax ? ldexpf(1.0f, -prescale_exponent(__ldg(J.amax))) : 1.0f;  // exact 2^-e
+  const float4* src = reinterpret_cast<const float4*>(o.data);
+  uint4* dst = reinterpret_cast<uint4*>(J.out);
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n8;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float4 a = __ldcs(src + 2 * e), c = __ldcs(src + 2 * e + 1);
+    const __half2 h0 = __floats2half2_rn(a.x * sc, a.y * sc), h1 = __floats2half2_rn(a.z * sc, a.w * sc);
+    const __half2 h2 = __floats2half2_rn(c.x * sc, c.y * sc), h3 = __floats2half2_rn(c.z * sc, c.w * sc);
+    uint4 w;
+    w.x = *reinterpret_cast<const uint32_t*>(&h0);
+    w.y = *reinterpret_cast<const uint32_t*>(&h1);
+    w.z = *reinterpret_cast<const uint32_t*>(&h2);
+    w.w = *reinterpret_cast<const uint32_t*>(&h3);
+    dst[e] = w;  // default store: the SYRK reads it next, from L2 where it still fits
+  }
+}
+
 bool k16_rows_ok(const dpk_im2col_job& j) {
   const dpk_operand& o = j.x;
   const RowsGeom g = rows_geom(o);
@@ -649,6 +684,39 @@ extern "C" int dpk_im2col_amax(const dpk_im2col_job* jobs, int n_jobs, dpk_strea
     dpk::amax_kernel<<<dim3(gx, cnt), 256, 0, st>>>(ab);
     dpk::note_launch();
     rc = dpk::cuda_status(cudaGetLastError(), "amax_kernel launch");
+    if (rc) return rc;
+  }
+  return DPK_OK;
+}
+
+extern "C" int dpk_im2col_convert_f16(const dpk_im2col_job* jobs, int n_jobs, dpk_stream_t stream) {
+  if (n_jobs == 0) return DPK_OK;
+  if (n_jobs < 0 || jobs == nullptr) {
+    dpk::set_error("dpk_im2col_convert_f16: bad job list");
+    return DPK_EARG;
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  thread_local dpk::I2cBatch cb;
+  for (int first = 0; first < n_jobs; first += dpk::I2C_MAX) {
+    const int cnt = std::min(dpk::I2C_MAX, n_jobs - first);
+    cb.n = cnt;
+    int64_t most = 0;
+    for (int i = 0; i < cnt; ++i) {
+      const dpk_im2col_job& j = jobs[first + i];
+      if (!dpk::convert_ok(j)) {
+        dpk::set_error("dpk_im2col_convert_f16: job " + std::to_string(first + i) +
+                       " needs a dense channels-last fp32 input (DPK_OPND_IM2COL_TAPMAJOR), C % 8 == 0, "
+                       "16-byte aligned input and output");
+        return DPK_EARG;
+      }
+      cb.j[i] = j;
+      const dpk_operand& o = j.x;
+      most = std::max<int64_t>(most, (o.cols / (static_cast<int64_t>(o.OH) * o.OW)) * o.sn / 8);
+    }
+    const int gx = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((most + 255) / 256, 4 * 148)));
+    dpk::convert_f16_kernel<<<dim3(gx, cnt), 256, 0, st>>>(cb);
+    dpk::note_launch();
+    const int rc = dpk::cuda_status(cudaGetLastError(), "convert_f16_kernel launch");
     if (rc) return rc;
   }
   return DPK_OK;

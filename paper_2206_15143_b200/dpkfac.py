@@ -26,6 +26,7 @@ Semantics follow the reference's simulated cluster (kfaclab distsim.py:289-338,
 
 from __future__ import annotations
 
+import os
 from typing import Optional, Sequence, Union
 
 import torch
@@ -38,6 +39,10 @@ from .errors import ArgumentError, NumericError, OrderingError, ShapeError
 from .kfac import KfacHyper
 from .exchange import OwnerMajorExchange, OwnerMajorLayout, agree_max
 from .partition import round_robin_partition, step_time_partition, validate_partition
+
+
+# im2col="implicit16": largest input channel count routed to the implicit fp16 SYRK
+IMPLICIT16_MAX_C = int(os.environ.get("DPK_I16_MAXC", "1048576"))
 
 
 def _nhwc(t: torch.Tensor) -> bool:
@@ -83,6 +88,7 @@ class _Layer:
 
         self.patch: Optional[torch.Tensor] = None  # materialized patch matrix (M x ld), reused
         self.patch16: Optional[torch.Tensor] = None  # fp16 feature-major patch matrix (d x ld), reused
+        self.nhwc16: Optional[torch.Tensor] = None   # fp16 copy of the NHWC input (implicit fp16 SYRK)
         self.amax: Optional[torch.Tensor] = None     # int32 slot: amax|X| bits of the fp16 patches
 
     # ---- operand views of the captures (reference layout: d x M, columns = samples)
@@ -116,6 +122,18 @@ class _Layer:
             # at tap-shifted coordinates, patches never reach HBM
             return op, None
         d = op.rows + op.bias_row
+        if f16 and im2col == "implicit16" and tap and nhwc and x.shape[1] % 64 == 0 and not self.has_bias \
+                and x.shape[1] <= IMPLICIT16_MAX_C \
+                and x.is_contiguous(memory_format=torch.channels_last) and x.data_ptr() % 16 == 0 \
+                and max(m.padding) <= 127 and max(m.stride) <= 8:
+            # implicit fp16 SYRK: the input is copied once as prescaled fp16 NHWC (1/(kh kw)
+            # of the patch bytes) and the SYRK gathers the patches by TMA im2col loads
+            n_, c_, h_, w_ = x.shape
+            if self.nhwc16 is None or self.nhwc16.shape != (n_, h_, w_, c_):
+                self.nhwc16 = torch.empty(n_, h_, w_, c_, dtype=torch.float16, device=x.device)
+            if self.amax is None:
+                self.amax = torch.zeros(1, dtype=torch.int32, device=x.device)
+            return ops.operand_im2col_f16(op, self.nhwc16), (op, self.nhwc16, self.amax)
         # fp16 patches: the tiled transpose kernel (NHWC, C % 32 == 0) or the row-staged
         # one (small-C stems, output width a multiple of 8); else the fp32 paths
         tiled = tap and nhwc and x.shape[1] % 32 == 0 and not self.has_bias and x.data_ptr() % 16 == 0
@@ -273,8 +291,8 @@ class DPKFAC:
         # Default "materialize": the sample-blocked tap boxes measured slower (factor
         # stage 2.9 -> 6.3 ms on ResNet-50) and hang under the dynamic tile
         # scheduler in grouped launches -- under investigation.
-        if im2col not in ("auto", "materialize", "implicit"):
-            raise ArgumentError("im2col must be 'auto', 'materialize' or 'implicit'")
+        if im2col not in ("auto", "materialize", "implicit", "implicit16"):
+            raise ArgumentError("im2col must be 'auto', 'materialize', 'implicit' or 'implicit16'")
         self.im2col = im2col
         if precision == "auto":
             precision = "3xtf32" if inv_type == "eigen" else "tf32"

@@ -132,28 +132,53 @@ def operand_rows_k_f16(x: torch.Tensor, cols: int) -> L.Operand:
     return o
 
 
+def operand_im2col_f16(op: L.Operand, x16: torch.Tensor) -> L.Operand:
+    """The dense fp16 NHWC copy ``x16`` (N x H x W x C halves, written by
+    im2col_materialize_f16) of ``op``'s channels-last input, viewed with op's geometry
+    as DPK_OPND_IM2COL_TAPMAJOR_F16: the SYRK gathers the patches itself by TMA im2col
+    loads (kind::f16), so no patch matrix is written."""
+    n, h, w, c = x16.shape
+    if x16.dtype != torch.float16 or not x16.is_contiguous() or (c, h, w) != (op.C, op.H, op.W):
+        raise ShapeError("fp16 implicit-im2col input must be a dense N x H x W x C half tensor of op's shape")
+    o = L.Operand.from_buffer_copy(op)
+    o.kind = L.OPND_IM2COL_TAPMAJOR_F16
+    o.data = x16.data_ptr()
+    o.sn, o.sc, o.shs, o.sws = h * w * c, 1, w * c, c
+    return o
+
+
 def im2col_materialize_f16(pairs):
-    """pairs: [(im2col operand, out half tensor d x ld[, amax int32 slot])] ->
-    out[r, k] = half(X[r, k] * 2^-e) (feature-major).  With an amax slot, one
+    """pairs: [(im2col operand, out half tensor[, amax int32 slot])].  A 2-D out
+    (d x ld) receives the feature-major patches out[r, k] = half(X[r, k] * 2^-e); a
+    4-D out (N x H x W x C) receives the channels-last input itself as half(x * 2^-e)
+    for the implicit fp16 SYRK (operand_im2col_f16).  With amax slots, one
     dpk_im2col_amax launch first measures amax|X| and e puts the largest value in
     [2^14, 2^15) (no fp16 overflow); the SYRK job must carry the same slot
     (factor_job(..., x_amax=slot)) to undo the scale.  Without it, e = 0."""
     if not pairs:
         return
-    jobs = []
+    jobs, kinds = [], []
     for pr in pairs:
         op, out = pr[0], pr[1]
         amax = pr[2] if len(pr) > 2 else None
         j = L.Im2colJob()
         j.x = op
         j.out = out.data_ptr()
-        j.ld = out.stride(0)
+        j.ld = out.stride(0) if out.dim() == 2 else 0
         j.amax = amax.data_ptr() if amax is not None else None
         jobs.append(j)
+        kinds.append(out.dim() == 4)
     arr = L.array(L.Im2colJob, jobs)
     if any(j.amax for j in jobs):
         L.check(lib().dpk_im2col_amax(arr, len(jobs), stream_handle()), "dpk_im2col_amax")
-    L.check(lib().dpk_im2col_materialize_f16(arr, len(jobs), stream_handle()), "dpk_im2col_materialize_f16")
+    pj = [j for j, k in zip(jobs, kinds) if not k]
+    cj = [j for j, k in zip(jobs, kinds) if k]
+    if pj:
+        L.check(lib().dpk_im2col_materialize_f16(L.array(L.Im2colJob, pj), len(pj), stream_handle()),
+                "dpk_im2col_materialize_f16")
+    if cj:
+        L.check(lib().dpk_im2col_convert_f16(L.array(L.Im2colJob, cj), len(cj), stream_handle()),
+                "dpk_im2col_convert_f16")
 
 
 def im2col_materialize(pairs):

@@ -39,9 +39,20 @@ for c, h in ((64, 56), (128, 28), (256, 14), (512, 7)):
     def f16_syrk():
         ops.syrk_ema([ops.factor_job(op16, out, 1.0 / op.cols, 0.0, x_amax=amax)], "tf32")
 
+    x16 = torch.empty(32, h, h, c, dtype=torch.float16, device="cuda")
+    op_i16 = ops.operand_im2col_f16(op, x16)
+
+    def implicit16():
+        ops.im2col_materialize_f16([(op, x16, amax)])
+        ops.syrk_ema([ops.factor_job(op_i16, out, 1.0 / op.cols, 0.0, x_amax=amax)], "tf32")
+
+    def implicit16_syrk():
+        ops.syrk_ema([ops.factor_job(op_i16, out, 1.0 / op.cols, 0.0, x_amax=amax)], "tf32")
+
     def implicit():
         ops.syrk_ema([ops.factor_job(op, out, 1.0 / op.cols, 0.0)], "tf32")
 
     # DPK_TAPS=0 in the environment selects the TMA im2col-mode form for "implicit"
-    r = {"f16 route": timed(f16_route), "f16 syrk only": timed(f16_syrk), "implicit": timed(implicit)}
+    r = {"f16 route": timed(f16_route), "f16 syrk only": timed(f16_syrk), "implicit fp32": timed(implicit),
+         "implicit16 route": timed(implicit16), "implicit16 syrk only": timed(implicit16_syrk)}
     print(f"C={c} H={h} d={d} M={op.cols}: " + ", ".join(f"{k} {v:.1f} us" for k, v in r.items()), flush=True)

@@ -626,3 +626,48 @@ def test_compute_conv_input_factor_matches_unfold(shape, k, s, p, bias, channels
     cols = K.unfold_columns(x, kk[0], kk[1], s, p, 1, bias)
     want, _ = K.compute_factors(cols, cols[:1])
     assert rel(N(a), want) <= 1e-5, rel(N(a), want)
+
+
+@pytest.mark.parametrize("scale", [1.0, 1e6])
+@pytest.mark.parametrize("shape,k,s,p", [((4, 64, 14, 14), 3, 1, 1), ((3, 128, 9, 11), 3, 2, 1),
+                                         ((2, 64, 12, 12), 1, 2, 0), ((5, 192, 7, 7), 3, 1, 1),
+                                         ((2, 64, 17, 17), (1, 7), 1, (0, 3)), ((2, 256, 6, 6), 3, 1, 1)])
+def test_implicit_f16_syrk_matches_unfold(shape, k, s, p, scale):
+    """DPK_OPND_IM2COL_TAPMAJOR_F16: the channels-last input copied once as prescaled
+    fp16 (dpk_im2col_convert_f16, bit-exact half(x * 2^-e)), the patches gathered by
+    TMA im2col boxes (64 pixels x 64 channels) inside the kind::f16 SYRK -- equal to
+    the fp16-patch route's factor and within TOL of the float64 reference; pixel
+    tails (M % 64 != 0), strides, 1x7 kernels and C = 192 / 256 (several 64-row
+    groups per tap) included."""
+    from paper_2206_15143_b200 import ops
+    kh, kw = (k, k) if isinstance(k, int) else k
+    ph, pw = (p, p) if isinstance(p, int) else p
+    rng = np.random.default_rng(sum(shape) + kh * kw)
+    x = np.maximum(rng.standard_normal(shape), 0) * scale
+    xt = T(x).to(memory_format=torch.channels_last)
+    op = ops.operand_im2col(xt, (kh, kw), (s, s), (ph, pw), (1, 1), tap_major=True)
+    n, c, h, w = shape
+    x16 = torch.full((n, h, w, c), float("nan"), dtype=torch.float16, device=dev())
+    amax = torch.zeros(1, dtype=torch.int32, device=dev())
+    ops.im2col_materialize_f16([(op, x16, amax)])
+    torch.cuda.synchronize()
+    e = int(np.floor(np.log2(np.abs(x.astype(np.float32)).max()))) - 14
+    want16 = torch.from_numpy(x.astype(np.float32) * 2.0 ** -e).half().permute(0, 2, 3, 1)
+    assert torch.equal(x16.cpu(), want16)  # RN half of the exactly prescaled input
+    cols = K.unfold_columns(x, kh, kw, s, p if isinstance(p, int) else (ph, pw))
+    perm = _tap_perm(c, kh, kw)
+    M = cols.shape[1]
+    out = torch.full((op.rows, op.rows), float("nan"), device=dev())
+    ops.syrk_ema([ops.factor_job(ops.operand_im2col_f16(op, x16), out, 1.0 / M, 0.0, x_amax=amax)], "tf32")
+    # the materialized fp16 route on the same values
+    ld = (M + 7) // 8 * 8
+    patch = torch.empty(op.rows, ld, dtype=torch.float16, device=dev())
+    amax2 = torch.zeros(1, dtype=torch.int32, device=dev())
+    ops.im2col_materialize_f16([(op, patch, amax2)])
+    ref16 = torch.full_like(out, float("nan"))
+    ops.syrk_ema([ops.factor_job(ops.operand_rows_k_f16(patch, M), ref16, 1.0 / M, 0.0, x_amax=amax2)], "tf32")
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()
+    assert rel(N(out), N(ref16)) <= 1e-6, rel(N(out), N(ref16))
+    want, _ = K.compute_factors(cols[perm], cols[:1])
+    assert rel(N(out), want) <= TOL, rel(N(out), want)
