@@ -213,8 +213,8 @@ bool vec_ok(const dpk_im2col_job& j) {
 }
 
 // ---------------------------------------------------------------- fp16, feature-major
-// out[r*ld + k] = half(X[r, k]).  Tiled: NHWC tap-major, C % 32 == 0 -- a block
-// gathers 64 output pixels x 32 channels of one tap (coalesced 128-B rows of the
+// out[r*ld + k] = half(X[r, k]).  Tiled: NHWC tap-major, C % 8 == 0 -- a block
+// gathers 64 output pixels x 32 feature rows (32 channels of one tap, or C-channel runs of several) (coalesced 128-B rows of the
 // input, zero outside the image), transposes through shared memory and writes
 // 32 rows x 64 halves (128 B each).  Generic: one element per thread, k fastest.
 constexpr int K16_PIX = 64;
@@ -262,16 +262,24 @@ __global__ void __launch_bounds__(256) im2col_k16_tiled_kernel(const __grid_cons
     const uint32_t n = kk / static_cast<uint32_t>(ohw);
     const int rem = static_cast<int>(kk - n * static_cast<uint32_t>(ohw));
     const int oh = rem / OW, ow = rem - (rem / OW) * OW;
-    base[h] = o.data + static_cast<int64_t>(n) * o.sn + 4 * qq;
+    base[h] = o.data + static_cast<int64_t>(n) * o.sn;
     ih0[h] = oh * sh - o.ph;
     iw0[h] = ow * sw - o.pw;
   }
   const float sc = J.amax ? ldexpf(1.0f, -prescale_exponent(__ldg(J.amax))) : 1.0f;  // exact 2^-e
-  const int nrg = (o.rows + 31) / 32;
-  const int cblk = C >> 5;  // 32-channel groups per tap
+  const int rows = o.rows, nrg = (rows + 31) / 32, kh = o.kh;
   int rg = gb * K16_GROUPS;
-  int tap = rg / cblk, c0 = (rg - tap * cblk) * 32;
-  int ti = tap / kw, tj = tap - (tap / kw) * kw;
+  // this thread's load row r = 32 rg + 4 qq: its tap (ti, tj) and channel c, walked
+  // incrementally (+32 rows per group; a tap boundary falls on a multiple of 4 rows
+  // since C % 4 == 0, so the thread's 4 channels never straddle one).  C % 32 == 0
+  // keeps the whole warp on one tap; C = 16 puts two taps in one row group.
+  int c = 32 * rg + 4 * qq, ti, tj;
+  {
+    const int tap = c / C;
+    c -= tap * C;
+    ti = tap / kw;
+    tj = tap - ti * kw;
+  }
   // store-phase coordinates: row = tid >> 3 (channel), segment = tid & 7 (8 pixels)
   const int srow = tid >> 3, sseg = tid & 7;
   const int64_t kk0 = k0 + sseg * 8;
@@ -286,9 +294,9 @@ __global__ void __launch_bounds__(256) im2col_k16_tiled_kernel(const __grid_cons
     for (int h = 0; h < 2; ++h) {
       v[h] = make_float4(0.f, 0.f, 0.f, 0.f);
       const int ih = ih0[h] + ti * dh, iw = iw0[h] + tj * dw;
-      if (pin[h] && static_cast<unsigned>(ih) < static_cast<unsigned>(H) &&
+      if (pin[h] && ti < kh && static_cast<unsigned>(ih) < static_cast<unsigned>(H) &&
           static_cast<unsigned>(iw) < static_cast<unsigned>(W))
-        v[h] = __ldg(reinterpret_cast<const float4*>(base[h] + (ih * shs + iw * sws + c0)));
+        v[h] = __ldg(reinterpret_cast<const float4*>(base[h] + (ih * shs + iw * sws + c)));
     }
     const __half2 h0 = __floats2half2_rn(v[0].x * sc, v[1].x * sc);
     const __half2 h1 = __floats2half2_rn(v[0].y * sc, v[1].y * sc);
@@ -301,16 +309,18 @@ __global__ void __launch_bounds__(256) im2col_k16_tiled_kernel(const __grid_cons
     tw[96] = *reinterpret_cast<const uint32_t*>(&h3);
     __syncthreads();  // (double-buffered T: one barrier per group)
     const uint4 w = *reinterpret_cast<const uint4*>(Tb + srow * 32 + rsw);
-    if (kk0 + 8 <= cols) {
-      __stcs(reinterpret_cast<uint4*>(out), w);
-    } else {
-      const __half* hv = reinterpret_cast<const __half*>(&w);
-      for (int e = 0; e < 8 && kk0 + e < cols; ++e) out[e] = hv[e];
+    if (32 * rg + srow < rows) {  // the last group of d % 32 != 0 (C = 16 with an odd tap count)
+      if (kk0 + 8 <= cols) {
+        __stcs(reinterpret_cast<uint4*>(out), w);
+      } else {
+        const __half* hv = reinterpret_cast<const __half*>(&w);
+        for (int e = 0; e < 8 && kk0 + e < cols; ++e) out[e] = hv[e];
+      }
     }
     out += 32 * ld;
-    c0 += 32;
-    if (c0 == C) {
-      c0 = 0;
+    c += 32;
+    while (c >= C) {
+      c -= C;
       if (++tj == kw) {
         tj = 0;
         ++ti;
@@ -553,7 +563,7 @@ bool k16_rows_ok(const dpk_im2col_job& j) {
 
 bool k16_tiled_ok(const dpk_im2col_job& j) {
   const dpk_operand& o = j.x;
-  return o.kind == DPK_OPND_IM2COL_TAPMAJOR && o.sc == 1 && o.C % 32 == 0 && !o.bias_row &&
+  return o.kind == DPK_OPND_IM2COL_TAPMAJOR && o.sc == 1 && o.C % 8 == 0 && !o.bias_row &&
          (reinterpret_cast<uintptr_t>(o.data) & 15) == 0 && o.sn % 4 == 0 && o.shs % 4 == 0 && o.sws % 4 == 0 &&
          static_cast<int64_t>(o.H) * o.shs + static_cast<int64_t>(o.W) * o.sws + o.C < (int64_t{1} << 31) &&
          o.cols < (int64_t{1} << 31);

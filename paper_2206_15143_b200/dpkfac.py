@@ -134,9 +134,9 @@ class _Layer:
             if self.amax is None:
                 self.amax = torch.zeros(1, dtype=torch.int32, device=x.device)
             return ops.operand_im2col_f16(op, self.nhwc16), (op, self.nhwc16, self.amax)
-        # fp16 patches: the tiled transpose kernel (NHWC, C % 32 == 0) or the row-staged
+        # fp16 patches: the tiled transpose kernel (NHWC, C % 8 == 0) or the row-staged
         # one (small-C stems, output width a multiple of 8); else the fp32 paths
-        tiled = tap and nhwc and x.shape[1] % 32 == 0 and not self.has_bias and x.data_ptr() % 16 == 0
+        tiled = tap and nhwc and x.shape[1] % 8 == 0 and not self.has_bias and x.data_ptr() % 16 == 0
         if f16 and (tiled or op.OW % 8 == 0):
             # feature-major fp16 patches: half the HBM bytes, tcgen05 kind::f16 SYRK
             ld = (op.cols + 7) // 8 * 8

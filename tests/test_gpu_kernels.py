@@ -486,7 +486,15 @@ def test_syrk_taps_dilated_matches_unfold(shape, k, s, p, dil):
                                                            # row-staged fp16 kernel: stem-like 7x7/2
                                                            # (OW % 8 == 0), NHWC and NCHW, bias row
                                                            ((2, 3, 32, 32), 7, 2, 3, False, True),
-                                                           ((2, 3, 32, 32), 7, 2, 3, True, False)])
+                                                           ((2, 3, 32, 32), 7, 2, 3, True, False),
+                                                           # tiled kernel with C % 32 != 0: two taps per
+                                                           # 32-row group (C = 16, odd tap count -> a
+                                                           # half group), C = 24 / 8 / 48 runs
+                                                           ((4, 16, 32, 32), 3, 1, 1, False, True),
+                                                           ((3, 16, 15, 17), 3, 2, 1, False, True),
+                                                           ((2, 24, 9, 9), 3, 1, 1, False, True),
+                                                           ((2, 8, 10, 10), 5, 1, 2, False, True),
+                                                           ((2, 48, 7, 7), 3, 1, 1, False, True)])
 def test_f16_patches_and_syrk_match_unfold(shape, k, s, p, bias, channels_last):
     from paper_2206_15143_b200 import ops
     rng = np.random.default_rng(sum(shape) + k)
