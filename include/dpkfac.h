@@ -371,6 +371,9 @@ const char* dpk_last_error(void);
 unsigned long long dpk_launch_count(void);
 /* debug: %globaltimer checkpoints (ns) of CTA 0 of the last GEMM launched with DPK_DEBUG_TS=1 */
 int dpk_debug_timestamps(unsigned long long* host16);
+/* debug: per work unit of CTA 0 of that launch (first 64 units), 5 checkpoints each: MMA
+ * start, first chunk ready, last MMA issued, epilogue start, epilogue end */
+int dpk_debug_unit_timestamps(unsigned long long* host320);
 
 #ifdef __cplusplus
 }

@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdpkfac.so")
+LIB_PATH = os.environ.get("DPK_LIB_PATH") or os.path.join(_HERE, "libdpkfac.so")  # override: experiments only
 
 DPK_OK, DPK_EARG, DPK_ESHAPE, DPK_ECUDA, DPK_ENOSPACE = 0, 1, 2, 3, 4
 DPK_PREC_TF32, DPK_PREC_TF32_TRUNC, DPK_PREC_3XTF32 = 1, 2, 3
@@ -123,6 +123,7 @@ _SIGNATURES = [
     ("dpk_last_error", C.c_char_p, []),
     ("dpk_launch_count", C.c_ulonglong, []),
     ("dpk_debug_timestamps", C.c_int, [C.POINTER(C.c_ulonglong)]),
+    ("dpk_debug_unit_timestamps", C.c_int, [C.POINTER(C.c_ulonglong)]),
 ]
 
 EXPORTED = tuple(name for name, _, _ in _SIGNATURES)

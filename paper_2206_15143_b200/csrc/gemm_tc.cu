@@ -130,6 +130,18 @@ struct Batch {
 static_assert(sizeof(Batch) <= 32764, "kernel parameter space is 32764 bytes");
 
 __device__ unsigned long long g_dbg_ts[16];
+// per-unit checkpoints of CTA 0 (DPK_DEBUG_TS=1): [it][0] MMA start (accumulator free),
+// [1] first chunk's data ready, [2] last MMA issued, [3] epilogue start (accumulator
+// full), [4] epilogue end
+constexpr int DBG_UNITS = 64;
+__device__ unsigned long long g_dbg_unit[DBG_UNITS][5];
+__device__ __forceinline__ void dbg_unit(const Batch& bt, int it, int slot) {
+  if (bt.debug_ts && blockIdx.x == 0 && it < DBG_UNITS) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_dbg_unit[it][slot] = t;
+  }
+}
 
 __device__ __forceinline__ void dbg_ts(const Batch& bt, int slot) {
   if (bt.debug_ts && blockIdx.x == 0) {
@@ -990,16 +1002,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         else
           mbar_wait(tempty_bar(acc), ((it >> 1) & 1) ^ 1);
         tc_fence_after();
+        dbg_unit(bt, it, 0);
         const uint32_t d = tmem_base + acc * ACC_COLS;
         int kc0, kc1;
         chunk_range<CG>(P, tm, tn, split, kc0, kc1);
         for (int kc = kc0; kc < kc1; ++kc) {
           if (CG == 2) {
-            mbar_wait_cluster(full_bar(stage), phase);  // producers of both CTAs (TMA forwarded)
+            // producers of both CTAs (TMA forwarded) arrive with release.cluster: acquire at
+            // cluster scope (emits an L1 invalidate per chunk).  Producer-free launches only
+            // see TMA complete_tx (async proxy, like the MMA) and the leader's own
+            // expect_tx: the CTA-scope wait suffices and keeps the MMA issue loop short.
+            if (prods)
+              mbar_wait_cluster(full_bar(stage), phase);
+            else
+              mbar_wait(full_bar(stage), phase);
           } else {
             mbar_wait(full_bar(stage), phase);
             mbar_wait(tma_bar(stage), phase);
           }
+          if (kc == kc0) dbg_unit(bt, it, 1);
           tc_fence_after();
           const uint32_t sa = base + stage * C::STAGE_BYTES;
           const uint32_t sb = skip_b ? sa : sa + TILE_BYTES;
@@ -1048,6 +1069,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
             phase ^= 1;
           }
         }
+        dbg_unit(bt, it, 2);
         if (CG == 2)
           mma_commit_pair(tfull_bar(acc), 0x3);
         else
@@ -1068,6 +1090,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
       const Problem& P = bt.p[pi];
       const int acc = it & 1;
       mbar_wait(tfull_bar(acc), (it >> 1) & 1);
+      if (threadIdx.x == 0) dbg_unit(bt, it, 3);
       if (it == 0 && threadIdx.x == 0) dbg_ts(bt, 9);
       tc_fence_after();
       const uint32_t taddr = tmem_base + acc * ACC_COLS + (static_cast<uint32_t>(warp * 32) << 16);
@@ -1094,6 +1117,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         if (it == 0 && c == 0 && threadIdx.x == 0) dbg_ts(bt, 11);
       }
       tc_fence_before();
+      if (threadIdx.x == 0) dbg_unit(bt, it, 4);
       if (CG == 2 && !leader)
         mbar_arrive_remote(mapa_shared(tempty_bar(acc), 0));
       else
@@ -2176,6 +2200,12 @@ int dpk_conv_im2col_syrk_ema(const dpk_factor_job* jobs, int n_jobs, void* works
 // Debug: %globaltimer checkpoints (ns) of CTA 0 of the last GEMM launch made with
 // DPK_DEBUG_TS=1: start, set-up done, TMA done, gathers done, MMA done,
 // epilogue unit 0 / last unit done, final barrier, TMEM released.
+extern "C" int dpk_debug_unit_timestamps(unsigned long long* host320) {
+  if (!host320) return DPK_EARG;
+  return dpk::cuda_status(cudaMemcpyFromSymbol(host320, dpk::g_dbg_unit, sizeof(unsigned long long) * 320),
+                          "cudaMemcpyFromSymbol");
+}
+
 extern "C" int dpk_debug_timestamps(unsigned long long* host16) {
   if (!host16) return DPK_EARG;
   return dpk::cuda_status(cudaMemcpyFromSymbol(host16, dpk::g_dbg_ts, sizeof(unsigned long long) * 16),
