@@ -982,11 +982,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
     if (ptid == 0) dbg_ts(bt, 3);
   } else if (warp == MMA_WARP) {
     // =============================== MMA issuer (CG=2: the leader CTA only)
-    if (lane == 0 && leader) {
+    // The whole warp runs the loop (every value warp-uniform, so descriptors live in
+    // uniform registers); each tcgen05.mma / commit is issued by one elected lane.
+    if (leader) {
       int stage = 0;
       uint32_t phase = 0;
       for (int it = 0;; ++it) {
-        const int u = ring_take(it, true);
+        const int u = ring_take(it, lane == 0);
         if (u < 0) break;
         int pi, tm, tn, tile, split;
         decode_unit(bt, u, pi, tm, tn, tile, split);
@@ -1006,6 +1008,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         const uint32_t d = tmem_base + acc * ACC_COLS;
         int kc0, kc1;
         chunk_range<CG>(P, tm, tn, split, kc0, kc1);
+        // stage-0 descriptors of the A / B tiles and the per-UMMA_K step (16-byte units):
+        // K-major +32 B along the 128 B row; MN-major the next 8-row k group (+1024 B),
+        // two groups for a 16-deep f16 step (+2048 B, 64-wide M/N blocks 8 KB apart)
+        const uint32_t sa0 = base, sb0 = skip_b ? base : base + TILE_BYTES;
+        const uint64_t da0 = a_mn ? (f16 ? sdesc_mnmajor_sw128_16b(sa0, 8192) : sdesc_mnmajor_sw128(sa0, 4096))
+                                  : sdesc_kmajor_sw128(sa0);
+        const uint64_t db0 = b_mn ? (f16 ? sdesc_mnmajor_sw128_16b(sb0, 8192) : sdesc_mnmajor_sw128(sb0, 4096))
+                                  : sdesc_kmajor_sw128(sb0);
+        const uint32_t astep = a_mn ? (f16 ? 128u : 64u) : 2u;
+        const uint32_t bstep = b_mn ? (f16 ? 128u : 64u) : 2u;
         for (int kc = kc0; kc < kc1; ++kc) {
           if (CG == 2) {
             // producers of both CTAs (TMA forwarded) arrive with release.cluster: acquire at
@@ -1022,41 +1034,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
           }
           if (kc == kc0) dbg_unit(bt, it, 1);
           tc_fence_after();
-          const uint32_t sa = base + stage * C::STAGE_BYTES;
-          const uint32_t sb = skip_b ? sa : sa + TILE_BYTES;
-          const uint32_t sal = sa + 2 * TILE_BYTES;
-          const uint32_t sbl = skip_b ? sal : sa + 3 * TILE_BYTES;
+          // descriptors: the unit's stage-0 descriptors plus the address-field offset
+          // (16-byte units; the field never carries: every operand lies below 256 KB)
+          const uint64_t so = static_cast<uint64_t>(stage) * (C::STAGE_BYTES >> 4);
+          const uint64_t da = da0 + so, db = db0 + so;
+          const uint32_t accum0 = kc > kc0 ? 1u : 0u;
+          if (NPASS == 1 && f16) {  // UMMA_K = 16 fp16 = the same 32 B step
 #pragma unroll
-          for (int s = 0; s < BK / 8; ++s) {  // UMMA_K = 8 for tf32 (16 for f16: the same 32 B)
-            // K-major: +32 B along the 128 B row; MN-major: next 8-row k group (+1024 B),
-            // two groups for a 16-deep f16 step (+2048 B, 64-wide M/N blocks 8 KB apart)
-            const uint32_t mstep = f16 ? 2048u : 1024u;
-            const uint32_t oa = a_mn ? s * mstep : s * 32;
-            const uint32_t ob = b_mn ? s * mstep : s * 32;
-            const uint64_t da = a_mn ? (f16 ? sdesc_mnmajor_sw128_16b(sa + oa, 8192) : sdesc_mnmajor_sw128(sa + oa, 4096))
-                                     : sdesc_kmajor_sw128(sa + oa);
-            const uint64_t db = b_mn ? (f16 ? sdesc_mnmajor_sw128_16b(sb + ob, 8192) : sdesc_mnmajor_sw128(sb + ob, 4096))
-                                     : sdesc_kmajor_sw128(sb + ob);
-            const uint32_t accum = (kc > kc0 || s > 0) ? 1u : 0u;
-            if (NPASS == 1 && f16) {  // UMMA_K = 16 fp16 = the same 32 B step
+            for (int s = 0; s < BK / 8; ++s) {
               if (CG == 2)
-                mma_f16_pair(d, da, db, idesc, accum);
+                mma_f16_pair(d, da + s * astep, db + s * bstep, idesc, s > 0 ? 1u : accum0);
               else
-                mma_f16(d, da, db, idesc, accum);
-            } else if (CG == 2) {
-              mma_tf32_pair(d, da, db, idesc, accum);
-            } else {
-              mma_tf32(d, da, db, idesc, accum);
+                mma_f16(d, da + s * astep, db + s * bstep, idesc, s > 0 ? 1u : accum0);
             }
-            if (NPASS == 3) {
-              const uint64_t dbl = b_mn ? sdesc_mnmajor_sw128(sbl + ob, 4096) : sdesc_kmajor_sw128(sbl + ob);
-              const uint64_t dal = a_mn ? sdesc_mnmajor_sw128(sal + oa, 4096) : sdesc_kmajor_sw128(sal + oa);
-              if (CG == 2) {
-                mma_tf32_pair(d, da, dbl, idesc, 1u);
-                mma_tf32_pair(d, dal, db, idesc, 1u);
-              } else {
-                mma_tf32(d, da, dbl, idesc, 1u);
-                mma_tf32(d, dal, db, idesc, 1u);
+          } else {
+#pragma unroll
+            for (int s = 0; s < BK / 8; ++s) {  // UMMA_K = 8 for tf32
+              const uint64_t das = da + s * astep, dbs = db + s * bstep;
+              if (CG == 2)
+                mma_tf32_pair(d, das, dbs, idesc, s > 0 ? 1u : accum0);
+              else
+                mma_tf32(d, das, dbs, idesc, s > 0 ? 1u : accum0);
+              if (NPASS == 3) {  // + hi*lo + lo*hi (the low parts sit 2 / 3 tiles further)
+                const uint64_t dal = das + 2 * (TILE_BYTES >> 4);
+                const uint64_t dbl = skip_b ? dal : dbs + 2 * (TILE_BYTES >> 4);
+                if (CG == 2) {
+                  mma_tf32_pair(d, das, dbl, idesc, 1u);
+                  mma_tf32_pair(d, dal, dbs, idesc, 1u);
+                } else {
+                  mma_tf32(d, das, dbl, idesc, 1u);
+                  mma_tf32(d, dal, dbs, idesc, 1u);
+                }
               }
             }
           }
@@ -1075,7 +1083,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         else
           mma_commit(tfull_bar(acc));
       }
-      dbg_ts(bt, 4);
+      if (lane == 0) dbg_ts(bt, 4);
     }
   } else if (warp < EPI_WARPS) {
     // =============================== epilogue (warps 0-3, thread = tile row)
