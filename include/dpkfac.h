@@ -25,7 +25,12 @@
  *     round-to-nearest TF32 operands; DPK_PREC_TF32_TRUNC feeds the raw fp32
  *     bits (the tensor core truncates to TF32, no conversion pass);
  *     DPK_PREC_3XTF32 splits every operand into hi + lo TF32 parts and
- *     accumulates hi*hi + hi*lo + lo*hi (fp32-grade).
+ *     accumulates hi*hi + hi*lo + lo*hi (fp32-grade).  DPK_PREC_3XF16 (SPD inverse and
+ *     preconditioning entry points) is the same 3-product split with fp16 hi / lo
+ *     parts (11-bit significands: hi + lo carry 22 bits like 3xTF32) on kind::f16
+ *     MMAs at twice the tf32 rate; each operand is first scaled by an exact power of
+ *     two from its measured amax (largest magnitude in [2^14, 2^15)) and the epilogue
+ *     undoes both scales exactly.
  */
 #ifndef DPKFAC_H_
 #define DPKFAC_H_
@@ -47,7 +52,7 @@ enum {
   DPK_ENOSPACE = 4  /* workspace too small */
 };
 
-enum { DPK_PREC_TF32 = 1, DPK_PREC_TF32_TRUNC = 2, DPK_PREC_3XTF32 = 3 };
+enum { DPK_PREC_TF32 = 1, DPK_PREC_TF32_TRUNC = 2, DPK_PREC_3XTF32 = 3, DPK_PREC_3XF16 = 4 };
 
 /* info codes written to device info words */
 enum {

@@ -14,7 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DPK_LIB_PATH") or os.path.join(_HERE, "libdpkfac.so")  # override: experiments only
 
 DPK_OK, DPK_EARG, DPK_ESHAPE, DPK_ECUDA, DPK_ENOSPACE = 0, 1, 2, 3, 4
-DPK_PREC_TF32, DPK_PREC_TF32_TRUNC, DPK_PREC_3XTF32 = 1, 2, 3
+DPK_PREC_TF32, DPK_PREC_TF32_TRUNC, DPK_PREC_3XTF32, DPK_PREC_3XF16 = 1, 2, 3, 4
 INFO_OK, INFO_TRACE, INFO_NOT_SPD_A, INFO_NOT_SPD_G, INFO_EIG_DENOM, INFO_NONFINITE = range(6)
 OPND_ROWS_K, OPND_ROWS_MN, OPND_IM2COL, OPND_IM2COL_TAPMAJOR, OPND_ROWS_K_F16, OPND_IM2COL_TAPMAJOR_F16 = 0, 1, 2, 3, 4, 5
 

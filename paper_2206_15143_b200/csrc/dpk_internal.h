@@ -54,6 +54,10 @@ struct GemmSpec {
   // optional: device float bits of amax|operand| -- the operands hold X * 2^-e
   // (fp16 prescaled patches), the epilogue multiplies alpha by 2^(2e)
   const int32_t* alpha_amax = nullptr;
+  // DPK_PREC_3XF16: device float bits of amax|A| and amax|B| (required); the
+  // operands are split as x * 2^-e = hi + lo in fp16 and alpha gets 2^(e_a + e_b)
+  const int32_t* amax_a = nullptr;
+  const int32_t* amax_b = nullptr;
 };
 
 // Power-of-two prescale of fp16 patch operands (dpk_im2col_job.amax): the largest
@@ -173,6 +177,8 @@ inline void key_spec(std::string& k, const GemmSpec& g) {
   key_put(k, g.tri_b);
   key_put(k, g.lower_only);
   key_put(k, g.alpha_amax);
+  key_put(k, g.amax_a);
+  key_put(k, g.amax_b);
 }
 
 // Kernel launch with optional programmatic dependent launch (DPK_PDL=1) and an

@@ -128,6 +128,18 @@ __device__ __forceinline__ uint64_t sdesc_kmajor_sw128(uint32_t saddr) {
   return d;
 }
 
+// Shared-memory matrix descriptor: K-major operand, 64-byte swizzle, rows of
+// 64 B (32 fp16), 8-row core groups 512 B apart (SBO) -- the 3xF16 hi / lo tiles.
+__device__ __forceinline__ uint64_t sdesc_kmajor_sw64(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(1) << 16;            // LBO (unused for swizzled K-major)
+  d |= static_cast<uint64_t>(512 >> 4) << 32;     // SBO = 512 B
+  d |= static_cast<uint64_t>(1) << 46;            // descriptor version (Blackwell)
+  d |= static_cast<uint64_t>(4) << 61;            // SWIZZLE_64B
+  return d;
+}
+
 // Shared-memory matrix descriptor: MN-major tf32 operand.  The only MN-major
 // layout tcgen05 accepts for 32-bit types is SWIZZLE_128B_BASE32B (32-byte
 // chunks of each 128 B row XOR'd with the row index mod 4; TMA's

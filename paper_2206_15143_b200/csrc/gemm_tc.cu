@@ -29,6 +29,7 @@
 // kfac.py:107-125 (alpha/beta epilogue), precondition_inverse / _eigen
 // kfac.py:165-191 (plain and eigen-divide epilogues).
 #include <cuda.h>  // CUtensorMap / enums only; the encoder is fetched through the runtime
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -76,8 +77,10 @@ static_assert(NPROD % 8 == 0, "im2col chunk sharing needs NPROD % 8 == 0");
 // a K chunk is 64 output pixels; per 64-row group (one tap, 64 channels) one TMA
 // im2col box of 64 pixels x 128 B lands as the MN-major SWIZZLE_128B kind::f16
 // operand (8 KB, two per 128-row tile).
+// TMA_ROWS_MN_PLAIN (3xF16 only): an MN-major fp32 tile without swizzle, k rows of
+// 128 floats (512 B) -- read by the producer warps, never by the MMA.
 enum { TMA_NONE = 0, TMA_ROWS_K = 1, TMA_ROWS_MN = 2, TMA_SLAB = 3, TMA_IM2COL = 4, TMA_ROWS_MN3 = 5, TMA_TAPS = 6,
-       TMA_ROWS_K16 = 7, TMA_IM2COL16 = 8 };
+       TMA_ROWS_K16 = 7, TMA_IM2COL16 = 8, TMA_ROWS_MN_PLAIN = 9 };
 __host__ __device__ __forceinline__ bool tma_mn(int kind) {
   return kind == TMA_ROWS_MN || kind == TMA_IM2COL || kind == TMA_ROWS_MN3 || kind == TMA_TAPS ||
          kind == TMA_IM2COL16;
@@ -103,6 +106,8 @@ struct alignas(64) Problem {
   int64_t ldo;
   int64_t ldc;
   const int32_t* alpha_amax;  // optional: prescaled fp16 operands, alpha *= 2^(2e)
+  const int32_t* amax_a;      // 3xF16: operand amax bits (scales 2^-e_a, 2^-e_b; alpha *= 2^(e_a+e_b))
+  const int32_t* amax_b;
   float alpha, beta, gamma;
   int M, N;
   int symmetric, same_ab, epi;  // symmetric: 1 lower tiles + mirror, 2 lower tiles only
@@ -431,6 +436,105 @@ __device__ __forceinline__ void convert_tile(uint8_t* tile, uint8_t* tile_lo, in
   }
 }
 
+// ---- 3xF16: fp32 -> (hi, lo) fp16 parts of x * sc in K-major SWIZZLE_64B tiles
+// (128 rows x 32 k halves = 64 B rows, 8 KB each; hi at dst, lo at dst + 8 KB).
+// Element (r, k) of such a tile sits at byte (r>>3)*512 + (r&7)*64 + (((k>>3) ^ ((r>>1)&3)) << 4) + (k&7)*2.
+__device__ __forceinline__ uint32_t sw64_chunk_offset(int row, int c) {
+  return static_cast<uint32_t>((row >> 3) * 512 + (row & 7) * 64 + ((c ^ ((row >> 1) & 3)) << 4));
+}
+__device__ __forceinline__ void split_f16(float x, float sc, __half& hi, __half& lo) {
+  const float v = x * sc;
+  hi = __float2half_rn(v);
+  lo = __float2half_rn(v - __half2float(hi));
+}
+constexpr uint32_t F16_TILE = 8192;  // one 128 x 32 fp16 tile
+
+// manual (gathered) operand tasks straight into the fp16 tiles: task (row, fp32 chunk q)
+// = k 4q..4q+3 = halves 0-3 or 4-7 of 16-byte chunk q/2
+__device__ __forceinline__ void store_tasks_f16x3(const dpk_operand& o, int ptid, uint8_t* dst, float sc,
+                                                  const float4 (&v)[NTASK]) {
+  const bool kf = kfast(o);
+#pragma unroll
+  for (int j = 0; j < NTASK; ++j) {
+    int row, chunk;
+    if (!task_row_chunk(kf, ptid, j, row, chunk)) continue;
+    const uint32_t off = sw64_chunk_offset(row, chunk >> 1) + (chunk & 1) * 8;
+    const float x[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+    __half h[4], l[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) split_f16(x[e], sc, h[e], l[e]);
+    __half2 h01 = __halves2half2(h[0], h[1]), h23 = __halves2half2(h[2], h[3]);
+    __half2 l01 = __halves2half2(l[0], l[1]), l23 = __halves2half2(l[2], l[3]);
+    *reinterpret_cast<uint2*>(dst + off) =
+        make_uint2(*reinterpret_cast<uint32_t*>(&h01), *reinterpret_cast<uint32_t*>(&h23));
+    *reinterpret_cast<uint2*>(dst + F16_TILE + off) =
+        make_uint2(*reinterpret_cast<uint32_t*>(&l01), *reinterpret_cast<uint32_t*>(&l23));
+  }
+}
+
+// 8 scaled values -> the 16-byte hi chunk and the 16-byte lo chunk (packed
+// conversions: cvt.rn.f16x2.f32 twice and f16x2 -> f32 once per pair)
+__device__ __forceinline__ void split8_f16(const float (&x)[8], float sc, uint4& hi, uint4& lo) {
+  uint32_t h[4], l[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 v = make_float2(x[2 * e] * sc, x[2 * e + 1] * sc);
+    const __half2 hh = __float22half2_rn(v);
+    const float2 back = __half22float2(hh);
+    const __half2 ll = __float22half2_rn(make_float2(v.x - back.x, v.y - back.y));
+    h[e] = *reinterpret_cast<const uint32_t*>(&hh);
+    l[e] = *reinterpret_cast<const uint32_t*>(&ll);
+  }
+  hi = make_uint4(h[0], h[1], h[2], h[3]);
+  lo = make_uint4(l[0], l[1], l[2], l[3]);
+}
+
+// a TMA-landed fp32 tile (K-major SW128, or TMA_ROWS_MN_PLAIN) -> hi / lo fp16 tiles.
+// K-major: thread -> (row r = idx & 127, 16-byte chunk c = idx >> 7), two 16-byte
+// loads (consecutive lanes take consecutive rows: conflict-free with the SW128
+// swizzle).  MN plain: thread -> (row pair 2p, 2p+1, chunk c), eight 8-byte loads of
+// the pair (a warp reads 256 contiguous bytes per k).  All loads are issued before
+// the conversions.
+__device__ __forceinline__ void convert_tile_f16x3(const uint8_t* src, bool mn_plain, uint8_t* dst, float sc,
+                                                   int ptid) {
+  if (mn_plain) {
+    for (int idx = ptid; idx < 64 * 4; idx += NPROD) {
+      const int p = idx & 63, c = idx >> 6;
+      const float2* f = reinterpret_cast<const float2*>(src) + p + (8 * c) * 64;  // k row = 128 floats = 64 float2
+      float2 y[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) y[e] = f[e * 64];
+      float x0[8], x1[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        x0[e] = y[e].x;
+        x1[e] = y[e].y;
+      }
+      uint4 h, l;
+      split8_f16(x0, sc, h, l);
+      uint32_t off = sw64_chunk_offset(2 * p, c);
+      *reinterpret_cast<uint4*>(dst + off) = h;
+      *reinterpret_cast<uint4*>(dst + F16_TILE + off) = l;
+      split8_f16(x1, sc, h, l);
+      off = sw64_chunk_offset(2 * p + 1, c);
+      *reinterpret_cast<uint4*>(dst + off) = h;
+      *reinterpret_cast<uint4*>(dst + F16_TILE + off) = l;
+    }
+    return;
+  }
+  for (int idx = ptid; idx < 128 * 4; idx += NPROD) {
+    const int r = idx & 127, c = idx >> 7;
+    const float4 a = *reinterpret_cast<const float4*>(src + sw128_offset(r, 2 * c));
+    const float4 b = *reinterpret_cast<const float4*>(src + sw128_offset(r, 2 * c + 1));
+    const float x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint4 h, l;
+    split8_f16(x, sc, h, l);
+    const uint32_t off = sw64_chunk_offset(r, c);
+    *reinterpret_cast<uint4*>(dst + off) = h;
+    *reinterpret_cast<uint4*>(dst + F16_TILE + off) = l;
+  }
+}
+
 // Bytes one TMA'd operand tile delivers.  Box loads always count their full
 // (zero-filled) size; im2col tiles skip 32-row groups past the operand's rows
 // (those smem rows only feed accumulator rows the epilogue never stores).
@@ -458,6 +562,8 @@ __device__ __forceinline__ void issue_tma(int kind, const CUtensorMap* map, cons
     ld2(dst, kc * BK, row0);
   } else if (kind == TMA_ROWS_K16) {
     ld2(dst, kc * 2 * BK, row0);
+  } else if (kind == TMA_ROWS_MN_PLAIN) {  // one {128 rows, 32 k} box, k rows of 512 B
+    ld2(dst, row0, kc * BK);
   } else if (kind == TMA_ROWS_MN) {
 #pragma unroll
     for (int b = 0; b < BM / 32; ++b) ld2(dst + b * 4096, row0 + 32 * b, kc * BK);
@@ -616,6 +722,8 @@ __device__ __forceinline__ Epi load_epi(const Problem& P, int tile, int split) {
   e.ldt = pin(P.ldt);
   e.alpha = pin(P.alpha);
   if (P.alpha_amax) e.alpha = ldexpf(e.alpha, 2 * prescale_exponent(__ldg(P.alpha_amax)));
+  if (P.amax_a)
+    e.alpha = ldexpf(e.alpha, prescale_exponent(__ldg(P.amax_a)) + prescale_exponent(__ldg(P.amax_b)));
   e.beta = pin(P.beta);
   e.gamma = pin(P.gamma);
   e.M = pin(P.M);
@@ -743,6 +851,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   // TMA'd tiles need a pass before the MMA only for the 3xTF32 low parts: in RN
   // mode the tensor map's TFLOAT32 data type rounds during the copy itself.
   constexpr bool CONVERT = (NPASS == 3);
+  // NPASS == 3 with RN set: 3xF16 (fp16 hi / lo parts of the scaled operands, kind::f16)
+  constexpr bool F16X3 = (NPASS == 3 && RN);
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -931,6 +1041,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
       const bool mB = CG == 1 && !skip_b && !tB;
       const bool cA = tA;  // 3-pass: TMA'd tiles get their low part computed here
       const bool cB = tB;
+      // 3xF16: the operands' exact power-of-two scales
+      const float sc_a = F16X3 ? ldexpf(1.0f, -prescale_exponent(__ldg(P.amax_a))) : 1.0f;
+      const float sc_b = F16X3 ? ldexpf(1.0f, -prescale_exponent(__ldg(P.amax_b))) : 1.0f;
       RowTask ta[NTASK], tb[NTASK];
       if (mA) setup_tasks(P.a, tm * UT, ptid, ta);
       if (mB) setup_tasks(P.b, tn * UT, ptid, tb);
@@ -948,15 +1061,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         }
         mbar_wait(empty_bar(stage), phase ^ 1);
         uint8_t* st = gbase + stage * C::STAGE_BYTES;
-        if (mA) store_tasks<NPASS, RN>(P.a, ptid, st, st + 2 * TILE_BYTES, va);
-        if (mB) store_tasks<NPASS, RN>(P.b, ptid, st + TILE_BYTES, st + 3 * TILE_BYTES, vb);
+        if (F16X3) {  // hi / lo fp16 tiles of A in slot 2, of B in slot 3
+          if (mA) store_tasks_f16x3(P.a, ptid, st + 2 * TILE_BYTES, sc_a, va);
+          if (mB) store_tasks_f16x3(P.b, ptid, st + 3 * TILE_BYTES, sc_b, vb);
+        } else {
+          if (mA) store_tasks<NPASS, RN>(P.a, ptid, st, st + 2 * TILE_BYTES, va);
+          if (mB) store_tasks<NPASS, RN>(P.b, ptid, st + TILE_BYTES, st + 3 * TILE_BYTES, vb);
+        }
         // CG=2 with a conversion: the leader's MMA cannot see this CTA's TMA
         // barrier, so the producers forward its completion with their arrival
         // (without one, the loads signal the leader's full barrier directly)
         if (CONVERT && (cA || cB)) {
           mbar_wait(tma_bar(stage), phase);
-          if (cA) convert_tile<NPASS>(st, st + 2 * TILE_BYTES, ptid);
-          if (cB) convert_tile<NPASS>(st + TILE_BYTES, st + 3 * TILE_BYTES, ptid);
+          if (F16X3) {
+            if (cA) convert_tile_f16x3(st, P.tma_a == TMA_ROWS_MN_PLAIN, st + 2 * TILE_BYTES, sc_a, ptid);
+            if (cB) convert_tile_f16x3(st + TILE_BYTES, P.tma_b == TMA_ROWS_MN_PLAIN, st + 3 * TILE_BYTES, sc_b, ptid);
+          } else {
+            if (cA) convert_tile<NPASS>(st, st + 2 * TILE_BYTES, ptid);
+            if (cB) convert_tile<NPASS>(st + TILE_BYTES, st + 3 * TILE_BYTES, ptid);
+          }
         }
         // one arrival per producer warp (measured faster than a named barrier +
         // a single elected arrival: the warps' cluster-scope releases overlap)
@@ -997,7 +1120,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         const int a_mn = tma_mn(P.tma_a);
         const int b_mn = skip_b ? a_mn : tma_mn(P.tma_b);
         const bool f16 = tma_f16(P.tma_a);  // SYRK on fp16 operands (both sides)
-        const uint32_t idesc = f16 ? idesc_f16(UT, UT, a_mn, b_mn) : idesc_tf32(UT, UT, a_mn, b_mn);
+        const uint32_t idesc = F16X3 ? idesc_f16(UT, UT)  // K-major fp16 hi / lo tiles
+                               : f16 ? idesc_f16(UT, UT, a_mn, b_mn) : idesc_tf32(UT, UT, a_mn, b_mn);
         const int acc = it & 1;
         if (CG == 2)
           mbar_wait_cluster(tempty_bar(acc), ((it >> 1) & 1) ^ 1);
@@ -1039,7 +1163,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
           const uint64_t so = static_cast<uint64_t>(stage) * (C::STAGE_BYTES >> 4);
           const uint64_t da = da0 + so, db = db0 + so;
           const uint32_t accum0 = kc > kc0 ? 1u : 0u;
-          if (NPASS == 1 && f16) {  // UMMA_K = 16 fp16 = the same 32 B step
+          if (F16X3) {  // hi*hi + hi*lo + lo*hi on the SW64 fp16 tiles: 2 x (K = 16) per chunk
+            const uint32_t s0 = base + stage * C::STAGE_BYTES;
+            const uint64_t ah = sdesc_kmajor_sw64(s0 + 2 * TILE_BYTES), al = ah + (F16_TILE >> 4);
+            const uint64_t bh = skip_b ? ah : sdesc_kmajor_sw64(s0 + 3 * TILE_BYTES), bl = bh + (F16_TILE >> 4);
+#pragma unroll
+            for (int s = 0; s < 2; ++s) {
+              const uint32_t o = 2u * s;  // +32 B along the 64 B row
+              if (CG == 2) {
+                mma_f16_pair(d, ah + o, bh + o, idesc, s > 0 ? 1u : accum0);
+                mma_f16_pair(d, ah + o, bl + o, idesc, 1u);
+                mma_f16_pair(d, al + o, bh + o, idesc, 1u);
+              } else {
+                mma_f16(d, ah + o, bh + o, idesc, s > 0 ? 1u : accum0);
+                mma_f16(d, ah + o, bl + o, idesc, 1u);
+                mma_f16(d, al + o, bh + o, idesc, 1u);
+              }
+            }
+          } else if (NPASS == 1 && f16) {  // UMMA_K = 16 fp16 = the same 32 B step
 #pragma unroll
             for (int s = 0; s < BK / 8; ++s) {
               if (CG == 2)
@@ -1161,6 +1302,38 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
   }
 }
 
+// ------------------------------------------------------------------ 3xF16 operand scales
+// amax|op| of every operand view of a 3xF16 call (the float bits, int-compared:
+// order-preserving for non-negative floats; NaN sorts above inf and propagates).
+// Elements a triangular operand never contributes (TRI_LOWER / TRI_UPPER) are
+// skipped -- they may hold anything -- and a bias row counts as 1.
+constexpr int AMAX_MAXV = 256;
+struct AmaxView {
+  const float* data;
+  int64_t ld, cols;
+  int rows, mn, tri, bias;
+  int32_t* out;
+};
+struct AmaxBatch {
+  int n;
+  AmaxView v[AMAX_MAXV];
+};
+__global__ void __launch_bounds__(256) operand_amax_kernel(const __grid_constant__ AmaxBatch b) {
+  const AmaxView& V = b.v[blockIdx.y];
+  const int64_t R = V.mn ? V.cols : V.rows, C = V.mn ? V.rows : V.cols;  // memory rows / columns
+  int m = (V.bias && blockIdx.x == 0 && threadIdx.x == 0) ? __float_as_int(1.0f) : 0;
+  for (int64_t i = blockIdx.x; i < R; i += gridDim.x) {
+    const float* row = V.data + i * V.ld;
+    for (int64_t j = threadIdx.x; j < C; j += blockDim.x) {
+      const int64_t r = V.mn ? j : i, k = V.mn ? i : j;  // operand (row, k)
+      if ((V.tri == TRI_LOWER && k > r) || (V.tri == TRI_UPPER && k < r)) continue;
+      m = max(m, __float_as_int(__ldg(row + j)) & 0x7fffffff);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0) atomicMax(V.out, m);
+}
+
 // ------------------------------------------------------------------ split-K reduction
 // One CTA per (split tile, 8-row slab): 256 threads, each owns 4 consecutive
 // columns of one row, sums the partials in split order (deterministic) and
@@ -1175,6 +1348,8 @@ struct RedJob {
   float* out_t;
   int64_t ldo, ldc, ldt;
   const int32_t* alpha_amax;
+  const int32_t* amax_a;
+  const int32_t* amax_b;
   float alpha, beta, gamma;
   int M, N, symmetric, epi, tiles_n, splits;
   int ut;          // unit tile edge (128 or 256)
@@ -1242,7 +1417,8 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const __grid_constan
   for (int q = 0; q < 4; ++q) acc[q] = (acc4[0][q] + acc4[1][q]) + (acc4[2][q] + acc4[3][q]);
   const int gn = gn0 + tx;
   const float vc = (J.epi == EPI_EIGDIV && gn < J.N) ? fmaxf(J.vcol[gn], 0.0f) : 0.0f;
-  const float alpha = J.alpha_amax ? ldexpf(J.alpha, 2 * prescale_exponent(__ldg(J.alpha_amax))) : J.alpha;
+  float alpha = J.alpha_amax ? ldexpf(J.alpha, 2 * prescale_exponent(__ldg(J.alpha_amax))) : J.alpha;
+  if (J.amax_a) alpha = ldexpf(alpha, prescale_exponent(__ldg(J.amax_a)) + prescale_exponent(__ldg(J.amax_b)));
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int r = ty + 8 * q;
@@ -1416,6 +1592,15 @@ int plan_tma_2d(const dpk_operand& o, CUtensorMap* m, bool rn) {
     return encode(m, 2, o.data, dims, strides, box, rn, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) ? TMA_ROWS_MN : TMA_NONE;
   }
   return TMA_NONE;
+}
+
+// 3xF16 MN-major operand for the producers: one {128 rows, 32 k} box, no swizzle.
+int plan_tma_mn_plain(const dpk_operand& o, CUtensorMap* m) {
+  if (tma_disabled() || o.bias_row || o.rows < 1 || !aligned16(o.data) || (o.ld * 4) % 16 != 0) return TMA_NONE;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(o.rows), static_cast<cuuint64_t>(o.cols)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(o.ld) * 4};
+  const cuuint32_t box[2] = {BM, BK};
+  return encode(m, 2, o.data, dims, strides, box, false, CU_TENSOR_MAP_SWIZZLE_NONE) ? TMA_ROWS_MN_PLAIN : TMA_NONE;
 }
 
 // NCHW 1x1/s1 capture (or any conv grad_output): per sample a contiguous C x HW
@@ -1649,6 +1834,18 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
     P.ldc = j.ldc;
     P.alpha = j.alpha;
     P.alpha_amax = specs[i].alpha_amax;
+    P.amax_a = specs[i].amax_a;
+    P.amax_b = specs[i].amax_b;
+    if (precision == DPK_PREC_3XF16) {
+      auto plain = [](const dpk_operand& o) { return o.kind == DPK_OPND_ROWS_K || o.kind == DPK_OPND_ROWS_MN; };
+      if (!P.amax_a || !P.amax_b || !plain(j.a) || !plain(j.b) || specs[i].alpha_amax) {
+        set_error("dpk_gemm: 3xF16 needs amax slots for both operands and plain row / column views");
+        return DPK_EARG;
+      }
+    } else if (P.amax_a || P.amax_b) {
+      set_error("dpk_gemm: operand amax slots are a 3xF16 feature");
+      return DPK_EARG;
+    }
     P.beta = j.beta;
     P.M = operand_rows(j.a);
     P.N = operand_rows(j.b);
@@ -1722,6 +1919,7 @@ int make_plan(const GemmSpec* specs, int n, Plan& plan, bool with_maps, int prec
         if (o.kind == DPK_OPND_IM2COL_TAPMAJOR_F16) return plan_tma_im2col16(o, m) ? TMA_IM2COL16 : TMA_NONE;
         if (o.kind == DPK_OPND_IM2COL_TAPMAJOR)
           return (im2col_eligible(o) && plan_tma_im2col(o, m, rn)) ? TMA_IM2COL : TMA_NONE;
+        if (precision == DPK_PREC_3XF16 && o.kind == DPK_OPND_ROWS_MN) return plan_tma_mn_plain(o, m);
         return plan_tma_2d(o, m, rn);
       };
       P.tma_a = plan_one(j.a, &P.tmap_a);
@@ -1842,6 +2040,8 @@ int launch_reduce(const std::vector<Problem>& probs, int ut, cudaStream_t st) {
     J.ldt = P.ldt;
     J.alpha = P.alpha;
     J.alpha_amax = P.alpha_amax;
+    J.amax_a = P.amax_a;
+    J.amax_b = P.amax_b;
     J.beta = P.beta;
     J.gamma = P.gamma;
     J.M = P.M;
@@ -1901,6 +2101,7 @@ int launch_batch(const Batch& bt, cudaStream_t st) {
 template <int CG>
 int launch_group(const Batch& bt, int precision, cudaStream_t st) {
   if (precision == DPK_PREC_3XTF32) return launch_batch<3, false, CG>(bt, st);
+  if (precision == DPK_PREC_3XF16) return launch_batch<3, true, CG>(bt, st);  // RN slot = the fp16 split
   if (precision == DPK_PREC_TF32_TRUNC) return launch_batch<1, false, CG>(bt, st);
   return launch_batch<1, true, CG>(bt, st);
 }
@@ -1940,7 +2141,7 @@ int run_plan(Plan& plan, void* ws, size_t ws_bytes, int precision, cudaStream_t 
     bt.sched = sched;
     bt.dynamic = dynamic_schedule() ? 1 : 0;
     // producer warps are needed for 3xTF32 low parts and for operands TMA cannot address
-    bt.producers = precision == DPK_PREC_3XTF32 ? 1 : 0;
+    bt.producers = (precision == DPK_PREC_3XTF32 || precision == DPK_PREC_3XF16) ? 1 : 0;
     for (int i = 0; i < cnt; ++i)
       if (bt.p[i].tma_a == TMA_NONE || bt.p[i].tma_b == TMA_NONE) bt.producers = 1;
     if (units == 0) continue;
@@ -2028,6 +2229,43 @@ size_t gemm_workspace_bytes(const GemmSpec* specs, int n) {
   return ws;
 }
 
+// 3xF16: two amax slots per job at the END of the caller's workspace
+size_t amax_region(int n) { return align_up(static_cast<size_t>(n) * 8, 1024); }
+
+int launch_operand_amax(const GemmSpec* specs, int n, int32_t* slots, cudaStream_t st) {
+  int rc = cuda_status(cudaMemsetAsync(slots, 0, static_cast<size_t>(n) * 8, st), "cudaMemsetAsync(amax slots)");
+  if (rc) return rc;
+  thread_local AmaxBatch ab;
+  ab.n = 0;
+  int64_t most = 1;
+  auto flush = [&]() -> int {
+    if (ab.n == 0) return DPK_OK;
+    const int gx = static_cast<int>(std::min<int64_t>(most, 2 * num_sms()));
+    operand_amax_kernel<<<dim3(gx, ab.n), 256, 0, st>>>(ab);
+    note_launch();
+    ab.n = 0;
+    most = 1;
+    return cuda_status(cudaGetLastError(), "operand_amax_kernel launch");
+  };
+  for (int i = 0; i < n; ++i) {
+    for (int side = 0; side < 2; ++side) {
+      const dpk_operand& o = side ? specs[i].job.b : specs[i].job.a;
+      AmaxView& v = ab.v[ab.n++];
+      v.data = o.data;
+      v.ld = o.ld;
+      v.cols = o.cols;
+      v.rows = o.rows;
+      v.mn = o.kind == DPK_OPND_ROWS_MN;
+      v.tri = side ? specs[i].tri_b : specs[i].tri_a;
+      v.bias = o.bias_row;
+      v.out = slots + 2 * i + side;
+      most = std::max<int64_t>(most, v.mn ? o.cols : o.rows);
+      if (ab.n == AMAX_MAXV && (rc = flush())) return rc;
+    }
+  }
+  return flush();
+}
+
 size_t gemm_workspace_bytes_uncached(const GemmSpec* specs, int n) {
   std::vector<GemmSpec> g1, g2;
   partition_cg(specs, n, g1, g2);
@@ -2038,9 +2276,10 @@ size_t gemm_workspace_bytes_uncached(const GemmSpec* specs, int n) {
   if (!g2.empty() && make_plan(g2.data(), static_cast<int>(g2.size()), plan, false, DPK_PREC_TF32, 2) == DPK_OK)
     w2 = plan.ws_bytes;
   // both unit shapes present: the single-CTA plan runs concurrently with the pair
-  // plan in its own workspace region behind the pair plan's
-  if (w1 && w2 && concurrent_plans()) return align_up(w2, 1024) + w1;
-  return std::max(w1, w2);
+  // plan in its own workspace region behind the pair plan's; the 3xF16 operand
+  // scales take the last bytes
+  if (w1 && w2 && concurrent_plans()) return align_up(w2, 1024) + w1 + amax_region(n);
+  return std::max(w1, w2) + amax_region(n);
 }
 
 int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int precision, cudaStream_t st,
@@ -2050,12 +2289,32 @@ int gemm_launch(const GemmSpec* specs, int n, void* ws, size_t ws_bytes, int pre
     set_error("dpk_gemm: bad job list");
     return DPK_EARG;
   }
-  if (precision != DPK_PREC_TF32 && precision != DPK_PREC_TF32_TRUNC && precision != DPK_PREC_3XTF32) {
-    set_error("dpk_gemm: precision must be DPK_PREC_TF32, DPK_PREC_TF32_TRUNC or DPK_PREC_3XTF32");
+  if (precision != DPK_PREC_TF32 && precision != DPK_PREC_TF32_TRUNC && precision != DPK_PREC_3XTF32 &&
+      precision != DPK_PREC_3XF16) {
+    set_error("dpk_gemm: precision must be DPK_PREC_TF32, DPK_PREC_TF32_TRUNC, DPK_PREC_3XTF32 or DPK_PREC_3XF16");
     return DPK_EARG;
   }
   // small 3xTF32 groups (deep SPD-recursion rounds): latency path on CUDA cores
   if (simt_eligible(specs, n, precision)) return simt_gemm_launch(specs, n, st);
+  // 3xF16: every operand's amax into the slots at the end of the workspace (one launch)
+  thread_local std::vector<GemmSpec> scaled;
+  if (precision == DPK_PREC_3XF16 && !specs[0].amax_a) {
+    const size_t reg = amax_region(n);
+    if (ws == nullptr || ws_bytes < reg + SCHED_BYTES) {
+      set_error("dpk_gemm: workspace too small for the 3xF16 operand scales");
+      return DPK_ENOSPACE;
+    }
+    ws_bytes -= reg;
+    int32_t* slots = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + ws_bytes);
+    scaled.assign(specs, specs + n);
+    for (int i = 0; i < n; ++i) {
+      scaled[i].amax_a = slots + 2 * i;
+      scaled[i].amax_b = slots + 2 * i + 1;
+    }
+    const int rc = launch_operand_amax(scaled.data(), n, slots, st);
+    if (rc) return rc;
+    specs = scaled.data();
+  }
   if (zero_counters && ws != nullptr && ws_bytes >= SCHED_BYTES) {
     const int rc = cuda_status(cudaMemsetAsync(ws, 0, SCHED_BYTES, st), "cudaMemsetAsync(scheduler counters)");
     if (rc) return rc;

@@ -840,6 +840,19 @@ bool spd_trace() {
   return on == 1;
 }
 
+// Rounds of at least this many useful FMAs run as 3xF16 (fp16 hi / lo parts on
+// kind::f16 MMAs, twice the 3xTF32 rate; one extra amax launch): DPK_SPD_F16_MIN,
+// 0 = every tensor-core round, negative = never.
+double spd_f16_min_fma() {
+  static double v = -2.0;
+  if (v == -2.0) {
+    const char* e = getenv("DPK_SPD_F16_MIN");
+    v = e ? atof(e) : -1.0;
+    if (v < 0.0) v = 1e300;
+  }
+  return v;
+}
+
 double spec_fma(const GemmSpec& g) {
   const double M = g.job.a.rows, N = g.job.b.rows, K = static_cast<double>(g.job.a.cols);
   double f = M * N * K;
@@ -1218,8 +1231,10 @@ int run_lockstep(const SpdPlan& plan, const std::vector<int>& grp, char* gemm_ws
         if (rc) return rc;
         counters_zeroed = true;
       }
-      int rc = dpk::gemm_launch(g.data(), static_cast<int>(g.size()), gemm_ws, gemm_bytes, DPK_PREC_3XTF32, st,
-                                false);
+      double fma = 0.0;
+      for (auto& x : g) fma += dpk::spec_fma(x);
+      int rc = dpk::gemm_launch(g.data(), static_cast<int>(g.size()), gemm_ws, gemm_bytes,
+                                fma >= dpk::spd_f16_min_fma() ? DPK_PREC_3XF16 : DPK_PREC_3XTF32, st, false);
       if (rc) return rc;
     }
     if (trace) {

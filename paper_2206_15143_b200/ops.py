@@ -16,7 +16,8 @@ import torch
 from . import _lib as L
 from .errors import ArgumentError, ShapeError
 
-PRECISIONS = {"tf32": L.DPK_PREC_TF32, "tf32-trunc": L.DPK_PREC_TF32_TRUNC, "3xtf32": L.DPK_PREC_3XTF32}
+PRECISIONS = {"tf32": L.DPK_PREC_TF32, "tf32-trunc": L.DPK_PREC_TF32_TRUNC, "3xtf32": L.DPK_PREC_3XTF32,
+              "3xf16": L.DPK_PREC_3XF16}
 
 
 def lib():

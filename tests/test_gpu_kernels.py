@@ -162,6 +162,37 @@ def test_gemm_all_operand_majors(m, n, k):
         assert rel(N(out), 0.5 * a @ b.T - 2.0 * c) <= 1e-5
 
 
+@pytest.mark.parametrize("scale", [1.0, 3e4, 1e-6])
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (130, 70, 45), (512, 785, 300), (1000, 2049, 33), (600, 600, 700)])
+def test_gemm_3xf16_all_operand_majors(m, n, k, scale):
+    """DPK_PREC_3XF16: fp16 hi / lo parts of the amax-prescaled operands on kind::f16
+    MMAs -- fp32-grade like 3xTF32 for operands far above the fp16 range (3e4 squared
+    and beyond 65504 after the product) and far below it (1e-6), single CTAs and
+    CTA pairs, every operand major (MN-major tiles go through the plain TMA map)."""
+    from paper_2206_15143_b200 import _lib as L, ops
+    rng = np.random.default_rng(m + n + k + 1)
+    a = rng.standard_normal((m, k)) * scale
+    a[:, :1] *= 1e-3  # graded columns: small entries keep their relative accuracy
+    b = rng.standard_normal((n, k)) * scale
+    c = rng.standard_normal((m, n)) * scale * scale
+    at, bt, ct = T(a), T(b), T(c)
+    atr, btr = T(a.T), T(b.T)
+    for a_op, b_op in [(ops.operand_rows_k(at), ops.operand_rows_k(bt)),
+                       (ops.operand_rows_mn(atr), ops.operand_rows_k(bt)),
+                       (ops.operand_rows_k(at), ops.operand_rows_mn(btr)),
+                       (ops.operand_rows_mn(atr), ops.operand_rows_mn(btr))]:
+        out = torch.full((m, n), float("nan"), device=dev())
+        j = L.GemmJob()
+        j.a, j.b = a_op, b_op
+        j.out, j.ldo = out.data_ptr(), n
+        j.cin, j.ldc = ct.data_ptr(), n
+        j.alpha, j.beta = 0.5, -2.0
+        ops.gemm([j], "3xf16")
+        torch.cuda.synchronize()
+        want = 0.5 * a.astype(np.float32).astype(np.float64) @ b.astype(np.float32).astype(np.float64).T - 2.0 * c
+        assert rel(N(out), want) <= 1e-5, rel(N(out), want)
+
+
 # ---------------------------------------------------------------- K3 damped inverse
 def _spd(rng, n, cond_floor=1e-2):
     b = rng.standard_normal((n, n + 3))
@@ -219,11 +250,13 @@ def test_factored_spd_inverse_matches_oracle(n, shift):
     assert rel(X.T @ X, want) <= max(1e-4, 20 * cond * 2.0 ** -23), (rel(X.T @ X, want), cond)
 
 
+@pytest.mark.parametrize("precision", ["3xtf32", "3xf16"])
 @pytest.mark.parametrize("din,dout,gamma", [(785, 512, 0.03), (65, 9, 0.002), (2049, 1000, 0.002), (3, 2, 0.03),
                                             (4608, 512, 0.002)])
-def test_precondition_factored_matches_oracle(din, dout, gamma):
+def test_precondition_factored_matches_oracle(din, dout, gamma, precision):
     """dpk_precond_factored with the factors of dpk_chol_factor_inv_batched equals the
-    reference's G_inv @ grad @ A_inv (kfac.precondition_inverse, kfac.py:165-171)."""
+    reference's G_inv @ grad @ A_inv (kfac.precondition_inverse, kfac.py:165-171), in
+    both fp32-grade precisions (3xF16: amax-prescaled fp16 hi / lo parts)."""
     from paper_2206_15143_b200 import _lib as L, ops
     rng = np.random.default_rng(din * 3 + dout)
     x = np.maximum(rng.standard_normal((din, 256)), 0)
@@ -240,7 +273,7 @@ def test_precondition_factored_matches_oracle(din, dout, gamma):
     ops.chol_factor_inv([ops.spd_factor_job(ta, xa, shifts[0], info, L.INFO_NOT_SPD_A),
                          ops.spd_factor_job(tg, xg, shifts[1], info, L.INFO_NOT_SPD_G)])
     gr, out, tmp = T(grad), torch.empty(dout, din, device=dev()), torch.empty(dout, din, device=dev())
-    ops.precondition_factored([ops.precond_factor_job(gr, xa, xg, out, tmp)], "3xtf32")
+    ops.precondition_factored([ops.precond_factor_job(gr, xa, xg, out, tmp)], precision)
     torch.cuda.synchronize()
     assert int(info.item()) == 0
     want = K.precondition_inverse(a, gg, grad, gamma)
