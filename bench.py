@@ -66,6 +66,7 @@ def parse():
     ap.add_argument("--max-classes", type=int, default=None, help="tuning: DPKFAC.MAX_CLASSES")
     ap.add_argument("--class-ratio", type=float, default=None, help="tuning: DPKFAC.CLASS_RATIO")
     ap.add_argument("--factor-order", type=int, default=None, help="tuning: DPKFAC.FACTOR_ORDER")
+    ap.add_argument("--side-cap", type=int, default=None, help="tuning: DPKFAC.SIDE_CAP")
     ap.add_argument("--comm-overlap", action="store_true",
                     help="bucketed gradient reduce-scatter launched from the backward hooks (e2e)")
     ap.add_argument("--bucket-mb", type=float, default=16.0)
@@ -277,7 +278,7 @@ def run_ours(args, rank, world, local_rank):
                 overlap=not args.no_overlap, early=False, algorithm=args.algorithm, im2col=args.im2col,
                 comm_overlap=args.comm_overlap, bucket_mb=args.bucket_mb)  # captures are replayed below; e2e turns early on
     for attr, val in (("MAX_CLASSES", args.max_classes), ("CLASS_RATIO", args.class_ratio),
-                      ("FACTOR_ORDER", args.factor_order)):
+                      ("FACTOR_ORDER", args.factor_order), ("SIDE_CAP", args.side_cap)):
         if val is not None:
             setattr(kf, attr, val)
     opt = torch.optim.SGD(model.parameters(), lr=1e-3, momentum=0.9)

@@ -372,6 +372,10 @@ int dpk_unpack_owner_major_klclip(const dpk_segment* segs, int n_segs, const flo
 /* Library / device introspection. */
 const char* dpk_version(void);
 const char* dpk_last_error(void);
+/* Host-thread setting: tensor-core launches made from this thread use at most `sms`
+ * SMs (0 = all).  DPKFAC caps the throughput-bound size classes so the latency-bound
+ * inversion chain of the largest factors keeps SMs free while they run. */
+int dpk_set_launch_cap(int sms);
 /* number of kernels this library has launched in the process (bench evidence) */
 unsigned long long dpk_launch_count(void);
 /* debug: %globaltimer checkpoints (ns) of CTA 0 of the last GEMM launched with DPK_DEBUG_TS=1 */

@@ -124,6 +124,7 @@ _SIGNATURES = [
     ("dpk_launch_count", C.c_ulonglong, []),
     ("dpk_debug_timestamps", C.c_int, [C.POINTER(C.c_ulonglong)]),
     ("dpk_debug_unit_timestamps", C.c_int, [C.POINTER(C.c_ulonglong)]),
+    ("dpk_set_launch_cap", C.c_int, [C.c_int]),
 ]
 
 EXPORTED = tuple(name for name, _, _ in _SIGNATURES)

@@ -80,6 +80,7 @@ size_t gemm_workspace_bytes(const GemmSpec* specs, int n);
 // tcgen05 launches made by this thread use at most `cap` SMs (0 = all): a
 // concurrent stream keeps the rest (spd_inv.cu's right-looking trailing updates)
 void set_grid_cap_override(int cap);
+int grid_cap_override();
 // split-K depth of the tcgen05 plans made by this thread (units per SM; 0 = default 3)
 int units_per_sm();
 int split_min_chunks();

@@ -1499,6 +1499,7 @@ thread_local int g_cap_override = 0;
 thread_local int g_units_override = 0;
 }  // namespace
 void set_grid_cap_override(int cap) { g_cap_override = cap; }
+int grid_cap_override() { return g_cap_override; }
 int units_per_sm_override() { return g_units_override; }
 void set_units_per_sm_override(int u) { g_units_override = u; }
 // split-K target: about this many units per worker.  Callers set it per context
@@ -2467,6 +2468,15 @@ int dpk_conv_im2col_syrk_ema(const dpk_factor_job* jobs, int n_jobs, void* works
 // Debug: %globaltimer checkpoints (ns) of CTA 0 of the last GEMM launch made with
 // DPK_DEBUG_TS=1: start, set-up done, TMA done, gathers done, MMA done,
 // epilogue unit 0 / last unit done, final barrier, TMEM released.
+extern "C" int dpk_set_launch_cap(int sms) {
+  if (sms < 0) {
+    dpk::set_error("dpk_set_launch_cap: sms must be >= 0");
+    return DPK_EARG;
+  }
+  dpk::set_grid_cap_override(sms);
+  return DPK_OK;
+}
+
 extern "C" int dpk_debug_unit_timestamps(unsigned long long* host320) {
   if (!host320) return DPK_EARG;
   return dpk::cuda_status(cudaMemcpyFromSymbol(host320, dpk::g_dbg_unit, sizeof(unsigned long long) * 320),

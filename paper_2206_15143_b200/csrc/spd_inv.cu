@@ -1287,8 +1287,11 @@ int run_cached_graph(const SpdReq* jobs, int n_jobs, void* workspace, size_t ws_
   int dev = 0;
   int rc = cuda_status(cudaGetDevice(&dev), "cudaGetDevice");
   if (rc) return rc;
-  std::vector<char> key(sizeof(SpdReq) * n_jobs + sizeof(void*) + sizeof(size_t) + sizeof(int));
+  std::vector<char> key(sizeof(SpdReq) * n_jobs + sizeof(void*) + sizeof(size_t) + 2 * sizeof(int));
   char* k = key.data();
+  const int capv = grid_cap_override();  // the captured launches bake the grid size in
+  std::memcpy(k, &capv, sizeof(int));
+  k += sizeof(int);
   std::memcpy(k, jobs, sizeof(SpdReq) * n_jobs);
   k += sizeof(SpdReq) * n_jobs;
   std::memcpy(k, &workspace, sizeof(void*));

@@ -252,6 +252,11 @@ class DPKFAC:
     MAX_CLASSES = 3      # size classes of the overlapped step (the last on the caller's stream)
     CLASS_RATIO = 0.6    # a new class starts below this fraction of the current class's largest
     FACTOR_ORDER = 0     # see step(): gating of the classes' factor SYRKs
+    SIDE_CAP = 112       # >0: tensor-core launches of every class but the largest use at most
+                         # this many SMs while the largest class holds a long inversion chain
+    SIDE_CAP_MIN_DIM = 3072  # ... i.e. a factor of at least this dimension (measured: ResNet-50
+                             # 7.41 -> 7.20 ms, Inception-v4 11.60 -> 11.38, N=2 5.40 -> 5.30;
+                             # DenseNet-201, largest factor 1921, 10.22 -> 10.44 with a cap)
 
     def __init__(self, model: nn.Module, *, gamma: float = 0.03, xi: float = 0.95, inv_type: str = "eigen",
                  f_freq: int = 1, k_freq: int = 1,
@@ -632,6 +637,7 @@ class DPKFAC:
         owned = self.owned
         classes = self._size_classes(owned)
         sides, rest = classes[:-1], classes[-1]
+        self._long_chain = len(classes) > 1 and max(max(ly.d_in, ly.d_out) for ly in classes[0]) >= self.SIDE_CAP_MIN_DIM
         main = torch.cuda.current_stream(self.device)
         self._mark("start")
         # the larger size classes (long, latency-bound inversion chains) run their
@@ -649,7 +655,7 @@ class DPKFAC:
             st.wait_event(ev0)
             if gate is not None:
                 st.wait_event(gate)
-            with torch.cuda.stream(st):
+            with torch.cuda.stream(st), self._cap(ci):
                 self._factor_stage(cls, t, f_up, st)
                 done = st.record_event()
                 if self.FACTOR_ORDER == 2 or (self.FACTOR_ORDER == 1 and ci == 0):
@@ -670,18 +676,19 @@ class DPKFAC:
             st.wait_event(ev_rs)
             if self._launched.get(ci) == t:
                 st.wait_event(self._early_done[ci])
-            with torch.cuda.stream(st):
+            with torch.cuda.stream(st), self._cap(ci):
                 self._precondition_stage(cls)
         # (1) Kronecker factors + running average: one grouped tcgen05 launch
         if gate is not None:
             main.wait_event(gate)
-        self._factor_stage(rest, t, f_up, None)
-        self._mark("factors")
-        # (2) inverses / eigendecompositions
-        self._inverse_stage(rest, t, k_up)
-        self._mark("inversion")
-        # (5) precondition owned layers, one grouped launch per GEMM phase
-        self._precondition_stage(rest)
+        with self._cap(len(sides)):
+            self._factor_stage(rest, t, f_up, None)
+            self._mark("factors")
+            # (2) inverses / eigendecompositions
+            self._inverse_stage(rest, t, k_up)
+            self._mark("inversion")
+            # (5) precondition owned layers, one grouped launch per GEMM phase
+            self._precondition_stage(rest)
         for st in streams:
             main.wait_stream(st)
         self._mark("precondition")
@@ -739,7 +746,7 @@ class DPKFAC:
                 self._early_st = {}
             st = self._early_st.setdefault(ci, torch.cuda.Stream(self.device, priority=0))
         st.wait_stream(torch.cuda.current_stream(self.device))  # the captures' producer stream
-        with torch.cuda.stream(st):
+        with torch.cuda.stream(st), self._cap(ci):
             self._factor_stage(cls, t, t % h.f_freq == 0, st)
             self._inverse_stage(cls, t, t % h.k_freq == 0)
         self._early_done = getattr(self, "_early_done", {})
@@ -747,6 +754,12 @@ class DPKFAC:
         self._launched[ci] = t
 
     # ------------------------------------------------------------ stages
+    def _cap(self, ci: int):
+        """SM cap for size class ci's launches (class 0, the largest, is never capped;
+        the others only while class 0 holds a factor of SIDE_CAP_MIN_DIM or more)."""
+        on = ci > 0 and self.overlap and self.SIDE_CAP > 0 and getattr(self, "_long_chain", False)
+        return ops.launch_cap(self.SIDE_CAP if on else 0)
+
     def _side_streams(self, n):
         if self._side is None:
             self._side = []

@@ -48,6 +48,22 @@ class Workspace:
         return buf.data_ptr()
 
 
+class launch_cap:
+    """Context manager: tensor-core launches issued from this thread inside the block
+    use at most ``sms`` SMs (0 = all)."""
+
+    def __init__(self, sms: int):
+        self.sms = int(sms)
+
+    def __enter__(self):
+        L.check(lib().dpk_set_launch_cap(self.sms), "dpk_set_launch_cap")
+        return self
+
+    def __exit__(self, *exc):
+        lib().dpk_set_launch_cap(0)
+        return False
+
+
 def precision_code(precision: str) -> int:
     try:
         return PRECISIONS[precision]
