@@ -331,6 +331,275 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) spd_leaf_kernel(const __grid_
     }
 }
 
+// ---- tensor-core leaf (TRI mode, n <= 128): the same fused right-looking Cholesky +
+// L^-1 sweep, 8 columns per step, with the rank-8 updates of the trailing A block and
+// of the X rows below the panel as mma.sync m16n8k8 TF32 products in 3xTF32 form
+// (hi*hi + hi*lo + lo*hi: fp32-grade).  A and X live in registers as 16x8 accumulator
+// tiles (lower tiles only: 72 + 72, nine per warp, tile w + 16j of warp w); per step
+//   1. owners publish A's column block k..k+7 (Pan) and X's rows k..k+7 (XR);
+//   2. threads 0-127 / 128-255 each factor the 8x8 pivot block themselves and form a
+//      panel row L[i][k..k+7] = A[i][k..k+7] L_kk^-T (LP) / a column of the finished
+//      X rows L_kk^-1 XR (XRn);
+//   3. every warp updates its active tiles: A -= LP LP^T, X -= LP XRn, and copies
+//      the finished X rows.
+// 16 steps x 2 barriers; the SIMT leaf needs 32 x 2 and ~4x the instructions.
+constexpr int LM_THREADS = 512;
+constexpr int LM_PS = 12;    // Pan / LP row stride (floats): conflict-free fragment loads
+constexpr int LM_XS = 136;   // XR / XRn row stride
+__device__ __forceinline__ uint32_t lm_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ void lm_split(float x, uint32_t& hi, uint32_t& lo) {
+  hi = lm_tf32(x);
+  lo = lm_tf32(x - __uint_as_float(hi));
+}
+__device__ __forceinline__ void lm_mma(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                       uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// lower tile index -> (tile row tr: 16 rows, tile column tc: 8 columns), tc <= 2 tr + 1
+__device__ __forceinline__ void lm_tile(int i, int& tr, int& tc) {
+  int r = static_cast<int>((sqrtf(4.0f * i + 1.0f) - 1.0f) * 0.5f);
+  while ((r + 1) * (r + 2) <= i) ++r;
+  while (r * (r + 1) > i) --r;
+  tr = r;
+  tc = i - r * (r + 1);
+}
+
+__global__ void __launch_bounds__(LM_THREADS, 1) spd_leaf_mma_kernel(const __grid_constant__ LeafBatch b) {
+  __shared__ float Pan[128 * LM_PS];
+  __shared__ uint32_t LPh[128 * LM_PS], LPl[128 * LM_PS];     // panel rows, TF32 hi / lo
+  __shared__ float XR[8 * LM_XS];
+  __shared__ float XRn[8 * LM_XS];                            // finished X rows
+  __shared__ uint32_t XNh[8 * LM_XS], XNl[8 * LM_XS];         // -XRn, TF32 hi / lo
+  __shared__ int s_fail;
+  if (threadIdx.x == 0) s_fail = 0;
+  pdl_wait();
+  pdl_trigger();
+  const LeafJob& J = b.j[blockIdx.x];
+  const int n = J.n;
+  const float* src = J.src;
+  const int64_t lds = J.lds;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t4 = lane & 3;
+  // tiles j = 0..8 of this warp: global index w + 16 j; < 72 an A tile, else an X tile
+  float acc[9][4];
+  int ttr[9], ttc[9];
+#pragma unroll
+  for (int j = 0; j < 9; ++j) {
+    const int id = warp + 16 * j;
+    const bool isa = id < 72;
+    lm_tile(isa ? id : id - 72, ttr[j], ttc[j]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int r = 16 * ttr[j] + g + 8 * (e >> 1), c = 8 * ttc[j] + 2 * t4 + (e & 1);
+      float v = (r == c) ? 1.0f : 0.0f;
+      if (isa && r < n && c < n) v = __ldg(src + static_cast<int64_t>(r) * lds + c);
+      acc[j][e] = v;
+    }
+  }
+  for (int k = 0; k < 128; k += 8) {
+    const int kc = k >> 3;
+#ifdef DPK_LEAF_PROF
+    long long c0 = clock64();
+#endif
+    // ---- 1. publish column block kc of A (rows >= k) and X rows k..k+7
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+      const bool isa = warp + 16 * j < 72;
+      const int r0 = 16 * ttr[j];
+      if (isa && ttc[j] == kc && r0 + 15 >= k) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) Pan[(r0 + g + 8 * (e >> 1)) * LM_PS + 2 * t4 + (e & 1)] = acc[j][e];
+      }
+      if (!isa && r0 == (k & ~15) && ttc[j] <= kc) {
+        const bool h = (k >> 3) & 1;  // which 8-row half of the tile holds rows k..k+7
+        XR[g * LM_XS + 8 * ttc[j] + 2 * t4] = h ? acc[j][2] : acc[j][0];  // (no dynamic register index)
+        XR[g * LM_XS + 8 * ttc[j] + 2 * t4 + 1] = h ? acc[j][3] : acc[j][1];
+      }
+    }
+#ifdef DPK_LEAF_PROF
+    long long c1 = clock64();
+#endif
+    __syncthreads();
+#ifdef DPK_LEAF_PROF
+    long long c2 = clock64();
+#endif
+    // ---- 2. pivot block, panel rows, finished X rows
+    if (tid < 256) {
+      float L[8][8], inv[8];
+      bool ok = true;
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        float d = Pan[(k + jj) * LM_PS + jj];
+#pragma unroll
+        for (int q = 0; q < jj; ++q) d = fmaf(-L[jj][q], L[jj][q], d);
+        inv[jj] = rsqrtf(d);
+        ok = ok && d > 0.0f && isfinite(inv[jj]);
+#pragma unroll
+        for (int m = jj + 1; m < 8; ++m) {
+          float v = Pan[(k + m) * LM_PS + jj];
+#pragma unroll
+          for (int q = 0; q < jj; ++q) v = fmaf(-L[m][q], L[jj][q], v);
+          L[m][jj] = v * inv[jj];
+        }
+      }
+      if (!ok && tid == 0) s_fail = 1;
+      // Linv = L^-1 (lower): column c by forward substitution
+      float Li[8][8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          if (r < c) {
+            Li[r][c] = 0.0f;
+          } else if (r == c) {
+            Li[r][c] = inv[r];
+          } else {
+            float v = 0.0f;
+#pragma unroll
+            for (int q = c; q < r; ++q) v = fmaf(L[r][q], Li[q][c], v);
+            Li[r][c] = -v * inv[r];
+          }
+        }
+      }
+      if (tid < 128) {  // panel row i: L[i][k..k+7] = A[i][k..k+7] L_kk^-T (zero above the panel)
+        const int i = tid;
+        float a[8], o[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] = Pan[i * LM_PS + q];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          float v = 0.0f;
+#pragma unroll
+          for (int m = 0; m <= q; ++m) v = fmaf(a[m], Li[q][m], v);
+          o[q] = v;
+        }
+        const bool live = i >= k + 8;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          uint32_t hi, lo;
+          lm_split(live ? o[q] : 0.0f, hi, lo);
+          LPh[i * LM_PS + q] = hi;
+          LPl[i * LM_PS + q] = lo;
+        }
+      } else {  // finished X rows, column jc: XRn[a][jc] = sum_m Linv[a][m] XR[m][jc]
+        const int jc = tid - 128;
+        if (jc < k + 8) {
+          float xr[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) xr[q] = XR[q * LM_XS + jc];
+#pragma unroll
+          for (int a = 0; a < 8; ++a) {
+            float v = 0.0f;
+#pragma unroll
+            for (int m = 0; m <= a; ++m) v = fmaf(Li[a][m], xr[m], v);
+            XRn[a * LM_XS + jc] = v;
+            uint32_t hi, lo;
+            lm_split(-v, hi, lo);
+            XNh[a * LM_XS + jc] = hi;
+            XNl[a * LM_XS + jc] = lo;
+          }
+        }
+      }
+    }
+#ifdef DPK_LEAF_PROF
+    long long c3 = clock64();
+#endif
+    __syncthreads();
+#ifdef DPK_LEAF_PROF
+    long long c4 = clock64();
+#endif
+    if (s_fail) {  // a non-positive pivot: exactly where cho_factor raises
+      if (tid == 0 && J.info) *J.info = J.fail_code;
+      return;
+    }
+    // ---- 3. rank-8 updates on the tensor cores
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+      const bool isa = warp + 16 * j < 72;
+      const int r0 = 16 * ttr[j], c0 = 8 * ttc[j];
+      if (r0 + 15 < k + 8) continue;  // no row below the panel
+      if (isa ? (c0 + 7 < k + 8) : (ttc[j] > kc)) continue;  // finished A columns / X columns >= k+8
+      // A fragment: LP rows r0+g / r0+g+8, k-columns t4 / t4+4 (pre-split TF32 hi / lo)
+      const int ia = (r0 + g) * LM_PS + t4, ib = ia + 8 * LM_PS;
+      const uint32_t ah0 = LPh[ia], ah1 = LPh[ib], ah2 = LPh[ia + 4], ah3 = LPh[ib + 4];
+      const uint32_t al0 = LPl[ia], al1 = LPl[ib], al2 = LPl[ia + 4], al3 = LPl[ib + 4];
+      uint32_t bh0, bh1, bl0, bl1;  // B fragment: -LP^T (A update) or -XRn (X update)
+      if (isa) {
+        const int ic = (c0 + g) * LM_PS + t4;
+        bh0 = LPh[ic] ^ 0x80000000u;
+        bh1 = LPh[ic + 4] ^ 0x80000000u;
+        bl0 = LPl[ic] ^ 0x80000000u;
+        bl1 = LPl[ic + 4] ^ 0x80000000u;
+      } else {
+        const int ic = t4 * LM_XS + c0 + g;
+        bh0 = XNh[ic];
+        bh1 = XNh[ic + 4 * LM_XS];
+        bl0 = XNl[ic];
+        bl1 = XNl[ic + 4 * LM_XS];
+      }
+      lm_mma(acc[j], ah0, ah1, ah2, ah3, bh0, bh1);
+      lm_mma(acc[j], ah0, ah1, ah2, ah3, bl0, bl1);
+      lm_mma(acc[j], al0, al1, al2, al3, bh0, bh1);
+    }
+    // finished X rows k..k+7 into their tiles (their LP rows are zero: the mma left them)
+#pragma unroll
+    for (int j = 0; j < 9; ++j) {
+      if (warp + 16 * j < 72 || 16 * ttr[j] != (k & ~15) || ttc[j] > kc) continue;
+      const bool h = (k >> 3) & 1;
+      const float v0 = XRn[g * LM_XS + 8 * ttc[j] + 2 * t4], v1 = XRn[g * LM_XS + 8 * ttc[j] + 2 * t4 + 1];
+      acc[j][0] = h ? acc[j][0] : v0;
+      acc[j][1] = h ? acc[j][1] : v1;
+      acc[j][2] = h ? v0 : acc[j][2];
+      acc[j][3] = h ? v1 : acc[j][3];
+    }
+#ifdef DPK_LEAF_PROF
+    long long c5 = clock64();
+    if (blockIdx.x == 0 && (tid == 0 || tid == 511)) {
+      unsigned long long* gp = g_leaf_prof + (tid ? 6 : 0);
+      atomicAdd(gp + 0, c1 - c0); atomicAdd(gp + 1, c2 - c1); atomicAdd(gp + 2, c3 - c2);
+      atomicAdd(gp + 3, c4 - c3); atomicAdd(gp + 4, c5 - c4); atomicAdd(gp + 5, 1ull);
+    }
+#endif
+  }
+  // X = L^-1 (zero above the diagonal): the lower tiles; the rest of the block is zeroed
+  float* dst = J.dst;
+  const int64_t ldd = J.ldd;
+#pragma unroll
+  for (int j = 0; j < 9; ++j) {
+    if (warp + 16 * j < 72) continue;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int r = 16 * ttr[j] + g + 8 * (e >> 1), c = 8 * ttc[j] + 2 * t4 + (e & 1);
+      if (r < n && c < n) dst[static_cast<int64_t>(r) * ldd + c] = acc[j][e];
+    }
+  }
+  for (int e = tid; e < 128 * 128; e += LM_THREADS) {
+    const int r = e >> 7, c = e & 127;
+    if (r < n && c < n && (c >> 3) > 2 * (r >> 4) + 1) dst[static_cast<int64_t>(r) * ldd + c] = 0.0f;
+  }
+}
+
+// DPK_LEAF_MMA=1: the tensor-core leaf for TRI-mode leaves.  Parity-green but measured
+// slower than the SIMT leaf (~36 vs 27 us per 128 leaf): per step the redundant 8x8
+// pivot factor + inverse costs ~1600 cycles and the 432 legacy mma.sync TF32
+// instructions (3 per tile) ~1300-2400 cycles, against ~1200 cycles for a 4-column
+// SIMT step -- so it is off by default.
+bool leaf_mma_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DPK_LEAF_MMA");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
 template <int RB, int W>
 constexpr int leaf_smem_bytes() {
   return (4 * 16 * RB * W + 16 * RB * (16 * RB + 1)) * 4;  // 4 panels of N x W + the X^T X copy
@@ -817,8 +1086,14 @@ int launch_leaves(std::vector<LeafJob>& leaves, cudaStream_t st) {
       b.j[i] = leaves[first + i];
       maxn = std::max(maxn, b.j[i].n);
     }
+    bool tri = true;
+    for (int i = 0; i < cnt; ++i) tri = tri && b.j[i].full == 0;
     int rc;
-    if (maxn <= 32)
+    if (tri && maxn > 64 && leaf_mma_enabled()) {
+      rc = cuda_status(launch_k(spd_leaf_mma_kernel, dim3(cnt), dim3(LM_THREADS), 0, st, 1, b),
+                       "spd_leaf_mma_kernel launch");
+      note_launch();
+    } else if (maxn <= 32)
       rc = launch_leaf_w<2>(b, cnt, st);
     else if (maxn <= 64)
       rc = launch_leaf_w<4>(b, cnt, st);
