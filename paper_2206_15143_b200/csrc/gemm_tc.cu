@@ -535,6 +535,49 @@ __device__ __forceinline__ void convert_tile_f16x3(const uint8_t* src, bool mn_p
   }
 }
 
+// 3xTF32 low parts of both TMA-landed tiles of a stage (A at st, B at st + TILE_BYTES,
+// lows 2 tiles further): every load of the thread's 16-byte chunks is issued before
+// any is converted -- with six producer warps the pass is otherwise bound by the
+// shared-memory load latency (measured ~1150 cycles per chunk, more than the
+// single-CTA chunk's 12 MMAs).
+template <int J0, int NJ>
+__device__ __forceinline__ void convert_lo_part(uint8_t* st, bool cA, bool cB, int ptid) {
+  const uint4* ta = reinterpret_cast<const uint4*>(st);
+  const uint4* tb = reinterpret_cast<const uint4*>(st + TILE_BYTES);
+  uint4 va[NJ], vb[NJ];
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int i = ptid + NPROD * (J0 + j);
+    if (i < TILE_BYTES / 16) {
+      if (cA) va[j] = ta[i];
+      if (cB) vb[j] = tb[i];
+    }
+  }
+  auto lo4 = [](const uint4 v) {
+    const float x[4] = {__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z), __uint_as_float(v.w)};
+    uint32_t r[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) r[e] = __float_as_uint(x[e] - __uint_as_float(tf32_trunc_bits(x[e])));
+    return make_uint4(r[0], r[1], r[2], r[3]);
+  };
+  uint4* la = reinterpret_cast<uint4*>(st + 2 * TILE_BYTES);
+  uint4* lb = reinterpret_cast<uint4*>(st + 3 * TILE_BYTES);
+#pragma unroll
+  for (int j = 0; j < NJ; ++j) {
+    const int i = ptid + NPROD * (J0 + j);
+    if (i < TILE_BYTES / 16) {
+      if (cA) la[i] = lo4(va[j]);
+      if (cB) lb[i] = lo4(vb[j]);
+    }
+  }
+}
+__device__ __forceinline__ void convert_lo_pair(uint8_t* st, bool cA, bool cB, int ptid) {
+  constexpr int PER = (TILE_BYTES / 16 + NPROD - 1) / NPROD;  // chunks per thread per tile (6)
+  static_assert(PER == 6, "two batches of three");
+  convert_lo_part<0, 3>(st, cA, cB, ptid);
+  convert_lo_part<3, 3>(st, cA, cB, ptid);
+}
+
 // Bytes one TMA'd operand tile delivers.  Box loads always count their full
 // (zero-filled) size; im2col tiles skip 32-row groups past the operand's rows
 // (those smem rows only feed accumulator rows the epilogue never stores).
@@ -842,7 +885,10 @@ __device__ __forceinline__ void store_chunk(const Epi& e, bool diag, int gm0, in
 // 128 rows x 256 columns.  Producers of both CTAs arrive on the leader's full
 // barrier, both epilogues arrive on the leader's TMEM-empty barrier, and the
 // leader's commits multicast to both CTAs' stage-empty / TMEM-full barriers.
-template <int NPASS, bool RN, int CG>
+// GATHER=false: every operand of the launch is TMA-planned -- the producers' gather
+// path is compiled out (3xTF32 single-CTA launches then keep their conversion loop
+// free of the gather arrays' registers)
+template <int NPASS, bool RN, int CG, bool GATHER = true>
 __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_constant__ Batch bt) {
   using C = Cfg<NPASS>;
   constexpr int UT = 128 * CG;                  // unit tile edge (rows and columns)
@@ -1037,18 +1083,43 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
       const bool skip_b = P.same_ab && tm == tn;
       const bool tA = P.tma_a != TMA_NONE;
       const bool tB = !skip_b && P.tma_b != TMA_NONE;
-      const bool mA = CG == 1 && !tA;  // CG=2 problems are planned TMA-only
-      const bool mB = CG == 1 && !skip_b && !tB;
+      const bool mA = GATHER && CG == 1 && !tA;  // CG=2 problems are planned TMA-only
+      const bool mB = GATHER && CG == 1 && !skip_b && !tB;
       const bool cA = tA;  // 3-pass: TMA'd tiles get their low part computed here
       const bool cB = tB;
       // 3xF16: the operands' exact power-of-two scales
       const float sc_a = F16X3 ? ldexpf(1.0f, -prescale_exponent(__ldg(P.amax_a))) : 1.0f;
       const float sc_b = F16X3 ? ldexpf(1.0f, -prescale_exponent(__ldg(P.amax_b))) : 1.0f;
+      int kc0, kc1;
+      chunk_range<CG>(P, tm, tn, split, kc0, kc1);
+      if (!GATHER && !F16X3) {
+        // every operand of the launch arrives by TMA: the loop only derives the 3xTF32
+        // low parts, all of a stage's loads in flight at once (convert_lo_pair)
+        for (int kc = kc0; kc < kc1; ++kc) {
+          mbar_wait(empty_bar(stage), phase ^ 1);
+          uint8_t* st = gbase + stage * C::STAGE_BYTES;
+          if (CONVERT && (cA || cB)) {
+            mbar_wait(tma_bar(stage), phase);
+            convert_lo_pair(st, cA, cB, ptid);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (CG == 2 && !leader)
+              mbar_arrive_remote(mapa_shared(full_bar(stage), 0));
+            else
+              mbar_arrive(full_bar(stage));
+          }
+          if (++stage == C::STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        continue;
+      }
       RowTask ta[NTASK], tb[NTASK];
       if (mA) setup_tasks(P.a, tm * UT, ptid, ta);
       if (mB) setup_tasks(P.b, tn * UT, ptid, tb);
-      int kc0, kc1;
-      chunk_range<CG>(P, tm, tn, split, kc0, kc1);
       // manual operands: chunk kc+1's gathers are in flight while chunk kc is stored
       float4 va[NTASK], vb[NTASK], na[NTASK], nb[NTASK];
       if (mA) fetch_tasks(P.a, ta, ptid, static_cast<int64_t>(kc0) * BK, va);
@@ -1059,7 +1130,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
           if (mA) fetch_tasks(P.a, ta, ptid, knext, na);
           if (mB) fetch_tasks(P.b, tb, ptid, knext, nb);
         }
+        const bool pdbg = bt.debug_ts && blockIdx.x == 0 && ptid == 0;
+        long long q0 = pdbg ? clock64() : 0;
         mbar_wait(empty_bar(stage), phase ^ 1);
+        long long q1 = pdbg ? clock64() : 0, q2 = q1;
         uint8_t* st = gbase + stage * C::STAGE_BYTES;
         if (F16X3) {  // hi / lo fp16 tiles of A in slot 2, of B in slot 3
           if (mA) store_tasks_f16x3(P.a, ptid, st + 2 * TILE_BYTES, sc_a, va);
@@ -1073,6 +1147,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
         // (without one, the loads signal the leader's full barrier directly)
         if (CONVERT && (cA || cB)) {
           mbar_wait(tma_bar(stage), phase);
+          q2 = pdbg ? clock64() : 0;
           if (F16X3) {
             if (cA) convert_tile_f16x3(st, P.tma_a == TMA_ROWS_MN_PLAIN, st + 2 * TILE_BYTES, sc_a, ptid);
             if (cB) convert_tile_f16x3(st + TILE_BYTES, P.tma_b == TMA_ROWS_MN_PLAIN, st + 3 * TILE_BYTES, sc_b, ptid);
@@ -1080,6 +1155,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
             if (cA) convert_tile<NPASS>(st, st + 2 * TILE_BYTES, ptid);
             if (cB) convert_tile<NPASS>(st + TILE_BYTES, st + 3 * TILE_BYTES, ptid);
           }
+        }
+        if (pdbg) {  // debug timeline: producer cycles waiting for a free stage / for the TMA data / converting
+          const long long q3 = clock64();
+          atomicAdd(&g_dbg_unit[DBG_UNITS - 1][0], static_cast<unsigned long long>(q1 - q0));
+          atomicAdd(&g_dbg_unit[DBG_UNITS - 1][1], static_cast<unsigned long long>(q2 - q1));
+          atomicAdd(&g_dbg_unit[DBG_UNITS - 1][2], static_cast<unsigned long long>(q3 - q2));
+          atomicAdd(&g_dbg_unit[DBG_UNITS - 1][3], 1ull);
         }
         // one arrival per producer warp (measured faster than a named barrier +
         // a single elected arrival: the warps' cluster-scope releases overlap)
@@ -2058,14 +2140,15 @@ int launch_reduce(const std::vector<Problem>& probs, int ut, cudaStream_t st) {
   return flush();
 }
 
-template <int NPASS, bool RN, int CG>
+template <int NPASS, bool RN, int CG, bool GATHER = true>
 int launch_batch(const Batch& bt, cudaStream_t st) {
   using C = Cfg<NPASS>;
   static std::atomic<uint64_t> configured_on{0};
   static int max_pairs = 0;
   if (first_on_device(configured_on)) {
     cudaError_t e =
-        cudaFuncSetAttribute(tc_gemm_kernel<NPASS, RN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_SM_EXCL);
+        cudaFuncSetAttribute(tc_gemm_kernel<NPASS, RN, CG, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             SMEM_SM_EXCL);
     if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(tc_gemm_kernel)");
     if (CG == 2) {
       cudaLaunchConfig_t q = {};
@@ -2080,7 +2163,7 @@ int launch_batch(const Batch& bt, cudaStream_t st) {
       q.attrs = at;
       q.numAttrs = 1;
       int clusters = 0;
-      e = cudaOccupancyMaxActiveClusters(&clusters, tc_gemm_kernel<NPASS, RN, CG>, &q);
+      e = cudaOccupancyMaxActiveClusters(&clusters, tc_gemm_kernel<NPASS, RN, CG, GATHER>, &q);
       if (e != cudaSuccess) return cuda_status(e, "cudaOccupancyMaxActiveClusters(tc_gemm_kernel)");
       max_pairs = std::max(clusters, 1);
     }
@@ -2094,14 +2177,20 @@ int launch_batch(const Batch& bt, cudaStream_t st) {
   const int upc = units_per_cta();
   const int want = upc > 0 ? std::max(workers, (bt.total_units + upc - 1) / upc) : workers;
   const int grid = CG == 1 ? std::min(bt.total_units, want) : 2 * std::min(bt.total_units, want);
-  const cudaError_t e = launch_k(tc_gemm_kernel<NPASS, RN, CG>, dim3(grid), dim3(NTHREADS), SMEM_SM_EXCL, st, CG, bt);
+  const cudaError_t e =
+      launch_k(tc_gemm_kernel<NPASS, RN, CG, GATHER>, dim3(grid), dim3(NTHREADS), SMEM_SM_EXCL, st, CG, bt);
   note_launch();
   return cuda_status(e, "tc_gemm_kernel launch");
 }
 
 template <int CG>
 int launch_group(const Batch& bt, int precision, cudaStream_t st) {
-  if (precision == DPK_PREC_3XTF32) return launch_batch<3, false, CG>(bt, st);
+  if (precision == DPK_PREC_3XTF32) {
+    bool tma_only = true;
+    for (int i = 0; i < bt.nprob; ++i) tma_only = tma_only && bt.p[i].tma_a != TMA_NONE && bt.p[i].tma_b != TMA_NONE;
+    if (CG == 1 && tma_only) return launch_batch<3, false, CG, false>(bt, st);
+    return launch_batch<3, false, CG>(bt, st);
+  }
   if (precision == DPK_PREC_3XF16) return launch_batch<3, true, CG>(bt, st);  // RN slot = the fp16 split
   if (precision == DPK_PREC_TF32_TRUNC) return launch_batch<1, false, CG>(bt, st);
   return launch_batch<1, true, CG>(bt, st);

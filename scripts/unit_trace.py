@@ -33,6 +33,11 @@ torch.cuda.synchronize()
 buf = (C.c_ulonglong * 320)()
 L.check(ops.lib().dpk_debug_unit_timestamps(buf), "ts")
 t = [[buf[5 * i + k] for k in range(5)] for i in range(64)]
+pw = t[63]
+if pw[3]:
+    print(f"producer (CTA 0, thread 0): {pw[3]} chunks, per chunk cycles: wait free stage {pw[0] / pw[3]:.0f}, "
+          f"wait TMA {pw[1] / pw[3]:.0f}, convert {pw[2] / pw[3]:.0f}")
+t = t[:63]
 t0 = t[0][0]
 print(dt, N)
 for i, r in enumerate(t):
