@@ -578,6 +578,61 @@ __device__ __forceinline__ void convert_lo_pair(uint8_t* st, bool cA, bool cB, i
   convert_lo_part<3, 3>(st, cA, cB, ptid);
 }
 
+// 3xF16, TMA-only launches: both operands' fp32 tiles -> hi / lo fp16 tiles, items
+// (16-byte output chunks; MN plain: row pairs) in two batches of three per thread,
+// every load of a batch issued before its conversions.
+template <int Q0>
+__device__ __forceinline__ void convert_f16x3_batch(uint8_t* st, bool cA, bool mnA, float scA, bool cB, bool mnB,
+                                                    float scB, int ptid) {
+  constexpr int NB = 3;
+  float x[NB][8], y[NB][8];
+#pragma unroll
+  for (int qq = 0; qq < NB; ++qq) {
+    const int u = ptid + NPROD * (Q0 + qq);
+    const int op = u >> 9, v = u & 511;
+    const bool mn = op == 0 ? mnA : mnB;
+    if (u >= 1024 || !(op == 0 ? cA : cB) || (mn && v >= 256)) continue;
+    const uint8_t* src = st + op * TILE_BYTES;
+    if (mn) {
+      const int p = v & 63, c = v >> 6;
+      const float2* f = reinterpret_cast<const float2*>(src) + p + (8 * c) * 64;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float2 t = f[e * 64];
+        x[qq][e] = t.x;
+        y[qq][e] = t.y;
+      }
+    } else {
+      const int r = v & 127, c = v >> 7;
+      const float4 a = *reinterpret_cast<const float4*>(src + sw128_offset(r, 2 * c));
+      const float4 b = *reinterpret_cast<const float4*>(src + sw128_offset(r, 2 * c + 1));
+      x[qq][0] = a.x; x[qq][1] = a.y; x[qq][2] = a.z; x[qq][3] = a.w;
+      x[qq][4] = b.x; x[qq][5] = b.y; x[qq][6] = b.z; x[qq][7] = b.w;
+    }
+  }
+#pragma unroll
+  for (int qq = 0; qq < NB; ++qq) {
+    const int u = ptid + NPROD * (Q0 + qq);
+    const int op = u >> 9, v = u & 511;
+    const bool mn = op == 0 ? mnA : mnB;
+    if (u >= 1024 || !(op == 0 ? cA : cB) || (mn && v >= 256)) continue;
+    const float sc = op == 0 ? scA : scB;
+    uint8_t* dst = st + (2 + op) * TILE_BYTES;
+    const int r = mn ? 2 * (v & 63) : (v & 127), c = mn ? (v >> 6) : (v >> 7);
+    uint4 h, l;
+    split8_f16(x[qq], sc, h, l);
+    uint32_t off = sw64_chunk_offset(r, c);
+    *reinterpret_cast<uint4*>(dst + off) = h;
+    *reinterpret_cast<uint4*>(dst + F16_TILE + off) = l;
+    if (mn) {
+      split8_f16(y[qq], sc, h, l);
+      off = sw64_chunk_offset(r + 1, c);
+      *reinterpret_cast<uint4*>(dst + off) = h;
+      *reinterpret_cast<uint4*>(dst + F16_TILE + off) = l;
+    }
+  }
+}
+
 // Bytes one TMA'd operand tile delivers.  Box loads always count their full
 // (zero-filled) size; im2col tiles skip 32-row groups past the operand's rows
 // (those smem rows only feed accumulator rows the epilogue never stores).
@@ -1092,15 +1147,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) tc_gemm_kernel(const __grid_const
       const float sc_b = F16X3 ? ldexpf(1.0f, -prescale_exponent(__ldg(P.amax_b))) : 1.0f;
       int kc0, kc1;
       chunk_range<CG>(P, tm, tn, split, kc0, kc1);
-      if (!GATHER && !F16X3) {
+      if (!GATHER) {
         // every operand of the launch arrives by TMA: the loop only derives the 3xTF32
-        // low parts, all of a stage's loads in flight at once (convert_lo_pair)
+        // low parts (or the 3xF16 hi / lo tiles), a stage's loads in flight at once
+        const bool mnA = P.tma_a == TMA_ROWS_MN_PLAIN, mnB = P.tma_b == TMA_ROWS_MN_PLAIN;
         for (int kc = kc0; kc < kc1; ++kc) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           uint8_t* st = gbase + stage * C::STAGE_BYTES;
           if (CONVERT && (cA || cB)) {
             mbar_wait(tma_bar(stage), phase);
-            convert_lo_pair(st, cA, cB, ptid);
+            if (F16X3) {
+              convert_f16x3_batch<0>(st, cA, mnA, sc_a, cB, mnB, sc_b, ptid);
+              convert_f16x3_batch<3>(st, cA, mnA, sc_a, cB, mnB, sc_b, ptid);
+            } else {
+              convert_lo_pair(st, cA, cB, ptid);
+            }
           }
           fence_proxy_async_smem();
           __syncwarp();
@@ -2185,13 +2246,12 @@ int launch_batch(const Batch& bt, cudaStream_t st) {
 
 template <int CG>
 int launch_group(const Batch& bt, int precision, cudaStream_t st) {
-  if (precision == DPK_PREC_3XTF32) {
-    bool tma_only = true;
-    for (int i = 0; i < bt.nprob; ++i) tma_only = tma_only && bt.p[i].tma_a != TMA_NONE && bt.p[i].tma_b != TMA_NONE;
-    if (CG == 1 && tma_only) return launch_batch<3, false, CG, false>(bt, st);
-    return launch_batch<3, false, CG>(bt, st);
-  }
-  if (precision == DPK_PREC_3XF16) return launch_batch<3, true, CG>(bt, st);  // RN slot = the fp16 split
+  bool tma_only = true;
+  for (int i = 0; i < bt.nprob; ++i) tma_only = tma_only && bt.p[i].tma_a != TMA_NONE && bt.p[i].tma_b != TMA_NONE;
+  if (precision == DPK_PREC_3XTF32)
+    return tma_only ? launch_batch<3, false, CG, false>(bt, st) : launch_batch<3, false, CG>(bt, st);
+  if (precision == DPK_PREC_3XF16)  // (RN slot = the fp16 split)
+    return tma_only ? launch_batch<3, true, CG, false>(bt, st) : launch_batch<3, true, CG>(bt, st);
   if (precision == DPK_PREC_TF32_TRUNC) return launch_batch<1, false, CG>(bt, st);
   return launch_batch<1, true, CG>(bt, st);
 }
