@@ -202,7 +202,7 @@ double simt_fma_limit() {
   static double v = -1.0;
   if (v < 0.0) {
     const char* e = getenv("DPK_SIMT_FMA");
-    v = e ? atof(e) : 1.5e8;
+    v = e ? atof(e) : 5e7;  // re-tuned after the 3-pass producer fix (ResNet-50 N=1 6.75 -> 6.62 ms)
   }
   return v;
 }
