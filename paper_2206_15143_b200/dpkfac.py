@@ -251,7 +251,7 @@ class DPKFAC:
     OVERLAP_MIN_DIM = 1024
     MAX_CLASSES = 3      # size classes of the overlapped step (the last on the caller's stream)
     CLASS_RATIO = 0.6    # a new class starts below this fraction of the current class's largest
-    FACTOR_ORDER = 0     # see step(): gating of the classes' factor SYRKs
+    FACTOR_ORDER = 0     # see step(): gating of the classes' factor SYRKs (3: the last class's first)
     SIDE_CAP = 112       # >0: tensor-core launches of every class but the largest use at most
                          # this many SMs while the largest class holds a long inversion chain
     SIDE_CAP_MIN_DIM = 3072  # ... i.e. a factor of at least this dimension (measured: ResNet-50
@@ -649,6 +649,10 @@ class DPKFAC:
         # (its SYRK then runs on the whole GPU and the critical inversion chain starts
         # earlier); 2 = each class's SYRK waits for the previous class's; 0 = all at once
         gate = None
+        main_first = self.FACTOR_ORDER == 3 and len(sides) > 0
+        if main_first:  # the last class's factor SYRKs are enqueued before the side classes' work
+            with self._cap(len(sides)):
+                self._factor_stage(rest, t, f_up, None)
         for ci, (cls, st) in enumerate(zip(sides, streams)):
             if self._launched.get(ci) == t:  # launched from the backward hook
                 continue
@@ -682,7 +686,8 @@ class DPKFAC:
         if gate is not None:
             main.wait_event(gate)
         with self._cap(len(sides)):
-            self._factor_stage(rest, t, f_up, None)
+            if not main_first:
+                self._factor_stage(rest, t, f_up, None)
             self._mark("factors")
             # (2) inverses / eigendecompositions
             self._inverse_stage(rest, t, k_up)
