@@ -712,3 +712,23 @@ def test_implicit_f16_syrk_matches_unfold(shape, k, s, p, scale):
     assert rel(N(out), N(ref16)) <= 1e-6, rel(N(out), N(ref16))
     want, _ = K.compute_factors(cols[perm], cols[:1])
     assert rel(N(out), want) <= TOL, rel(N(out), want)
+
+
+def test_launch_cap_gives_identical_results():
+    """dpk_set_launch_cap (ops.launch_cap): fewer persistent CTAs walk the same units --
+    the result is bit-identical, and the cap is thread-local and reset on exit."""
+    from paper_2206_15143_b200 import _lib as L, ops
+    rng = np.random.default_rng(5)
+    a, b = T(rng.standard_normal((1000, 700))), T(rng.standard_normal((900, 700)))
+    outs = []
+    for cap in (0, 16, 3):
+        out = torch.empty(1000, 900, device=dev())
+        j = L.GemmJob()
+        j.a, j.b = ops.operand_rows_k(a), ops.operand_rows_k(b)
+        j.out, j.ldo, j.alpha = out.data_ptr(), 900, 1.0
+        with ops.launch_cap(cap):
+            ops.gemm([j], "3xtf32")
+        outs.append(out)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
+    assert ops.lib().dpk_set_launch_cap(-1) != 0  # invalid
