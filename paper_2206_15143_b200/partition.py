@@ -19,6 +19,8 @@ placement in decreasing size, then deterministic move/swap improvement.
 
 from __future__ import annotations
 
+import os
+
 from typing import Sequence
 
 from .errors import ArgumentError
@@ -84,15 +86,23 @@ def imbalance(costs: Sequence[float], assignment: Sequence[Sequence[int]]) -> fl
     return max(loads) / mean if mean > 0 else 1.0
 
 
-# B200 rates of the stages, measured: factor SYRKs ~340 TF/s,
+# B200 rates of the stages, measured: factor SYRKs ~500 TF/s
+# effective (kind::f16 conv patches after the MMA issue-loop fix; 340 before),
 # 3xTF32 inversion rounds ~100 TF/s, preconditioning ~110 TF/s; the blocked SPD
-# inversion of an n > 128 factor is a dependent chain of ~0.8 us per row (4608: 3.7 ms);
-# NCCL reduce-scatter + all-gather at ~450 GB/s bus bandwidth.
-RATE_SYRK = 340e12
+# inversion of an n > 128 factor is a dependent chain of ~0.7 us per row (4608: ~3 ms);
+# NCCL reduce-scatter + all-gather at ~450 GB/s bus bandwidth.  Re-fit at the end of
+# round 2 by measuring the step (scripts/gpu_runs/r2_balfit*.sh): N=4 4.06 -> 3.79 ms,
+# N=2 4.90 -> 4.92 ms.
+RATE_SYRK = 500e12
 RATE_INV = 100e12
 RATE_PRE = 110e12
-CHAIN_S_PER_ROW = 0.8e-6
+CHAIN_S_PER_ROW = 0.7e-6
 BUS_BYTES_PER_S = 450e9
+
+
+def _rate(name: str, default: float) -> float:  # DPK_BAL_<NAME>: model re-fit experiments
+    v = os.environ.get("DPK_BAL_" + name)
+    return float(v) if v else default
 
 
 def layer_time(d_in: int, d_out: int, m: int, inv_type: str = "inverse") -> tuple[float, float]:
@@ -101,9 +111,9 @@ def layer_time(d_in: int, d_out: int, m: int, inv_type: str = "inverse") -> tupl
     cube = float(d_in) ** 3 + float(d_out) ** 3
     inv = (2.0 / 3.0) * cube if inv_type == "inverse" else 9.0 * cube
     pre = 2.0 * (d_out * d_out * d_in + d_out * d_in * d_in) * (1 if inv_type == "inverse" else 2)
-    work = syrk / RATE_SYRK + inv / RATE_INV + pre / RATE_PRE
+    work = syrk / _rate("SYRK", RATE_SYRK) + inv / _rate("INV", RATE_INV) + pre / _rate("PRE", RATE_PRE)
     big = max(d_in, d_out)
-    chain = CHAIN_S_PER_ROW * big if (big > 128 and inv_type == "inverse") else 0.0
+    chain = _rate("CHAIN", CHAIN_S_PER_ROW) * big if (big > 128 and inv_type == "inverse") else 0.0
     return work, chain
 
 
