@@ -252,6 +252,7 @@ class DPKFAC:
     MAX_CLASSES = 3      # size classes of the overlapped step (the last on the caller's stream)
     CLASS_RATIO = 0.6    # a new class starts below this fraction of the current class's largest
     FACTOR_ORDER = 0     # see step(): gating of the classes' factor SYRKs (3: the last class's first)
+    SIDE_PRIORITIES = tuple(int(v) for v in os.environ.get("DPK_SIDE_PRIO", "-2,-1").split(","))
     SIDE_CAP = 112       # >0: tensor-core launches of every class but the largest use at most
                          # this many SMs while the largest class holds a long inversion chain
     SIDE_CAP_MIN_DIM = 3072  # ... i.e. a factor of at least this dimension (measured: ResNet-50
@@ -769,7 +770,8 @@ class DPKFAC:
         if self._side is None:
             self._side = []
         while len(self._side) < n:  # class 0 (largest factors) gets the highest priority
-            self._side.append(torch.cuda.Stream(self.device, priority=-1 - (len(self._side) == 0)))
+            prio = self.SIDE_PRIORITIES[min(len(self._side), len(self.SIDE_PRIORITIES) - 1)]
+            self._side.append(torch.cuda.Stream(self.device, priority=prio))
         return self._side[:n]
 
     def _size_classes(self, owned):
