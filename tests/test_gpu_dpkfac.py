@@ -593,10 +593,11 @@ def test_inception_asymmetric_convs_match_reference_layer_step(inv_type, channel
         hk.remove()
 
 
-@pytest.mark.parametrize("inv_type", ["inverse", "eigen"])
-def test_kl_clip_scale_matches_formula(inv_type):
+@pytest.mark.parametrize("inv_type,comm_overlap", [("inverse", False), ("eigen", False), ("inverse", True)])
+def test_kl_clip_scale_matches_formula(inv_type, comm_overlap):
     """Opt-in KL-clip (north_star; the reference has none): the oracle's
-    preconditioned gradients scaled by nu = min(1, sqrt(kl / |lr^2 sum <pre, grad>|))."""
+    preconditioned gradients scaled by nu = min(1, sqrt(kl / |lr^2 sum <pre, grad>|)) --
+    also with the bucketed reduce-scatter layout (the KL slot behind the last bucket)."""
     from paper_2206_15143_b200 import DPKFAC
     dev = torch.device("cuda", 0)
     spec = MLP.MlpSpec((784, 512, 256, 10), "relu", "softmax_cross_entropy", True)
@@ -604,7 +605,8 @@ def test_kl_clip_scale_matches_formula(inv_type):
     cl = MLP.build_cluster(spec, 1, seed=0)
     model, lins = torch_mlp([w.copy() for w in cl.weights], dev)
     lr, kl = 0.05, 1e-4
-    kf = DPKFAC(model, gamma=0.03, xi=0.95, inv_type=inv_type, kl_clip=kl, lr=lambda: lr)
+    kf = DPKFAC(model, gamma=0.03, xi=0.95, inv_type=inv_type, kl_clip=kl, lr=lambda: lr,
+                comm_overlap=comm_overlap, bucket_mb=1e-4)
     rng = np.random.default_rng(5)
     nus = []
     for t in range(2):
