@@ -255,9 +255,11 @@ class DPKFAC:
     SIDE_PRIORITIES = tuple(int(v) for v in os.environ.get("DPK_SIDE_PRIO", "-2,-1").split(","))
     SIDE_CAP = 112       # >0: tensor-core launches of every class but the largest use at most
                          # this many SMs while the largest class holds a long inversion chain
-    SIDE_CAP_MIN_DIM = 3072  # ... i.e. a factor of at least this dimension (measured: ResNet-50
-                             # 7.41 -> 7.20 ms, Inception-v4 11.60 -> 11.38, N=2 5.40 -> 5.30;
-                             # DenseNet-201, largest factor 1921, 10.22 -> 10.44 with a cap)
+    SIDE_CAP_MIN_DIM = 4096  # ... i.e. a factor of at least this dimension (measured: ResNet-50,
+                             # three 4608 factors, 7.07 -> 6.65 ms with the cap; Inception-v4,
+                             # largest 3456, 10.27 ms without vs 10.92 with; DenseNet-201 (1921)
+                             # slower with a cap) -- below it the many-layer classes, not the
+                             # largest factor's chain, are the critical path
 
     def __init__(self, model: nn.Module, *, gamma: float = 0.03, xi: float = 0.95, inv_type: str = "eigen",
                  f_freq: int = 1, k_freq: int = 1,
