@@ -6,13 +6,16 @@
 // with or without the mirror, triangular K clipping); exact fp32 products, so
 // it is at least as accurate as the 3xTF32 path it stands in for.
 //
-// One CTA per (problem, 64 x 64 output tile), 256 threads in a 16 x 16 grid,
-// 4 x 4 outputs per thread; K in chunks of 32 staged through shared memory
-// (k-major, so the inner loop reads two float4 per 16 FMAs) with the next
-// chunk's global loads in flight during the current chunk's math.
+// One CTA per (problem, 64 x 64 or 32 x 32 output tile), 256 threads in a 16 x 16
+// grid, 4 x 4 (2 x 2) outputs per thread; K in chunks of 32 staged through shared
+// memory (k-major, so the inner loop reads two float4 per 16 FMAs) by cp.async in a
+// SNS-stage ring: the loads of up to SNS-1 chunks ahead are in flight together, so
+// a K <= 96 problem costs one global-load latency instead of one per chunk (these
+// launches are latency-bound: 2M FMA spread over 16+ SMs).
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <vector>
 
@@ -23,6 +26,7 @@ namespace dpk {
 namespace {
 
 constexpr int SK = 32;       // K chunk
+constexpr int SNS = 4;       // cp.async ring stages
 constexpr int SMAXP = 192;
 
 struct SimtProb {
@@ -58,10 +62,13 @@ __device__ __forceinline__ void tile_of(const SimtProb& P, int t, int& tm, int& 
   }
 }
 
-// T/8 elements per thread of one T x 32 operand chunk (rows r0.., k k0..)
+// T/8 elements per thread of one T x 32 operand chunk (rows r0.., k k0..) copied to
+// shared memory k-major (s[k][r]) by 4-byte cp.async; out-of-range elements are
+// zero-filled (src-size 0, nothing read)
 template <int T>
-__device__ __forceinline__ void load_chunk(const float* p, int64_t ld, int mn, int rows, int r0, int k0, int klo,
-                                           int khi, int tid, float (&v)[T / 8]) {
+__device__ __forceinline__ void copy_chunk(float* s, const float* p, int64_t ld, int mn, int rows, int r0, int k0,
+                                           int klo, int khi, int tid) {
+  constexpr int SP = T + 4;
 #pragma unroll
   for (int i = 0; i < T / 8; ++i) {
     const int idx = tid + 256 * i;
@@ -69,18 +76,18 @@ __device__ __forceinline__ void load_chunk(const float* p, int64_t ld, int mn, i
     const int k = mn ? idx / T : idx % SK;
     const int gr = r0 + r, gk = k0 + k;
     const bool ok = gr < rows && gk >= klo && gk < khi;
-    v[i] = ok ? __ldg(p + (mn ? static_cast<int64_t>(gk) * ld + gr : static_cast<int64_t>(gr) * ld + gk)) : 0.0f;
+    const float* src = ok ? p + (mn ? static_cast<int64_t>(gk) * ld + gr : static_cast<int64_t>(gr) * ld + gk) : p;
+    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(s + k * SP + r));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(ok ? 4 : 0) : "memory");
   }
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 template <int T>
-__device__ __forceinline__ void store_chunk(float* s, int mn, int tid, const float (&v)[T / 8]) {
-#pragma unroll
-  for (int i = 0; i < T / 8; ++i) {
-    const int idx = tid + 256 * i;
-    const int r = mn ? idx % T : idx / SK;
-    const int k = mn ? idx / T : idx % SK;
-    s[k * (T + 4) + r] = v[i];
-  }
+constexpr int simt_smem_bytes() {
+  return 2 * SNS * SK * (T + 4) * 4;
 }
 
 // T x T output tile per CTA (T = 32 or 64), R x R outputs per thread
@@ -88,8 +95,9 @@ template <int T>
 __global__ void __launch_bounds__(256, 1) simt_gemm_kernel(const __grid_constant__ SimtBatch bt) {
   constexpr int R = T / 16;
   constexpr int SP = T + 4;  // smem row stride: 16-byte aligned rows
-  __shared__ __align__(16) float As[2][SK * SP];
-  __shared__ __align__(16) float Bs[2][SK * SP];
+  extern __shared__ __align__(16) float simt_smem[];
+  float* As = simt_smem;                 // [SNS][SK * SP]
+  float* Bs = simt_smem + SNS * SK * SP;  // [SNS][SK * SP]
   pdl_wait();
   pdl_trigger();
   int pi = 0;
@@ -107,24 +115,24 @@ __global__ void __launch_bounds__(256, 1) simt_gemm_kernel(const __grid_constant
   if (P.tri_b == TRI_LOWER) khi = min(khi, n0 + T);
   if (P.tri_a == TRI_BLOCK || P.tri_b == TRI_BLOCK) return;  // never planned here (simt_eligible)
   const int kstart = (klo / SK) * SK;
+  const int nch = khi > kstart ? (khi - kstart + SK - 1) / SK : 0;
   float acc[R][R] = {};
-  float va[T / 8], vb[T / 8];
-  int buf = 0;
-  if (kstart < khi) {
-    load_chunk<T>(P.a, P.lda, P.a_mn, P.M, m0, kstart, klo, khi, tid, va);
-    load_chunk<T>(P.b, P.ldb, P.b_mn, P.N, n0, kstart, klo, khi, tid, vb);
-    store_chunk<T>(As[0], P.a_mn, tid, va);
-    store_chunk<T>(Bs[0], P.b_mn, tid, vb);
-  }
-  __syncthreads();
-  for (int k0 = kstart; k0 < khi; k0 += SK) {
-    const bool more = k0 + SK < khi;
-    if (more) {  // next chunk's loads overlap this chunk's math
-      load_chunk<T>(P.a, P.lda, P.a_mn, P.M, m0, k0 + SK, klo, khi, tid, va);
-      load_chunk<T>(P.b, P.ldb, P.b_mn, P.N, n0, k0 + SK, klo, khi, tid, vb);
+  auto issue = [&](int c) {  // chunk c into stage c % SNS (an empty group past the end)
+    if (c < nch) {
+      const int st = c % SNS;
+      copy_chunk<T>(As + st * SK * SP, P.a, P.lda, P.a_mn, P.M, m0, kstart + c * SK, klo, khi, tid);
+      copy_chunk<T>(Bs + st * SK * SP, P.b, P.ldb, P.b_mn, P.N, n0, kstart + c * SK, klo, khi, tid);
     }
-    const float* as = As[buf];
-    const float* bs = Bs[buf];
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int c = 0; c < SNS - 1; ++c) issue(c);
+  for (int c = 0; c < nch; ++c) {
+    cp_async_wait<SNS - 2>();  // this thread's copies of chunk c have landed
+    __syncthreads();           // everyone's have; stage (c - 1) % SNS is free again
+    issue(c + SNS - 1);
+    const float* as = As + (c % SNS) * SK * SP;
+    const float* bs = Bs + (c % SNS) * SK * SP;
 #pragma unroll 8
     for (int kk = 0; kk < SK; ++kk) {
       float ar[R], br[R];
@@ -144,13 +152,8 @@ __global__ void __launch_bounds__(256, 1) simt_gemm_kernel(const __grid_constant
 #pragma unroll
         for (int j = 0; j < R; ++j) acc[i][j] = fmaf(ar[i], br[j], acc[i][j]);
     }
-    if (more) {
-      store_chunk<T>(As[buf ^ 1], P.a_mn, tid, va);
-      store_chunk<T>(Bs[buf ^ 1], P.b_mn, tid, vb);
-    }
-    __syncthreads();
-    buf ^= 1;
   }
+  cp_async_wait<0>();  // no copy may outlive the CTA
   // epilogue: alpha * acc + beta * cin; symmetric diagonal tiles keep gn <= gm
   const bool diag = P.sym == 1 && tm == tn;
 #pragma unroll
@@ -246,8 +249,17 @@ int simt_gemm_launch(const GemmSpec* specs, int n, cudaStream_t st) {
   }
   bt.total = tiles;
   if (tiles == 0) return DPK_OK;
-  const cudaError_t e = T == 64 ? launch_k(simt_gemm_kernel<64>, dim3(tiles), dim3(256), 0, st, 1, bt)
-                                : launch_k(simt_gemm_kernel<32>, dim3(tiles), dim3(256), 0, st, 1, bt);
+  static std::atomic<uint64_t> configured_on{0};
+  if (first_on_device(configured_on)) {
+    cudaError_t e = cudaFuncSetAttribute(simt_gemm_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         simt_smem_bytes<64>());
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(simt_gemm_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               simt_smem_bytes<32>());
+    if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(simt_gemm_kernel)");
+  }
+  const cudaError_t e = T == 64 ? launch_k(simt_gemm_kernel<64>, dim3(tiles), dim3(256), simt_smem_bytes<64>(), st, 1, bt)
+                                : launch_k(simt_gemm_kernel<32>, dim3(tiles), dim3(256), simt_smem_bytes<32>(), st, 1, bt);
   note_launch();
   return cuda_status(e, "simt_gemm_kernel launch");
 }

@@ -1,5 +1,5 @@
 """Graph-mode factored SPD inverse (dpk_chol_factor_inv_batched) of the ResNet-50 factor set
-(SPD_ONLY=n restricts to one size): inv_factor_one.py [reps]"""
+(SPD_ONLY=n restricts to one size, SPD_COUNT=c to the first c): inv_factor_one.py [reps]"""
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -10,6 +10,8 @@ man = json.load(open(os.path.join(ROOT, "tests/golden/resnet50_manifest.json")))
 dims = [d for a, g in man["dims"] for d in (a, g)]
 if os.environ.get("SPD_ONLY"):
     dims = [d for d in dims if d == int(os.environ["SPD_ONLY"])]
+if os.environ.get("SPD_COUNT"):
+    dims = dims[:int(os.environ["SPD_COUNT"])]
 torch.manual_seed(0)
 jobs, keep = [], []
 for d in dims:

@@ -162,6 +162,34 @@ def test_gemm_all_operand_majors(m, n, k):
         assert rel(N(out), 0.5 * a @ b.T - 2.0 * c) <= 1e-5
 
 
+@pytest.mark.parametrize("m,n,k,sym", [(128, 128, 128, False), (64, 200, 300, False), (33, 17, 1, False),
+                                       (256, 256, 96, False), (300, 300, 257, True), (128, 128, 33, True)])
+def test_gemm_latency_path_exact_fp32(m, n, k, sym):
+    """Small 3xtf32 groups run on the CUDA-core latency path (gemm_simt.cu: cp.async
+    ring, K from one chunk to past the ring's depth, symmetric lower tiles + mirror):
+    exact fp32 products, so within fp32 accumulation error of the float64 product."""
+    from paper_2206_15143_b200 import _lib as L, ops
+    rng = np.random.default_rng(m * 7 + n + k)
+    a = rng.standard_normal((m, k)).astype(np.float32).astype(np.float64)
+    b = a if sym else rng.standard_normal((n, k)).astype(np.float32).astype(np.float64)
+    c = rng.standard_normal((m, n)).astype(np.float32).astype(np.float64)
+    at, bt, ct = T(a), T(b), T(c)
+    atr, btr = T(a.T), T(b.T)
+    pairs = [(ops.operand_rows_k(at), ops.operand_rows_k(bt)), (ops.operand_rows_mn(atr), ops.operand_rows_mn(btr))]
+    for a_op, b_op in pairs:
+        out = torch.full((m, n), float("nan"), device=dev())
+        j = L.GemmJob()
+        j.a, j.b = a_op, b_op
+        j.out, j.ldo = out.data_ptr(), n
+        j.cin, j.ldc = (0, 0) if sym else (ct.data_ptr(), n)
+        j.alpha, j.beta = (0.25, 0.0) if sym else (0.5, -2.0)
+        j.symmetric = int(sym)
+        ops.gemm([j], "3xtf32")
+        torch.cuda.synchronize()
+        want = 0.25 * a @ a.T if sym else 0.5 * a @ b.T - 2.0 * c
+        assert rel(N(out), want) <= 2e-6, rel(N(out), want)
+
+
 @pytest.mark.parametrize("scale", [1.0, 3e4, 1e-6])
 @pytest.mark.parametrize("m,n,k", [(1, 1, 1), (130, 70, 45), (512, 785, 300), (1000, 2049, 33), (600, 600, 700)])
 def test_gemm_3xf16_all_operand_majors(m, n, k, scale):
