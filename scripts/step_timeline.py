@@ -18,7 +18,8 @@ ctor, batch, shape, classes = BM.WORKLOADS[model_name]
 torch.manual_seed(0)
 model = ctor().to(dev).to(memory_format=torch.channels_last)
 kf = DPKFAC(model, gamma=0.002, xi=0.95, inv_type="inverse", assignment="balanced", check_numerics="deferred")
-kf.SIDE_CAP = int(os.environ.get("SIDE_CAP", "0"))
+if os.environ.get("SIDE_CAP"):
+    kf.SIDE_CAP = int(os.environ["SIDE_CAP"])
 x = torch.randn(batch, *shape, device=dev).contiguous(memory_format=torch.channels_last)
 y = torch.randint(0, classes, (batch,), device=dev)
 F.cross_entropy(model(x), y).backward()
