@@ -371,7 +371,6 @@ class DPKFAC:
         self._capturing = True
         self._hooks = []
         for ly in self.layers:
-            self._hooks.append(ly.module.register_forward_pre_hook(self._make_pre_hook(ly)))
             self._hooks.append(ly.module.register_forward_hook(self._make_fwd_hook(ly)))
         self._bufs_ready = False
         self.last_stage_ms = {}
@@ -413,22 +412,24 @@ class DPKFAC:
                         lambda _p, i=ly.index: self._on_grad(i)))
 
     # ------------------------------------------------------------ hooks
-    def _make_pre_hook(self, ly: _Layer):
-        def hook(module, inputs):
+    def _make_fwd_hook(self, ly: _Layer):
+        """One forward hook per layer captures the input (the hook receives the
+        module's inputs too) and registers the grad-output capture on the output.
+        A single hook and a per-layer prebuilt grad closure keep the per-layer host
+        cost low: host-bound models (DenseNet-201's ~200 layers) pay it on the
+        critical path of every iteration."""
+        def grab(g):
+            ly.g_out = g.detach()
+            if self._hook_classes is not None:
+                self._on_capture(ly)
+
+        def hook(module, inputs, output):
             if self._capturing and (ly.owned or self.mpd) and torch.is_grad_enabled():
                 x = inputs[0]
                 ly.a_in = x.detach()
                 ly.batch = x.shape[0]
-        return hook
-
-    def _make_fwd_hook(self, ly: _Layer):
-        def hook(module, inputs, output):
-            if self._capturing and (ly.owned or self.mpd) and torch.is_grad_enabled() and output.requires_grad:
-                def grab(g, ly=ly):
-                    ly.g_out = g.detach()
-                    if self._hook_classes is not None:
-                        self._on_capture(ly)
-                output.register_hook(grab)
+                if output.requires_grad:
+                    output.register_hook(grab)
         return hook
 
     def remove_hooks(self):
