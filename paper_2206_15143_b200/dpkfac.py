@@ -10,9 +10,10 @@ Semantics follow the reference's simulated cluster (kfaclab distsim.py:289-338,
   * layer -> rank assignment is the reference's round robin
     (costmodel.py:66-70) unless "balanced" or an explicit partition is asked
     for, always validated like distsim.validate_partition;
-  * each rank captures a (forward-pre) and B_local * dL/ds (backward) for its
-    OWN layers from its LOCAL batch (model.py:9-12, 217-218, 247), builds and
-    inverts their Kronecker factors; factors are never communicated;
+  * each rank captures a (the layer input, in its forward hook) and B_local * dL/ds
+    (a grad hook on the layer output) for its OWN layers from its LOCAL batch
+    (model.py:9-12, 217-218, 247), builds and inverts their Kronecker factors;
+    factors are never communicated;
   * ``step()`` (after ``loss.backward()``, before ``optimizer.step()``):
       1. factor SYRK + running average if t % f_freq == 0 (one grouped launch),
       2. refresh inverses / eigendecompositions if t % k_freq == 0,
