@@ -70,6 +70,8 @@ def parse():
     ap.add_argument("--comm-overlap", action="store_true",
                     help="bucketed gradient reduce-scatter launched from the backward hooks (e2e)")
     ap.add_argument("--bucket-mb", type=float, default=16.0)
+    ap.add_argument("--peer-gather", action="store_true",
+                    help="closing all-gather as one NVLink peer-copy kernel (IPC-mapped chunks) instead of NCCL")
     ap.add_argument("--early-priority", default="high", choices=["high", "low"],
                     help="e2e with --early: stream priority of the hook-launched pipelines")
     ap.add_argument("--ncu-step", action="store_true",
@@ -276,7 +278,8 @@ def run_ours(args, rank, world, local_rank):
     kf = DPKFAC(model, gamma=args.gamma, xi=args.xi, inv_type=args.inv_type, f_freq=1, k_freq=1,
                 assignment=args.assignment, precision=args.precision, check_numerics="deferred",
                 overlap=not args.no_overlap, early=False, algorithm=args.algorithm, im2col=args.im2col,
-                comm_overlap=args.comm_overlap, bucket_mb=args.bucket_mb)  # captures are replayed below; e2e turns early on
+                comm_overlap=args.comm_overlap, bucket_mb=args.bucket_mb,
+                peer_gather=args.peer_gather)  # captures are replayed below; e2e turns early on
     for attr, val in (("MAX_CLASSES", args.max_classes), ("CLASS_RATIO", args.class_ratio),
                       ("FACTOR_ORDER", args.factor_order), ("SIDE_CAP", args.side_cap)):
         if val is not None:
@@ -522,6 +525,8 @@ def run_ours(args, rank, world, local_rank):
                        "assignment": args.assignment, "algorithm": args.algorithm, "im2col": args.im2col,
                        "comm_overlap": (f"bucketed reduce-scatter from the backward hooks, {args.bucket_mb} MB buckets"
                                         if args.comm_overlap else False),
+                       "all_gather": ("NVLink peer-copy kernel" if getattr(getattr(kf, "xchg", None), "_peer_ptrs", None)
+                                      is not None else "NCCL"),
                        "memory_format": "channels_last" if mf is torch.channels_last else "contiguous",
                        "l2": "inputs (layer captures, >1.4 GB) larger than L2; no flush"},
             "overlap": overlap, "ms_per_step_serialized": ms_serial,

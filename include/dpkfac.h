@@ -369,6 +369,22 @@ int dpk_unpack_owner_major_klclip(const dpk_segment* segs, int n_segs, const flo
                                   const float* kl_slots, int n_slots, int64_t slot_stride, float kl_clip, float lr,
                                   dpk_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * Peer all-gather over NVLink (single node; DPKFAC(peer_gather=True)) -- replaces the
+ * closing all-gather of the owner-major exchange (distsim.py:333-336 broadcast of the
+ * owners' preconditioned gradients; NCCL all_gather_into_tensor otherwise):
+ *   dpk_ipc_export: the cudaIpcMemHandle_t (64 bytes) of the allocation holding ptr
+ *     and ptr's byte offset in it (caching allocators sub-allocate);
+ *   dpk_ipc_open: map another process's exported allocation into `device`'s context;
+ *   dpk_peer_gather: dst[i*count .. (i+1)*count) = srcs[i][0 .. count) for every
+ *     source (own chunk local, the others peer pointers), one launch; count % 4 == 0,
+ *     16-byte aligned.  The caller orders it after every rank's chunk is written.
+ * ------------------------------------------------------------------------ */
+int dpk_ipc_export(const void* ptr, int device, void* handle, int64_t* offset);
+int dpk_ipc_open(const void* handle, int device, void** base);
+int dpk_ipc_close(void* base);
+int dpk_peer_gather(float* dst, const float* const* srcs, int n_src, int64_t count, dpk_stream_t stream);
+
 /* Library / device introspection. */
 const char* dpk_version(void);
 const char* dpk_last_error(void);

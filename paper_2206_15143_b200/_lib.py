@@ -119,6 +119,10 @@ _SIGNATURES = [
     ("dpk_kl_dot", C.c_int, [_P, _P, C.c_int64, _P, _P, C.c_size_t, _P]),
     ("dpk_unpack_owner_major_klclip", C.c_int, [C.POINTER(Segment), C.c_int, _P, C.c_float, _P, C.c_int,
                                                 C.c_int64, C.c_float, C.c_float, _P]),
+    ("dpk_ipc_export", C.c_int, [_P, C.c_int, _P, C.POINTER(C.c_int64)]),
+    ("dpk_ipc_open", C.c_int, [_P, C.c_int, C.POINTER(C.c_void_p)]),
+    ("dpk_ipc_close", C.c_int, [_P]),
+    ("dpk_peer_gather", C.c_int, [_P, C.POINTER(C.c_void_p), C.c_int, C.c_int64, _P]),
     ("dpk_version", C.c_char_p, []),
     ("dpk_last_error", C.c_char_p, []),
     ("dpk_launch_count", C.c_ulonglong, []),

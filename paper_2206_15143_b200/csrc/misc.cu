@@ -248,6 +248,30 @@ __global__ void __launch_bounds__(256) kl_dot_kernel(const float* a, const float
   }
 }
 
+// Peer all-gather (DPKFAC peer_gather): one launch copies every rank's owner-major
+// chunk -- read in place from the other GPUs' memory over NVLink (IPC-mapped) -- into
+// the local gathered buffer; blockIdx.y = source rank, 4 independent 16-byte loads in
+// flight per thread.
+constexpr int PEER_MAX = 8;
+struct PeerSrcs {
+  const float4* src[PEER_MAX];
+};
+__global__ void __launch_bounds__(256) peer_gather_kernel(float4* __restrict__ dst, const __grid_constant__ PeerSrcs s,
+                                                          int64_t n4) {
+  const float4* __restrict__ src = s.src[blockIdx.y];
+  float4* __restrict__ d = dst + static_cast<int64_t>(blockIdx.y) * n4;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t k = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (; k + 3 * stride < n4; k += 4 * stride) {
+    const float4 v0 = src[k], v1 = src[k + stride], v2 = src[k + 2 * stride], v3 = src[k + 3 * stride];
+    d[k] = v0;
+    d[k + stride] = v1;
+    d[k + 2 * stride] = v2;
+    d[k + 3 * stride] = v3;
+  }
+  for (; k < n4; k += stride) d[k] = src[k];
+}
+
 }  // namespace
 }  // namespace dpk
 
@@ -279,6 +303,79 @@ int dpk_unpack_owner_major_klclip(const dpk_segment* segs, int n_segs, const flo
   }
   return dpk::run_segments<false>(segs, n_segs, const_cast<float*>(flat), scale, static_cast<cudaStream_t>(stream),
                                   kl_slots, n_slots, slot_stride, kl_clip, lr * lr);
+}
+
+int dpk_ipc_export(const void* ptr, int device, void* handle, int64_t* offset) {
+  if (ptr == nullptr || handle == nullptr || offset == nullptr || device < 0) {
+    dpk::set_error("dpk_ipc_export: bad arguments");
+    return DPK_EARG;
+  }
+  int rc = dpk::cuda_status(cudaSetDevice(device), "cudaSetDevice");
+  if (rc) return rc;
+  // the allocation holding ptr (a caching allocator's block lives inside a larger
+  // cudaMalloc segment): its IPC handle plus ptr's offset from the segment base
+  using AddrRangeFn = int (*)(unsigned long long*, size_t*, unsigned long long);
+  static AddrRangeFn range = nullptr;
+  if (range == nullptr) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      range = reinterpret_cast<AddrRangeFn>(p);
+  }
+  if (range == nullptr) {
+    dpk::set_error("dpk_ipc_export: cuMemGetAddressRange unavailable");
+    return DPK_ECUDA;
+  }
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (range(&base, &size, reinterpret_cast<unsigned long long>(ptr)) != 0) {
+    dpk::set_error("dpk_ipc_export: cuMemGetAddressRange failed");
+    return DPK_ECUDA;
+  }
+  cudaIpcMemHandle_t h;
+  rc = dpk::cuda_status(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)), "cudaIpcGetMemHandle");
+  if (rc) return rc;
+  std::memcpy(handle, &h, sizeof(h));
+  *offset = static_cast<int64_t>(reinterpret_cast<unsigned long long>(ptr) - base);
+  return DPK_OK;
+}
+
+int dpk_ipc_open(const void* handle, int device, void** base) {
+  if (handle == nullptr || base == nullptr || device < 0) {
+    dpk::set_error("dpk_ipc_open: bad arguments");
+    return DPK_EARG;
+  }
+  int rc = dpk::cuda_status(cudaSetDevice(device), "cudaSetDevice");
+  if (rc) return rc;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  return dpk::cuda_status(cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+}
+
+int dpk_ipc_close(void* base) { return dpk::cuda_status(cudaIpcCloseMemHandle(base), "cudaIpcCloseMemHandle"); }
+
+int dpk_peer_gather(float* dst, const float* const* srcs, int n_src, int64_t count, dpk_stream_t stream) {
+  if (dst == nullptr || srcs == nullptr || n_src < 1 || n_src > dpk::PEER_MAX || count < 0 || count % 4 != 0 ||
+      (reinterpret_cast<uintptr_t>(dst) & 15) != 0) {
+    dpk::set_error("dpk_peer_gather: bad arguments (1..8 sources, count % 4 == 0, 16-byte aligned)");
+    return DPK_EARG;
+  }
+  dpk::PeerSrcs s{};
+  for (int i = 0; i < n_src; ++i) {
+    if (srcs[i] == nullptr || (reinterpret_cast<uintptr_t>(srcs[i]) & 15) != 0) {
+      dpk::set_error("dpk_peer_gather: null or unaligned source");
+      return DPK_EARG;
+    }
+    s.src[i] = reinterpret_cast<const float4*>(srcs[i]);
+  }
+  if (count == 0) return DPK_OK;
+  const int64_t n4 = count / 4;
+  const int bx = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(2 * dpk::num_sms() / n_src, (n4 + 1023) / 1024)));
+  dpk::peer_gather_kernel<<<dim3(bx, n_src), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<float4*>(dst), s, n4);
+  dpk::note_launch();
+  return dpk::cuda_status(cudaGetLastError(), "peer_gather_kernel launch");
 }
 
 const char* dpk_version(void) { return "dpkfac-b200 0.1.0 (sm_100a, tcgen05 tf32/3xtf32)"; }

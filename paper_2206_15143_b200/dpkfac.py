@@ -269,7 +269,8 @@ class DPKFAC:
                  grad_scale: Union[str, float] = "batch", check_numerics: Union[bool, str] = True,
                  im2col: str = "materialize", overlap: bool = True, early: bool = False,
                  algorithm: str = "dp_kfac", patch_dtype: str = "auto", kl_clip: Optional[float] = None,
-                 lr=None, eig_solver: str = "cusolver", comm_overlap: bool = False, bucket_mb: float = 16.0):
+                 lr=None, eig_solver: str = "cusolver", comm_overlap: bool = False, bucket_mb: float = 16.0,
+                 peer_gather: bool = False):
         self.hyper = KfacHyper(gamma=gamma, xi=xi, inv_type=inv_type, f_freq=f_freq, k_freq=k_freq)
         # KL-clip (north_star; off by default: the reference has none):
         # every preconditioned gradient is scaled by nu = min(1, sqrt(kl_clip / |lr^2 sum
@@ -404,6 +405,9 @@ class DPKFAC:
         if not bucket_mb > 0:
             raise ArgumentError("bucket_mb must be > 0")
         self.comm_overlap = bool(comm_overlap)
+        # peer_gather=True: the closing all-gather reads the owners' chunks in place over
+        # NVLink (IPC-mapped, one copy kernel) instead of NCCL all_gather; single node
+        self.peer_gather = bool(peer_gather) or os.environ.get("DPK_PEER_AG") == "1"
         self.bucket_mb = float(bucket_mb)
         self._bucket_ev = {}        # bucket -> event of its hook-launched pack + reduce-scatter
         if self.comm_overlap:
@@ -477,6 +481,8 @@ class DPKFAC:
         if self.kl_clip is not None:
             self._kl_ws = ops.kl_dot_workspace(dev)
         self.xchg = OwnerMajorExchange(self.layout, self.rank, dev, self.pg)
+        if self.peer_gather and self.world > 1:
+            self.xchg.enable_peer_gather()
         self.offsets = self.layout.offsets
         # pack offsets (bucket-major); the same dict object when there is one bucket
         self.in_offsets = self.offsets if len(self.layout.buckets) == 1 else self.layout.in_offsets

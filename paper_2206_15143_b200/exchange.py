@@ -117,6 +117,41 @@ class OwnerMajorExchange:
             self.chunk_out = torch.zeros(c, device=device)
             self.out_flat = torch.zeros(P * c, device=device)
         self.chunk_tmp = torch.zeros(c, device=device)
+        self._peer_ptrs = None  # enable_peer_gather(): every rank's chunk_out, IPC-mapped
+
+    def enable_peer_gather(self) -> bool:
+        """Replace the closing NCCL all-gather by one copy kernel that reads every
+        rank's chunk_out in place over NVLink (dpk_peer_gather): the chunk buffers are
+        IPC-mapped once here.  Single node only; every rank takes the same decision
+        (it returns False, and the NCCL collective stays, unless all ranks can)."""
+        import ctypes as C
+        import socket
+        from . import _lib as L
+        from .ops import lib
+        P = self.layout.world
+        if P == 1 or P > 8:
+            return False
+        co = self.chunk_out
+        buf, off = C.create_string_buffer(64), C.c_int64(0)
+        # e.g. expandable segments (no cudaMalloc segment behind the block): NCCL stays
+        ok = lib().dpk_ipc_export(co.data_ptr(), co.device.index, buf, C.byref(off)) == L.DPK_OK
+        handle, off = buf.raw, int(off.value)
+        mine = (socket.gethostname(), handle, off, ok)
+        objs = [None] * P
+        dist.all_gather_object(objs, mine, group=self.group)
+        if not all(o[3] for o in objs) or len({o[0] for o in objs}) != 1:
+            return False
+        ptrs = []
+        for r, (_, h, o, _) in enumerate(objs):
+            if r == self.rank:
+                ptrs.append(co.data_ptr())
+                continue
+            base = C.c_void_p()
+            L.check(lib().dpk_ipc_open(h, co.device.index, C.byref(base)), "dpk_ipc_open")
+            ptrs.append(base.value + o)
+        self._peer_ptrs = (C.c_void_p * P)(*ptrs)
+        self._ready = torch.zeros(1, device=co.device)
+        return True
 
     def reduce_scatter(self):
         """flat must already hold grad / P (pack scale); SUM then equals the mean."""
@@ -133,6 +168,14 @@ class OwnerMajorExchange:
 
     def all_gather(self):
         if self.layout.world > 1:
+            if self._peer_ptrs is not None:
+                # stream-ordered readiness: this tiny all-reduce completes only once
+                # every rank has reached it, i.e. finished writing its chunk_out; the
+                # next step's reduce-scatter orders the reads before any rewrite
+                dist.all_reduce(self._ready, group=self.group)
+                from .ops import peer_gather
+                peer_gather(self.out_flat, self._peer_ptrs, self.layout.world, self.layout.chunk)
+                return
             dist.all_gather_into_tensor(self.out_flat, self.chunk_out, group=self.group)
 
     def view_in(self, layer: int, shape):

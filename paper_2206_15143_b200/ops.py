@@ -570,6 +570,13 @@ def unpack(segs, flat: torch.Tensor, scale: float = 1.0):
                 "dpk_unpack_owner_major")
 
 
+def peer_gather(out: torch.Tensor, ptrs, n_src: int, count: int):
+    """out[i*count:(i+1)*count] = source i (device pointers, own chunk local, the others
+    IPC-mapped peer memory read over NVLink), one launch on the current stream."""
+    L.check(lib().dpk_peer_gather(out.data_ptr(), ptrs, int(n_src), int(count), stream_handle()),
+            "dpk_peer_gather")
+
+
 # ------------------------------------------------------------------ KL-clip (opt-in)
 def kl_dot(pre: torch.Tensor, grad: torch.Tensor, n: int, out: torch.Tensor, ws: torch.Tensor):
     """out[0] = <pre[:n], grad[:n]> (fp64 accumulate, deterministic); ws: a zeroed

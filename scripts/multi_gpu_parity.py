@@ -30,9 +30,11 @@ def main():
     bad = []
     for algorithm, inv in [("dp_kfac", "inverse"), ("dp_kfac", "eigen"), ("mpd_kfac_co", "inverse"),
                            ("mpd_kfac_mo", "inverse"), ("mpd_kfac_co", "eigen"), ("dp_kfac:balanced", "inverse"),
-                           ("dp_kfac:round_robin+overlap", "inverse"), ("dp_kfac:balanced+overlap", "eigen")]:
+                           ("dp_kfac:round_robin+overlap", "inverse"), ("dp_kfac:balanced+overlap", "eigen"),
+                           ("dp_kfac:balanced+peer", "inverse"), ("dp_kfac:round_robin+peer", "eigen")]:
         alg, _, asg = algorithm.partition(":")
-        # +overlap: bucketed reduce-scatter from the backward hooks, one layer per bucket
+        # +overlap: bucketed reduce-scatter from the backward hooks, one layer per bucket;
+        # +peer: the closing all-gather as the NVLink peer-copy kernel
         asg, _, ov = asg.partition("+")
         h = K.Hyper(gamma=0.05, xi=0.9, inv_type=inv, f_freq=1, k_freq=2)
         cl = (MLP.build_cluster if alg == "dp_kfac" else MLP.build_mpd_cluster)(spec, P, seed=5)
@@ -46,7 +48,8 @@ def main():
         model = torch.nn.Sequential(*mods[:-1]).to(dev)
         lins = [m for m in model if isinstance(m, torch.nn.Linear)]
         kf = DPKFAC(model, gamma=0.05, xi=0.9, inv_type=inv, k_freq=2, precision="3xtf32", algorithm=alg,
-                    assignment=asg or "round_robin", comm_overlap=ov == "overlap", bucket_mb=1e-4)
+                    assignment=asg or "round_robin", comm_overlap=ov == "overlap", bucket_mb=1e-4,
+                    peer_gather=ov == "peer")
         opt = torch.optim.SGD(model.parameters(), lr=0.1, momentum=0.9)
         rng = np.random.default_rng(91)
         for t in range(4):
@@ -58,9 +61,11 @@ def main():
             opt.zero_grad()
             F.cross_entropy(model(torch.from_numpy(xs.T.copy()).float().to(dev)),
                             torch.from_numpy(ys).to(dev)).backward()
-            if ov and t > 0 and len(kf._bucket_ev) != len(kf.layout.buckets):
+            if ov == "overlap" and t > 0 and len(kf._bucket_ev) != len(kf.layout.buckets):
                 bad.append((algorithm, inv, t, "hooks did not launch every bucket"))
             kf.step()
+            if ov == "peer" and t == 0 and kf.xchg._peer_ptrs is None:
+                bad.append((algorithm, inv, "peer gather not enabled"))
             if asg == "balanced" and t == 0:
                 cl = MLP.build_cluster(spec, P, seed=5, assignment=kf.assignment)
             if alg == "dp_kfac":
@@ -80,7 +85,7 @@ def main():
         kf.remove_hooks()
     # KL-clip over NCCL: every rank's partial <pre, grad> rides the all-gather (one slot per
     # owner chunk); the unpack applies nu = min(1, sqrt(kl / |lr^2 sum <pre, grad>|))
-    for inv in ("inverse", "eigen"):
+    for inv, peer in (("inverse", False), ("eigen", False), ("inverse", True)):
         h = K.Hyper(gamma=0.05, xi=0.9, inv_type=inv, f_freq=1, k_freq=1)
         cl = MLP.build_cluster(spec, P, seed=7)
         mods = []
@@ -94,7 +99,7 @@ def main():
         lins = [m for m in model if isinstance(m, torch.nn.Linear)]
         lr, kl = 0.1, 1e-5
         kf = DPKFAC(model, gamma=0.05, xi=0.9, inv_type=inv, precision="3xtf32", kl_clip=kl, lr=lr,
-                    assignment="balanced")
+                    assignment="balanced", peer_gather=peer)
         rng = np.random.default_rng(17)
         x, y = rng.standard_normal((20, B)), rng.integers(0, 5, size=B)
         shards = MLP.shard(x, y, P)

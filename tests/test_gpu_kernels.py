@@ -760,3 +760,21 @@ def test_launch_cap_gives_identical_results():
     torch.cuda.synchronize()
     assert torch.equal(outs[0], outs[1]) and torch.equal(outs[0], outs[2])
     assert ops.lib().dpk_set_launch_cap(-1) != 0  # invalid
+
+
+def test_peer_gather_copies_every_source_in_rank_order():
+    """dpk_peer_gather (the NVLink all-gather of DPKFAC(peer_gather=True)) on local
+    sources: dst = concat(sources), bit-exact; bad counts are rejected like the C ABI says."""
+    import ctypes as C
+    from paper_2206_15143_b200 import ops
+    from paper_2206_15143_b200.errors import ArgumentError
+    for n_src, count in ((1, 4), (3, 1000), (4, 25557032 // 4 // 4 * 4), (8, 64)):
+        srcs = [torch.randn(count, device=dev()) for _ in range(n_src)]
+        dst = torch.full((n_src * count,), float("nan"), device=dev())
+        ptrs = (C.c_void_p * n_src)(*[s.data_ptr() for s in srcs])
+        ops.peer_gather(dst, ptrs, n_src, count)
+        torch.cuda.synchronize()
+        assert torch.equal(dst, torch.cat(srcs))
+    ptrs = (C.c_void_p * 1)(srcs[0].data_ptr())
+    with pytest.raises(ArgumentError):
+        ops.peer_gather(dst, ptrs, 1, 6)
