@@ -53,6 +53,7 @@ struct LeafJob {
 };
 struct LeafBatch {
   int n;
+  int skip_done;  // phase 3 skips the finished rows of the current row block
   LeafJob j[LEAF_MAX];
 };
 
@@ -212,6 +213,7 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) spd_leaf_kernel(const __grid_
         if (tid == 0 && J.info) *J.info = J.fail_code;
         return;
       }
+      const bool skip_done = b.skip_done;
       // ---- phase 3: rank-W updates (lower-triangle blocks of A; X columns < k+W).
       // Column-outer: each thread's column vectors (lane-distinct, 4 smem wavefronts
       // per float4) are loaded once per step; the row vectors are warp-uniform
@@ -244,6 +246,9 @@ __global__ void __launch_bounds__(LEAF_THREADS, 1) spd_leaf_kernel(const __grid_
 #pragma unroll
         for (int r = kr; r < RB; ++r) {
           if (RB > 2 && r <= 2 * c - 1) continue;  // block entirely above the diagonal
+          // this warp's row of block kr is finished (L[i][k..k+W) = 0: the updates are
+          // exact no-ops): skip it (warp-uniform; DPK_LEAF_SKIP=0 keeps the FMAs)
+          if (r == kr && skip_done && ty < W * kq + W) continue;
           float lr[W];
 #pragma unroll
           for (int q = 0; q < W4; ++q) {
@@ -1076,8 +1081,18 @@ int launch_leaf_w(const LeafBatch& b, int cnt, cudaStream_t st) {
   return leaf_width() == 4 ? launch_leaf_nb<NB, 4>(b, cnt, st) : launch_leaf_nb<NB, 8>(b, cnt, st);
 }
 
+bool leaf_skip_done() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("DPK_LEAF_SKIP");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 int launch_leaves(std::vector<LeafJob>& leaves, cudaStream_t st) {
   thread_local LeafBatch b;
+  b.skip_done = leaf_skip_done() ? 1 : 0;
   for (size_t first = 0; first < leaves.size(); first += LEAF_MAX) {
     const int cnt = static_cast<int>(std::min<size_t>(LEAF_MAX, leaves.size() - first));
     b.n = cnt;
