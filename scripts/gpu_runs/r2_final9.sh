@@ -1,4 +1,4 @@
-# (HEAD: latency-path cp.async ring, one capture hook per layer) 4 GPUs: full gpu suite (incl. the NCCL test at P=2/4), N=1/2/4 bench lines, P=4 parity with KL-clip
+# (HEAD: cp.async latency path, one capture hook per layer, leaf row skip) 4 GPUs: full gpu suite (incl. the NCCL test at P=2/4), N=1/2/4 bench lines, P=4 parity with KL-clip
 mkdir -p gpurun_out/final
 python scripts/tf32_peak.py gpurun_out/final/tf32_peak.json > /dev/null 2>&1; echo "tf32 peak rc=$?"
 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/final/gputest.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/final/gputest.log
