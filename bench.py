@@ -525,7 +525,8 @@ def run_ours(args, rank, world, local_rank):
                        "assignment": args.assignment, "algorithm": args.algorithm, "im2col": args.im2col,
                        "comm_overlap": (f"bucketed reduce-scatter from the backward hooks, {args.bucket_mb} MB buckets"
                                         if args.comm_overlap else False),
-                       "all_gather": ("NVLink peer-copy kernel" if getattr(getattr(kf, "xchg", None), "_peer_ptrs", None)
+                       "all_gather": ("none (one rank)" if world == 1 else
+                                      "NVLink peer-copy kernel" if getattr(getattr(kf, "xchg", None), "_peer_ptrs", None)
                                       is not None else "NCCL"),
                        "memory_format": "channels_last" if mf is torch.channels_last else "contiguous",
                        "l2": "inputs (layer captures, >1.4 GB) larger than L2; no flush"},
